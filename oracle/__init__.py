@@ -1,0 +1,275 @@
+"""ctypes bindings for the CPU checker (TEST INFRASTRUCTURE ONLY).
+
+Two libraries live here:
+  * ``liboracle.so``            -- the restatement (oracle/pisa_oracle.cpp)
+  * ``_ref/libpisa_ref*.so``    -- the unmodified reference, compiled from
+                                   /root/reference by oracle/Makefile
+
+Only tests/, ``__graft_entry__.smoke()`` and bench.py's CPU legs may import this
+package. The product package (paper_2602_01077_b200) never does.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+_f32p = np.ctypeslib.ndpointer(np.float32, flags="C_CONTIGUOUS")
+_f64p = np.ctypeslib.ndpointer(np.float64, flags="C_CONTIGUOUS")
+_i32p = np.ctypeslib.ndpointer(np.int32, flags="C_CONTIGUOUS")
+_u64p = np.ctypeslib.ndpointer(np.uint64, flags="C_CONTIGUOUS")
+i64 = C.c_int64
+
+
+def build() -> None:
+    subprocess.run(["make", "-s", "-C", HERE], check=True)
+
+
+def _cpu_has_avx512() -> bool:
+    try:
+        with open("/proc/cpuinfo") as f:
+            return " avx512f " in f.read()
+    except OSError:
+        return False
+
+
+_lib = None
+_ref = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        path = os.path.join(HERE, "liboracle.so")
+        if not os.path.exists(path):
+            build()
+        L = C.CDLL(path)
+        L.oracle_rng_u64.argtypes = [C.c_uint64, _u64p, i64]
+        L.oracle_rng_gaussian.argtypes = [C.c_uint64, _f64p, i64]
+        L.oracle_gen_gaussian.argtypes = [C.c_uint64, i64, i64, i64, C.c_double, _f32p, _f32p, _f32p]
+        L.oracle_gen_clustered.argtypes = [C.c_uint64, i64, i64, i64, i64, C.c_double, C.c_double,
+                                           _f32p, _f32p, _f32p]
+        L.oracle_round_bf16.argtypes = [_f32p, i64]
+        L.oracle_sparsity_to_k.argtypes = [C.c_double, i64, C.POINTER(i64), C.POINTER(C.c_double)]
+        L.oracle_block_stats.argtypes = [_f32p, _f32p, i64, i64, i64, _f64p, _f64p, _f64p, _f64p]
+        L.oracle_query_means.argtypes = [_f32p, i64, i64, i64, _f64p]
+        L.oracle_select_plain.argtypes = [_f64p, _f64p, i64, i64, i64, i64, C.c_double, C.c_int,
+                                          _i32p, C.c_void_p]
+        L.oracle_pisa_attention.argtypes = [_f32p, _f32p, _f32p, i64, i64, i64, _i32p, i64, _f64p,
+                                            _f64p, _f64p, _f64p, C.c_double, C.c_int, C.c_int,
+                                            i64, i64, C.c_int, _f64p, _f64p, _f64p, _f64p]
+        L.oracle_dense.argtypes = [_f32p, _f32p, _f32p, i64, i64, C.c_double, i64, i64, C.c_int,
+                                   _f64p]
+        L.oracle_multihead.argtypes = [_f32p, _f32p, _f32p, i64, i64, i64, i64, C.c_double, i64,
+                                       C.c_int, C.c_int, C.c_double, C.c_int, C.c_int, _f64p,
+                                       _i32p, _f64p, _f64p, _f64p]
+        _lib = L
+    return _lib
+
+
+def ref_available() -> bool:
+    return os.path.exists(os.path.join(HERE, "_ref", "libpisa_ref.so"))
+
+
+def ref():
+    """The unmodified reference library (AVX-512 build when the host has it)."""
+    global _ref
+    if _ref is None:
+        name = "libpisa_ref_v4.so" if _cpu_has_avx512() else "libpisa_ref.so"
+        path = os.path.join(HERE, "_ref", name)
+        if not os.path.exists(path):
+            path = os.path.join(HERE, "_ref", "libpisa_ref.so")
+        R = C.CDLL(path)
+        R.ref_rng_u64.argtypes = [C.c_uint64, _u64p, i64]
+        R.ref_rng_gaussian.argtypes = [C.c_uint64, _f64p, i64]
+        R.ref_gen.argtypes = [C.c_int, C.c_uint64, i64, i64, i64, C.c_double, i64, C.c_double,
+                              C.c_double, _f32p, _f32p, _f32p]
+        R.ref_sparsity_to_k.argtypes = [C.c_double, i64, C.POINTER(i64), C.POINTER(C.c_double)]
+        R.ref_block_stats.argtypes = [_f32p, _f32p, _f32p, i64, i64, i64, _f64p, _f64p, _f64p,
+                                      _f64p, _f64p]
+        R.ref_select_plain.argtypes = [_f64p, _f64p, i64, i64, i64, i64, C.c_double, C.c_int, _i32p]
+        R.ref_multihead.argtypes = [_f32p, _f32p, _f32p, i64, i64, i64, C.c_double, C.c_int,
+                                    C.c_int, i64, i64, C.c_double, C.c_int, C.c_int, C.c_int,
+                                    C.c_uint, _f32p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                    C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
+        R.ref_bench_sample.argtypes = [_f32p, _f32p, _f32p, i64, i64, C.c_double, i64, i64,
+                                       C.c_uint, _f32p, C.POINTER(C.c_double)]
+        R.ref_dense_online.argtypes = [_f32p, _f32p, _f32p, i64, i64, C.c_int, C.c_uint, _f32p]
+        R._path = path
+        _ref = R
+    return _ref
+
+
+# ----------------------------------------------------------------- helpers --
+class OracleError(RuntimeError):
+    def __init__(self, status: int, where: str):
+        super().__init__(f"{where}: status {status}")
+        self.status = status
+
+
+def _check(st: int, where: str) -> None:
+    if st != 0:
+        raise OracleError(st, where)
+
+
+def round_bf16(x: np.ndarray) -> np.ndarray:
+    x = np.ascontiguousarray(x, dtype=np.float32).copy()
+    lib().oracle_round_bf16(x, x.size)
+    return x
+
+
+def gen(kind: str, seed: int, heads: int, L: int, d: int, std: float = 1.0, clusters: int = 16,
+        concentration: float = 2.0, noise_std: float = 0.15, bf16: bool = True):
+    """Synthetic Q/K/V exactly as the reference generates them ([H][L][d] float32),
+    optionally rounded to bf16 (RNE) so the GPU and the oracle see the same values."""
+    n = heads * L * d
+    q = np.empty(n, np.float32)
+    k = np.empty(n, np.float32)
+    v = np.empty(n, np.float32)
+    if kind == "gaussian":
+        _check(lib().oracle_gen_gaussian(seed, heads, L, d, std, q, k, v), "gen_gaussian")
+    else:
+        _check(lib().oracle_gen_clustered(seed, heads, L, d, clusters, concentration, noise_std,
+                                          q, k, v), "gen_clustered")
+    out = [a.reshape(heads, L, d) for a in (q, k, v)]
+    if bf16:
+        out = [round_bf16(a) for a in out]
+    return out
+
+
+def sparsity_to_k(r: float, n: int):
+    k = i64()
+    real = C.c_double()
+    _check(lib().oracle_sparsity_to_k(r, n, C.byref(k), C.byref(real)), "sparsity_to_k")
+    return k.value, real.value
+
+
+def block_stats(k: np.ndarray, v: np.ndarray, B: int = 64):
+    L, d = k.shape
+    N = (L + B - 1) // B
+    kb = np.empty((N, d)); vh = np.empty((N, d)); hb = np.empty((d, d)); kg = np.empty(d)
+    _check(lib().oracle_block_stats(np.ascontiguousarray(k, np.float32),
+                                    np.ascontiguousarray(v, np.float32), L, d, B, kb, vh, hb, kg),
+           "block_stats")
+    return kb, vh, hb, kg
+
+
+def query_means(q: np.ndarray, B: int = 64):
+    L, d = q.shape
+    N = (L + B - 1) // B
+    qb = np.empty((N, d))
+    _check(lib().oracle_query_means(np.ascontiguousarray(q, np.float32), L, d, B, qb), "query_means")
+    return qb
+
+
+def select_plain(qbar, kbar, k: int, scale: float, force_diagonal: bool = False,
+                 return_scores: bool = False):
+    nq, d = qbar.shape
+    n = kbar.shape[0]
+    sel = np.empty((nq, k), np.int32)
+    scores = np.empty((nq, n)) if return_scores else None
+    _check(lib().oracle_select_plain(np.ascontiguousarray(qbar), np.ascontiguousarray(kbar), nq, n,
+                                     d, k, scale, int(force_diagonal), sel,
+                                     scores.ctypes.data if scores is not None else None),
+           "select_plain")
+    return (sel, scores) if return_scores else sel
+
+
+VARIANTS = {"sparse_only": 0, "zeroth": 1, "block_first": 2, "hybrid": 3, "global_centroid": 4}
+
+
+def pisa_attention(q, k, v, selected, stats, scale: float, variant="hybrid", literal_phase3=False,
+                   qb0: int = 0, qb1: int | None = None, B: int = 64, threads: int = 0):
+    L, d = q.shape
+    N = (L + B - 1) // B
+    qb1 = N if qb1 is None else qb1
+    kb, vh, hb, kg = stats
+    out = np.zeros((L, d)); m = np.zeros(L); ell = np.zeros(L); et = np.zeros(L)
+    sel = np.ascontiguousarray(selected, np.int32)
+    _check(lib().oracle_pisa_attention(np.ascontiguousarray(q, np.float32),
+                                       np.ascontiguousarray(k, np.float32),
+                                       np.ascontiguousarray(v, np.float32), L, d, B, sel,
+                                       sel.shape[1], kb, vh, hb, kg, scale,
+                                       VARIANTS[variant], int(literal_phase3), qb0, qb1, threads,
+                                       out, m, ell, et), "pisa_attention")
+    return out, m, ell, et
+
+
+def dense(q, k, v, scale: float, r0: int = 0, r1: int | None = None, threads: int = 0):
+    L, d = q.shape
+    r1 = L if r1 is None else r1
+    out = np.zeros((L, d))
+    _check(lib().oracle_dense(np.ascontiguousarray(q, np.float32), np.ascontiguousarray(k, np.float32),
+                              np.ascontiguousarray(v, np.float32), L, d, scale, r0, r1, threads, out),
+           "dense")
+    return out
+
+
+def multihead(q, k, v, r: float = 0.875, ksel: int = 0, variant="hybrid", force_diagonal=False,
+              scale: float = 0.0, literal_phase3=False, B: int = 64, threads: int = 0):
+    H, L, d = q.shape
+    N = (L + B - 1) // B
+    kk = ksel if ksel > 0 else sparsity_to_k(r, N)[0]
+    out = np.zeros((H, L, d)); sel = np.zeros((H, N, kk), np.int32)
+    m = np.zeros((H, L)); ell = np.zeros((H, L)); et = np.zeros((H, L))
+    _check(lib().oracle_multihead(np.ascontiguousarray(q, np.float32),
+                                  np.ascontiguousarray(k, np.float32),
+                                  np.ascontiguousarray(v, np.float32), H, L, d, B, r, kk,
+                                  VARIANTS[variant], int(force_diagonal), scale,
+                                  int(literal_phase3), threads, out, sel, m, ell, et), "multihead")
+    return dict(out=out, selected=sel, row_max=m, ell=ell, ell_tail=et, k=kk)
+
+
+# ------------------------------------------------------ reference wrappers --
+def ref_gen(kind: str, seed: int, heads: int, L: int, d: int, std=1.0, clusters=16,
+            concentration=2.0, noise_std=0.15):
+    n = heads * L * d
+    q = np.empty(n, np.float32); k = np.empty(n, np.float32); v = np.empty(n, np.float32)
+    _check(ref().ref_gen(int(kind == "clustered"), seed, heads, L, d, std, clusters, concentration,
+                         noise_std, q, k, v), "ref_gen")
+    return [a.reshape(heads, L, d) for a in (q, k, v)]
+
+
+def ref_block_stats(q, k, v, B: int = 64):
+    L, d = k.shape
+    N = L // B
+    kb = np.empty((N, d)); vh = np.empty((N, d)); hb = np.empty((d, d)); qb = np.empty((N, d))
+    kg = np.empty(d)
+    _check(ref().ref_block_stats(np.ascontiguousarray(q, np.float32),
+                                 np.ascontiguousarray(k, np.float32),
+                                 np.ascontiguousarray(v, np.float32), L, d, B, kb, vh, hb, qb, kg),
+           "ref_block_stats")
+    return kb, vh, hb, qb, kg
+
+
+def ref_select_plain(qbar, kbar, k: int, scale: float, force_diagonal=False):
+    nq, d = qbar.shape
+    sel = np.empty((nq, k), np.int32)
+    _check(ref().ref_select_plain(np.ascontiguousarray(qbar), np.ascontiguousarray(kbar), nq,
+                                  kbar.shape[0], d, k, scale, int(force_diagonal), sel),
+           "ref_select_plain")
+    return sel
+
+
+def ref_multihead(q, k, v, r=0.875, variant="hybrid", force_diagonal=False, B=64, group=8,
+                  scale=0.0, accum_f64=True, streaming=True, literal_phase3=False, threads=0):
+    H, L, d = q.shape
+    N = L // B
+    kk, _ = sparsity_to_k(r, N)
+    out = np.zeros((H, L, d), np.float32)
+    sel = np.zeros((H, N, kk), np.int32)
+    denom = np.zeros((H, L)); tm = np.zeros((H, L)); et = np.zeros((H, L)); rm = np.zeros((H, L))
+    times = np.zeros(3)
+    kout = i64()
+    _check(ref().ref_multihead(np.ascontiguousarray(q, np.float32),
+                               np.ascontiguousarray(k, np.float32),
+                               np.ascontiguousarray(v, np.float32), H, L, d, r, VARIANTS[variant],
+                               int(force_diagonal), B, group, scale, int(accum_f64),
+                               int(streaming), int(literal_phase3), threads, out,
+                               sel.ctypes.data, denom.ctypes.data, tm.ctypes.data, et.ctypes.data,
+                               rm.ctypes.data, times.ctypes.data, C.byref(kout)), "ref_multihead")
+    return dict(out=out, selected=sel, denom=denom, tail_mass=tm, ell_tail=et, row_max=rm,
+                times_ms=times, k=kout.value)

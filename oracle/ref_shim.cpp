@@ -1,0 +1,213 @@
+// C-ABI shim over the UNMODIFIED reference library (header-only C++20), so tests
+// and bench.py can call the reference itself through ctypes.
+//
+// TEST INFRASTRUCTURE ONLY: built by oracle/Makefile from the headers where they
+// lie (/root/reference/proj/include, never copied) into oracle/_ref/. Used as the
+// oracle's pin and as the timed CPU baseline (`bench.py --impl reference`).
+//
+// Every entry point calls the reference's public API: pisa::gen_gaussian,
+// pisa::gen_clustered, pisa::compute_block_stats, pisa::compute_global_stats,
+// pisa::query_block_means, pisa::select_topk_plain, pisa::pisa_streaming,
+// pisa::pisa_reference, pisa::pisa_multihead, pisa::dense_online.
+
+#include <chrono>
+#include <cstdint>
+#include <cstring>
+#include <exception>
+
+#include "pisa/pisa.hpp"
+
+namespace {
+
+// Same numbering as include/pisa_b200.h.
+int status_of(const std::exception& e) {
+    if (dynamic_cast<const pisa::BlockDivisibility*>(&e)) return 2;
+    if (dynamic_cast<const pisa::InvalidSparsity*>(&e)) return 3;
+    if (dynamic_cast<const pisa::InvalidEpsilon*>(&e)) return 4;
+    if (dynamic_cast<const pisa::EmptySelection*>(&e)) return 5;
+    if (dynamic_cast<const pisa::NumericalOverflow*>(&e)) return 6;
+    if (dynamic_cast<const pisa::DegenerateScale*>(&e)) return 7;
+    if (dynamic_cast<const pisa::InvalidDimension*>(&e)) return 1;
+    return 99;
+}
+
+pisa::AttentionConfig make_cfg(int64_t block, int64_t group, double scale, int accum_f64,
+                               int literal_phase3, unsigned threads) {
+    pisa::AttentionConfig cfg;
+    cfg.block_size = std::size_t(block);
+    cfg.group_size = std::size_t(group);
+    cfg.scale = scale;
+    cfg.accum = accum_f64 ? pisa::AccumDtype::F64 : pisa::AccumDtype::F32;
+    cfg.literal_phase3 = literal_phase3 != 0;
+    cfg.num_threads = threads;
+    return cfg;
+}
+
+template <class Fn>
+int guarded(Fn&& fn) {
+    try {
+        fn();
+        return 0;
+    } catch (const std::exception& e) {
+        return status_of(e);
+    }
+}
+
+}  // namespace
+
+extern "C" {
+
+int ref_rng_u64(uint64_t seed, uint64_t* out, int64_t n) {
+    pisa::Rng r(seed);
+    for (int64_t i = 0; i < n; ++i) out[i] = r.next_u64();
+    return 0;
+}
+
+int ref_rng_gaussian(uint64_t seed, double* out, int64_t n) {
+    pisa::Rng r(seed);
+    for (int64_t i = 0; i < n; ++i) out[i] = r.gaussian();
+    return 0;
+}
+
+int ref_gen(int clustered, uint64_t seed, int64_t heads, int64_t L, int64_t d, double std_dev,
+            int64_t n_clusters, double concentration, double noise_std, float* q, float* k,
+            float* v) {
+    return guarded([&] {
+        pisa::TensorBundle<float> b =
+            clustered ? pisa::gen_clustered<float>(seed, std::size_t(heads), std::size_t(L),
+                                                   std::size_t(d), std::size_t(n_clusters),
+                                                   concentration, noise_std)
+                      : pisa::gen_gaussian<float>(seed, std::size_t(heads), std::size_t(L),
+                                                  std::size_t(d), std_dev);
+        std::memcpy(q, b.q.data(), b.q.size() * sizeof(float));
+        std::memcpy(k, b.k.data(), b.k.size() * sizeof(float));
+        std::memcpy(v, b.v.data(), b.v.size() * sizeof(float));
+    });
+}
+
+int ref_sparsity_to_k(double r, int64_t n, int64_t* k, double* realized) {
+    return guarded([&] {
+        const auto res = pisa::sparsity_to_k(r, std::size_t(n));
+        *k = int64_t(res.k);
+        *realized = res.realized;
+    });
+}
+
+// One head: prepare products (block_stats.hpp:155-278). Norms off, as in the
+// Plain-router pisa_multihead path (engine.hpp:431,439).
+int ref_block_stats(const float* q, const float* k, const float* v, int64_t L, int64_t d,
+                    int64_t B, double* kbar, double* vhat, double* hbar, double* qbar,
+                    double* kbar_global) {
+    return guarded([&] {
+        pisa::ConstView<float> kv(k, std::size_t(L), std::size_t(d));
+        pisa::ConstView<float> vv(v, std::size_t(L), std::size_t(d));
+        pisa::ConstView<float> qv(q, std::size_t(L), std::size_t(d));
+        auto st = pisa::compute_block_stats(kv, vv, std::size_t(B));
+        pisa::compute_global_stats(st, pisa::SpectralMethod::Exact, false);
+        const auto qb = pisa::query_block_means(qv, std::size_t(B));
+        std::memcpy(kbar, st.k_bar.data.data(), st.k_bar.data.size() * sizeof(double));
+        std::memcpy(vhat, st.v_hat.data.data(), st.v_hat.data.size() * sizeof(double));
+        std::memcpy(hbar, st.h_bar.data.data(), st.h_bar.data.size() * sizeof(double));
+        std::memcpy(qbar, qb.data.data(), qb.data.size() * sizeof(double));
+        if (kbar_global)
+            std::memcpy(kbar_global, st.k_bar_global.data(), st.k_bar_global.size() * sizeof(double));
+    });
+}
+
+int ref_select_plain(const double* qbar, const double* kbar, int64_t nq, int64_t n, int64_t d,
+                     int64_t k, double scale, int force_diagonal, int32_t* selected) {
+    return guarded([&] {
+        pisa::ConstView<double> qb(qbar, std::size_t(nq), std::size_t(d));
+        pisa::ConstView<double> kb(kbar, std::size_t(n), std::size_t(d));
+        const auto plan = pisa::select_topk_plain(qb, kb, std::size_t(k), scale, force_diagonal != 0);
+        for (int64_t i = 0; i < nq; ++i)
+            for (int64_t p = 0; p < k; ++p) selected[i * k + p] = int32_t(plan.selected[i][p]);
+    });
+}
+
+// pisa_multihead (engine.hpp:408-470) on a [H][L][d] float bundle, Plain router.
+// out: [H][L][d] float; selected: [H][N][k]; diagnostics [H][L] doubles
+// (optional); times_ms[3] = prepare, select, attention (optional).
+int ref_multihead(const float* q, const float* k, const float* v, int64_t H, int64_t L,
+                  int64_t d, double r, int variant, int force_diagonal, int64_t block,
+                  int64_t group, double scale, int accum_f64, int streaming, int literal_phase3,
+                  unsigned threads, float* out, int32_t* selected, double* denom,
+                  double* tail_mass, double* ell_tail, double* row_max, double* times_ms,
+                  int64_t* k_out) {
+    return guarded([&] {
+        pisa::TensorBundle<float> b;
+        b.num_heads = std::size_t(H);
+        b.seq_len = std::size_t(L);
+        b.head_dim = std::size_t(d);
+        const std::size_t n = std::size_t(H * L * d);
+        b.q.assign(q, q + n);
+        b.k.assign(k, k + n);
+        b.v.assign(v, v + n);
+        const auto cfg = make_cfg(block, group, scale, accum_f64, literal_phase3, threads);
+        pisa::RouterOptions router;
+        router.force_diagonal = force_diagonal != 0;
+        const auto res = pisa::pisa_multihead(b, r, router, pisa::PisaVariant(variant), cfg,
+                                              streaming != 0);
+        const std::size_t nb = res.num_blocks, kk = res.k;
+        if (k_out) *k_out = int64_t(kk);
+        for (std::size_t h = 0; h < std::size_t(H); ++h) {
+            const auto& ho = res.heads[h];
+            std::memcpy(out + h * L * d, ho.output.data.data(), std::size_t(L * d) * sizeof(float));
+            if (selected)
+                for (std::size_t i = 0; i < nb; ++i)
+                    for (std::size_t p = 0; p < kk; ++p)
+                        selected[(h * nb + i) * kk + p] = int32_t(res.plans[h].selected[i][p]);
+            for (std::size_t t = 0; t < std::size_t(L); ++t) {
+                if (denom) denom[h * L + t] = ho.denom[t];
+                if (tail_mass) tail_mass[h * L + t] = ho.tail_mass[t];
+                if (ell_tail) ell_tail[h * L + t] = ho.ell_tail[t];
+                if (row_max) row_max[h * L + t] = ho.row_max[t];
+            }
+        }
+        if (times_ms) {
+            times_ms[0] = res.prepare_ms;
+            times_ms[1] = res.select_ms;
+            times_ms[2] = res.attention_ms;
+        }
+    });
+}
+
+// The cmd_bench hot path (pisa_cli.cpp:728-729) restricted to a contiguous range
+// of query blocks [qb0, qb1) of one head, through the reference's public step
+// functions: prepare over the full K/V, route the sampled query blocks, then
+// pisa_streaming with accum F32. Used by bench.py --impl reference to time a
+// bounded sample. Returns wall ms of the whole call in *ms.
+int ref_bench_sample(const float* q, const float* k, const float* v, int64_t L, int64_t d,
+                     double r, int64_t qb0, int64_t qb1, unsigned threads, float* out,
+                     double* ms) {
+    return guarded([&] {
+        const auto t0 = std::chrono::steady_clock::now();
+        const auto cfg = make_cfg(64, 8, 0.0, 0, 0, threads);
+        pisa::ConstView<float> kv(k, std::size_t(L), std::size_t(d));
+        pisa::ConstView<float> vv(v, std::size_t(L), std::size_t(d));
+        const std::size_t rows = std::size_t((qb1 - qb0) * 64);
+        pisa::ConstView<float> qv(q + qb0 * 64 * d, rows, std::size_t(d));
+        auto st = pisa::compute_block_stats(kv, vv, 64);
+        pisa::compute_global_stats(st, pisa::SpectralMethod::Exact, false);
+        const auto qb = pisa::query_block_means(qv, 64);
+        const auto res = pisa::sparsity_to_k(r, st.num_blocks);
+        const auto plan = pisa::select_topk_plain(qb, st.k_bar, res.k, cfg.resolved_scale(std::size_t(d)));
+        const auto o = pisa::pisa_streaming(qv, kv, vv, plan, st, cfg);
+        std::memcpy(out, o.output.data.data(), o.output.data.size() * sizeof(float));
+        *ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    });
+}
+
+int ref_dense_online(const float* q, const float* k, const float* v, int64_t L, int64_t d,
+                     int accum_f64, unsigned threads, float* out) {
+    return guarded([&] {
+        const auto cfg = make_cfg(64, 8, 0.0, accum_f64, 0, threads);
+        pisa::ConstView<float> qv(q, std::size_t(L), std::size_t(d));
+        pisa::ConstView<float> kv(k, std::size_t(L), std::size_t(d));
+        pisa::ConstView<float> vv(v, std::size_t(L), std::size_t(d));
+        const auto o = pisa::dense_online(qv, kv, vv, cfg);
+        std::memcpy(out, o.data.data(), o.data.size() * sizeof(float));
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,17 @@
+"""B200-native PISA (Piecewise Sparse Attention, arXiv 2602.01077) forward.
+
+The product is the C-ABI library lib/libpisa_b200.so (include/pisa_b200.h),
+built from csrc/ for sm_100a. This package is the Python host mirror of the
+reference's operator interface (``pisa::`` in /root/reference/proj/include).
+"""
+from .pisa import (  # noqa: F401
+    AccumDtype, AttentionConfig, BlockDivisibility, BlockStatistics, Context, CudaError,
+    DegenerateScale, EmptySelection, Error, ErrorKind, InvalidDimension, InvalidEpsilon,
+    InvalidSparsity, MultiheadResult, NumericalOverflow, PisaOutput, PisaVariant,
+    RouterOptions, RouterStrategy, SelectionPlan, SparsityResolution, TensorBundle,
+    Unsupported, compute_prepare, fwd, fwd_host, kernel_names, make_desc, pisa_attention,
+    pisa_multihead, pisa_reference, pisa_streaming, resolve, select_topk_plain, selftest_mma,
+    sparsity_to_k, variant_name,
+)
+
+__all__ = [n for n in dir() if not n.startswith("_")]

@@ -1,0 +1,292 @@
+// K1: block statistics (the "prepare" step of pisa_multihead, engine.hpp:437-441).
+//
+// Replaces compute_block_stats (block_stats.hpp:155-202), the H_bar part of
+// compute_global_stats (:207-226) and query_block_means (:259-278). One CTA
+// streams kStatsG consecutive 64-row blocks of one (batch, head):
+//   * warp 0     : TMA producer, 3-stage ring of {K, V, Q} 64-row tiles (128B swizzle)
+//   * warp 1     : tcgen05 MMA issuer: TMEM[a][c] += sum_rows K[r][a] V[r][c]
+//                  (both operands MN-major straight from the TMA image)
+//   * warps 2..5 : one thread per column: fp32 column sums -> k_bar, v_hat, q_bar;
+//                  epilogue: partial H = K^T V - sum_j k_bar_j (x) v_hat_j
+// The first-order moment uses the identity
+//   sum_n (k_n - k_bar)^T v_n = sum_n k_n^T v_n - k_bar^T v_hat      (per block)
+// so the tensor core sees exact bf16 inputs and accumulates in fp32; only the
+// rank-one correction runs on CUDA cores. HBM-bound: every input byte is read
+// once. Ragged last block: TMA zero-fills rows >= L, means divide by n_j.
+#include "kernels.h"
+#include "sm100.cuh"
+
+namespace pisa_b200 {
+using namespace pisa_sm100;
+
+namespace {
+
+constexpr int kStages = 3;
+constexpr int kThreads = 192;
+
+template <int D>
+struct StatsCfg {
+    static constexpr int kTile = 64 * D * 2;        // one 64-row tile of K, V or Q (bytes)
+    static constexpr int kStage = 3 * kTile;        // K | V | Q
+    static constexpr int kRing = kStages * kStage;
+    static constexpr int kKbS = kStatsG * D * 4;    // k_bar of the chunk (fp32)
+    static constexpr int kSmem = 1024 + kRing + 2 * kKbS + 256;
+};
+
+template <int D>
+__global__ void __launch_bounds__(kThreads, 1)
+    block_stats_kernel(const __grid_constant__ CUtensorMap tmQ,
+                       const __grid_constant__ CUtensorMap tmK,
+                       const __grid_constant__ CUtensorMap tmV, StatsArgs a) {
+    using Cfg = StatsCfg<D>;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                               ~uintptr_t(1023));
+    uint8_t* ring = smem;
+    float* kb_s = reinterpret_cast<float*>(smem + Cfg::kRing);
+    float* vh_s = kb_s + kStatsG * D;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Cfg::kRing + 2 * Cfg::kKbS);
+    uint64_t* full = bars;               // [kStages]
+    uint64_t* empty = bars + kStages;    // [kStages]
+    uint64_t* done = bars + 2 * kStages;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kStages + 1);
+
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    const int chunk = blockIdx.x;
+    const int bh = blockIdx.y;
+    const int b = bh / a.H, h = bh % a.H;
+    const int j0 = chunk * kStatsG;
+    const int nb = min(kStatsG, a.N - j0);
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kStages; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1 + 4);  // MMA commit + 4 column warps
+        }
+        mbar_init(done, 1);
+        fence_mbar_init();
+        tma_prefetch(&tmQ);
+        tma_prefetch(&tmK);
+        tma_prefetch(&tmV);
+    }
+    if (warp == 1) {
+        tmem_alloc(tmem_slot, 128);
+        tmem_relinquish();
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            for (int jl = 0; jl < nb; ++jl) {
+                const int s = jl % kStages;
+                mbar_wait(&empty[s], ((jl / kStages) & 1) ^ 1);
+                uint8_t* st = ring + s * Cfg::kStage;
+                mbar_expect_tx(&full[s], Cfg::kStage);
+                const int row = (j0 + jl) * 64;
+#pragma unroll
+                for (int half = 0; half < D / 64; ++half) {
+                    tma_load_4d(st + half * 8192, &tmK, &full[s], half * 64, row, h, b);
+                    tma_load_4d(st + Cfg::kTile + half * 8192, &tmV, &full[s], half * 64, row, h, b);
+                    tma_load_4d(st + 2 * Cfg::kTile + half * 8192, &tmQ, &full[s], half * 64, row, h, b);
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            // M = 128: for D = 128 the two MN chunks are K's column halves; for D = 64
+            // the second chunk is the V tile right behind K (rows 64..127 of the
+            // product are V^T V and are ignored). N = D.
+            constexpr uint32_t idesc = idesc_bf16(128, D, 1, 1);
+            for (int jl = 0; jl < nb; ++jl) {
+                const int s = jl % kStages;
+                mbar_wait(&full[s], (jl / kStages) & 1);
+                tc_fence_after();
+                const uint32_t kbase = smem_u32(ring + s * Cfg::kStage);
+                const uint32_t vbase = kbase + Cfg::kTile;
+#pragma unroll
+                for (int ks = 0; ks < 4; ++ks) {
+                    const uint64_t ad = sdesc_sw128(kbase + ks * 2048, 8192, 1024);
+                    const uint64_t bd = sdesc_sw128(vbase + ks * 2048, 8192, 1024);
+                    mma_ss(tmem, ad, bd, idesc, (jl | ks) != 0);
+                }
+                mma_commit(&empty[s]);
+            }
+            mma_commit(done);
+        }
+    } else {
+        // Column warps: column c == TMEM lane this thread reads in the epilogue.
+        const int q = warp & 3;
+        const int c = q * 32 + lane;
+        const bool has_col = c < D;
+        const float* kcol_unused = nullptr;
+        (void)kcol_unused;
+        for (int jl = 0; jl < nb; ++jl) {
+            const int s = jl % kStages;
+            mbar_wait(&full[s], (jl / kStages) & 1);
+            const int j = j0 + jl;
+            const int nrow = min(64, a.L - j * 64);
+            if (has_col) {
+                const uint8_t* st = ring + s * Cfg::kStage;
+                const uint32_t coff = (c >> 6) * 8192;
+                float sk = 0.f, sv = 0.f, sq = 0.f;
+                for (int r = 0; r < nrow; ++r) {
+                    const uint32_t off = coff + sw128_off(r, c & 63);
+                    sk += __bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(st + off));
+                    sv += __bfloat162float(
+                        *reinterpret_cast<const __nv_bfloat16*>(st + Cfg::kTile + off));
+                    sq += __bfloat162float(
+                        *reinterpret_cast<const __nv_bfloat16*>(st + 2 * Cfg::kTile + off));
+                }
+                const float inv = 1.0f / float(nrow);
+                const float kbv = sk * inv;
+                const size_t o = (size_t(bh) * a.N + j) * D + c;
+                a.kbar[o] = kbv;
+                a.vhat[o] = sv;
+                a.qbar[o] = sq * inv;
+                const size_t ob = (size_t(bh) * a.Npad + j) * D + c;
+                a.kbar_bf[ob] = __float2bfloat16_rn(kbv);
+                a.vhat_bf[ob] = __float2bfloat16_rn(sv);
+                kb_s[jl * D + c] = kbv;
+                vh_s[jl * D + c] = sv;
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[s]);
+        }
+        // Zero the bf16 padding rows [N, Npad) once per (b, h).
+        if (has_col && j0 + nb == a.N) {
+            for (int j = a.N; j < a.Npad; ++j) {
+                const size_t ob = (size_t(bh) * a.Npad + j) * D + c;
+                a.kbar_bf[ob] = __float2bfloat16_rn(0.f);
+                a.vhat_bf[ob] = __float2bfloat16_rn(0.f);
+            }
+        }
+        asm volatile("bar.sync 1, 128;" ::: "memory");  // kb_s / vh_s complete
+        mbar_wait(done, 0);
+        tc_fence_after();
+        // Epilogue: row a == c of the D x D partial.
+        if (q < D / 32) {
+            const int arow = c;
+            float* dst = a.hpart + ((size_t(bh) * a.nchunk + chunk) * D + arow) * D;
+#pragma unroll 1
+            for (int cc = 0; cc < D; cc += 32) {
+                uint32_t r[32];
+                tmem_ld32(tmem + (uint32_t(q * 32) << 16) + cc, r);
+                tmem_ld_wait(r);
+                float acc[32];
+#pragma unroll
+                for (int i = 0; i < 32; ++i) acc[i] = __uint_as_float(r[i]);
+                for (int jl = 0; jl < nb; ++jl) {
+                    const float ka = kb_s[jl * D + arow];
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) acc[i] = fmaf(-ka, vh_s[jl * D + cc + i], acc[i]);
+                }
+#pragma unroll
+                for (int i = 0; i < 32; i += 4)
+                    *reinterpret_cast<float4*>(dst + cc + i) =
+                        make_float4(acc[i], acc[i + 1], acc[i + 2], acc[i + 3]);
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) tmem_dealloc(tmem, 128);
+}
+
+template <int D>
+__global__ void hbar_reduce_kernel(const float* __restrict__ hpart, int nchunk, int N,
+                                   const float* __restrict__ kbar, float* __restrict__ hbar,
+                                   __nv_bfloat16* __restrict__ hbar_bf,
+                                   float* __restrict__ kbar_global) {
+    const int bh = blockIdx.y;
+    const int e = blockIdx.x * blockDim.x + threadIdx.x;
+    if (e < D * D) {
+        const float* p = hpart + size_t(bh) * nchunk * D * D + e;
+        float s = 0.f;
+        for (int c = 0; c < nchunk; ++c) s += p[size_t(c) * D * D];
+        s /= float(N);
+        hbar[size_t(bh) * D * D + e] = s;
+        hbar_bf[size_t(bh) * D * D + e] = __float2bfloat16_rn(s);
+    }
+    if (kbar_global != nullptr && blockIdx.x == 0 && threadIdx.x < D) {
+        const float* kb = kbar + size_t(bh) * N * D + threadIdx.x;
+        float s = 0.f;
+        for (int j = 0; j < N; ++j) s += kb[size_t(j) * D];
+        kbar_global[size_t(bh) * D + threadIdx.x] = s / float(N);
+    }
+}
+
+template <int D>
+__global__ void stats_to_bf16_kernel(const float* __restrict__ kbar,
+                                     const float* __restrict__ vhat,
+                                     const float* __restrict__ hbar, int N, int Npad,
+                                     __nv_bfloat16* __restrict__ kbar_bf,
+                                     __nv_bfloat16* __restrict__ vhat_bf,
+                                     __nv_bfloat16* __restrict__ hbar_bf,
+                                     float* __restrict__ kbar_global) {
+    const int bh = blockIdx.y;
+    const int total = Npad * D;
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
+        const int j = e / D;
+        const float kv = j < N ? kbar[size_t(bh) * N * D + e] : 0.f;
+        const float vv = j < N ? vhat[size_t(bh) * N * D + e] : 0.f;
+        kbar_bf[size_t(bh) * Npad * D + e] = __float2bfloat16_rn(kv);
+        vhat_bf[size_t(bh) * Npad * D + e] = __float2bfloat16_rn(vv);
+    }
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < D * D; e += gridDim.x * blockDim.x)
+        hbar_bf[size_t(bh) * D * D + e] = __float2bfloat16_rn(hbar[size_t(bh) * D * D + e]);
+    if (kbar_global != nullptr && blockIdx.x == 0 && threadIdx.x < D) {
+        const float* kb = kbar + size_t(bh) * N * D + threadIdx.x;
+        float s = 0.f;
+        for (int j = 0; j < N; ++j) s += kb[size_t(j) * D];
+        kbar_global[size_t(bh) * D + threadIdx.x] = s / float(N);
+    }
+}
+
+}  // namespace
+
+cudaError_t launch_block_stats(int D, const CUtensorMap& tmQ, const CUtensorMap& tmK,
+                               const CUtensorMap& tmV, const StatsArgs& a, int BH,
+                               cudaStream_t s) {
+    dim3 grid(a.nchunk, BH);
+    if (D == 128) {
+        auto k = block_stats_kernel<128>;
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, StatsCfg<128>::kSmem);
+        k<<<grid, kThreads, StatsCfg<128>::kSmem, s>>>(tmQ, tmK, tmV, a);
+    } else {
+        auto k = block_stats_kernel<64>;
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, StatsCfg<64>::kSmem);
+        k<<<grid, kThreads, StatsCfg<64>::kSmem, s>>>(tmQ, tmK, tmV, a);
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_hbar_reduce(int D, const float* hpart, int nchunk, int N, const float* kbar,
+                               float* hbar, __nv_bfloat16* hbar_bf, float* kbar_global, int BH,
+                               cudaStream_t s) {
+    dim3 grid((D * D + 255) / 256, BH);
+    if (D == 128)
+        hbar_reduce_kernel<128><<<grid, 256, 0, s>>>(hpart, nchunk, N, kbar, hbar, hbar_bf, kbar_global);
+    else
+        hbar_reduce_kernel<64><<<grid, 256, 0, s>>>(hpart, nchunk, N, kbar, hbar, hbar_bf, kbar_global);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_stats_to_bf16(int D, const float* kbar, const float* vhat, const float* hbar,
+                                 int N, int Npad, __nv_bfloat16* kbar_bf, __nv_bfloat16* vhat_bf,
+                                 __nv_bfloat16* hbar_bf, float* kbar_global, int BH,
+                                 cudaStream_t s) {
+    dim3 grid(32, BH);
+    if (D == 128)
+        stats_to_bf16_kernel<128><<<grid, 256, 0, s>>>(kbar, vhat, hbar, N, Npad, kbar_bf, vhat_bf,
+                                                       hbar_bf, kbar_global);
+    else
+        stats_to_bf16_kernel<64><<<grid, 256, 0, s>>>(kbar, vhat, hbar, N, Npad, kbar_bf, vhat_bf,
+                                                      hbar_bf, kbar_global);
+    return cudaGetLastError();
+}
+
+}  // namespace pisa_b200

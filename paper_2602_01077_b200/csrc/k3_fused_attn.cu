@@ -1,0 +1,475 @@
+// K3: fused piecewise attention -- Algorithm 1 of the paper as
+// implemented by pisa_streaming_impl (engine.hpp:232-370), in ONE kernel:
+//
+//   Phase 1  exact online softmax over the selected key blocks S_i
+//            (attend_block_row, attention.hpp:66-91)
+//   Phase 2  zeroth-order tail: centroid "keys" k_bar_j with value sums v_hat_j
+//            over the complement U_i, denominator weight n_j (= B) per centroid,
+//            ell_tail += p (engine.hpp:297-329)
+//   Phase 3  O = (acc + scale * ell_tail * (q . H_bar)) / ell   (engine.hpp:335-358)
+//
+// Tiling. One CTA owns 128 query rows = query blocks (2t, 2t+1), because the
+// tcgen05 M=128 MMA is the full-rate shape (M=64 runs at half rate). The CTA
+// walks the ascending UNION of the two selections; a per-half flag masks the
+// block for the half that did not select it (its P rows are zero). Since
+// |union| <= 2k this never does more MMA work than two M=64 passes, and with
+// correlated neighbours (real DiT activations, clustered data) |union| ~ k.
+// Phase 2 is the same loop over ceil(N/64) centroid tiles, with a per-half
+// column mask (the selection bitmask) and per-column weight n_j. Phase 3 is one
+// more MMA, Q . H_bar, into the S columns of TMEM.
+//
+// Warp roles (256 threads, two CTAs per SM so one CTA's softmax overlaps the
+// other's MMAs):
+//   warp 0     TMA producer: Q once; K/V (or k_bar/v_hat) 64-row tiles into a
+//              2-stage ring; H_bar into the K ring at the end
+//   warp 1     single-thread tcgen05.mma issuer: S_t = Q K_t^T (SS, K-major),
+//              O += P_{t-1} V_{t-1} (TS: P from TMEM, V MN-major), Q H_bar
+//   warp 2     TMEM allocator (256 columns: O | S0 | S1)
+//   warp 3     builds the union list from the two selection bitmasks
+//   warps 4-7  softmax / correction / epilogue, one thread per query row
+//              (TMEM lane), exp2 with log2(e)*scale folded in, lazy rescale of O
+//              (only when the running max grows by > 2^8), P written back to
+//              TMEM as bf16 over the S columns it came from.
+#include "kernels.h"
+#include "sm100.cuh"
+
+namespace pisa_b200 {
+using namespace pisa_sm100;
+
+namespace {
+
+constexpr int kThreads = 256;
+constexpr float kRescaleThresh = 8.0f;  // log2 units
+constexpr uint32_t kColO = 0, kColS = 128;
+
+template <int D>
+struct FusedCfg {
+    static constexpr int kQ = 128 * D * 2;  // Q tile bytes (2 halves of 128 rows for D=128)
+    static constexpr int kKV = 64 * D * 2;  // one K or V stage
+    static constexpr int kOffQ = 0;
+    static constexpr int kOffK = kQ;
+    static constexpr int kOffV = kQ + 2 * kKV;
+    static constexpr int kOffBar = kQ + 4 * kKV;
+    static constexpr int kBarBytes = 256;
+    static constexpr int kOffMask = kOffBar + kBarBytes;
+};
+
+struct Bars {
+    uint64_t q_full, h_full, qh_full;
+    uint64_t k_full[2], k_empty[2], v_full[2], v_empty[2];
+    uint64_t s_full[2], p_full[2];
+    uint64_t o_done;
+    uint32_t tmem_base;
+    uint32_t n_union;
+};
+
+template <int D>
+__global__ void __launch_bounds__(kThreads, 2)
+    fused_attn_kernel(const __grid_constant__ CUtensorMap tmQ,
+                      const __grid_constant__ CUtensorMap tmK,
+                      const __grid_constant__ CUtensorMap tmV,
+                      const __grid_constant__ CUtensorMap tmKb,
+                      const __grid_constant__ CUtensorMap tmVh,
+                      const __grid_constant__ CUtensorMap tmH, FusedArgs a) {
+    using Cfg = FusedCfg<D>;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                               ~uintptr_t(1023));
+    Bars& bar = *reinterpret_cast<Bars*>(smem + Cfg::kOffBar);
+    uint32_t* maskA = reinterpret_cast<uint32_t*>(smem + Cfg::kOffMask);
+    uint32_t* maskB = maskA + a.W;
+    uint16_t* ulist = reinterpret_cast<uint16_t*>(maskB + a.W);
+
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    const int tile = blockIdx.x;
+    const int bh = blockIdx.y;
+    const int b = bh / a.H, h = bh % a.H;
+    const int iA = 2 * tile, iB = 2 * tile + 1;
+    const bool hasB = iB < a.N;
+    const bool tail = a.variant != 0;                       // Zeroth, Hybrid, GlobalCentroid
+    const bool first_order = a.variant == 3 || a.variant == 4;
+    const int n_last = a.L - (a.N - 1) * 64;
+
+    // ------------------------------------------------------------ setup --
+    if (threadIdx.x == 0) {
+        mbar_init(&bar.q_full, 1);
+        mbar_init(&bar.h_full, 1);
+        mbar_init(&bar.qh_full, 1);
+        for (int s = 0; s < 2; ++s) {
+            mbar_init(&bar.k_full[s], 1);
+            mbar_init(&bar.k_empty[s], 1);
+            mbar_init(&bar.v_full[s], 1);
+            mbar_init(&bar.v_empty[s], 1);
+            mbar_init(&bar.s_full[s], 1);
+            mbar_init(&bar.p_full[s], 4);
+        }
+        mbar_init(&bar.o_done, 1);
+        fence_mbar_init();
+        tma_prefetch(&tmQ);
+        tma_prefetch(&tmK);
+        tma_prefetch(&tmV);
+    }
+    if (warp == 2) {
+        tmem_alloc(&bar.tmem_base, 256);
+        tmem_relinquish();
+    }
+    if (warp == 3) {
+        // selection bitmasks of the two query blocks -> ascending union with flags
+        const uint32_t* mA = a.mask + (size_t(bh) * a.N + iA) * a.W;
+        const uint32_t* mB = a.mask + (size_t(bh) * a.N + iB) * a.W;
+        uint32_t base = 0;
+        for (int w0 = 0; w0 < a.W; w0 += 32) {
+            const int w = w0 + lane;
+            const uint32_t wa = w < a.W ? mA[w] : 0u;
+            const uint32_t wb = (w < a.W && hasB) ? mB[w] : 0u;
+            if (w < a.W) {
+                maskA[w] = wa;
+                maskB[w] = hasB ? wb : 0xffffffffu;
+            }
+            uint32_t bits = wa | wb;
+            const uint32_t cnt = __popc(bits);
+            uint32_t incl = cnt;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += v;
+            }
+            uint32_t pos = base + incl - cnt;
+            while (bits) {
+                const int bit = __ffs(bits) - 1;
+                bits &= bits - 1;
+                const uint32_t j = uint32_t(w * 32 + bit);
+                ulist[pos++] = uint16_t(j | (((wa >> bit) & 1u) << 14) | (((wb >> bit) & 1u) << 15));
+            }
+            base += __shfl_sync(0xffffffffu, incl, 31);
+        }
+        if (lane == 0) bar.n_union = base;
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = bar.tmem_base;
+    const int U = int(bar.n_union);
+    const int T = U + (tail ? a.nchunk2 : 0);  // key tiles: union blocks, then centroid tiles
+
+    if (warp == 0) {
+        // --------------------------------------------------------- producer --
+        if (lane == 0) {
+            uint8_t* sQ = smem + Cfg::kOffQ;
+            mbar_expect_tx(&bar.q_full, Cfg::kQ);
+#pragma unroll
+            for (int half = 0; half < D / 64; ++half)
+                tma_load_4d(sQ + half * 16384, &tmQ, &bar.q_full, half * 64, tile * 128, h, b);
+            for (int t = 0; t < T; ++t) {
+                const int s = t & 1;
+                const uint32_t ph = ((t >> 1) & 1) ^ 1;
+                uint8_t* sK = smem + Cfg::kOffK + s * Cfg::kKV;
+                uint8_t* sV = smem + Cfg::kOffV + s * Cfg::kKV;
+                mbar_wait(&bar.k_empty[s], ph);
+                mbar_expect_tx(&bar.k_full[s], Cfg::kKV);
+                if (t < U) {
+                    const int row = int(ulist[t] & 0x3FFFu) * 64;
+#pragma unroll
+                    for (int half = 0; half < D / 64; ++half)
+                        tma_load_4d(sK + half * 8192, &tmK, &bar.k_full[s], half * 64, row, h, b);
+                    mbar_wait(&bar.v_empty[s], ph);
+                    mbar_expect_tx(&bar.v_full[s], Cfg::kKV);
+#pragma unroll
+                    for (int half = 0; half < D / 64; ++half)
+                        tma_load_4d(sV + half * 8192, &tmV, &bar.v_full[s], half * 64, row, h, b);
+                } else {
+                    const int row = (t - U) * 64;
+#pragma unroll
+                    for (int half = 0; half < D / 64; ++half)
+                        tma_load_3d(sK + half * 8192, &tmKb, &bar.k_full[s], half * 64, row, bh);
+                    mbar_wait(&bar.v_empty[s], ph);
+                    mbar_expect_tx(&bar.v_full[s], Cfg::kKV);
+#pragma unroll
+                    for (int half = 0; half < D / 64; ++half)
+                        tma_load_3d(sV + half * 8192, &tmVh, &bar.v_full[s], half * 64, row, bh);
+                }
+            }
+            if (first_order) {
+                // H_bar (D rows) into the K ring: half c lands in K stage c.
+                for (int t = T; t < T + 2; ++t)
+                    mbar_wait(&bar.k_empty[t & 1], ((t >> 1) & 1) ^ 1);
+                mbar_expect_tx(&bar.h_full, D * D * 2);
+#pragma unroll
+                for (int half = 0; half < D / 64; ++half)
+                    tma_load_3d(smem + Cfg::kOffK + half * Cfg::kKV, &tmH, &bar.h_full, half * 64, 0, bh);
+            }
+        }
+    } else if (warp == 1) {
+        // ------------------------------------------------------------- MMA --
+        if (lane == 0) {
+            constexpr uint32_t idS = idesc_bf16(128, 64, 0, 0);   // S = Q K^T
+            constexpr uint32_t idPV = idesc_bf16(128, D, 0, 1);   // O += P V (V MN-major)
+            constexpr uint32_t idQH = idesc_bf16(128, D, 0, 1);   // Q H_bar
+            const uint32_t qbase = smem_u32(smem + Cfg::kOffQ);
+            auto issue_pv = [&](int u) {
+                const int s = u & 1;
+                const uint32_t ph = (u >> 1) & 1;
+                mbar_wait(&bar.p_full[s], ph);
+                mbar_wait(&bar.v_full[s], ph);
+                tc_fence_after();
+                const uint32_t vb = smem_u32(smem + Cfg::kOffV + s * Cfg::kKV);
+#pragma unroll
+                for (int ks = 0; ks < 4; ++ks)
+                    mma_ts(tmem + kColO, tmem + kColS + s * 64 + ks * 8,
+                           sdesc_sw128(vb + ks * 2048, 8192, 1024), idPV, (u | ks) != 0);
+                mma_commit(&bar.v_empty[s]);
+                mma_commit(&bar.o_done);
+            };
+            mbar_wait(&bar.q_full, 0);
+            for (int t = 0; t < T; ++t) {
+                const int s = t & 1;
+                mbar_wait(&bar.k_full[s], (t >> 1) & 1);
+                tc_fence_after();
+                const uint32_t kb = smem_u32(smem + Cfg::kOffK + s * Cfg::kKV);
+#pragma unroll
+                for (int ks = 0; ks < D / 16; ++ks) {
+                    const uint32_t hq = (ks >> 2), kq = (ks & 3) * 32;
+                    mma_ss(tmem + kColS + s * 64,
+                           sdesc_sw128(qbase + hq * 16384 + kq, 16, 1024),
+                           sdesc_sw128(kb + hq * 8192 + kq, 16, 1024), idS, ks != 0);
+                }
+                mma_commit(&bar.k_empty[s]);
+                mma_commit(&bar.s_full[s]);
+                if (t > 0) issue_pv(t - 1);
+            }
+            issue_pv(T - 1);
+            if (first_order) {
+                mbar_wait(&bar.h_full, 0);
+                tc_fence_after();
+                const uint32_t hb = smem_u32(smem + Cfg::kOffK);
+#pragma unroll
+                for (int ks = 0; ks < D / 16; ++ks) {
+                    const uint32_t hq = (ks >> 2), kq = (ks & 3) * 32;
+                    mma_ss(tmem + kColS, sdesc_sw128(qbase + hq * 16384 + kq, 16, 1024),
+                           sdesc_sw128(hb + ks * 2048, Cfg::kKV, 1024), idQH, ks != 0);
+                }
+            }
+            mma_commit(&bar.qh_full);  // also: every PV done
+        }
+    } else if (warp >= 4) {
+        // ------------------------------------------------ softmax warpgroup --
+        const int q4 = warp & 3;            // TMEM lane quadrant
+        const int row = q4 * 32 + lane;     // 0..127 within the tile
+        const int half = row >> 6;          // 0: block iA, 1: block iB (warp-uniform)
+        const int grow = tile * 128 + row;  // query row within the sequence
+        const bool active = grow < a.L;
+        const uint32_t* hmask = half ? maskB : maskA;
+        const uint32_t lane_off = uint32_t(q4 * 32) << 16;
+        const float sl2 = a.scale * 1.4426950408889634f;
+
+        float m = -INFINITY, l = 0.f, lt = 0.f;
+        for (int t = 0; t < T; ++t) {
+            const int s = t & 1;
+            const uint32_t sc = tmem + lane_off + kColS + s * 64;
+            bool use;
+            int nvalid = 64;
+            uint32_t cm_lo = 0, cm_hi = 0;  // phase 2: masked columns
+            float w_last = 64.f;
+            int last_col = -1;
+            if (t < U) {
+                const uint32_t e = ulist[t];
+                use = ((e >> (14 + half)) & 1u) != 0;
+                if (int(e & 0x3FFFu) == a.N - 1) nvalid = n_last;
+            } else {
+                const int c = t - U;
+                use = true;
+                cm_lo = hmask[2 * c];
+                cm_hi = (2 * c + 1 < a.W) ? hmask[2 * c + 1] : 0xffffffffu;
+                const int jmax = a.N - c * 64;  // valid centroid columns in this tile
+                nvalid = jmax < 64 ? jmax : 64;
+                if (c * 64 <= a.N - 1 && a.N - 1 < c * 64 + 64) {
+                    last_col = a.N - 1 - c * 64;
+                    w_last = float(n_last);
+                }
+            }
+            mbar_wait(&bar.s_full[s], (t >> 1) & 1);
+            tc_fence_after();
+            uint32_t pk[32];
+            if (use) {  // warp-uniform
+                uint32_t ra[32], rb[32];
+                tmem_ld32(sc, ra);
+                tmem_ld32(sc + 32, rb);
+                tmem_ld_wait(ra);
+                tmem_ld_wait(rb);
+                float x[64];
+#pragma unroll
+                for (int i = 0; i < 32; ++i) {
+                    x[i] = __uint_as_float(ra[i]) * sl2;
+                    x[i + 32] = __uint_as_float(rb[i]) * sl2;
+                }
+                // column validity
+                const uint64_t cmask = (uint64_t(cm_hi) << 32) | cm_lo;
+                float bm = -INFINITY;
+#pragma unroll
+                for (int i = 0; i < 64; ++i) {
+                    const bool ok = active && i < nvalid && !((cmask >> i) & 1ull);
+                    x[i] = ok ? x[i] : -INFINITY;
+                    bm = fmaxf(bm, x[i]);
+                }
+                float m_use = m;
+                bool resc = false;
+                if (bm > -INFINITY) {
+                    if (m == -INFINITY) {
+                        m_use = bm;
+                    } else if (bm > m + kRescaleThresh) {
+                        m_use = bm;
+                        resc = true;
+                    }
+                }
+                if (__any_sync(0xffffffffu, resc)) {
+                    const float f = resc ? ex2(m - m_use) : 1.f;
+                    mbar_wait(&bar.o_done, (t - 1) & 1);  // t >= 1 whenever resc
+                    tc_fence_after();
+#pragma unroll 1
+                    for (int cc = 0; cc < D; cc += 32) {
+                        uint32_t ro[32];
+                        tmem_ld32(tmem + lane_off + kColO + cc, ro);
+                        tmem_ld_wait(ro);
+#pragma unroll
+                        for (int i = 0; i < 32; ++i) ro[i] = __float_as_uint(__uint_as_float(ro[i]) * f);
+                        tmem_st32(tmem + lane_off + kColO + cc, ro);
+                    }
+                    l *= f;
+                    lt *= f;
+                }
+                m = m_use;
+                const float mm = (m == -INFINITY) ? 0.f : m;  // all-masked row: p = 0, not NaN
+                float ps = 0.f, pw = 0.f;
+#pragma unroll
+                for (int i = 0; i < 64; i += 2) {
+                    const float p0 = ex2(x[i] - mm);
+                    const float p1 = ex2(x[i + 1] - mm);
+                    ps += p0 + p1;
+                    if (t >= U) {
+                        pw += (i == last_col ? w_last : 64.f) * p0 +
+                              (i + 1 == last_col ? w_last : 64.f) * p1;
+                    }
+                    pk[i >> 1] = pack_bf16(p0, p1);
+                }
+                if (t < U) {
+                    l += ps;
+                } else {
+                    l += pw;
+                    lt += ps;
+                }
+            } else {
+#pragma unroll
+                for (int i = 0; i < 32; ++i) pk[i] = 0u;
+            }
+            tmem_st32(sc, pk);  // P (bf16 pairs) over the first 32 S columns
+            tmem_st_wait();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&bar.p_full[s]);
+        }
+
+        // ------------------------------------------------------- epilogue --
+        mbar_wait(&bar.qh_full, 0);
+        tc_fence_after();
+        float cw = 0.f;
+        float lfin = l;
+        if (a.variant == 3) {
+            cw = a.scale * lt;
+            if (a.literal_phase3) cw *= (1.0f / 64.0f);
+        }
+        float fo = 1.f;  // extra scale on O and l (GlobalCentroid shift)
+        if (a.variant == 4 && active) {
+            // slope = |U_i| exp(scale q.k_bar_global - m)   (engine.hpp:202-205)
+            const uint8_t* sQ = smem + Cfg::kOffQ;
+            const float* kg = a.kbar_global + size_t(bh) * D;
+            float dot = 0.f;
+            for (int c = 0; c < D; ++c) {
+                const uint32_t off = (c >> 6) * 16384 + sw128_off(row, c & 63);
+                dot = fmaf(__bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(sQ + off)), kg[c], dot);
+            }
+            const float gx = dot * sl2;
+            const int nU = a.N - a.k;
+            if (nU > 0) {
+                const float mm = fmaxf(m, gx);
+                fo = ex2(m - mm);
+                cw = a.scale * float(nU) * ex2(gx - mm);
+                if (a.literal_phase3) cw *= (1.0f / 64.0f);
+                m = mm;
+                lfin = l * fo;
+                lt *= fo;
+            }
+        }
+        const float inv_l = 1.0f / lfin;
+        bool bad = false;
+        char* orow = reinterpret_cast<char*>(a.out) +
+                     (size_t(b) * a.os_b + size_t(h) * a.os_h + size_t(grow) * a.os_l) *
+                         (a.out_f32 ? 4 : 2);
+#pragma unroll 1
+        for (int cc = 0; cc < D; cc += 32) {
+            uint32_t ro[32], rq[32];
+            tmem_ld32(tmem + lane_off + kColO + cc, ro);
+            if (first_order) tmem_ld32(tmem + lane_off + kColS + cc, rq);
+            tmem_ld_wait(ro);
+            if (first_order) tmem_ld_wait(rq);
+            float o[32];
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+                float acc = __uint_as_float(ro[i]) * fo;
+                if (first_order) acc = fmaf(cw, __uint_as_float(rq[i]), acc);
+                o[i] = acc * inv_l;
+                bad |= active && !isfinite(o[i]);
+            }
+            if (active) {
+                if (a.out_f32) {
+                    float4* dst = reinterpret_cast<float4*>(orow) + cc / 4;
+#pragma unroll
+                    for (int i = 0; i < 32; i += 4) dst[i / 4] = make_float4(o[i], o[i + 1], o[i + 2], o[i + 3]);
+                } else {
+                    uint4* dst = reinterpret_cast<uint4*>(orow + cc * 2);
+#pragma unroll
+                    for (int i = 0; i < 32; i += 8)
+                        dst[i / 8] = make_uint4(pack_bf16(o[i], o[i + 1]), pack_bf16(o[i + 2], o[i + 3]),
+                                                pack_bf16(o[i + 4], o[i + 5]), pack_bf16(o[i + 6], o[i + 7]));
+                }
+            }
+        }
+        if (active) {
+            const size_t di = size_t(bh) * a.L + grow;
+            if (a.diag_m) a.diag_m[di] = m * 0.6931471805599453f;  // log2 units -> natural log
+            if (a.diag_l) a.diag_l[di] = lfin;
+            if (a.diag_lt) a.diag_lt[di] = lt;
+            if (bad && a.nonfinite) atomicExch(a.nonfinite, 1);
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 2) tmem_dealloc(tmem, 256);
+}
+
+}  // namespace
+
+size_t fused_smem_bytes(int D, int N, int W) {
+    const size_t core = (D == 128) ? size_t(FusedCfg<128>::kOffMask) : size_t(FusedCfg<64>::kOffMask);
+    return 1024 + core + size_t(2 * W) * 4 + size_t(N) * 2 + 16;
+}
+
+cudaError_t launch_fused(int D, const CUtensorMap& tmQ, const CUtensorMap& tmK,
+                         const CUtensorMap& tmV, const CUtensorMap& tmKb,
+                         const CUtensorMap& tmVh, const CUtensorMap& tmH, const FusedArgs& a,
+                         int BH, cudaStream_t s) {
+    const size_t smem = fused_smem_bytes(D, a.N, a.W);
+    dim3 grid((a.N + 1) / 2, BH);
+    if (D == 128) {
+        auto k = fused_attn_kernel<128>;
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        k<<<grid, kThreads, smem, s>>>(tmQ, tmK, tmV, tmKb, tmVh, tmH, a);
+    } else {
+        auto k = fused_attn_kernel<64>;
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        k<<<grid, kThreads, smem, s>>>(tmQ, tmK, tmV, tmKb, tmVh, tmH, a);
+    }
+    return cudaGetLastError();
+}
+
+}  // namespace pisa_b200

@@ -1,0 +1,83 @@
+// kernels.h -- launch interfaces of the four sm_100a kernels (host side).
+#pragma once
+
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace pisa_b200 {
+
+// K1: block statistics. One CTA per (chunk of kStatsG key blocks, batch*head).
+//   k_bar / v_hat / q_bar fp32 [BH][N][D]   (compute_block_stats / query_block_means)
+//   kbar_bf / vhat_bf bf16  [BH][Npad][D]   (operands of the fused kernel's Phase 2)
+//   hpart fp32 [BH][nchunk][D][D]            (per-chunk sum_j H_j, reduced by K1b)
+constexpr int kStatsG = 32;
+struct StatsArgs {
+    float* kbar;
+    float* vhat;
+    float* qbar;
+    __nv_bfloat16* kbar_bf;
+    __nv_bfloat16* vhat_bf;
+    float* hpart;
+    int L, N, Npad, H, nchunk;
+};
+cudaError_t launch_block_stats(int D, const CUtensorMap& tmQ, const CUtensorMap& tmK,
+                               const CUtensorMap& tmV, const StatsArgs& a, int BH,
+                               cudaStream_t s);
+
+// K1b: H_bar = (1/N) sum_chunks hpart (fixed order), fp32 + bf16 copies, plus
+// k_bar_global = mean_j k_bar_j.
+cudaError_t launch_hbar_reduce(int D, const float* hpart, int nchunk, int N, const float* kbar,
+                               float* hbar, __nv_bfloat16* hbar_bf, float* kbar_global, int BH,
+                               cudaStream_t s);
+
+// Conversion of externally supplied fp32 statistics into the fused kernel's
+// bf16 operands (pisa_b200_attention path).
+cudaError_t launch_stats_to_bf16(int D, const float* kbar, const float* vhat, const float* hbar,
+                                 int N, int Npad, __nv_bfloat16* kbar_bf, __nv_bfloat16* vhat_bf,
+                                 __nv_bfloat16* hbar_bf, float* kbar_global, int BH,
+                                 cudaStream_t s);
+
+// K2: fp32 block scoring + top-k (score desc, index asc) per query block.
+struct SelectArgs {
+    const float* qbar;  // [BH][N][D]
+    const float* kbar;  // [BH][N][D]
+    int32_t* selected;  // [BH][N][k]  (may be null)
+    uint32_t* mask;     // [BH][N][W]
+    int N, W, k, force_diagonal;
+    float scale;
+};
+cudaError_t launch_select(int D, const SelectArgs& a, int BH, cudaStream_t s);
+
+// Plan (ascending lists) -> bitmask, with SelectionPlan::validate semantics
+// (router.hpp:50-70): sets *bad = 1 on out-of-range / non-ascending entries.
+cudaError_t launch_plan_to_mask(const int32_t* selected, int N, int k, int W, uint32_t* mask,
+                                int* bad, int BH, cudaStream_t s);
+
+// K3: fused piecewise attention (Phase 1 exact over S_i, Phase 2 centroid tail,
+// Phase 3 global first-order correction), one CTA per pair of query blocks.
+struct FusedArgs {
+    const uint32_t* mask;      // [BH][N][W]
+    const float* kbar_global;  // [BH][D] (GlobalCentroid) or null
+    void* out;
+    int64_t os_b, os_h, os_l;
+    float* diag_m;   // [BH][L] or null
+    float* diag_l;
+    float* diag_lt;
+    int* nonfinite;  // device flag or null
+    int L, N, H, W, nchunk2, variant, literal_phase3, out_f32, k;
+    float scale;
+};
+cudaError_t launch_fused(int D, const CUtensorMap& tmQ, const CUtensorMap& tmK,
+                         const CUtensorMap& tmV, const CUtensorMap& tmKb,
+                         const CUtensorMap& tmVh, const CUtensorMap& tmH, const FusedArgs& a,
+                         int BH, cudaStream_t s);
+size_t fused_smem_bytes(int D, int N, int W);
+
+// Tensor-core self test (pisa_b200_selftest_mma).
+cudaError_t launch_selftest_mma(const CUtensorMap& tmA, const CUtensorMap& tmB128,
+                                const CUtensorMap& tmB64, const __nv_bfloat16* a, float* out,
+                                cudaStream_t s);
+
+}  // namespace pisa_b200

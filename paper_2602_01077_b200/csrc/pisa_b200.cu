@@ -1,0 +1,586 @@
+// pisa_b200.cu -- the C ABI (include/pisa_b200.h): validation with the
+// reference's error semantics, workspace management, TMA descriptor creation,
+// and the stream-ordered K1 -> K1b -> K2 -> K3 launch sequence.
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include "../../include/pisa_b200.h"
+#include "kernels.h"
+
+using namespace pisa_b200;
+
+struct pisa_ctx {
+    int device = 0;
+    std::string last_error;
+    // grow-only device arena
+    void* arena = nullptr;
+    size_t arena_bytes = 0;
+    int* flag_host = nullptr;  // pinned mirror of the non-finite flag
+    int64_t launches = 0;
+    // host-staged path
+    cudaStream_t st_h2d = nullptr, st_comp = nullptr, st_d2h = nullptr;
+    cudaEvent_t ev_h2d[2] = {}, ev_comp[2] = {}, ev_d2h[2] = {};
+    void* stage = nullptr;
+    size_t stage_bytes = 0;
+};
+
+namespace {
+
+const char* kKernelNames[] = {"block_stats_kernel", "hbar_reduce_kernel", "select_kernel",
+                              "fused_attn_kernel", nullptr};
+
+pisa_status fail(pisa_ctx* ctx, pisa_status st, const std::string& msg) {
+    if (ctx) {
+        static const char* cls[] = {"Ok",           "InvalidDimension", "BlockDivisibility",
+                                    "InvalidSparsity", "InvalidEpsilon", "EmptySelection",
+                                    "NumericalOverflow", "DegenerateScale", "Unsupported",
+                                    "CudaError"};
+        ctx->last_error = std::string(cls[int(st)]) + ": " + msg;
+    }
+    return st;
+}
+
+pisa_status cuda_fail(pisa_ctx* ctx, cudaError_t e, const char* where) {
+    return fail(ctx, PISA_ERR_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+// ------------------------------------------------------------ TMA maps --
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                   const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+    static EncodeTiledFn fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+                cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeTiledFn>(p);
+    });
+    return fn;
+}
+
+// bf16 tensor, 128B swizzle, zero OOB fill. dims/strides innermost first;
+// strides_bytes has rank-1 entries.
+bool make_map(CUtensorMap* m, const void* base, int rank, const uint64_t* dims,
+              const uint64_t* strides_bytes, const uint32_t* box) {
+    EncodeTiledFn fn = encode_fn();
+    if (!fn) return false;
+    cuuint64_t gd[5], gs[4];
+    cuuint32_t bx[5], es[5];
+    for (int i = 0; i < rank; ++i) {
+        gd[i] = dims[i];
+        bx[i] = box[i];
+        es[i] = 1;
+    }
+    for (int i = 0; i < rank - 1; ++i) gs[i] = strides_bytes[i];
+    const CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, cuuint32_t(rank),
+                          const_cast<void*>(base), gd, gs, bx, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                          CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
+// [B][L][H][d]-general strided input viewed as (d, L, H, B) with a box of `rows` rows.
+bool make_qkv_map(CUtensorMap* m, const void* base, const pisa_attn_desc& d,
+                  const int64_t* st, uint32_t rows) {
+    const uint64_t dims[4] = {uint64_t(d.head_dim), uint64_t(d.seq_len), uint64_t(d.heads),
+                              uint64_t(d.batch)};
+    uint64_t sb = uint64_t(st[0]) * 2;
+    if (d.batch == 1) sb = std::max<uint64_t>(16, (uint64_t(st[1]) * d.heads) * 2);
+    uint64_t sh = uint64_t(st[1]) * 2;
+    if (d.heads == 1) sh = std::max<uint64_t>(16, uint64_t(st[2]) * d.seq_len * 2);
+    const uint64_t strides[3] = {uint64_t(st[2]) * 2, sh, sb};
+    const uint32_t box[4] = {64, rows, 1, 1};
+    return make_map(m, base, 4, dims, strides, box);
+}
+
+bool make_3d_map(CUtensorMap* m, const void* base, uint64_t D, uint64_t rows, uint64_t BH,
+                 uint32_t box_rows) {
+    const uint64_t dims[3] = {D, rows, BH};
+    const uint64_t strides[2] = {D * 2, rows * D * 2};
+    const uint32_t box[3] = {64, box_rows, 1};
+    return make_map(m, base, 3, dims, strides, box);
+}
+
+// ------------------------------------------------------------ resolve --
+struct Plan {
+    int64_t BH, L, D, N, Npad, W, k, nchunk1, nchunk2;
+    double scale;
+};
+
+pisa_status resolve(pisa_ctx* ctx, const pisa_attn_desc* d, Plan* p) {
+    if (!d) return fail(ctx, PISA_ERR_INVALID_DIMENSION, "null descriptor");
+    if (d->batch < 1 || d->heads < 1 || d->seq_len < 1 || d->head_dim < 1)
+        return fail(ctx, PISA_ERR_INVALID_DIMENSION,
+                    "batch, heads, seq_len and head_dim must all be >= 1");
+    if (d->block_size < 1 || d->group_size < 1)  // attention.hpp:40-42
+        return fail(ctx, PISA_ERR_INVALID_DIMENSION, "block_size and group_size must be >= 1");
+    if (!d->ragged && d->seq_len % d->block_size != 0)  // attention.hpp:43-47
+        return fail(ctx, PISA_ERR_BLOCK_DIVISIBILITY,
+                    "seq_len " + std::to_string(d->seq_len) + " not divisible by block size " +
+                        std::to_string(d->block_size));
+    if (d->block_size != 64)
+        return fail(ctx, PISA_ERR_UNSUPPORTED, "the GPU path tiles 64-row blocks only");
+    if (d->head_dim != 64 && d->head_dim != 128)
+        return fail(ctx, PISA_ERR_UNSUPPORTED, "head_dim must be 64 or 128 on the GPU path");
+    if (d->variant < 0 || d->variant > 4)
+        return fail(ctx, PISA_ERR_INVALID_DIMENSION, "unknown variant");
+    if (d->variant == PISA_BLOCK_FIRST)
+        return fail(ctx, PISA_ERR_UNSUPPORTED, "BlockFirst is not on the GPU path");
+    if (d->router != PISA_ROUTER_PLAIN)
+        return fail(ctx, PISA_ERR_UNSUPPORTED, "only the Plain router runs on the GPU path");
+    const int64_t N = (d->seq_len + 63) / 64;
+    if (N > 8192) return fail(ctx, PISA_ERR_UNSUPPORTED, "more than 8192 key blocks");
+    int64_t k = d->topk;
+    if (k <= 0) {
+        if (k < 0) return fail(ctx, PISA_ERR_INVALID_SPARSITY, "k must lie in [1, N]");
+        const double r = d->sparsity;
+        if (!(r >= 0.0) || r >= 1.0)  // router.hpp:81-84
+            return fail(ctx, PISA_ERR_INVALID_SPARSITY,
+                        "sparsity must lie in [0, 1), got " + std::to_string(r));
+        k = std::llround((1.0 - r) * double(N));
+        k = std::max<int64_t>(1, std::min<int64_t>(k, N));
+    } else if (k > N) {
+        return fail(ctx, PISA_ERR_INVALID_SPARSITY,
+                    "k must lie in [1, N], got " + std::to_string(k) + " for N = " + std::to_string(N));
+    }
+    const int64_t D = d->head_dim;
+    auto st_ok = [&](const int64_t* s) {
+        return s[2] % 8 == 0 && s[1] % 8 == 0 && s[0] % 8 == 0 && s[2] >= D;
+    };
+    if (!st_ok(d->q_strides) || !st_ok(d->k_strides) || !st_ok(d->v_strides))
+        return fail(ctx, PISA_ERR_INVALID_DIMENSION, "q/k/v strides must be multiples of 8 elements");
+    p->BH = d->batch * d->heads;
+    p->L = d->seq_len;
+    p->D = D;
+    p->N = N;
+    p->Npad = (N + 63) / 64 * 64;
+    p->W = (N + 31) / 32;
+    p->k = k;
+    p->nchunk1 = (N + kStatsG - 1) / kStatsG;
+    p->nchunk2 = (N + 63) / 64;
+    p->scale = d->scale > 0.0 ? d->scale : 1.0 / std::sqrt(double(D));  // attention.hpp:34-37
+    return PISA_OK;
+}
+
+// ------------------------------------------------------------ workspace --
+struct Work {
+    float *kbar, *vhat, *qbar, *hpart, *hbar, *kglob;
+    __nv_bfloat16 *kbar_bf, *vhat_bf, *hbar_bf;
+    int32_t* selected;
+    uint32_t* mask;
+    int* flag;
+};
+
+size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
+
+pisa_status workspace(pisa_ctx* ctx, const Plan& p, Work* w) {
+    const size_t BH = size_t(p.BH), N = size_t(p.N), D = size_t(p.D);
+    size_t off = 0;
+    auto take = [&](size_t bytes) {
+        const size_t o = off;
+        off = align_up(off + bytes);
+        return o;
+    };
+    const size_t o_kbar = take(BH * N * D * 4), o_vhat = take(BH * N * D * 4),
+                 o_qbar = take(BH * N * D * 4), o_hpart = take(BH * p.nchunk1 * D * D * 4),
+                 o_hbar = take(BH * D * D * 4), o_kglob = take(BH * D * 4),
+                 o_kbf = take(BH * p.Npad * D * 2), o_vbf = take(BH * p.Npad * D * 2),
+                 o_hbf = take(BH * D * D * 2), o_sel = take(BH * N * p.k * 4),
+                 o_mask = take(BH * N * p.W * 4), o_flag = take(16);
+    if (off > ctx->arena_bytes) {
+        if (ctx->arena) cudaFree(ctx->arena);
+        ctx->arena = nullptr;
+        ctx->arena_bytes = 0;
+        const cudaError_t e = cudaMalloc(&ctx->arena, off);
+        if (e != cudaSuccess) return cuda_fail(ctx, e, "workspace cudaMalloc");
+        ctx->arena_bytes = off;
+    }
+    char* b = static_cast<char*>(ctx->arena);
+    w->kbar = reinterpret_cast<float*>(b + o_kbar);
+    w->vhat = reinterpret_cast<float*>(b + o_vhat);
+    w->qbar = reinterpret_cast<float*>(b + o_qbar);
+    w->hpart = reinterpret_cast<float*>(b + o_hpart);
+    w->hbar = reinterpret_cast<float*>(b + o_hbar);
+    w->kglob = reinterpret_cast<float*>(b + o_kglob);
+    w->kbar_bf = reinterpret_cast<__nv_bfloat16*>(b + o_kbf);
+    w->vhat_bf = reinterpret_cast<__nv_bfloat16*>(b + o_vbf);
+    w->hbar_bf = reinterpret_cast<__nv_bfloat16*>(b + o_hbf);
+    w->selected = reinterpret_cast<int32_t*>(b + o_sel);
+    w->mask = reinterpret_cast<uint32_t*>(b + o_mask);
+    w->flag = reinterpret_cast<int*>(b + o_flag);
+    return PISA_OK;
+}
+
+pisa_status run_stats(pisa_ctx* ctx, const pisa_attn_desc& d, const Plan& p, const Work& w,
+                      const void* q, const void* k, const void* v, cudaStream_t s) {
+    CUtensorMap tq, tk, tv;
+    if (!make_qkv_map(&tq, q, d, d.q_strides, 64) || !make_qkv_map(&tk, k, d, d.k_strides, 64) ||
+        !make_qkv_map(&tv, v, d, d.v_strides, 64))
+        return fail(ctx, PISA_ERR_INVALID_DIMENSION, "TMA descriptor rejected the q/k/v layout");
+    StatsArgs sa{w.kbar, w.vhat, w.qbar, w.kbar_bf, w.vhat_bf, w.hpart,
+                 int(p.L), int(p.N), int(p.Npad), int(d.heads), int(p.nchunk1)};
+    cudaError_t e = launch_block_stats(int(p.D), tq, tk, tv, sa, int(p.BH), s);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "block_stats launch");
+    e = launch_hbar_reduce(int(p.D), w.hpart, int(p.nchunk1), int(p.N), w.kbar, w.hbar, w.hbar_bf,
+                           d.variant == PISA_GLOBAL_CENTROID ? w.kglob : nullptr, int(p.BH), s);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "hbar_reduce launch");
+    ctx->launches += 2;
+    return PISA_OK;
+}
+
+pisa_status run_select(pisa_ctx* ctx, const pisa_attn_desc& d, const Plan& p, const float* qbar,
+                       const float* kbar, int32_t* selected, uint32_t* mask, cudaStream_t s) {
+    SelectArgs a{qbar, kbar, selected, mask, int(p.N), int(p.W), int(p.k), d.force_diagonal,
+                 float(p.scale)};
+    const cudaError_t e = launch_select(int(p.D), a, int(p.BH), s);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "select launch");
+    ctx->launches += 1;
+    return PISA_OK;
+}
+
+pisa_status run_fused(pisa_ctx* ctx, const pisa_attn_desc& d, const Plan& p, const Work& w,
+                      const void* q, const void* k, const void* v, void* o, const pisa_diag* diag,
+                      cudaStream_t s) {
+    CUtensorMap tq, tk, tv, tkb, tvh, th;
+    if (!make_qkv_map(&tq, q, d, d.q_strides, 128) || !make_qkv_map(&tk, k, d, d.k_strides, 64) ||
+        !make_qkv_map(&tv, v, d, d.v_strides, 64))
+        return fail(ctx, PISA_ERR_INVALID_DIMENSION, "TMA descriptor rejected the q/k/v layout");
+    if (!make_3d_map(&tkb, w.kbar_bf, p.D, p.Npad, p.BH, 64) ||
+        !make_3d_map(&tvh, w.vhat_bf, p.D, p.Npad, p.BH, 64) ||
+        !make_3d_map(&th, w.hbar_bf, p.D, p.D, p.BH, uint32_t(p.D)))
+        return fail(ctx, PISA_ERR_CUDA, "TMA descriptor creation failed");
+    FusedArgs a{};
+    a.mask = w.mask;
+    a.kbar_global = w.kglob;
+    a.out = o;
+    a.os_b = d.o_strides[0];
+    a.os_h = d.o_strides[1];
+    a.os_l = d.o_strides[2];
+    a.diag_m = diag ? diag->row_max : nullptr;
+    a.diag_l = diag ? diag->ell : nullptr;
+    a.diag_lt = diag ? diag->ell_tail : nullptr;
+    a.nonfinite = d.check_finite ? w.flag : nullptr;
+    a.L = int(p.L);
+    a.N = int(p.N);
+    a.H = int(d.heads);
+    a.W = int(p.W);
+    a.nchunk2 = int(p.nchunk2);
+    a.variant = d.variant;
+    a.literal_phase3 = d.literal_phase3;
+    a.out_f32 = d.out_dtype == PISA_DTYPE_F32;
+    a.k = int(p.k);
+    a.scale = float(p.scale);
+    if (d.check_finite) {
+        const cudaError_t e = cudaMemsetAsync(w.flag, 0, sizeof(int), s);
+        if (e != cudaSuccess) return cuda_fail(ctx, e, "flag reset");
+    }
+    const cudaError_t e = launch_fused(int(p.D), tq, tk, tv, tkb, tvh, th, a, int(p.BH), s);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "fused launch");
+    ctx->launches += 1;
+    if (d.check_finite) {
+        cudaError_t e2 = cudaMemcpyAsync(ctx->flag_host, w.flag, sizeof(int), cudaMemcpyDeviceToHost, s);
+        if (e2 == cudaSuccess) e2 = cudaStreamSynchronize(s);
+        if (e2 != cudaSuccess) return cuda_fail(ctx, e2, "non-finite check");
+        if (*ctx->flag_host)  // engine.hpp:83-93
+            return fail(ctx, PISA_ERR_NUMERICAL_OVERFLOW, "non-finite output");
+    }
+    return PISA_OK;
+}
+
+bool out_dtype_ok(const pisa_attn_desc* d) {
+    return d->out_dtype == PISA_DTYPE_BF16 || d->out_dtype == PISA_DTYPE_F32;
+}
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        cudaGetDevice(&prev);
+        if (prev != dev) cudaSetDevice(dev);
+    }
+    ~DeviceGuard() {
+        int cur;
+        cudaGetDevice(&cur);
+        if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+}  // namespace
+
+extern "C" {
+
+int pisa_b200_abi_version(void) { return PISA_B200_ABI_VERSION; }
+
+pisa_status pisa_b200_create(pisa_ctx** out, int device) {
+    if (!out) return PISA_ERR_INVALID_DIMENSION;
+    *out = nullptr;
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || device < 0 || device >= n) return PISA_ERR_CUDA;
+    cudaDeviceProp prop;
+    if (cudaGetDeviceProperties(&prop, device) != cudaSuccess) return PISA_ERR_CUDA;
+    if (prop.major != 10) return PISA_ERR_UNSUPPORTED;  // sm_100a kernels only
+    pisa_ctx* c = new pisa_ctx;
+    c->device = device;
+    DeviceGuard g(device);
+    if (cudaMallocHost(&c->flag_host, sizeof(int)) != cudaSuccess) {
+        delete c;
+        return PISA_ERR_CUDA;
+    }
+    *out = c;
+    return PISA_OK;
+}
+
+void pisa_b200_destroy(pisa_ctx* c) {
+    if (!c) return;
+    DeviceGuard g(c->device);
+    cudaDeviceSynchronize();
+    if (c->arena) cudaFree(c->arena);
+    if (c->stage) cudaFree(c->stage);
+    if (c->flag_host) cudaFreeHost(c->flag_host);
+    for (int i = 0; i < 2; ++i) {
+        if (c->ev_h2d[i]) cudaEventDestroy(c->ev_h2d[i]);
+        if (c->ev_comp[i]) cudaEventDestroy(c->ev_comp[i]);
+        if (c->ev_d2h[i]) cudaEventDestroy(c->ev_d2h[i]);
+    }
+    if (c->st_h2d) cudaStreamDestroy(c->st_h2d);
+    if (c->st_comp) cudaStreamDestroy(c->st_comp);
+    if (c->st_d2h) cudaStreamDestroy(c->st_d2h);
+    delete c;
+}
+
+const char* pisa_b200_last_error(const pisa_ctx* c) { return c ? c->last_error.c_str() : ""; }
+
+int64_t pisa_b200_last_launch_count(const pisa_ctx* c) { return c ? c->launches : 0; }
+
+const char* pisa_b200_kernel_name(int i) {
+    if (i < 0 || i >= 4) return nullptr;
+    return kKernelNames[i];
+}
+
+pisa_status pisa_b200_sparsity_to_k(double r, int64_t n, int64_t* k, double* realized) {
+    if (!(r >= 0.0) || r >= 1.0) return PISA_ERR_INVALID_SPARSITY;
+    if (n <= 0) return PISA_ERR_INVALID_DIMENSION;
+    int64_t kk = std::llround((1.0 - r) * double(n));
+    kk = std::max<int64_t>(1, std::min<int64_t>(kk, n));
+    if (k) *k = kk;
+    if (realized) *realized = double(n - kk) / double(n);
+    return PISA_OK;
+}
+
+pisa_status pisa_b200_resolve(const pisa_attn_desc* d, int64_t* num_blocks, int64_t* k,
+                              double* scale) {
+    Plan p;
+    const pisa_status st = resolve(nullptr, d, &p);
+    if (st != PISA_OK) return st;
+    if (num_blocks) *num_blocks = p.N;
+    if (k) *k = p.k;
+    if (scale) *scale = p.scale;
+    return PISA_OK;
+}
+
+pisa_status pisa_b200_fwd(pisa_ctx* ctx, const pisa_attn_desc* d, const void* q, const void* k,
+                          const void* v, void* o, const pisa_diag* diag, void* stream) {
+    if (!ctx) return PISA_ERR_INVALID_DIMENSION;
+    ctx->launches = 0;
+    Plan p;
+    pisa_status st = resolve(ctx, d, &p);
+    if (st != PISA_OK) return st;
+    if (!q || !k || !v || !o) return fail(ctx, PISA_ERR_INVALID_DIMENSION, "null tensor pointer");
+    if (!out_dtype_ok(d)) return fail(ctx, PISA_ERR_UNSUPPORTED, "output dtype");
+    DeviceGuard g(ctx->device);
+    const cudaStream_t s = static_cast<cudaStream_t>(stream);
+    Work w;
+    if ((st = workspace(ctx, p, &w)) != PISA_OK) return st;
+    if ((st = run_stats(ctx, *d, p, w, q, k, v, s)) != PISA_OK) return st;
+    int32_t* sel = (diag && diag->selected) ? diag->selected : nullptr;
+    if ((st = run_select(ctx, *d, p, w.qbar, w.kbar, sel, w.mask, s)) != PISA_OK) return st;
+    return run_fused(ctx, *d, p, w, q, k, v, o, diag, s);
+}
+
+pisa_status pisa_b200_block_stats(pisa_ctx* ctx, const pisa_attn_desc* d, const void* q,
+                                  const void* k, const void* v, float* k_bar, float* v_hat,
+                                  float* q_bar, float* h_bar, void* stream) {
+    if (!ctx) return PISA_ERR_INVALID_DIMENSION;
+    ctx->launches = 0;
+    Plan p;
+    pisa_status st = resolve(ctx, d, &p);
+    if (st != PISA_OK) return st;
+    if (!q || !k || !v) return fail(ctx, PISA_ERR_INVALID_DIMENSION, "null tensor pointer");
+    DeviceGuard g(ctx->device);
+    const cudaStream_t s = static_cast<cudaStream_t>(stream);
+    Work w;
+    if ((st = workspace(ctx, p, &w)) != PISA_OK) return st;
+    if ((st = run_stats(ctx, *d, p, w, q, k, v, s)) != PISA_OK) return st;
+    const size_t nd = size_t(p.BH) * p.N * p.D * 4, dd = size_t(p.BH) * p.D * p.D * 4;
+    cudaError_t e = cudaSuccess;
+    if (k_bar && e == cudaSuccess) e = cudaMemcpyAsync(k_bar, w.kbar, nd, cudaMemcpyDeviceToDevice, s);
+    if (v_hat && e == cudaSuccess) e = cudaMemcpyAsync(v_hat, w.vhat, nd, cudaMemcpyDeviceToDevice, s);
+    if (q_bar && e == cudaSuccess) e = cudaMemcpyAsync(q_bar, w.qbar, nd, cudaMemcpyDeviceToDevice, s);
+    if (h_bar && e == cudaSuccess) e = cudaMemcpyAsync(h_bar, w.hbar, dd, cudaMemcpyDeviceToDevice, s);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "block_stats copy-out");
+    return PISA_OK;
+}
+
+pisa_status pisa_b200_select(pisa_ctx* ctx, const pisa_attn_desc* d, const float* q_bar,
+                             const float* k_bar, int32_t* selected, uint32_t* mask, void* stream) {
+    if (!ctx) return PISA_ERR_INVALID_DIMENSION;
+    ctx->launches = 0;
+    Plan p;
+    pisa_status st = resolve(ctx, d, &p);
+    if (st != PISA_OK) return st;
+    if (!q_bar || !k_bar || (!selected && !mask))
+        return fail(ctx, PISA_ERR_INVALID_DIMENSION, "null pointer");
+    DeviceGuard g(ctx->device);
+    const cudaStream_t s = static_cast<cudaStream_t>(stream);
+    Work w;
+    if ((st = workspace(ctx, p, &w)) != PISA_OK) return st;
+    return run_select(ctx, *d, p, q_bar, k_bar, selected, mask ? mask : w.mask, s);
+}
+
+pisa_status pisa_b200_attention(pisa_ctx* ctx, const pisa_attn_desc* d, const void* q,
+                                const void* k, const void* v, const int32_t* selected,
+                                const float* k_bar, const float* v_hat, const float* h_bar,
+                                void* o, const pisa_diag* diag, void* stream) {
+    if (!ctx) return PISA_ERR_INVALID_DIMENSION;
+    ctx->launches = 0;
+    Plan p;
+    pisa_status st = resolve(ctx, d, &p);
+    if (st != PISA_OK) return st;
+    if (!q || !k || !v || !o || !selected || !k_bar || !v_hat || !h_bar)
+        return fail(ctx, PISA_ERR_INVALID_DIMENSION, "null pointer");
+    if (!out_dtype_ok(d)) return fail(ctx, PISA_ERR_UNSUPPORTED, "output dtype");
+    DeviceGuard g(ctx->device);
+    const cudaStream_t s = static_cast<cudaStream_t>(stream);
+    Work w;
+    if ((st = workspace(ctx, p, &w)) != PISA_OK) return st;
+    // plan -> mask, with SelectionPlan::validate (router.hpp:50-70)
+    cudaError_t e = cudaMemsetAsync(w.flag + 1, 0, sizeof(int), s);
+    if (e == cudaSuccess)
+        e = launch_plan_to_mask(selected, int(p.N), int(p.k), int(p.W), w.mask, w.flag + 1, int(p.BH), s);
+    if (e == cudaSuccess)
+        e = launch_stats_to_bf16(int(p.D), k_bar, v_hat, h_bar, int(p.N), int(p.Npad), w.kbar_bf,
+                                 w.vhat_bf, w.hbar_bf,
+                                 d->variant == PISA_GLOBAL_CENTROID ? w.kglob : nullptr, int(p.BH), s);
+    if (e == cudaSuccess)
+        e = cudaMemcpyAsync(ctx->flag_host, w.flag + 1, sizeof(int), cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "plan upload");
+    ctx->launches += 2;
+    if (*ctx->flag_host)
+        return fail(ctx, PISA_ERR_INVALID_SPARSITY, "plan has out-of-range or non-ascending indices");
+    return run_fused(ctx, *d, p, w, q, k, v, o, diag, s);
+}
+
+pisa_status pisa_b200_fwd_host(pisa_ctx* ctx, const pisa_attn_desc* d, const void* q,
+                               const void* k, const void* v, void* o) {
+    if (!ctx) return PISA_ERR_INVALID_DIMENSION;
+    Plan p;
+    pisa_status st = resolve(ctx, d, &p);
+    if (st != PISA_OK) return st;
+    if (!q || !k || !v || !o) return fail(ctx, PISA_ERR_INVALID_DIMENSION, "null tensor pointer");
+    if (!out_dtype_ok(d)) return fail(ctx, PISA_ERR_UNSUPPORTED, "output dtype");
+    DeviceGuard g(ctx->device);
+    // host layout: dense [B][H][L][d]; stage a few (b,h) slices at a time
+    const int64_t BH = p.BH, L = p.L, D = p.D;
+    const size_t in_bytes = size_t(L) * D * 2;
+    const size_t out_bytes = size_t(L) * D * (d->out_dtype == PISA_DTYPE_F32 ? 4 : 2);
+    const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(BH, (BH + 7) / 8));
+    const size_t set_bytes = size_t(chunk) * (3 * in_bytes + out_bytes);
+    cudaError_t e = cudaSuccess;
+    if (!ctx->st_h2d) {
+        e = cudaStreamCreateWithFlags(&ctx->st_h2d, cudaStreamNonBlocking);
+        if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->st_comp, cudaStreamNonBlocking);
+        if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->st_d2h, cudaStreamNonBlocking);
+        for (int i = 0; i < 2 && e == cudaSuccess; ++i) {
+            e = cudaEventCreateWithFlags(&ctx->ev_h2d[i], cudaEventDisableTiming);
+            if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->ev_comp[i], cudaEventDisableTiming);
+            if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->ev_d2h[i], cudaEventDisableTiming);
+        }
+        if (e != cudaSuccess) return cuda_fail(ctx, e, "stream setup");
+    }
+    if (2 * set_bytes > ctx->stage_bytes) {
+        if (ctx->stage) cudaFree(ctx->stage);
+        ctx->stage = nullptr;
+        ctx->stage_bytes = 0;
+        e = cudaMalloc(&ctx->stage, 2 * set_bytes);
+        if (e != cudaSuccess) return cuda_fail(ctx, e, "staging cudaMalloc");
+        ctx->stage_bytes = 2 * set_bytes;
+    }
+    int64_t launches = 0;
+    const int64_t nchunks = (BH + chunk - 1) / chunk;
+    for (int64_t c = 0; c < nchunks; ++c) {
+        const int sidx = int(c & 1);
+        const int64_t h0 = c * chunk, hc = std::min(chunk, BH - h0);
+        char* set = static_cast<char*>(ctx->stage) + sidx * set_bytes;
+        char* dq = set;
+        char* dk = dq + chunk * in_bytes;
+        char* dv = dk + chunk * in_bytes;
+        char* dout = dv + chunk * in_bytes;
+        if (c >= 2) cudaStreamWaitEvent(ctx->st_h2d, ctx->ev_comp[sidx], 0);
+        e = cudaMemcpyAsync(dq, static_cast<const char*>(q) + h0 * in_bytes, hc * in_bytes, cudaMemcpyHostToDevice, ctx->st_h2d);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(dk, static_cast<const char*>(k) + h0 * in_bytes, hc * in_bytes, cudaMemcpyHostToDevice, ctx->st_h2d);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(dv, static_cast<const char*>(v) + h0 * in_bytes, hc * in_bytes, cudaMemcpyHostToDevice, ctx->st_h2d);
+        if (e == cudaSuccess) e = cudaEventRecord(ctx->ev_h2d[sidx], ctx->st_h2d);
+        if (e != cudaSuccess) return cuda_fail(ctx, e, "H2D");
+        cudaStreamWaitEvent(ctx->st_comp, ctx->ev_h2d[sidx], 0);
+        if (c >= 2) cudaStreamWaitEvent(ctx->st_comp, ctx->ev_d2h[sidx], 0);
+        pisa_attn_desc dc = *d;
+        dc.batch = 1;
+        dc.heads = hc;
+        const int64_t ld = L * D;
+        for (int t = 0; t < 3; ++t) {
+            int64_t* s3 = t == 0 ? dc.q_strides : t == 1 ? dc.k_strides : dc.v_strides;
+            s3[0] = hc * ld;
+            s3[1] = ld;
+            s3[2] = D;
+        }
+        dc.o_strides[0] = hc * ld;
+        dc.o_strides[1] = ld;
+        dc.o_strides[2] = D;
+        dc.check_finite = 0;
+        st = pisa_b200_fwd(ctx, &dc, dq, dk, dv, dout, nullptr, ctx->st_comp);
+        if (st != PISA_OK) return st;
+        launches += ctx->launches;
+        cudaEventRecord(ctx->ev_comp[sidx], ctx->st_comp);
+        cudaStreamWaitEvent(ctx->st_d2h, ctx->ev_comp[sidx], 0);
+        e = cudaMemcpyAsync(static_cast<char*>(o) + h0 * out_bytes, dout, hc * out_bytes, cudaMemcpyDeviceToHost, ctx->st_d2h);
+        if (e == cudaSuccess) e = cudaEventRecord(ctx->ev_d2h[sidx], ctx->st_d2h);
+        if (e != cudaSuccess) return cuda_fail(ctx, e, "D2H");
+    }
+    e = cudaStreamSynchronize(ctx->st_d2h);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->st_comp);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "host-path sync");
+    ctx->launches = launches;
+    return PISA_OK;
+}
+
+pisa_status pisa_b200_selftest_mma(pisa_ctx* ctx, const void* a, const void* b, float* out,
+                                   void* stream) {
+    if (!ctx || !a || !b || !out) return PISA_ERR_INVALID_DIMENSION;
+    DeviceGuard g(ctx->device);
+    CUtensorMap ta, tb128, tb64;
+    if (!make_3d_map(&ta, a, 128, 128, 1, 128) || !make_3d_map(&tb128, b, 128, 128, 1, 128) ||
+        !make_3d_map(&tb64, b, 128, 128, 1, 64))
+        return fail(ctx, PISA_ERR_CUDA, "TMA descriptor creation failed");
+    const cudaStream_t s = static_cast<cudaStream_t>(stream);
+    cudaError_t e = cudaMemsetAsync(out, 0, 4 * 128 * 128 * sizeof(float), s);
+    if (e == cudaSuccess)
+        e = launch_selftest_mma(ta, tb128, tb64, static_cast<const __nv_bfloat16*>(a), out, s);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "selftest launch");
+    return PISA_OK;
+}
+
+}  // extern "C"
