@@ -1,0 +1,407 @@
+#!/usr/bin/env python3
+"""PISA attention forward benchmark (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...
+
+A step is one PISA forward (Hybrid, block 64, density 12.5 %) over the whole
+workload: prepare (K1) -> select (K2) -> fused piecewise attention (K3). Default
+workload: Wan2.1-14B 720p attention, B=1 H=40 L=75600 d=128 (BASELINE.json
+configs[3]; it fits one B200). Heads are sharded across ranks (no data-path
+collective); the reported latency is the max over ranks.
+
+value = dense-equivalent TFLOPS of the whole job = H * 4 L^2 d / t.
+Inputs (2.3 GB) are larger than L2 (126 MB), so no L2 flush between steps.
+Prints ONE JSON line on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "PISA attn fwd latency (ms) & dense-equiv TFLOPS at Wan2.1-14B shape, 1/2/4/8 B200"
+WORKLOADS = {
+    # name: (B, H, L, d, density, BASELINE.json config)
+    "wan14b": (1, 40, 75600, 128, 0.125, "Wan2.1-14B 720p 81-frame video attention"),
+    "wan13b": (1, 12, 32760, 128, 0.125, "Wan2.1-1.3B 480p 81-frame video attention"),
+    "flux": (1, 24, 4608, 128, 0.125, "FLUX.1 1024px image DiT attention"),
+    "hunyuan": (1, 24, 118800, 128, 0.125, "HunyuanVideo 720p 129-frame attention"),
+    "smoke": (1, 2, 4096, 64, 0.25, "CPU-oracle smoke"),
+}
+
+
+def flops_dense(L, d):
+    return 4.0 * L * L * d  # analysis.hpp:322
+
+
+def flops_fused(L, d, N, k):
+    # exact + full Phase-2 scan + first-order + normalize, per head
+    return 4.0 * L * k * 64 * d + 4.0 * L * N * d + 2.0 * L * d * d + L * d
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            j = json.load(f)
+        return j["bf16_tflops"], j["bf16_tflops_sustained"], j["hbm_gbs"], "measured"
+    except Exception:
+        return 1590.0, 1400.0, 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[2:6]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ------------------------------------------------------------ CPU legs --
+def cpu_reference_sample(wl, steps, warmup, log):
+    """Times the unmodified reference (oracle/_ref, compiled from /root/reference)
+    on the host cores: prepare over a full head + route + pisa_streaming for a
+    bounded range of query blocks (pisa_cli.cpp:728-729 semantics, accum F32)."""
+    import ctypes as C
+
+    import numpy as np
+
+    import oracle as O
+
+    B, H, L, d, density, _ = WORKLOADS[wl]
+    Lf = (L // 64) * 64  # the reference rejects L % 64 != 0 (attention.hpp:43-47)
+    N = Lf // 64
+    threads = os.cpu_count() or 1
+    os.environ.setdefault("PISA_THREADS", str(threads))
+    if not O.ref_available():
+        O.build()
+    R = O.ref()
+    q, k, v = O.ref_gen("gaussian", 0, 1, Lf, d)
+    q, k, v = (O.round_bf16(x[0]) for x in (q, k, v))
+    # Bounded sample: prepare over the full head, routing + streaming attention for a
+    # range of query blocks sized to ~2 s of CPU work. The full-head time is
+    # extrapolated linearly in query blocks (heads are serial, engine.hpp:432, and
+    # query blocks are independent, engine.hpp:272): t_head = t_prep + t_qb * N / n_qb.
+    out = np.zeros((N * 64, d), np.float32)
+    ms = np.zeros(3)
+
+    def run(nqb):
+        st = R.ref_bench_sample(q, k, v, Lf, d, 1.0 - density, 0, nqb, threads, out, ms)
+        if st != 0:
+            raise RuntimeError(f"ref_bench_sample status {st}")
+        return ms.copy()
+
+    m = run(16)
+    per_block = max(1e-3, (m[1] + m[2]) / 16)
+    qb1 = int(max(16, min(N, 2000.0 / per_block)))
+    heads = []
+    for i in range(warmup + steps):
+        m = run(qb1)
+        if i >= warmup:
+            heads.append(m[0] + (m[1] + m[2]) * N / qb1)
+    tm = statistics.median(heads)
+    value = 4.0 * Lf * Lf * d / (tm * 1e-3) / 1e12  # dense-equivalent TFLOPS of one head
+    sample = (f"1 head of {wl} at L={Lf} (floored to a multiple of 64): prepare over the full "
+              f"head + routing and Hybrid streaming (accum f32) for query blocks [0,{qb1}) of "
+              f"{N}, extrapolated to the head (t_prep + t_blocks*N/{qb1}); gen_gaussian seed 0 "
+              f"bf16-rounded; median of {len(heads)} after {warmup} warmup; "
+              f"PISA_THREADS={threads}")
+    return {"value": value, "unit": "TFLOPS (dense-equivalent)", "cores": threads,
+            "kind": "reference", "sample": sample, "ms_per_sample": tm,
+            "lib": os.path.basename(R._path), "ms_per_head": tm}
+
+
+# ---------------------------------------------------------- GPU arm ----
+def union_executed_flops(sel, N, d, C2, first_order=True):
+    """Executed MMA FLOPs of the fused kernel: per 128-row tile the union of the two
+    query blocks' selections plus the centroid tiles plus Q.H_bar."""
+    import torch
+    Hr = sel.shape[0]
+    k = sel.shape[-1]
+    m = torch.zeros((Hr, N, N), dtype=torch.bool, device=sel.device)
+    m.scatter_(2, sel.long(), True)
+    if N % 2:
+        m = torch.cat([m, torch.zeros((Hr, 1, N), dtype=torch.bool, device=sel.device)], 1)
+    u = (m[:, 0::2] | m[:, 1::2]).sum(-1).double()  # [Hr][tiles]
+    per_tile = (u + C2) * (4.0 * 128 * 64 * d) + (2.0 * 128 * d * d if first_order else 0.0)
+    return float(per_tile.sum().item()), float(u.mean().item()) / k
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="wan14b", choices=list(WORKLOADS))
+    ap.add_argument("--data", default="gaussian", choices=["gaussian", "clustered"])
+    ap.add_argument("--density", type=float, default=None)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-dense", action="store_true")
+    args = ap.parse_args()
+    warmup = max(3, args.warmup)
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    B, H, L, d, density, cfg_name = WORKLOADS[args.workload]
+    if args.density is not None:
+        density = args.density
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        res = cpu_reference_sample(args.workload, args.steps, warmup, None)
+        line = {"impl": "reference", "metric": METRIC, "value": res["value"], "unit": res["unit"],
+                "n_gpus": args.gpus, "steps": args.steps, "warmup": warmup,
+                "ms_per_step": res["ms_per_sample"] * H, "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+                "data": "synthetic gen_gaussian(seed 0) rounded to bf16",
+                "config": {"workload": f"{cfg_name} (bounded CPU sample)", "B": B, "H": H,
+                           "L": L, "d": d, "density": density, "block": 64,
+                           "variant": "hybrid", "router": "plain"},
+                "cpu_baseline": {k: res[k] for k in ("value", "unit", "cores", "kind", "sample")},
+                "e2e": {"value": res["value"], "unit": res["unit"], "h2d_bytes_per_step": 0,
+                        "d2h_bytes_per_step": 0}}
+        print(json.dumps(line), flush=True)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2602_01077_b200 as P
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    # (batch x head) sharding: contiguous head ranges per rank
+    h0 = rank * H // world
+    h1 = (rank + 1) * H // world
+    Hr = h1 - h0
+    N = -(-L // 64)
+    k = P.sparsity_to_k(1.0 - density, N).k
+    C2 = -(-N // 64)
+
+    g = torch.Generator(device=dev)
+    g.manual_seed(1234 + rank)
+    shape = (B, Hr, L, d)
+    if args.data == "gaussian":
+        q, kk, v = (torch.randn(shape, generator=g, device=dev, dtype=torch.bfloat16)
+                    for _ in range(3))
+    else:  # gen_clustered-like structure (generate.hpp:132-190) drawn on the GPU
+        nc = 16
+        run = -(-L // nc)
+        ctr = torch.randn((B, Hr, nc, d), generator=g, device=dev)
+        zi = torch.clamp(torch.arange(L, device=dev) // run, max=nc - 1)
+        kk = (ctr[:, :, zi] + 0.15 * torch.randn(shape, generator=g, device=dev)).bfloat16()
+        sub = torch.randint(0, nc, (B, Hr, max(1, nc // 4)), generator=g, device=dev)
+        pick = torch.gather(sub, 2, torch.randint(0, sub.shape[-1], (B, Hr, L), generator=g, device=dev))
+        q = (2.0 * torch.gather(ctr, 2, pick.unsqueeze(-1).expand(B, Hr, L, d))
+             + torch.randn(shape, generator=g, device=dev)).bfloat16()
+        v = torch.randn(shape, generator=g, device=dev, dtype=torch.bfloat16)
+    out = torch.empty(shape, device=dev, dtype=torch.bfloat16)
+    ctx = P.Context.get(local_rank)
+    kw = dict(sparsity=1.0 - density, variant=P.PisaVariant.Hybrid)
+
+    # warmup (+ the plan, for executed-FLOP accounting)
+    _, ex = P.fwd(q, kk, v, out, return_plan=True, **kw)
+    for _ in range(warmup - 1):
+        P.fwd(q, kk, v, out, **kw)
+    torch.cuda.synchronize()
+    exec_flops, union_ratio = union_executed_flops(ex["selected"][0], N, d, C2)
+    del ex
+
+    # timed region
+    stream = torch.cuda.current_stream()
+    ctx.set_profiling(True)
+    ctx.read_profile()
+    launches = 0
+    with ClockSampler(local_rank) as clk:
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            P.fwd(q, kk, v, out, **kw)
+            launches += ctx.last_launch_count()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+    ctx.set_profiling(False)
+    prof = ctx.read_profile()
+    t_ms = e0.elapsed_time(e1) / args.steps
+    t = torch.tensor([t_ms], device=dev, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    t_ms = float(t.item())
+    clocks = clk.summary()
+
+    total_dense = H * B * flops_dense(L, d)
+    value = total_dense / (t_ms * 1e-3) / 1e12
+    # roofline of the dominant kernel (fused) on this rank
+    peak, peak_sus, hbm, peak_src = load_peaks()
+    fused_ms, fused_n = prof.get("fused_attn_kernel", (0.0, 0))
+    fused_avg = fused_ms / max(1, fused_n)
+    alg = Hr * B * flops_fused(L, d, N, k)
+    achieved = alg / (fused_avg * 1e-3) / 1e12 if fused_avg > 0 else None
+    executed = exec_flops / (fused_avg * 1e-3) / 1e12 if fused_avg > 0 else None
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tp):
+        try:
+            with open(tp) as f:
+                traffic = json.load(f).get(args.workload, {}).get("fused_attn_kernel_bytes")
+        except Exception:
+            traffic = None
+    kernels = {n: {"ms_per_launch": ms / max(1, c), "launches": c,
+                   "share": ms / max(1e-9, sum(x[0] for x in prof.values()))}
+               for n, (ms, c) in prof.items()}
+
+    # dense attention baseline on the same B200 (cuDNN/flash SDPA via torch), this rank's heads
+    dense = None
+    if not args.no_dense:
+        import torch.nn.functional as F
+        try:
+            F.scaled_dot_product_attention(q, kk, v)
+            torch.cuda.synchronize()
+            a0 = torch.cuda.Event(enable_timing=True)
+            a1 = torch.cuda.Event(enable_timing=True)
+            a0.record(stream)
+            for _ in range(3):
+                F.scaled_dot_product_attention(q, kk, v)
+            a1.record(stream)
+            torch.cuda.synchronize()
+            dms = a0.elapsed_time(a1) / 3
+            dense = {"impl": "torch SDPA (cuDNN / flash backend)", "ms": dms,
+                     "pisa_speedup": dms / t_ms, "tflops": Hr * B * flops_dense(L, d) / (dms * 1e-3) / 1e12}
+        except Exception as e:  # noqa: BLE001
+            dense = {"error": str(e)[:200]}
+
+    # end to end through the C-ABI host path: pinned host buffers, H2D + D2H timed
+    e2e = None
+    if not args.no_e2e:
+        hq, hk, hv = (x.cpu().pin_memory() for x in (q, kk, v))
+        ho = torch.empty(shape, dtype=torch.bfloat16).pin_memory()
+        for _ in range(2):
+            P.fwd_host(hq, hk, hv, ho, device=local_rank, **kw)
+        if world > 1:
+            dist.barrier()
+        ts = time.perf_counter()
+        for _ in range(args.steps):
+            P.fwd_host(hq, hk, hv, ho, device=local_rank, **kw)
+        te = (time.perf_counter() - ts) * 1e3 / args.steps
+        tt = torch.tensor([te], device=dev, dtype=torch.float64)
+        if world > 1:
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        te = float(tt.item())
+        nb = 2 * B * Hr * L * d
+        e2e = {"value": total_dense / (te * 1e-3) / 1e12, "unit": "TFLOPS (dense-equivalent)",
+               "ms_per_step": te, "h2d_bytes_per_step": 3 * nb * world,
+               "d2h_bytes_per_step": nb * world,
+               "path": "pisa_b200_fwd_host (pinned host Q/K/V/O; H2D, compute, D2H overlapped per head chunk)"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        try:
+            cpu = cpu_reference_sample(args.workload, 3, 1, None)
+            cpu.pop("ms_per_sample", None)
+            cpu.pop("lib", None)
+        except Exception as e:  # noqa: BLE001
+            cpu = {"error": str(e)[:200]}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "TFLOPS (dense-equivalent)",
+            "n_gpus": world, "steps": args.steps, "warmup": warmup, "ms_per_step": t_ms,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
+            "data": f"synthetic {args.data} (torch RNG on device), bf16",
+            "config": {"workload": cfg_name, "B": B, "H": H, "L": L, "d": d, "N": N, "k": k,
+                       "density": density, "block": 64, "variant": "hybrid", "router": "plain",
+                       "parallelism": f"head-sharded x{world}", "heads_per_gpu": Hr,
+                       "l2": "inputs 2.3 GB > 126 MB L2, no flush"},
+            "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                         "frac": (achieved / peak) if achieved else None, "traffic": traffic,
+                         "kernel": "fused_attn_kernel", "kernel_ms": fused_avg,
+                         "algorithmic_flops_per_launch": alg, "executed_flops_per_launch": exec_flops,
+                         "executed_tflops": executed,
+                         "executed_frac": (executed / peak) if executed else None,
+                         "union_over_k": union_ratio, "peak_source": peak_src,
+                         "peak_sustained": peak_sus},
+            "kernels": kernels,
+            "dense_baseline": dense,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": launches,
+            "clocks": clocks,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

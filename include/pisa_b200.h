@@ -160,6 +160,12 @@ pisa_status pisa_b200_attention(pisa_ctx* ctx, const pisa_attn_desc* desc, const
 int64_t pisa_b200_last_launch_count(const pisa_ctx* ctx);
 /* Name of kernel i of the fused forward (for profiles). NULL past the end. */
 const char* pisa_b200_kernel_name(int i);
+/* Per-kernel CUDA-event timing: while enabled, every launch is bracketed by a pair
+ * of events recorded on the launching stream. read_profile synchronises on the
+ * recorded events, writes the summed milliseconds and launch counts per kernel id
+ * (ids as pisa_b200_kernel_name; arrays of length 8), and clears the record. */
+pisa_status pisa_b200_set_profiling(pisa_ctx* ctx, int enable);
+pisa_status pisa_b200_read_profile(pisa_ctx* ctx, double* ms, int64_t* launches);
 
 /* Standalone tensor-core self test: runs the three tcgen05 operand modes the fused
  * kernel uses (K-major SS, MN-major SS, TMEM-A TS) on small tiles and writes the

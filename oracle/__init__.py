@@ -96,7 +96,7 @@ def ref():
                                     C.c_uint, _f32p, C.c_void_p, C.c_void_p, C.c_void_p,
                                     C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
         R.ref_bench_sample.argtypes = [_f32p, _f32p, _f32p, i64, i64, C.c_double, i64, i64,
-                                       C.c_uint, _f32p, C.POINTER(C.c_double)]
+                                       C.c_uint, _f32p, _f64p]
         R.ref_dense_online.argtypes = [_f32p, _f32p, _f32p, i64, i64, C.c_int, C.c_uint, _f32p]
         R._path = path
         _ref = R

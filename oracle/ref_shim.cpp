@@ -176,12 +176,18 @@ int ref_multihead(const float* q, const float* k, const float* v, int64_t H, int
 // of query blocks [qb0, qb1) of one head, through the reference's public step
 // functions: prepare over the full K/V, route the sampled query blocks, then
 // pisa_streaming with accum F32. Used by bench.py --impl reference to time a
-// bounded sample. Returns wall ms of the whole call in *ms.
+// bounded sample. ms[0] = prepare over the full head (compute_block_stats +
+// compute_global_stats), ms[1] = query means + routing of the sampled blocks,
+// ms[2] = pisa_streaming over the sampled blocks.
 int ref_bench_sample(const float* q, const float* k, const float* v, int64_t L, int64_t d,
                      double r, int64_t qb0, int64_t qb1, unsigned threads, float* out,
                      double* ms) {
     return guarded([&] {
-        const auto t0 = std::chrono::steady_clock::now();
+        using clk = std::chrono::steady_clock;
+        const auto since = [](clk::time_point t) {
+            return std::chrono::duration<double, std::milli>(clk::now() - t).count();
+        };
+        auto t0 = clk::now();
         const auto cfg = make_cfg(64, 8, 0.0, 0, 0, threads);
         pisa::ConstView<float> kv(k, std::size_t(L), std::size_t(d));
         pisa::ConstView<float> vv(v, std::size_t(L), std::size_t(d));
@@ -189,12 +195,16 @@ int ref_bench_sample(const float* q, const float* k, const float* v, int64_t L, 
         pisa::ConstView<float> qv(q + qb0 * 64 * d, rows, std::size_t(d));
         auto st = pisa::compute_block_stats(kv, vv, 64);
         pisa::compute_global_stats(st, pisa::SpectralMethod::Exact, false);
+        ms[0] = since(t0);
+        t0 = clk::now();
         const auto qb = pisa::query_block_means(qv, 64);
         const auto res = pisa::sparsity_to_k(r, st.num_blocks);
         const auto plan = pisa::select_topk_plain(qb, st.k_bar, res.k, cfg.resolved_scale(std::size_t(d)));
+        ms[1] = since(t0);
+        t0 = clk::now();
         const auto o = pisa::pisa_streaming(qv, kv, vv, plan, st, cfg);
+        ms[2] = since(t0);
         std::memcpy(out, o.output.data.data(), o.output.data.size() * sizeof(float));
-        *ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
     });
 }
 

@@ -38,6 +38,7 @@ EXPORTED = [
     "pisa_b200_sparsity_to_k", "pisa_b200_resolve", "pisa_b200_fwd", "pisa_b200_fwd_host",
     "pisa_b200_block_stats", "pisa_b200_select", "pisa_b200_attention",
     "pisa_b200_last_launch_count", "pisa_b200_kernel_name", "pisa_b200_selftest_mma",
+    "pisa_b200_set_profiling", "pisa_b200_read_profile",
 ]
 
 _lib = None
@@ -78,7 +79,9 @@ def load(build_if_missing: bool = False):
     L.pisa_b200_kernel_name.argtypes = [C.c_int]
     L.pisa_b200_kernel_name.restype = C.c_char_p
     L.pisa_b200_selftest_mma.argtypes = [vp, vp, vp, vp, vp]
-    for name in ("pisa_b200_create", "pisa_b200_sparsity_to_k", "pisa_b200_resolve",
+    L.pisa_b200_set_profiling.argtypes = [vp, C.c_int]
+    L.pisa_b200_read_profile.argtypes = [vp, C.POINTER(C.c_double), C.POINTER(i64)]
+    for name in ("pisa_b200_set_profiling", "pisa_b200_read_profile", "pisa_b200_create", "pisa_b200_sparsity_to_k", "pisa_b200_resolve",
                  "pisa_b200_fwd", "pisa_b200_fwd_host", "pisa_b200_block_stats",
                  "pisa_b200_select", "pisa_b200_attention", "pisa_b200_selftest_mma"):
         getattr(L, name).restype = C.c_int

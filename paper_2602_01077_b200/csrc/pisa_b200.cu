@@ -11,6 +11,7 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <vector>
 
 #include "../../include/pisa_b200.h"
 #include "kernels.h"
@@ -30,12 +31,54 @@ struct pisa_ctx {
     cudaEvent_t ev_h2d[2] = {}, ev_comp[2] = {}, ev_d2h[2] = {};
     void* stage = nullptr;
     size_t stage_bytes = 0;
+    // per-kernel event timing
+    bool prof = false;
+    struct Rec {
+        int id;
+        cudaEvent_t a, b;
+    };
+    std::vector<Rec> recs;
+    std::vector<cudaEvent_t> pool;
 };
 
 namespace {
 
 const char* kKernelNames[] = {"block_stats_kernel", "hbar_reduce_kernel", "select_kernel",
-                              "fused_attn_kernel", nullptr};
+                              "fused_attn_kernel",  "plan_to_mask_kernel", "stats_to_bf16_kernel",
+                              nullptr};
+enum KernelId { kK1 = 0, kK1b = 1, kK2 = 2, kK3 = 3, kPlan = 4, kToBf16 = 5 };
+
+cudaEvent_t pooled_event(pisa_ctx* c) {
+    if (!c->pool.empty()) {
+        cudaEvent_t e = c->pool.back();
+        c->pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e = nullptr;
+    cudaEventCreate(&e);
+    return e;
+}
+
+// Brackets one launch with events on its stream when profiling is on.
+struct ProfScope {
+    pisa_ctx* c;
+    int id;
+    cudaStream_t s;
+    cudaEvent_t a = nullptr;
+    ProfScope(pisa_ctx* c_, int id_, cudaStream_t s_) : c(c_), id(id_), s(s_) {
+        if (c->prof) {
+            a = pooled_event(c);
+            cudaEventRecord(a, s);
+        }
+    }
+    ~ProfScope() {
+        if (a) {
+            cudaEvent_t b = pooled_event(c);
+            cudaEventRecord(b, s);
+            c->recs.push_back({id, a, b});
+        }
+    }
+};
 
 pisa_status fail(pisa_ctx* ctx, pisa_status st, const std::string& msg) {
     if (ctx) {
@@ -233,8 +276,13 @@ pisa_status run_stats(pisa_ctx* ctx, const pisa_attn_desc& d, const Plan& p, con
         return fail(ctx, PISA_ERR_INVALID_DIMENSION, "TMA descriptor rejected the q/k/v layout");
     StatsArgs sa{w.kbar, w.vhat, w.qbar, w.kbar_bf, w.vhat_bf, w.hpart,
                  int(p.L), int(p.N), int(p.Npad), int(d.heads), int(p.nchunk1)};
-    cudaError_t e = launch_block_stats(int(p.D), tq, tk, tv, sa, int(p.BH), s);
+    cudaError_t e;
+    {
+        ProfScope ps(ctx, kK1, s);
+        e = launch_block_stats(int(p.D), tq, tk, tv, sa, int(p.BH), s);
+    }
     if (e != cudaSuccess) return cuda_fail(ctx, e, "block_stats launch");
+    ProfScope ps(ctx, kK1b, s);
     e = launch_hbar_reduce(int(p.D), w.hpart, int(p.nchunk1), int(p.N), w.kbar, w.hbar, w.hbar_bf,
                            d.variant == PISA_GLOBAL_CENTROID ? w.kglob : nullptr, int(p.BH), s);
     if (e != cudaSuccess) return cuda_fail(ctx, e, "hbar_reduce launch");
@@ -246,6 +294,7 @@ pisa_status run_select(pisa_ctx* ctx, const pisa_attn_desc& d, const Plan& p, co
                        const float* kbar, int32_t* selected, uint32_t* mask, cudaStream_t s) {
     SelectArgs a{qbar, kbar, selected, mask, int(p.N), int(p.W), int(p.k), d.force_diagonal,
                  float(p.scale)};
+    ProfScope ps(ctx, kK2, s);
     const cudaError_t e = launch_select(int(p.D), a, int(p.BH), s);
     if (e != cudaSuccess) return cuda_fail(ctx, e, "select launch");
     ctx->launches += 1;
@@ -288,7 +337,11 @@ pisa_status run_fused(pisa_ctx* ctx, const pisa_attn_desc& d, const Plan& p, con
         const cudaError_t e = cudaMemsetAsync(w.flag, 0, sizeof(int), s);
         if (e != cudaSuccess) return cuda_fail(ctx, e, "flag reset");
     }
-    const cudaError_t e = launch_fused(int(p.D), tq, tk, tv, tkb, tvh, th, a, int(p.BH), s);
+    cudaError_t e;
+    {
+        ProfScope ps(ctx, kK3, s);
+        e = launch_fused(int(p.D), tq, tk, tv, tkb, tvh, th, a, int(p.BH), s);
+    }
     if (e != cudaSuccess) return cuda_fail(ctx, e, "fused launch");
     ctx->launches += 1;
     if (d.check_finite) {
@@ -350,6 +403,11 @@ void pisa_b200_destroy(pisa_ctx* c) {
     if (c->arena) cudaFree(c->arena);
     if (c->stage) cudaFree(c->stage);
     if (c->flag_host) cudaFreeHost(c->flag_host);
+    for (auto& r : c->recs) {
+        cudaEventDestroy(r.a);
+        cudaEventDestroy(r.b);
+    }
+    for (auto e : c->pool) cudaEventDestroy(e);
     for (int i = 0; i < 2; ++i) {
         if (c->ev_h2d[i]) cudaEventDestroy(c->ev_h2d[i]);
         if (c->ev_comp[i]) cudaEventDestroy(c->ev_comp[i]);
@@ -366,8 +424,35 @@ const char* pisa_b200_last_error(const pisa_ctx* c) { return c ? c->last_error.c
 int64_t pisa_b200_last_launch_count(const pisa_ctx* c) { return c ? c->launches : 0; }
 
 const char* pisa_b200_kernel_name(int i) {
-    if (i < 0 || i >= 4) return nullptr;
+    if (i < 0 || i >= 6) return nullptr;
     return kKernelNames[i];
+}
+
+pisa_status pisa_b200_set_profiling(pisa_ctx* c, int enable) {
+    if (!c) return PISA_ERR_INVALID_DIMENSION;
+    c->prof = enable != 0;
+    return PISA_OK;
+}
+
+pisa_status pisa_b200_read_profile(pisa_ctx* c, double* ms, int64_t* launches) {
+    if (!c) return PISA_ERR_INVALID_DIMENSION;
+    DeviceGuard g(c->device);
+    for (int i = 0; i < 8; ++i) {
+        if (ms) ms[i] = 0.0;
+        if (launches) launches[i] = 0;
+    }
+    for (auto& r : c->recs) {
+        cudaError_t e = cudaEventSynchronize(r.b);
+        float t = 0.f;
+        if (e == cudaSuccess) e = cudaEventElapsedTime(&t, r.a, r.b);
+        if (e != cudaSuccess) return cuda_fail(c, e, "read_profile");
+        if (ms) ms[r.id] += t;
+        if (launches) launches[r.id] += 1;
+        c->pool.push_back(r.a);
+        c->pool.push_back(r.b);
+    }
+    c->recs.clear();
+    return PISA_OK;
 }
 
 pisa_status pisa_b200_sparsity_to_k(double r, int64_t n, int64_t* k, double* realized) {
@@ -468,12 +553,16 @@ pisa_status pisa_b200_attention(pisa_ctx* ctx, const pisa_attn_desc* d, const vo
     if ((st = workspace(ctx, p, &w)) != PISA_OK) return st;
     // plan -> mask, with SelectionPlan::validate (router.hpp:50-70)
     cudaError_t e = cudaMemsetAsync(w.flag + 1, 0, sizeof(int), s);
-    if (e == cudaSuccess)
+    if (e == cudaSuccess) {
+        ProfScope ps(ctx, kPlan, s);
         e = launch_plan_to_mask(selected, int(p.N), int(p.k), int(p.W), w.mask, w.flag + 1, int(p.BH), s);
-    if (e == cudaSuccess)
+    }
+    if (e == cudaSuccess) {
+        ProfScope ps(ctx, kToBf16, s);
         e = launch_stats_to_bf16(int(p.D), k_bar, v_hat, h_bar, int(p.N), int(p.Npad), w.kbar_bf,
                                  w.vhat_bf, w.hbar_bf,
                                  d->variant == PISA_GLOBAL_CENTROID ? w.kglob : nullptr, int(p.BH), s);
+    }
     if (e == cudaSuccess)
         e = cudaMemcpyAsync(ctx->flag_host, w.flag + 1, sizeof(int), cudaMemcpyDeviceToHost, s);
     if (e == cudaSuccess) e = cudaStreamSynchronize(s);

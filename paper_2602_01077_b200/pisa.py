@@ -255,6 +255,17 @@ class Context:
     def last_launch_count(self) -> int:
         return int(self.lib.pisa_b200_last_launch_count(self.handle))
 
+    def set_profiling(self, on: bool) -> None:
+        _raise(self.lib.pisa_b200_set_profiling(self.handle, int(on)), self.handle)
+
+    def read_profile(self) -> dict:
+        """{kernel_name: (total_ms, launches)} since the last read (syncs on events)."""
+        ms = (C.c_double * 8)()
+        n = (_abi.i64 * 8)()
+        _raise(self.lib.pisa_b200_read_profile(self.handle, ms, n), self.handle)
+        names = kernel_names()
+        return {names[i]: (ms[i], n[i]) for i in range(len(names)) if n[i] > 0}
+
 
 def _strides_bhld(t: torch.Tensor, layout: str):
     """Element strides (b, h, l) of a 4-D tensor in 'bhld' or 'blhd' order."""
