@@ -165,6 +165,9 @@ const char* pisa_b200_kernel_name(int i);
  * recorded events, writes the summed milliseconds and launch counts per kernel id
  * (ids as pisa_b200_kernel_name; arrays of length 8), and clears the record. */
 pisa_status pisa_b200_set_profiling(pisa_ctx* ctx, int enable);
+/* Debug timeline of one fused-kernel CTA (tile index `tile`, head 0): only
+ * libraries built with -DPISA_TRACE=1 write it. dev_buf: 8*1024 u64 (device). */
+pisa_status pisa_b200_debug_trace(pisa_ctx* ctx, unsigned long long* dev_buf, int tile);
 pisa_status pisa_b200_read_profile(pisa_ctx* ctx, double* ms, int64_t* launches);
 
 /* Standalone tensor-core self test: runs the three tcgen05 operand modes the fused

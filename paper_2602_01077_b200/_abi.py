@@ -38,17 +38,19 @@ EXPORTED = [
     "pisa_b200_sparsity_to_k", "pisa_b200_resolve", "pisa_b200_fwd", "pisa_b200_fwd_host",
     "pisa_b200_block_stats", "pisa_b200_select", "pisa_b200_attention",
     "pisa_b200_last_launch_count", "pisa_b200_kernel_name", "pisa_b200_selftest_mma",
-    "pisa_b200_set_profiling", "pisa_b200_read_profile",
+    "pisa_b200_set_profiling", "pisa_b200_read_profile", "pisa_b200_debug_trace",
 ]
 
 _lib = None
 
 
 def load(build_if_missing: bool = False):
-    """Returns the loaded C-ABI library; raises if the sm_100a build is absent."""
-    global _lib
+    """Returns the loaded C-ABI library; raises if the sm_100a build is absent.
+    PISA_B200_LIB overrides the path (e.g. the PISA_TRACE debug build)."""
+    global _lib, LIB_PATH
     if _lib is not None:
         return _lib
+    LIB_PATH = os.environ.get("PISA_B200_LIB", LIB_PATH)
     if not os.path.exists(LIB_PATH):
         if build_if_missing:
             from . import build as _b
@@ -80,6 +82,8 @@ def load(build_if_missing: bool = False):
     L.pisa_b200_kernel_name.restype = C.c_char_p
     L.pisa_b200_selftest_mma.argtypes = [vp, vp, vp, vp, vp]
     L.pisa_b200_set_profiling.argtypes = [vp, C.c_int]
+    L.pisa_b200_debug_trace.argtypes = [vp, vp, C.c_int]
+    L.pisa_b200_debug_trace.restype = C.c_int
     L.pisa_b200_read_profile.argtypes = [vp, C.POINTER(C.c_double), C.POINTER(i64)]
     for name in ("pisa_b200_set_profiling", "pisa_b200_read_profile", "pisa_b200_create", "pisa_b200_sparsity_to_k", "pisa_b200_resolve",
                  "pisa_b200_fwd", "pisa_b200_fwd_host", "pisa_b200_block_stats",

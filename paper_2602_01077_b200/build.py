@@ -37,17 +37,19 @@ def _stale() -> bool:
     return False
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not _stale():
+def build(force: bool = False, verbose: bool = False, trace: bool = False) -> str:
+    lib = LIB if not trace else os.path.join(LIBDIR, "libpisa_b200_trace.so")
+    if not force and not trace and not _stale():
         return LIB
     os.makedirs(LIBDIR, exist_ok=True)
-    objdir = os.path.join(LIBDIR, "obj")
+    objdir = os.path.join(LIBDIR, "obj_trace" if trace else "obj")
     os.makedirs(objdir, exist_ok=True)
     objs = []
     logs = []
     for src in SOURCES:
         obj = os.path.join(objdir, src.replace(".cu", ".o"))
-        cmd = [NVCC, *ARCH, *FLAGS, "-I", CSRC, "-I", os.path.join(ROOT, "include"), "-c",
+        cmd = [NVCC, *ARCH, *FLAGS, *(["-DPISA_TRACE=1"] if trace else []), "-I", CSRC,
+               "-I", os.path.join(ROOT, "include"), "-c",
                os.path.join(CSRC, src), "-o", obj]
         r = subprocess.run(cmd, capture_output=True, text=True)
         logs.append(f"== {src}\n{r.stdout}{r.stderr}")
@@ -55,19 +57,19 @@ def build(force: bool = False, verbose: bool = False) -> str:
             sys.stderr.write("".join(logs))
             raise RuntimeError(f"nvcc failed on {src}")
         objs.append(obj)
-    tmp = LIB + ".tmp"
+    tmp = lib + ".tmp"
     cmd = [NVCC, *ARCH, "-shared", "-cudart", "static", "-o", tmp, *objs]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)
         raise RuntimeError("nvcc link failed")
-    os.replace(tmp, LIB)
-    with open(os.path.join(LIBDIR, "ptxas.log"), "w") as f:
+    os.replace(tmp, lib)
+    with open(os.path.join(LIBDIR, "ptxas_trace.log" if trace else "ptxas.log"), "w") as f:
         f.write("".join(logs))
     if verbose:
         sys.stdout.write("".join(logs))
-    return LIB
+    return lib
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose=True)
+    build(force="--force" in sys.argv, verbose=True, trace="--trace" in sys.argv)

@@ -1,14 +1,15 @@
 // K2: block scoring + top-k routing (the "select" step, engine.hpp:443-457).
 //
-// Replaces sparsity_to_k's consumer select_topk_plain (router.hpp:126-151) with
-// topk_ascending (:96-108) and force_block (:111-121). One CTA scores kQB query
-// blocks of one (batch, head) against every key centroid:
-//   s_ij = scale * <q_bar_i, k_bar_j>     fp32 FMA, fixed summation order over d
-// (fp32 scoring keeps the index sets bit-exact against the fp64
-// reference on the Wan shapes; bf16 / TF32 scoring does not). Each row's k-th
-// largest score is found by an 8-bit-digit radix select on the order-preserving
-// uint32 image of the float, ties resolve to the LOWER index, and a ballot
-// compaction emits the ascending index list plus a bitmask row in one pass.
+// Replaces select_topk_plain (router.hpp:126-151) with topk_ascending (:96-108)
+// and force_block (:111-121), in two launches:
+//   K2a score_kernel : s_ij = scale * <q_bar_i, k_bar_j>, a register-tiled fp32
+//                      FMA GEMM per (batch, head), fixed summation order over d
+//                      (fp32 scoring keeps the index sets bit-exact
+//                      against the fp64 reference on the Wan shapes; bf16 / TF32
+//                      scoring does not), stored as order-preserving uint32 keys
+//   K2b topk_kernel  : one warp per query block: radix select of the k-th largest
+//                      key, ties to the LOWER index, ballot compaction to the
+//                      ascending index list plus the bitmask row.
 #include "kernels.h"
 #include "sm100.cuh"
 
@@ -17,9 +18,6 @@ using namespace pisa_sm100;
 
 namespace {
 
-constexpr int kQB = 4;        // query blocks per CTA
-constexpr int kKeyTile = 64;  // centroids staged per step
-constexpr int kThreads = 256;
 
 __device__ __forceinline__ uint32_t order_key(float f) {
     if (f == 0.0f) f = 0.0f;  // -0 == +0 as in the fp64 comparison
@@ -27,51 +25,75 @@ __device__ __forceinline__ uint32_t order_key(float f) {
     return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
 }
 
+// K2a: score tile. keys[bh][i][j] = order_key(scale * <q_bar_i, k_bar_j>) for a
+// 64 x 64 tile of (query block, key block) pairs; 256 threads, 4 x 4 outputs
+// each. Every output accumulates a = 0 .. D-1 in order with fp32 FMA (the
+// same order as the reference's dot_d loop), so results are reproducible.
+constexpr int kTile = 64, kAK = 32;
+
 template <int D>
-__global__ void __launch_bounds__(kThreads) select_kernel(SelectArgs a) {
-    extern __shared__ float sm[];
-    float* q_s = sm;                              // [kQB][D]
-    float* kt_s = q_s + kQB * D;                  // [kKeyTile][D + 1]
-    uint32_t* keys = reinterpret_cast<uint32_t*>(kt_s + kKeyTile * (D + 1));  // [kQB][N]
-    uint32_t* hist = keys + kQB * a.N;            // [kQB][256]
-
-    const int bh = blockIdx.y;
-    const int i0 = blockIdx.x * kQB;
-    const int tid = threadIdx.x;
-    const float* qb = a.qbar + size_t(bh) * a.N * D;
-    const float* kb = a.kbar + size_t(bh) * a.N * D;
-
-    for (int e = tid; e < kQB * D; e += kThreads) {
-        const int r = e / D, i = i0 + r;
-        q_s[e] = i < a.N ? qb[size_t(i) * D + (e % D)] : 0.f;
-    }
-    // ---- scores
-    const int r = tid / kKeyTile;   // query row of this thread (warp-uniform)
-    const int jj = tid % kKeyTile;  // centroid within the tile
-    for (int j0 = 0; j0 < a.N; j0 += kKeyTile) {
+__global__ void __launch_bounds__(256) score_kernel(const float* __restrict__ qbar,
+                                                    const float* __restrict__ kbar,
+                                                    uint32_t* __restrict__ keys, int N,
+                                                    float scale) {
+    __shared__ float As[kAK][kTile + 4];
+    __shared__ float Bs[kAK][kTile + 4];
+    const int bh = blockIdx.z;
+    const int i0 = blockIdx.y * kTile, j0 = blockIdx.x * kTile;
+    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+    const float* qb = qbar + size_t(bh) * N * D;
+    const float* kb = kbar + size_t(bh) * N * D;
+    float acc[4][4] = {};
+    for (int a0 = 0; a0 < D; a0 += kAK) {
         __syncthreads();
-        for (int e = tid; e < kKeyTile * D; e += kThreads) {
-            const int row = e / D, col = e % D;
-            kt_s[row * (D + 1) + col] = (j0 + row < a.N) ? kb[size_t(j0 + row) * D + col] : 0.f;
+        for (int e = threadIdx.x; e < kTile * kAK; e += 256) {
+            const int r = e / kAK, c = e % kAK;
+            As[c][r] = (i0 + r < N) ? qb[size_t(i0 + r) * D + a0 + c] : 0.f;
+            Bs[c][r] = (j0 + r < N) ? kb[size_t(j0 + r) * D + a0 + c] : 0.f;
         }
         __syncthreads();
-        const float* qr = q_s + r * D;
-        const float* kr = kt_s + jj * (D + 1);
-        float acc = 0.f;
-#pragma unroll 16
-        for (int c = 0; c < D; ++c) acc = fmaf(qr[c], kr[c], acc);
-        if (j0 + jj < a.N) keys[r * a.N + j0 + jj] = order_key(a.scale * acc);
+#pragma unroll 8
+        for (int c = 0; c < kAK; ++c) {
+            const float4 av = *reinterpret_cast<const float4*>(&As[c][ty * 4]);
+            const float4 bv = *reinterpret_cast<const float4*>(&Bs[c][tx * 4]);
+            const float ar[4] = {av.x, av.y, av.z, av.w};
+            const float br[4] = {bv.x, bv.y, bv.z, bv.w};
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+#pragma unroll
+                for (int w = 0; w < 4; ++w) acc[u][w] = fmaf(ar[u], br[w], acc[u][w]);
+        }
     }
-    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+        const int i = i0 + ty * 4 + u;
+        if (i >= N) continue;
+#pragma unroll
+        for (int w = 0; w < 4; ++w) {
+            const int j = j0 + tx * 4 + w;
+            if (j < N) keys[(size_t(bh) * N + i) * N + j] = order_key(scale * acc[u][w]);
+        }
+    }
+}
 
-    // ---- per-row radix select + ballot compaction: warp w < kQB owns row w
-    const int warp = tid >> 5, lane = tid & 31;
-    if (warp >= kQB) return;
-    const int i = i0 + warp;
-    if (i >= a.N) return;
-    const uint32_t* kr = keys + warp * a.N;
-    uint32_t* hw = hist + warp * 256;
+// K2b: per query block, radix-select the k-th largest key (8-bit digits from the
+// top), then a ballot compaction in ascending index order takes every key above
+// it plus the lowest-index ties: topk_ascending semantics (router.hpp:96-108).
+constexpr int kRowsPerCta = 4;
+
+__global__ void __launch_bounds__(kRowsPerCta * 32) topk_kernel(const uint32_t* __restrict__ keys,
+                                                                SelectArgs a) {
+    extern __shared__ uint32_t smk[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int bh = blockIdx.y;
+    const int i = blockIdx.x * kRowsPerCta + warp;
     const int N = a.N;
+    uint32_t* kr = smk + warp * (N + 256);
+    uint32_t* hw = kr + N;
+    if (i >= N) return;
+    const uint32_t* src = keys + (size_t(bh) * N + i) * N;
+    for (int j = lane; j < N; j += 32) kr[j] = src[j];
+    __syncwarp();
 
     uint32_t prefix = 0, pmask = 0;
     int rem = a.k;  // rank (1-based) of the wanted element among prefix matches
@@ -110,9 +132,9 @@ __global__ void __launch_bounds__(kThreads) select_kernel(SelectArgs a) {
             }
         }
         const uint32_t owner = __ballot_sync(0xffffffffu, digit >= 0);
-        const int src = __ffs(owner) - 1;
-        digit = __shfl_sync(0xffffffffu, digit, src);
-        above = __shfl_sync(0xffffffffu, above, src);
+        const int src_lane = __ffs(owner) - 1;
+        digit = __shfl_sync(0xffffffffu, digit, src_lane);
+        above = __shfl_sync(0xffffffffu, above, src_lane);
         rem -= above;
         prefix |= uint32_t(digit) << shift;
         pmask |= 255u << shift;
@@ -138,8 +160,7 @@ __global__ void __launch_bounds__(kThreads) select_kernel(SelectArgs a) {
             if (tb) last_tie = j0 + 31 - __clz(tb);
             ties += __popc(eqb);
         }
-        diag_sel = __shfl_sync(0xffffffffu, diag_sel, i & 31) ;
-        // diag_sel was set by the lane whose j == i in the chunk holding i
+        diag_sel = __shfl_sync(0xffffffffu, diag_sel, i & 31);
         if (!diag_sel) {
             swap_out = last_tie;
             swap_in = true;
@@ -187,17 +208,18 @@ __global__ void plan_to_mask_kernel(const int32_t* __restrict__ selected, int N,
 
 }  // namespace
 
-cudaError_t launch_select(int D, const SelectArgs& a, int BH, cudaStream_t s) {
-    const size_t smem = sizeof(float) * (kQB * D + kKeyTile * (D + 1)) +
-                        sizeof(uint32_t) * (size_t(kQB) * a.N + kQB * 256);
-    dim3 grid((a.N + kQB - 1) / kQB, BH);
-    if (D == 128) {
-        cudaFuncSetAttribute(select_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-        select_kernel<128><<<grid, kThreads, smem, s>>>(a);
-    } else {
-        cudaFuncSetAttribute(select_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-        select_kernel<64><<<grid, kThreads, smem, s>>>(a);
-    }
+cudaError_t launch_select(int D, const SelectArgs& a, int BH, uint32_t* keys, cudaStream_t s) {
+    const int nt = (a.N + kTile - 1) / kTile;
+    dim3 g1(nt, nt, BH);
+    if (D == 128)
+        score_kernel<128><<<g1, 256, 0, s>>>(a.qbar, a.kbar, keys, a.N, a.scale);
+    else
+        score_kernel<64><<<g1, 256, 0, s>>>(a.qbar, a.kbar, keys, a.N, a.scale);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    const size_t smem = sizeof(uint32_t) * size_t(kRowsPerCta) * (a.N + 256);
+    cudaFuncSetAttribute(topk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    topk_kernel<<<dim3((a.N + kRowsPerCta - 1) / kRowsPerCta, BH), kRowsPerCta * 32, smem, s>>>(keys, a);
     return cudaGetLastError();
 }
 

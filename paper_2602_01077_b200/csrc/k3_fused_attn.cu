@@ -20,18 +20,22 @@
 //
 // Warp roles (256 threads, two CTAs per SM so one CTA's softmax overlaps the
 // other's MMAs):
-//   warp 0     TMA producer: Q once; K/V (or k_bar/v_hat) 64-row tiles into a
-//              2-stage ring; H_bar into the K ring at the end
+//   warp 0     TMA producer for Q (once), K / k_bar tiles (2-stage ring), H_bar
 //   warp 1     single-thread tcgen05.mma issuer: S_t = Q K_t^T (SS, K-major),
 //              O += P_{t-1} V_{t-1} (TS: P from TMEM, V MN-major), Q H_bar
 //   warp 2     TMEM allocator (256 columns: O | S0 | S1)
-//   warp 3     builds the union list from the two selection bitmasks
+//   warp 3     builds the union list from the two selection bitmasks, then is
+//              the TMA producer for V / v_hat tiles (2-stage ring)
 //   warps 4-7  softmax / correction / epilogue, one thread per query row
-//              (TMEM lane), exp2 with log2(e)*scale folded in, lazy rescale of O
-//              (only when the running max grows by > 2^8), P written back to
-//              TMEM as bf16 over the S columns it came from.
+//              (TMEM lane), exp2 with log2(e)*scale folded into one FFMA, lazy
+//              rescale of O (only when the running max grows by > 2^8), P
+//              written back to TMEM as bf16 over the S columns it came from.
 #include "kernels.h"
 #include "sm100.cuh"
+
+#ifndef PISA_TRACE
+#define PISA_TRACE 0
+#endif
 
 namespace pisa_b200 {
 using namespace pisa_sm100;
@@ -63,6 +67,40 @@ struct Bars {
     uint32_t n_union;
 };
 
+#if PISA_TRACE
+// Timeline of one CTA: trace[role][t] = clock64 delta from kernel start.
+__device__ __forceinline__ void trace_mark(const FusedArgs& a, int role, int t, long long t0) {
+    if (a.trace && blockIdx.x == a.trace_tile && blockIdx.y == 0 && t < 1024)
+        a.trace[role * 1024 + t] = (unsigned long long)(clock64() - t0);
+}
+#define TRACE(role, t) trace_mark(a, role, t, tstart)
+#else
+#define TRACE(role, t) ((void)0)
+#endif
+
+// Writes P (bf16 pairs) over the first 32 S columns and releases the S buffer.
+__device__ __forceinline__ void publish_p(uint32_t sc, const uint32_t (&pk)[32], uint64_t* bar,
+                                          int lane) {
+    tmem_st32(sc, pk);
+    tmem_st_wait();
+    tc_fence_before();
+    __syncwarp();
+    if (lane == 0) mbar_arrive(bar);
+}
+
+template <int D>
+__device__ __forceinline__ void rescale_o(uint32_t tmem_o, float f) {
+#pragma unroll 1
+    for (int cc = 0; cc < D; cc += 32) {
+        uint32_t ro[32];
+        tmem_ld32(tmem_o + cc, ro);
+        tmem_ld_wait(ro);
+#pragma unroll
+        for (int i = 0; i < 32; ++i) ro[i] = __float_as_uint(__uint_as_float(ro[i]) * f);
+        tmem_st32(tmem_o + cc, ro);
+    }
+}
+
 template <int D>
 __global__ void __launch_bounds__(kThreads, 2)
     fused_attn_kernel(const __grid_constant__ CUtensorMap tmQ,
@@ -79,6 +117,9 @@ __global__ void __launch_bounds__(kThreads, 2)
     uint32_t* maskA = reinterpret_cast<uint32_t*>(smem + Cfg::kOffMask);
     uint32_t* maskB = maskA + a.W;
     uint16_t* ulist = reinterpret_cast<uint16_t*>(maskB + a.W);
+#if PISA_TRACE
+    const long long tstart = clock64();
+#endif
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -154,7 +195,7 @@ __global__ void __launch_bounds__(kThreads, 2)
     const int T = U + (tail ? a.nchunk2 : 0);  // key tiles: union blocks, then centroid tiles
 
     if (warp == 0) {
-        // --------------------------------------------------------- producer --
+        // ------------------------------------------------ producer: Q, K, H --
         if (lane == 0) {
             uint8_t* sQ = smem + Cfg::kOffQ;
             mbar_expect_tx(&bar.q_full, Cfg::kQ);
@@ -163,32 +204,21 @@ __global__ void __launch_bounds__(kThreads, 2)
                 tma_load_4d(sQ + half * 16384, &tmQ, &bar.q_full, half * 64, tile * 128, h, b);
             for (int t = 0; t < T; ++t) {
                 const int s = t & 1;
-                const uint32_t ph = ((t >> 1) & 1) ^ 1;
                 uint8_t* sK = smem + Cfg::kOffK + s * Cfg::kKV;
-                uint8_t* sV = smem + Cfg::kOffV + s * Cfg::kKV;
-                mbar_wait(&bar.k_empty[s], ph);
+                mbar_wait(&bar.k_empty[s], ((t >> 1) & 1) ^ 1);
                 mbar_expect_tx(&bar.k_full[s], Cfg::kKV);
                 if (t < U) {
                     const int row = int(ulist[t] & 0x3FFFu) * 64;
 #pragma unroll
                     for (int half = 0; half < D / 64; ++half)
                         tma_load_4d(sK + half * 8192, &tmK, &bar.k_full[s], half * 64, row, h, b);
-                    mbar_wait(&bar.v_empty[s], ph);
-                    mbar_expect_tx(&bar.v_full[s], Cfg::kKV);
-#pragma unroll
-                    for (int half = 0; half < D / 64; ++half)
-                        tma_load_4d(sV + half * 8192, &tmV, &bar.v_full[s], half * 64, row, h, b);
                 } else {
                     const int row = (t - U) * 64;
 #pragma unroll
                     for (int half = 0; half < D / 64; ++half)
                         tma_load_3d(sK + half * 8192, &tmKb, &bar.k_full[s], half * 64, row, bh);
-                    mbar_wait(&bar.v_empty[s], ph);
-                    mbar_expect_tx(&bar.v_full[s], Cfg::kKV);
-#pragma unroll
-                    for (int half = 0; half < D / 64; ++half)
-                        tma_load_3d(sV + half * 8192, &tmVh, &bar.v_full[s], half * 64, row, bh);
                 }
+                TRACE(0, t);
             }
             if (first_order) {
                 // H_bar (D rows) into the K ring: half c lands in K stage c.
@@ -198,6 +228,28 @@ __global__ void __launch_bounds__(kThreads, 2)
 #pragma unroll
                 for (int half = 0; half < D / 64; ++half)
                     tma_load_3d(smem + Cfg::kOffK + half * Cfg::kKV, &tmH, &bar.h_full, half * 64, 0, bh);
+            }
+        }
+    } else if (warp == 3) {
+        // ----------------------------------------------------- producer: V --
+        if (lane == 0) {
+            for (int t = 0; t < T; ++t) {
+                const int s = t & 1;
+                uint8_t* sV = smem + Cfg::kOffV + s * Cfg::kKV;
+                mbar_wait(&bar.v_empty[s], ((t >> 1) & 1) ^ 1);
+                mbar_expect_tx(&bar.v_full[s], Cfg::kKV);
+                if (t < U) {
+                    const int row = int(ulist[t] & 0x3FFFu) * 64;
+#pragma unroll
+                    for (int half = 0; half < D / 64; ++half)
+                        tma_load_4d(sV + half * 8192, &tmV, &bar.v_full[s], half * 64, row, h, b);
+                } else {
+                    const int row = (t - U) * 64;
+#pragma unroll
+                    for (int half = 0; half < D / 64; ++half)
+                        tma_load_3d(sV + half * 8192, &tmVh, &bar.v_full[s], half * 64, row, bh);
+                }
+                TRACE(1, t);
             }
         }
     } else if (warp == 1) {
@@ -220,6 +272,7 @@ __global__ void __launch_bounds__(kThreads, 2)
                            sdesc_sw128(vb + ks * 2048, 8192, 1024), idPV, (u | ks) != 0);
                 mma_commit(&bar.v_empty[s]);
                 mma_commit(&bar.o_done);
+                TRACE(3, u);
             };
             mbar_wait(&bar.q_full, 0);
             for (int t = 0; t < T; ++t) {
@@ -236,6 +289,7 @@ __global__ void __launch_bounds__(kThreads, 2)
                 }
                 mma_commit(&bar.k_empty[s]);
                 mma_commit(&bar.s_full[s]);
+                TRACE(2, t);
                 if (t > 0) issue_pv(t - 1);
             }
             issue_pv(T - 1);
@@ -259,39 +313,50 @@ __global__ void __launch_bounds__(kThreads, 2)
         const int half = row >> 6;          // 0: block iA, 1: block iB (warp-uniform)
         const int grow = tile * 128 + row;  // query row within the sequence
         const bool active = grow < a.L;
+        const bool warp_active = __all_sync(0xffffffffu, active);
         const uint32_t* hmask = half ? maskB : maskA;
         const uint32_t lane_off = uint32_t(q4 * 32) << 16;
         const float sl2 = a.scale * 1.4426950408889634f;
 
         float m = -INFINITY, l = 0.f, lt = 0.f;
-        for (int t = 0; t < T; ++t) {
-            const int s = t & 1;
-            const uint32_t sc = tmem + lane_off + kColS + s * 64;
-            bool use;
-            int nvalid = 64;
-            uint32_t cm_lo = 0, cm_hi = 0;  // phase 2: masked columns
-            float w_last = 64.f;
-            int last_col = -1;
-            if (t < U) {
-                const uint32_t e = ulist[t];
-                use = ((e >> (14 + half)) & 1u) != 0;
-                if (int(e & 0x3FFFu) == a.N - 1) nvalid = n_last;
-            } else {
-                const int c = t - U;
-                use = true;
-                cm_lo = hmask[2 * c];
-                cm_hi = (2 * c + 1 < a.W) ? hmask[2 * c + 1] : 0xffffffffu;
-                const int jmax = a.N - c * 64;  // valid centroid columns in this tile
-                nvalid = jmax < 64 ? jmax : 64;
-                if (c * 64 <= a.N - 1 && a.N - 1 < c * 64 + 64) {
-                    last_col = a.N - 1 - c * 64;
-                    w_last = float(n_last);
+        // Online-softmax step shared by both phases. x: raw scores (masked = -inf).
+        // Returns the shift to exponentiate against; rescales O when needed.
+        auto update_max = [&](float bm_raw, int t) -> float {
+            const float bm = bm_raw * sl2;
+            float m_use = m;
+            bool resc = false;
+            if (bm > -INFINITY) {
+                if (m == -INFINITY) {
+                    m_use = bm;
+                } else if (bm > m + kRescaleThresh) {
+                    m_use = bm;
+                    resc = true;
                 }
             }
+            if (__any_sync(0xffffffffu, resc)) {
+                const float f = resc ? ex2(m - m_use) : 1.f;
+                mbar_wait(&bar.o_done, (t - 1) & 1);  // PV_{t-1} done (t >= 1 whenever resc)
+                tc_fence_after();
+                rescale_o<D>(tmem + lane_off + kColO, f);
+                l *= f;
+                lt *= f;
+            }
+            m = m_use;
+            return (m == -INFINITY) ? 0.f : m;  // all-masked row: p = 0, not NaN
+        };
+
+        // ---- Phase 1: exact blocks of the union
+        for (int t = 0; t < U; ++t) {
+            const int s = t & 1;
+            const uint32_t sc = tmem + lane_off + kColS + s * 64;
+            const uint32_t e = ulist[t];
+            const bool use = ((e >> (14 + half)) & 1u) != 0;  // warp-uniform
+            const int nvalid = (int(e & 0x3FFFu) == a.N - 1) ? n_last : 64;
             mbar_wait(&bar.s_full[s], (t >> 1) & 1);
             tc_fence_after();
+            TRACE(4 + (q4 >> 1), t);
             uint32_t pk[32];
-            if (use) {  // warp-uniform
+            if (use) {
                 uint32_t ra[32], rb[32];
                 tmem_ld32(sc, ra);
                 tmem_ld32(sc + 32, rb);
@@ -300,73 +365,85 @@ __global__ void __launch_bounds__(kThreads, 2)
                 float x[64];
 #pragma unroll
                 for (int i = 0; i < 32; ++i) {
-                    x[i] = __uint_as_float(ra[i]) * sl2;
-                    x[i + 32] = __uint_as_float(rb[i]) * sl2;
+                    x[i] = __uint_as_float(ra[i]);
+                    x[i + 32] = __uint_as_float(rb[i]);
                 }
-                // column validity
-                const uint64_t cmask = (uint64_t(cm_hi) << 32) | cm_lo;
-                float bm = -INFINITY;
+                if (!(warp_active && nvalid == 64)) {  // ragged last key block / rows past L
 #pragma unroll
-                for (int i = 0; i < 64; ++i) {
-                    const bool ok = active && i < nvalid && !((cmask >> i) & 1ull);
-                    x[i] = ok ? x[i] : -INFINITY;
-                    bm = fmaxf(bm, x[i]);
+                    for (int i = 0; i < 64; ++i) x[i] = (active && i < nvalid) ? x[i] : -INFINITY;
                 }
-                float m_use = m;
-                bool resc = false;
-                if (bm > -INFINITY) {
-                    if (m == -INFINITY) {
-                        m_use = bm;
-                    } else if (bm > m + kRescaleThresh) {
-                        m_use = bm;
-                        resc = true;
-                    }
-                }
-                if (__any_sync(0xffffffffu, resc)) {
-                    const float f = resc ? ex2(m - m_use) : 1.f;
-                    mbar_wait(&bar.o_done, (t - 1) & 1);  // t >= 1 whenever resc
-                    tc_fence_after();
-#pragma unroll 1
-                    for (int cc = 0; cc < D; cc += 32) {
-                        uint32_t ro[32];
-                        tmem_ld32(tmem + lane_off + kColO + cc, ro);
-                        tmem_ld_wait(ro);
+                float bm = x[0];
 #pragma unroll
-                        for (int i = 0; i < 32; ++i) ro[i] = __float_as_uint(__uint_as_float(ro[i]) * f);
-                        tmem_st32(tmem + lane_off + kColO + cc, ro);
-                    }
-                    l *= f;
-                    lt *= f;
-                }
-                m = m_use;
-                const float mm = (m == -INFINITY) ? 0.f : m;  // all-masked row: p = 0, not NaN
-                float ps = 0.f, pw = 0.f;
+                for (int i = 1; i < 64; ++i) bm = fmaxf(bm, x[i]);
+                const float mm = update_max(bm, t);
+                float ps0 = 0.f, ps1 = 0.f;
 #pragma unroll
                 for (int i = 0; i < 64; i += 2) {
-                    const float p0 = ex2(x[i] - mm);
-                    const float p1 = ex2(x[i + 1] - mm);
-                    ps += p0 + p1;
-                    if (t >= U) {
-                        pw += (i == last_col ? w_last : 64.f) * p0 +
-                              (i + 1 == last_col ? w_last : 64.f) * p1;
-                    }
+                    const float p0 = ex2(fmaf(x[i], sl2, -mm));
+                    const float p1 = ex2(fmaf(x[i + 1], sl2, -mm));
+                    ps0 += p0;
+                    ps1 += p1;
                     pk[i >> 1] = pack_bf16(p0, p1);
                 }
-                if (t < U) {
-                    l += ps;
-                } else {
-                    l += pw;
-                    lt += ps;
-                }
+                l += ps0 + ps1;
             } else {
 #pragma unroll
                 for (int i = 0; i < 32; ++i) pk[i] = 0u;
             }
-            tmem_st32(sc, pk);  // P (bf16 pairs) over the first 32 S columns
-            tmem_st_wait();
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&bar.p_full[s]);
+            publish_p(sc, pk, &bar.p_full[s], lane);
+            TRACE(6 + (q4 >> 1), t);
+        }
+        // ---- Phase 2: centroid tiles, column mask = own selection, weight n_j
+        for (int t = U; t < T; ++t) {
+            const int s = t & 1;
+            const uint32_t sc = tmem + lane_off + kColS + s * 64;
+            const int c = t - U;
+            const uint32_t cm_lo = hmask[2 * c];
+            const uint32_t cm_hi = (2 * c + 1 < a.W) ? hmask[2 * c + 1] : 0xffffffffu;
+            const int nvalid = min(64, a.N - c * 64);
+            const bool has_last = (c == a.nchunk2 - 1) && n_last != 64;
+            mbar_wait(&bar.s_full[s], (t >> 1) & 1);
+            tc_fence_after();
+            uint32_t ra[32], rb[32];
+            tmem_ld32(sc, ra);
+            tmem_ld32(sc + 32, rb);
+            tmem_ld_wait(ra);
+            tmem_ld_wait(rb);
+            float x[64];
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+                const bool ok_lo = active && i < nvalid && !((cm_lo >> i) & 1u);
+                const bool ok_hi = active && i + 32 < nvalid && !((cm_hi >> i) & 1u);
+                x[i] = ok_lo ? __uint_as_float(ra[i]) : -INFINITY;
+                x[i + 32] = ok_hi ? __uint_as_float(rb[i]) : -INFINITY;
+            }
+            float bm = x[0];
+#pragma unroll
+            for (int i = 1; i < 64; ++i) bm = fmaxf(bm, x[i]);
+            const float mm = update_max(bm, t);
+            uint32_t pk[32];
+            float ps0 = 0.f, ps1 = 0.f;
+#pragma unroll
+            for (int i = 0; i < 64; i += 2) {
+                const float p0 = ex2(fmaf(x[i], sl2, -mm));
+                const float p1 = ex2(fmaf(x[i + 1], sl2, -mm));
+                ps0 += p0;
+                ps1 += p1;
+                pk[i >> 1] = pack_bf16(p0, p1);
+            }
+            const float ps = ps0 + ps1;
+            float pw = 64.f * ps;
+            if (has_last) {  // the ragged last block weighs n_last, not 64
+                const int lc = a.N - 1 - c * 64;
+                float plast = 0.f;
+#pragma unroll
+                for (int i = 0; i < 64; ++i)
+                    if (i == lc) plast = ex2(fmaf(x[i], sl2, -mm));
+                pw += (float(n_last) - 64.f) * plast;
+            }
+            l += pw;
+            lt += ps;
+            publish_p(sc, pk, &bar.p_full[s], lane);
         }
 
         // ------------------------------------------------------- epilogue --

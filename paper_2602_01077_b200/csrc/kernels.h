@@ -48,7 +48,8 @@ struct SelectArgs {
     int N, W, k, force_diagonal;
     float scale;
 };
-cudaError_t launch_select(int D, const SelectArgs& a, int BH, cudaStream_t s);
+// keys: scratch uint32 [BH][N][N]
+cudaError_t launch_select(int D, const SelectArgs& a, int BH, uint32_t* keys, cudaStream_t s);
 
 // Plan (ascending lists) -> bitmask, with SelectionPlan::validate semantics
 // (router.hpp:50-70): sets *bad = 1 on out-of-range / non-ascending entries.
@@ -68,6 +69,8 @@ struct FusedArgs {
     int* nonfinite;  // device flag or null
     int L, N, H, W, nchunk2, variant, literal_phase3, out_f32, k;
     float scale;
+    unsigned long long* trace;  // PISA_TRACE builds only: [8][1024] clock deltas
+    int trace_tile;
 };
 cudaError_t launch_fused(int D, const CUtensorMap& tmQ, const CUtensorMap& tmK,
                          const CUtensorMap& tmV, const CUtensorMap& tmKb,

@@ -39,11 +39,13 @@ struct pisa_ctx {
     };
     std::vector<Rec> recs;
     std::vector<cudaEvent_t> pool;
+    unsigned long long* trace = nullptr;  // debug timeline (PISA_TRACE builds)
+    int trace_tile = 0;
 };
 
 namespace {
 
-const char* kKernelNames[] = {"block_stats_kernel", "hbar_reduce_kernel", "select_kernel",
+const char* kKernelNames[] = {"block_stats_kernel", "hbar_reduce_kernel", "select_kernels",
                               "fused_attn_kernel",  "plan_to_mask_kernel", "stats_to_bf16_kernel",
                               nullptr};
 enum KernelId { kK1 = 0, kK1b = 1, kK2 = 2, kK3 = 3, kPlan = 4, kToBf16 = 5 };
@@ -225,6 +227,7 @@ struct Work {
     __nv_bfloat16 *kbar_bf, *vhat_bf, *hbar_bf;
     int32_t* selected;
     uint32_t* mask;
+    uint32_t* keys;
     int* flag;
 };
 
@@ -243,7 +246,8 @@ pisa_status workspace(pisa_ctx* ctx, const Plan& p, Work* w) {
                  o_hbar = take(BH * D * D * 4), o_kglob = take(BH * D * 4),
                  o_kbf = take(BH * p.Npad * D * 2), o_vbf = take(BH * p.Npad * D * 2),
                  o_hbf = take(BH * D * D * 2), o_sel = take(BH * N * p.k * 4),
-                 o_mask = take(BH * N * p.W * 4), o_flag = take(16);
+                 o_mask = take(BH * N * p.W * 4), o_keys = take(BH * N * N * 4),
+                 o_flag = take(16);
     if (off > ctx->arena_bytes) {
         if (ctx->arena) cudaFree(ctx->arena);
         ctx->arena = nullptr;
@@ -264,6 +268,7 @@ pisa_status workspace(pisa_ctx* ctx, const Plan& p, Work* w) {
     w->hbar_bf = reinterpret_cast<__nv_bfloat16*>(b + o_hbf);
     w->selected = reinterpret_cast<int32_t*>(b + o_sel);
     w->mask = reinterpret_cast<uint32_t*>(b + o_mask);
+    w->keys = reinterpret_cast<uint32_t*>(b + o_keys);
     w->flag = reinterpret_cast<int*>(b + o_flag);
     return PISA_OK;
 }
@@ -291,13 +296,14 @@ pisa_status run_stats(pisa_ctx* ctx, const pisa_attn_desc& d, const Plan& p, con
 }
 
 pisa_status run_select(pisa_ctx* ctx, const pisa_attn_desc& d, const Plan& p, const float* qbar,
-                       const float* kbar, int32_t* selected, uint32_t* mask, cudaStream_t s) {
+                       const float* kbar, int32_t* selected, uint32_t* mask, uint32_t* keys,
+                       cudaStream_t s) {
     SelectArgs a{qbar, kbar, selected, mask, int(p.N), int(p.W), int(p.k), d.force_diagonal,
                  float(p.scale)};
     ProfScope ps(ctx, kK2, s);
-    const cudaError_t e = launch_select(int(p.D), a, int(p.BH), s);
+    const cudaError_t e = launch_select(int(p.D), a, int(p.BH), keys, s);
     if (e != cudaSuccess) return cuda_fail(ctx, e, "select launch");
-    ctx->launches += 1;
+    ctx->launches += 2;
     return PISA_OK;
 }
 
@@ -333,6 +339,8 @@ pisa_status run_fused(pisa_ctx* ctx, const pisa_attn_desc& d, const Plan& p, con
     a.out_f32 = d.out_dtype == PISA_DTYPE_F32;
     a.k = int(p.k);
     a.scale = float(p.scale);
+    a.trace = ctx->trace;
+    a.trace_tile = ctx->trace_tile;
     if (d.check_finite) {
         const cudaError_t e = cudaMemsetAsync(w.flag, 0, sizeof(int), s);
         if (e != cudaSuccess) return cuda_fail(ctx, e, "flag reset");
@@ -428,6 +436,13 @@ const char* pisa_b200_kernel_name(int i) {
     return kKernelNames[i];
 }
 
+pisa_status pisa_b200_debug_trace(pisa_ctx* c, unsigned long long* dev_buf, int tile) {
+    if (!c) return PISA_ERR_INVALID_DIMENSION;
+    c->trace = dev_buf;
+    c->trace_tile = tile;
+    return PISA_OK;
+}
+
 pisa_status pisa_b200_set_profiling(pisa_ctx* c, int enable) {
     if (!c) return PISA_ERR_INVALID_DIMENSION;
     c->prof = enable != 0;
@@ -491,7 +506,7 @@ pisa_status pisa_b200_fwd(pisa_ctx* ctx, const pisa_attn_desc* d, const void* q,
     if ((st = workspace(ctx, p, &w)) != PISA_OK) return st;
     if ((st = run_stats(ctx, *d, p, w, q, k, v, s)) != PISA_OK) return st;
     int32_t* sel = (diag && diag->selected) ? diag->selected : nullptr;
-    if ((st = run_select(ctx, *d, p, w.qbar, w.kbar, sel, w.mask, s)) != PISA_OK) return st;
+    if ((st = run_select(ctx, *d, p, w.qbar, w.kbar, sel, w.mask, w.keys, s)) != PISA_OK) return st;
     return run_fused(ctx, *d, p, w, q, k, v, o, diag, s);
 }
 
@@ -532,7 +547,7 @@ pisa_status pisa_b200_select(pisa_ctx* ctx, const pisa_attn_desc* d, const float
     const cudaStream_t s = static_cast<cudaStream_t>(stream);
     Work w;
     if ((st = workspace(ctx, p, &w)) != PISA_OK) return st;
-    return run_select(ctx, *d, p, q_bar, k_bar, selected, mask ? mask : w.mask, s);
+    return run_select(ctx, *d, p, q_bar, k_bar, selected, mask ? mask : w.mask, w.keys, s);
 }
 
 pisa_status pisa_b200_attention(pisa_ctx* ctx, const pisa_attn_desc* d, const void* q,

@@ -35,25 +35,34 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
                  "r"(bytes)
                  : "memory");
 }
+// try_wait with a suspend-time hint: the thread sleeps in hardware until the
+// phase completes or the hint expires, instead of spinning on the issue port.
 __device__ __forceinline__ bool mbar_try_wait(uint32_t addr, uint32_t parity) {
     uint32_t ok;
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
         "selp.u32 %0, 1, 0, p;\n\t}"
         : "=r"(ok)
-        : "r"(addr), "r"(parity)
+        : "r"(addr), "r"(parity), "r"(0x989680u)
         : "memory");
     return ok != 0;
 }
+__device__ __forceinline__ uint64_t global_ns() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
 // Blocks until the phase with the given parity has completed. With the
-// watchdog on, a wait that never completes traps instead of hanging the GPU.
+// watchdog on, a wait still pending after ~4 s traps instead of hanging the GPU
+// (the timer is only read on the slow path).
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     const uint32_t addr = smem_u32(bar);
+    if (mbar_try_wait(addr, parity)) return;
 #if PISA_WATCHDOG
-    uint32_t spins = 0;
+    const uint64_t t0 = global_ns();
     while (!mbar_try_wait(addr, parity)) {
-        if (++spins > (1u << 26)) __trap();
+        if (global_ns() - t0 > 4000000000ull) __trap();
     }
 #else
     while (!mbar_try_wait(addr, parity)) {
