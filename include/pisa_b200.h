@@ -128,9 +128,10 @@ pisa_status pisa_b200_fwd(pisa_ctx* ctx, const pisa_attn_desc* desc, const void*
 /* Same, with Q/K/V/O in (ideally pinned) HOST memory: the ctx stages heads through
  * device buffers on its own streams, overlapping H2D copy, compute and D2H copy.
  * Host layout must be dense [batch][heads][seq_len][d] (the reference bundle).
- * Synchronous: returns when O is in host memory. */
+ * `diag` (optional) holds HOST pointers with the pisa_diag layout.
+ * Synchronous: returns when O (and diag) are in host memory. */
 pisa_status pisa_b200_fwd_host(pisa_ctx* ctx, const pisa_attn_desc* desc, const void* q,
-                               const void* k, const void* v, void* o);
+                               const void* k, const void* v, void* o, const pisa_diag* diag);
 
 /* ---- the three steps, for parity against the reference's step functions ---- */
 /* Prepare (compute_block_stats + compute_global_stats(norms off) + query_block_means).

@@ -71,7 +71,7 @@ def load(build_if_missing: bool = False):
     L.pisa_b200_resolve.argtypes = [C.POINTER(AttnDesc), C.POINTER(i64), C.POINTER(i64),
                                     C.POINTER(C.c_double)]
     L.pisa_b200_fwd.argtypes = [vp, C.POINTER(AttnDesc), vp, vp, vp, vp, C.POINTER(Diag), vp]
-    L.pisa_b200_fwd_host.argtypes = [vp, C.POINTER(AttnDesc), vp, vp, vp, vp]
+    L.pisa_b200_fwd_host.argtypes = [vp, C.POINTER(AttnDesc), vp, vp, vp, vp, C.POINTER(Diag)]
     L.pisa_b200_block_stats.argtypes = [vp, C.POINTER(AttnDesc), vp, vp, vp, vp, vp, vp, vp, vp]
     L.pisa_b200_select.argtypes = [vp, C.POINTER(AttnDesc), vp, vp, vp, vp, vp]
     L.pisa_b200_attention.argtypes = [vp, C.POINTER(AttnDesc), vp, vp, vp, vp, vp, vp, vp, vp,

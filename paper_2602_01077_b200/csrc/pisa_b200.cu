@@ -589,7 +589,7 @@ pisa_status pisa_b200_attention(pisa_ctx* ctx, const pisa_attn_desc* d, const vo
 }
 
 pisa_status pisa_b200_fwd_host(pisa_ctx* ctx, const pisa_attn_desc* d, const void* q,
-                               const void* k, const void* v, void* o) {
+                               const void* k, const void* v, void* o, const pisa_diag* hdiag) {
     if (!ctx) return PISA_ERR_INVALID_DIMENSION;
     Plan p;
     pisa_status st = resolve(ctx, d, &p);
@@ -602,7 +602,9 @@ pisa_status pisa_b200_fwd_host(pisa_ctx* ctx, const pisa_attn_desc* d, const voi
     const size_t in_bytes = size_t(L) * D * 2;
     const size_t out_bytes = size_t(L) * D * (d->out_dtype == PISA_DTYPE_F32 ? 4 : 2);
     const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(BH, (BH + 7) / 8));
-    const size_t set_bytes = size_t(chunk) * (3 * in_bytes + out_bytes);
+    const bool want_diag = hdiag && (hdiag->row_max || hdiag->ell || hdiag->ell_tail || hdiag->selected);
+    const size_t diag_bytes = want_diag ? size_t(L) * 4 * 3 + size_t(p.N) * p.k * 4 : 0;
+    const size_t set_bytes = size_t(chunk) * (3 * in_bytes + out_bytes + diag_bytes);
     cudaError_t e = cudaSuccess;
     if (!ctx->st_h2d) {
         e = cudaStreamCreateWithFlags(&ctx->st_h2d, cudaStreamNonBlocking);
@@ -633,6 +635,14 @@ pisa_status pisa_b200_fwd_host(pisa_ctx* ctx, const pisa_attn_desc* d, const voi
         char* dk = dq + chunk * in_bytes;
         char* dv = dk + chunk * in_bytes;
         char* dout = dv + chunk * in_bytes;
+        char* ddiag = dout + chunk * out_bytes;
+        pisa_diag dd{};
+        if (want_diag) {
+            dd.row_max = reinterpret_cast<float*>(ddiag);
+            dd.ell = dd.row_max + chunk * L;
+            dd.ell_tail = dd.ell + chunk * L;
+            dd.selected = reinterpret_cast<int32_t*>(dd.ell_tail + chunk * L);
+        }
         if (c >= 2) cudaStreamWaitEvent(ctx->st_h2d, ctx->ev_comp[sidx], 0);
         e = cudaMemcpyAsync(dq, static_cast<const char*>(q) + h0 * in_bytes, hc * in_bytes, cudaMemcpyHostToDevice, ctx->st_h2d);
         if (e == cudaSuccess) e = cudaMemcpyAsync(dk, static_cast<const char*>(k) + h0 * in_bytes, hc * in_bytes, cudaMemcpyHostToDevice, ctx->st_h2d);
@@ -655,12 +665,24 @@ pisa_status pisa_b200_fwd_host(pisa_ctx* ctx, const pisa_attn_desc* d, const voi
         dc.o_strides[1] = ld;
         dc.o_strides[2] = D;
         dc.check_finite = 0;
-        st = pisa_b200_fwd(ctx, &dc, dq, dk, dv, dout, nullptr, ctx->st_comp);
+        st = pisa_b200_fwd(ctx, &dc, dq, dk, dv, dout, want_diag ? &dd : nullptr, ctx->st_comp);
         if (st != PISA_OK) return st;
         launches += ctx->launches;
         cudaEventRecord(ctx->ev_comp[sidx], ctx->st_comp);
         cudaStreamWaitEvent(ctx->st_d2h, ctx->ev_comp[sidx], 0);
         e = cudaMemcpyAsync(static_cast<char*>(o) + h0 * out_bytes, dout, hc * out_bytes, cudaMemcpyDeviceToHost, ctx->st_d2h);
+        if (want_diag && e == cudaSuccess) {
+            const size_t rb = size_t(hc) * L * 4;
+            if (hdiag->row_max && e == cudaSuccess)
+                e = cudaMemcpyAsync(hdiag->row_max + h0 * L, dd.row_max, rb, cudaMemcpyDeviceToHost, ctx->st_d2h);
+            if (hdiag->ell && e == cudaSuccess)
+                e = cudaMemcpyAsync(hdiag->ell + h0 * L, dd.ell, rb, cudaMemcpyDeviceToHost, ctx->st_d2h);
+            if (hdiag->ell_tail && e == cudaSuccess)
+                e = cudaMemcpyAsync(hdiag->ell_tail + h0 * L, dd.ell_tail, rb, cudaMemcpyDeviceToHost, ctx->st_d2h);
+            if (hdiag->selected && e == cudaSuccess)
+                e = cudaMemcpyAsync(hdiag->selected + h0 * p.N * p.k, dd.selected,
+                                    size_t(hc) * p.N * p.k * 4, cudaMemcpyDeviceToHost, ctx->st_d2h);
+        }
         if (e == cudaSuccess) e = cudaEventRecord(ctx->ev_d2h[sidx], ctx->st_d2h);
         if (e != cudaSuccess) return cuda_fail(ctx, e, "D2H");
     }

@@ -374,7 +374,7 @@ def fwd_host(q, k, v, out, ctx: Optional[Context] = None, device: int = 0, **kw)
     ctx = ctx or Context.get(device)
     desc = make_desc(q, k, v, out, layout="bhld", **kw)
     st = ctx.lib.pisa_b200_fwd_host(ctx.handle, C.byref(desc), _ptr(q), _ptr(k), _ptr(v),
-                                    _ptr(out))
+                                    _ptr(out), None)
     _raise(st, ctx.handle)
     return out
 

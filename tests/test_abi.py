@@ -126,3 +126,15 @@ def test_no_cpu_fallback_in_product():
                     src = fh.read()
                 assert "import oracle" not in src and "liboracle" not in src, f
                 assert "pisa_oracle" not in src, f
+
+
+def test_cpp_shim_header_compiles(tmp_path):
+    """include/pisa_b200.hpp + a reference-style caller build with plain g++."""
+    import subprocess
+    obj = tmp_path / "shim.o"
+    subprocess.run(["g++", "-std=c++17", "-fsyntax-only", "-Wall", "-Werror", "-I",
+                    os.path.join(ROOT, "include"), os.path.join(ROOT, "tests", "cpp", "shim_demo.cpp")],
+                   check=True)
+    subprocess.run(["gcc", "-std=c99", "-fsyntax-only", "-Wall", "-Werror", "-x", "c",
+                    os.path.join(ROOT, "include", "pisa_b200.h")], check=True)
+    del obj

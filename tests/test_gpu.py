@@ -336,3 +336,36 @@ def test_full_size_head_parity(P, oracle_mod, name, L, r):
     assert np.array_equal(out, out2)
     assert np.isfinite(out).all()
     torch.cuda.empty_cache()
+
+
+def test_cpp_shim_drop_in(P, oracle_mod, tmp_path):
+    """A reference-style C++ caller (tests/cpp/shim_demo.cpp) compiled against
+    include/pisa_b200.hpp and linked to the C ABI library."""
+    import subprocess
+    O = oracle_mod
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    exe = tmp_path / "shim_demo"
+    subprocess.run(["g++", "-std=c++17", "-O2", "-I", os.path.join(root, "include"),
+                    os.path.join(root, "tests", "cpp", "shim_demo.cpp"),
+                    "-L", os.path.join(root, "paper_2602_01077_b200", "lib"), "-lpisa_b200",
+                    "-Wl,-rpath," + os.path.join(root, "paper_2602_01077_b200", "lib"),
+                    "-o", str(exe)], check=True)
+    H, L, d, r = 2, 1000, 128, 0.75
+    q, k, v = O.gen("clustered", 9, H, L, d)
+    inp = tmp_path / "in.bin"
+    with open(inp, "wb") as f:
+        for x in (q, k, v):
+            f.write(np.ascontiguousarray(x, np.float32).tobytes())
+    out_p, plan_p = tmp_path / "out.bin", tmp_path / "plan.bin"
+    res = subprocess.run([str(exe), str(inp), str(out_p), str(plan_p), str(H), str(L), str(d), str(r)],
+                         capture_output=True, text=True, timeout=300)
+    assert res.returncode == 0, res.stderr
+    assert "BlockDivisibility ok" in res.stdout
+    out = np.fromfile(out_p, np.float32).reshape(H, L, d)
+    N = 16
+    kk = int(res.stdout.split()[0])
+    plan = np.fromfile(plan_p, np.int32).reshape(H, N, kk)
+    ref = O.multihead(q, k, v, r=r)
+    assert np.array_equal(plan, ref["selected"])
+    for h in range(H):
+        check_close(out[h], ref["out"][h])
