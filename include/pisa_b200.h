@@ -167,7 +167,7 @@ const char* pisa_b200_kernel_name(int i);
  * (ids as pisa_b200_kernel_name; arrays of length 8), and clears the record. */
 pisa_status pisa_b200_set_profiling(pisa_ctx* ctx, int enable);
 /* Debug timeline of one fused-kernel CTA (tile index `tile`, head 0): only
- * libraries built with -DPISA_TRACE=1 write it. dev_buf: 8*1024 u64 (device). */
+ * libraries built with -DPISA_TRACE=1 write it. dev_buf: 16*1024 u64 (device). */
 pisa_status pisa_b200_debug_trace(pisa_ctx* ctx, unsigned long long* dev_buf, int tile);
 pisa_status pisa_b200_read_profile(pisa_ctx* ctx, double* ms, int64_t* launches);
 

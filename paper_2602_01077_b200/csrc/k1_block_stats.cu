@@ -80,13 +80,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t tmem = *tmem_slot;
 
     if (warp == 0) {
-        if (lane == 0) {
-            for (int jl = 0; jl < nb; ++jl) {
-                const int s = jl % kStages;
-                mbar_wait(&empty[s], ((jl / kStages) & 1) ^ 1);
-                uint8_t* st = ring + s * Cfg::kStage;
+        for (int jl = 0; jl < nb; ++jl) {
+            const int s = jl % kStages;
+            mbar_wait(&empty[s], ((jl / kStages) & 1) ^ 1);
+            uint8_t* st = ring + s * Cfg::kStage;
+            const int row = (j0 + jl) * 64;
+            if (elect_one()) {
                 mbar_expect_tx(&full[s], Cfg::kStage);
-                const int row = (j0 + jl) * 64;
 #pragma unroll
                 for (int half = 0; half < D / 64; ++half) {
                     tma_load_4d(st + half * 8192, &tmK, &full[s], half * 64, row, h, b);
@@ -94,19 +94,20 @@ __global__ void __launch_bounds__(kThreads, 1)
                     tma_load_4d(st + 2 * Cfg::kTile + half * 8192, &tmQ, &full[s], half * 64, row, h, b);
                 }
             }
+            __syncwarp();
         }
     } else if (warp == 1) {
-        if (lane == 0) {
-            // M = 128: for D = 128 the two MN chunks are K's column halves; for D = 64
-            // the second chunk is the V tile right behind K (rows 64..127 of the
-            // product are V^T V and are ignored). N = D.
-            constexpr uint32_t idesc = idesc_bf16(128, D, 1, 1);
-            for (int jl = 0; jl < nb; ++jl) {
-                const int s = jl % kStages;
-                mbar_wait(&full[s], (jl / kStages) & 1);
-                tc_fence_after();
-                const uint32_t kbase = smem_u32(ring + s * Cfg::kStage);
-                const uint32_t vbase = kbase + Cfg::kTile;
+        // M = 128: for D = 128 the two MN chunks are K's column halves; for D = 64
+        // the second chunk is the V tile right behind K (rows 64..127 of the
+        // product are V^T V and are ignored). N = D.
+        constexpr uint32_t idesc = idesc_bf16(128, D, 1, 1);
+        for (int jl = 0; jl < nb; ++jl) {
+            const int s = jl % kStages;
+            mbar_wait(&full[s], (jl / kStages) & 1);
+            tc_fence_after();
+            const uint32_t kbase = smem_u32(ring + s * Cfg::kStage);
+            const uint32_t vbase = kbase + Cfg::kTile;
+            if (elect_one()) {
 #pragma unroll
                 for (int ks = 0; ks < 4; ++ks) {
                     const uint64_t ad = sdesc_sw128(kbase + ks * 2048, 8192, 1024);
@@ -115,8 +116,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
                 mma_commit(&empty[s]);
             }
-            mma_commit(done);
+            __syncwarp();
         }
+        if (elect_one()) mma_commit(done);
+        __syncwarp();
     } else {
         // Column warps: column c == TMEM lane this thread reads in the epilogue.
         const int q = warp & 3;

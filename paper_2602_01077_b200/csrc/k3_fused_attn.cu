@@ -23,9 +23,12 @@
 //   warp 0     TMA producer for Q (once), K / k_bar tiles (2-stage ring), H_bar
 //   warp 1     single-thread tcgen05.mma issuer: S_t = Q K_t^T (SS, K-major),
 //              O += P_{t-1} V_{t-1} (TS: P from TMEM, V MN-major), Q H_bar
-//   warp 2     TMEM allocator (256 columns: O | S0 | S1)
+//   warp 2     TMEM allocator (256 columns: O | S0 | S1), then TMA producer for
+//              the second 64-column half of every V / v_hat tile
 //   warp 3     builds the union list from the two selection bitmasks, then is
-//              the TMA producer for V / v_hat tiles (2-stage ring)
+//              the TMA producer for the first half of every V / v_hat tile
+//              (a TMA issue stream runs at ~32 B/clk, so two streams halve the
+//              latency of the V loads on the critical path; tools/tma_bw.cu)
 //   warps 4-7  softmax / correction / epilogue, one thread per query row
 //              (TMEM lane), exp2 with log2(e)*scale folded into one FFMA, lazy
 //              rescale of O (only when the running max grows by > 2^8), P
@@ -44,6 +47,7 @@ namespace {
 
 constexpr int kThreads = 256;
 constexpr float kRescaleThresh = 8.0f;  // log2 units
+constexpr int kPolyEvery = 4;           // 1 in 4 softmax exponentials via ex2_poly (FMA pipe)
 constexpr uint32_t kColO = 0, kColS = 128;
 
 template <int D>
@@ -140,7 +144,7 @@ __global__ void __launch_bounds__(kThreads, 2)
         for (int s = 0; s < 2; ++s) {
             mbar_init(&bar.k_full[s], 1);
             mbar_init(&bar.k_empty[s], 1);
-            mbar_init(&bar.v_full[s], 1);
+            mbar_init(&bar.v_full[s], D / 64);  // one arrive per V producer (one per 64-col half)
             mbar_init(&bar.v_empty[s], 1);
             mbar_init(&bar.s_full[s], 1);
             mbar_init(&bar.p_full[s], 4);
@@ -196,76 +200,83 @@ __global__ void __launch_bounds__(kThreads, 2)
 
     if (warp == 0) {
         // ------------------------------------------------ producer: Q, K, H --
-        if (lane == 0) {
-            uint8_t* sQ = smem + Cfg::kOffQ;
+        uint8_t* sQ = smem + Cfg::kOffQ;
+        if (elect_one()) {
             mbar_expect_tx(&bar.q_full, Cfg::kQ);
 #pragma unroll
             for (int half = 0; half < D / 64; ++half)
                 tma_load_4d(sQ + half * 16384, &tmQ, &bar.q_full, half * 64, tile * 128, h, b);
-            for (int t = 0; t < T; ++t) {
-                const int s = t & 1;
-                uint8_t* sK = smem + Cfg::kOffK + s * Cfg::kKV;
-                mbar_wait(&bar.k_empty[s], ((t >> 1) & 1) ^ 1);
+        }
+        __syncwarp();
+        for (int t = 0; t < T; ++t) {
+            const int s = t & 1;
+            uint8_t* sK = smem + Cfg::kOffK + s * Cfg::kKV;
+            mbar_wait(&bar.k_empty[s], ((t >> 1) & 1) ^ 1);
+            const bool exact = t < U;
+            const int row = exact ? int(ulist[t] & 0x3FFFu) * 64 : (t - U) * 64;
+            if (elect_one()) {
                 mbar_expect_tx(&bar.k_full[s], Cfg::kKV);
-                if (t < U) {
-                    const int row = int(ulist[t] & 0x3FFFu) * 64;
 #pragma unroll
-                    for (int half = 0; half < D / 64; ++half)
+                for (int half = 0; half < D / 64; ++half) {
+                    if (exact)
                         tma_load_4d(sK + half * 8192, &tmK, &bar.k_full[s], half * 64, row, h, b);
-                } else {
-                    const int row = (t - U) * 64;
-#pragma unroll
-                    for (int half = 0; half < D / 64; ++half)
+                    else
                         tma_load_3d(sK + half * 8192, &tmKb, &bar.k_full[s], half * 64, row, bh);
                 }
                 TRACE(0, t);
             }
-            if (first_order) {
-                // H_bar (D rows) into the K ring: half c lands in K stage c.
-                for (int t = T; t < T + 2; ++t)
-                    mbar_wait(&bar.k_empty[t & 1], ((t >> 1) & 1) ^ 1);
+            __syncwarp();
+        }
+        if (first_order) {
+            // H_bar (D rows) into the K ring: half c lands in K stage c.
+            for (int t = T; t < T + 2; ++t) mbar_wait(&bar.k_empty[t & 1], ((t >> 1) & 1) ^ 1);
+            if (elect_one()) {
                 mbar_expect_tx(&bar.h_full, D * D * 2);
 #pragma unroll
                 for (int half = 0; half < D / 64; ++half)
                     tma_load_3d(smem + Cfg::kOffK + half * Cfg::kKV, &tmH, &bar.h_full, half * 64, 0, bh);
             }
+            __syncwarp();
         }
-    } else if (warp == 3) {
-        // ----------------------------------------------------- producer: V --
-        if (lane == 0) {
-            for (int t = 0; t < T; ++t) {
-                const int s = t & 1;
-                uint8_t* sV = smem + Cfg::kOffV + s * Cfg::kKV;
-                mbar_wait(&bar.v_empty[s], ((t >> 1) & 1) ^ 1);
-                mbar_expect_tx(&bar.v_full[s], Cfg::kKV);
-                if (t < U) {
-                    const int row = int(ulist[t] & 0x3FFFu) * 64;
-#pragma unroll
-                    for (int half = 0; half < D / 64; ++half)
-                        tma_load_4d(sV + half * 8192, &tmV, &bar.v_full[s], half * 64, row, h, b);
-                } else {
-                    const int row = (t - U) * 64;
-#pragma unroll
-                    for (int half = 0; half < D / 64; ++half)
-                        tma_load_3d(sV + half * 8192, &tmVh, &bar.v_full[s], half * 64, row, bh);
-                }
-                TRACE(1, t);
+    } else if (warp == 3 || (warp == 2 && D == 128)) {
+        // -------------------------------------------- producers: V halves --
+        // Each 64-column half of a V tile has its own issuing warp (two TMA
+        // issue streams; V is on the critical path: V_t can only load once
+        // PV_{t-2} has retired).
+        const int vh = (warp == 3) ? 0 : 1;
+        for (int t = 0; t < T; ++t) {
+            const int s = t & 1;
+            uint8_t* sV = smem + Cfg::kOffV + s * Cfg::kKV + vh * 8192;
+            mbar_wait(&bar.v_empty[s], ((t >> 1) & 1) ^ 1);
+            const bool exact = t < U;
+            const int row = exact ? int(ulist[t] & 0x3FFFu) * 64 : (t - U) * 64;
+            if (elect_one()) {
+                mbar_expect_tx(&bar.v_full[s], 8192);
+                if (exact)
+                    tma_load_4d(sV, &tmV, &bar.v_full[s], vh * 64, row, h, b);
+                else
+                    tma_load_3d(sV, &tmVh, &bar.v_full[s], vh * 64, row, bh);
+                if (vh == 0) TRACE(1, t);
             }
+            __syncwarp();
         }
     } else if (warp == 1) {
         // ------------------------------------------------------------- MMA --
-        if (lane == 0) {
-            constexpr uint32_t idS = idesc_bf16(128, 64, 0, 0);   // S = Q K^T
-            constexpr uint32_t idPV = idesc_bf16(128, D, 0, 1);   // O += P V (V MN-major)
-            constexpr uint32_t idQH = idesc_bf16(128, D, 0, 1);   // Q H_bar
-            const uint32_t qbase = smem_u32(smem + Cfg::kOffQ);
-            auto issue_pv = [&](int u) {
-                const int s = u & 1;
-                const uint32_t ph = (u >> 1) & 1;
-                mbar_wait(&bar.p_full[s], ph);
-                mbar_wait(&bar.v_full[s], ph);
-                tc_fence_after();
-                const uint32_t vb = smem_u32(smem + Cfg::kOffV + s * Cfg::kKV);
+        // Whole-warp loop, one elected lane issues (and commits: a commit
+        // tracks the MMAs of the thread that executes it).
+        constexpr uint32_t idS = idesc_bf16(128, 64, 0, 0);   // S = Q K^T
+        constexpr uint32_t idPV = idesc_bf16(128, D, 0, 1);   // O += P V (V MN-major)
+        constexpr uint32_t idQH = idesc_bf16(128, D, 0, 1);   // Q H_bar
+        const uint32_t qbase = smem_u32(smem + Cfg::kOffQ);
+        auto issue_pv = [&](int u) {
+            const int s = u & 1;
+            const uint32_t ph = (u >> 1) & 1;
+            mbar_wait(&bar.p_full[s], ph);
+            mbar_wait(&bar.v_full[s], ph);
+            tc_fence_after();
+            const uint32_t vb = smem_u32(smem + Cfg::kOffV + s * Cfg::kKV);
+            if (elect_one()) {
+                TRACE(10, u);
 #pragma unroll
                 for (int ks = 0; ks < 4; ++ks)
                     mma_ts(tmem + kColO, tmem + kColS + s * 64 + ks * 8,
@@ -273,13 +284,17 @@ __global__ void __launch_bounds__(kThreads, 2)
                 mma_commit(&bar.v_empty[s]);
                 mma_commit(&bar.o_done);
                 TRACE(3, u);
-            };
-            mbar_wait(&bar.q_full, 0);
-            for (int t = 0; t < T; ++t) {
-                const int s = t & 1;
-                mbar_wait(&bar.k_full[s], (t >> 1) & 1);
-                tc_fence_after();
-                const uint32_t kb = smem_u32(smem + Cfg::kOffK + s * Cfg::kKV);
+            }
+            __syncwarp();
+        };
+        mbar_wait(&bar.q_full, 0);
+        for (int t = 0; t < T; ++t) {
+            const int s = t & 1;
+            mbar_wait(&bar.k_full[s], (t >> 1) & 1);
+            tc_fence_after();
+            const uint32_t kb = smem_u32(smem + Cfg::kOffK + s * Cfg::kKV);
+            if (elect_one()) {
+                TRACE(8, t);
 #pragma unroll
                 for (int ks = 0; ks < D / 16; ++ks) {
                     const uint32_t hq = (ks >> 2), kq = (ks & 3) * 32;
@@ -290,13 +305,18 @@ __global__ void __launch_bounds__(kThreads, 2)
                 mma_commit(&bar.k_empty[s]);
                 mma_commit(&bar.s_full[s]);
                 TRACE(2, t);
-                if (t > 0) issue_pv(t - 1);
             }
-            issue_pv(T - 1);
+            __syncwarp();
+            if (t > 0) issue_pv(t - 1);
+        }
+        issue_pv(T - 1);
+        if (first_order) {
+            mbar_wait(&bar.h_full, 0);
+            tc_fence_after();
+        }
+        const uint32_t hb = smem_u32(smem + Cfg::kOffK);
+        if (elect_one()) {
             if (first_order) {
-                mbar_wait(&bar.h_full, 0);
-                tc_fence_after();
-                const uint32_t hb = smem_u32(smem + Cfg::kOffK);
 #pragma unroll
                 for (int ks = 0; ks < D / 16; ++ks) {
                     const uint32_t hq = (ks >> 2), kq = (ks & 3) * 32;
@@ -306,6 +326,7 @@ __global__ void __launch_bounds__(kThreads, 2)
             }
             mma_commit(&bar.qh_full);  // also: every PV done
         }
+        __syncwarp();
     } else if (warp >= 4) {
         // ------------------------------------------------ softmax warpgroup --
         const int q4 = warp & 3;            // TMEM lane quadrant
@@ -368,7 +389,8 @@ __global__ void __launch_bounds__(kThreads, 2)
                     x[i] = __uint_as_float(ra[i]);
                     x[i + 32] = __uint_as_float(rb[i]);
                 }
-                if (!(warp_active && nvalid == 64)) {  // ragged last key block / rows past L
+                const bool full_tile = warp_active && nvalid == 64;
+                if (!full_tile) {  // ragged last key block / rows past L
 #pragma unroll
                     for (int i = 0; i < 64; ++i) x[i] = (active && i < nvalid) ? x[i] : -INFINITY;
                 }
@@ -376,16 +398,27 @@ __global__ void __launch_bounds__(kThreads, 2)
 #pragma unroll
                 for (int i = 1; i < 64; ++i) bm = fmaxf(bm, x[i]);
                 const float mm = update_max(bm, t);
-                float ps0 = 0.f, ps1 = 0.f;
+                float ps[4] = {0.f, 0.f, 0.f, 0.f};
+                if (full_tile) {
+                    // every kPolyEvery-th exponential on the FMA pipe, the rest on MUFU
 #pragma unroll
-                for (int i = 0; i < 64; i += 2) {
-                    const float p0 = ex2(fmaf(x[i], sl2, -mm));
-                    const float p1 = ex2(fmaf(x[i + 1], sl2, -mm));
-                    ps0 += p0;
-                    ps1 += p1;
-                    pk[i >> 1] = pack_bf16(p0, p1);
+                    for (int i = 0; i < 64; i += 2) {
+                        const float a0 = fmaf(x[i], sl2, -mm), a1 = fmaf(x[i + 1], sl2, -mm);
+                        const float p0 = (i % kPolyEvery == kPolyEvery - 1) ? ex2_poly(a0) : ex2(a0);
+                        const float p1 = ((i + 1) % kPolyEvery == kPolyEvery - 1) ? ex2_poly(a1) : ex2(a1);
+                        ps[(i >> 1) & 3] += p0 + p1;
+                        pk[i >> 1] = pack_bf16(p0, p1);
+                    }
+                } else {
+#pragma unroll
+                    for (int i = 0; i < 64; i += 2) {
+                        const float p0 = ex2(fmaf(x[i], sl2, -mm));
+                        const float p1 = ex2(fmaf(x[i + 1], sl2, -mm));
+                        ps[(i >> 1) & 3] += p0 + p1;
+                        pk[i >> 1] = pack_bf16(p0, p1);
+                    }
                 }
-                l += ps0 + ps1;
+                l += (ps[0] + ps[1]) + (ps[2] + ps[3]);
             } else {
 #pragma unroll
                 for (int i = 0; i < 32; ++i) pk[i] = 0u;

@@ -227,9 +227,35 @@ __device__ __forceinline__ float ex2(float x) {
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
     return y;
 }
+// 2^x on the FMA/ALU pipes (for finite x): round-to-nearest split x = r + f,
+// f in [-1/2, 1/2], near-minimax cubic for 2^f (max rel err 7.8e-5, far below
+// the bf16 rounding of P), exponent added in the integer domain. Used for a
+// fraction of the softmax exponentials so MUFU and FMA share the work (FA4).
+__device__ __forceinline__ float ex2_poly(float x) {
+    x = fmaxf(x, -126.0f);
+    const float t = x + 12582912.0f;  // 1.5 * 2^23: integer part in the low mantissa bits
+    const float r = t - 12582912.0f;
+    const float f = x - r;
+    float p = fmaf(0.05508868380751114f, f, 0.24260405145947936f);
+    p = fmaf(p, f, 0.6932762416819607f);
+    p = fmaf(p, f, 0.9999289403695112f);
+    return __int_as_float(__float_as_int(p) + ((__float_as_int(t) - 0x4B400000) << 23));
+}
 __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
     __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
     return *reinterpret_cast<uint32_t*>(&v);
+}
+// One lane of a converged warp (the same lane every call). Issue loops run on
+// the WHOLE warp with warp-uniform values and issue tcgen05 / TMA under
+// elect_one(): a loop run by lane 0 alone makes the compiler wrap every
+// UTCHMMA in an R2UR-broadcast / ELECT sequence (~215 cycles per MMA instead
+// of ~48, tools/mma_rate.cu).
+__device__ __forceinline__ bool elect_one() {
+    uint32_t pred;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\telect.sync _|p, 0xffffffff;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(pred));
+    return pred != 0;
 }
 __device__ __forceinline__ uint32_t lane_id() {
     uint32_t l;

@@ -13,7 +13,7 @@ import ctypes as C  # noqa: E402
 import paper_2602_01077_b200 as P  # noqa: E402
 
 ROLES = ["K issued", "V issued", "S issued", "PV issued", "smA got S", "smB got S",
-         "smA P done", "smB P done"]
+         "smA P done", "smB P done", "mma K rdy", "mma P rdy", "mma V rdy", "mma wait K"]
 
 
 def main():
@@ -22,17 +22,17 @@ def main():
     dev = torch.device("cuda", 0)
     q, k, v = (torch.randn((1, H, L, d), device=dev, dtype=torch.bfloat16) for _ in range(3))
     ctx = P.Context.get(0)
-    buf = torch.zeros(8 * 1024, dtype=torch.int64, device=dev)
+    buf = torch.zeros(16 * 1024, dtype=torch.int64, device=dev)
     for _ in range(2):
         P.fwd(q, k, v, sparsity=0.875)
     ctx.lib.pisa_b200_debug_trace(ctx.handle, C.c_void_p(buf.data_ptr()), tile)
     P.fwd(q, k, v, sparsity=0.875)
     torch.cuda.synchronize()
-    tr = buf.view(8, 1024).cpu().tolist()
+    tr = buf.view(16, 1024).cpu().tolist()
     n = max(i for i in range(1024) if tr[2][i] or i == 0) + 1
     print("t  " + " ".join(f"{r:>11s}" for r in ROLES))
     for t in range(n):
-        print(f"{t:3d} " + " ".join(f"{tr[r][t]:11d}" for r in range(8)))
+        print(f"{t:3d} " + " ".join(f"{tr[r][t]:11d}" for r in range(len(ROLES))))
     # per-tile deltas in steady state
     ds = [tr[2][t + 1] - tr[2][t] for t in range(20, n - 30)]
     print("median S-issue period (cycles):", sorted(ds)[len(ds) // 2] if ds else None)
