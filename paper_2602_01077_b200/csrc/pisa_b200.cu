@@ -212,7 +212,7 @@ pisa_status resolve(pisa_ctx* ctx, const pisa_attn_desc* d, Plan* p) {
     p->L = d->seq_len;
     p->D = D;
     p->N = N;
-    p->Npad = (N + 63) / 64 * 64;
+    p->Npad = (N + 127) / 128 * 128;  // K3 reads 128-centroid tiles
     p->W = (N + 31) / 32;
     p->k = k;
     p->nchunk1 = (N + kStatsG - 1) / kStatsG;

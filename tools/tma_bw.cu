@@ -74,6 +74,37 @@ __global__ void __launch_bounds__(32) gather_lanes(const __grid_constant__ CUten
     }
 }
 
+__global__ void __launch_bounds__(512) gather_sweep(const __grid_constant__ CUtensorMap tm, int nblocks,
+                                                   int stages, int iters, int nl, unsigned long long* lat) {
+    extern __shared__ uint8_t raw[];
+    uint8_t* smem0 = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(raw) + 1023) & ~uintptr_t(1023));
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    if (l >= nl) return;
+    const int id = w * nl + l;
+    uint8_t* smem = smem0 + id * (stages * 16384);
+    __shared__ uint64_t fulls[64 * 4];
+    uint64_t* full = fulls + id * 4;
+    for (int s = 0; s < stages; ++s) mbar_init(&full[s], 1);
+    fence_mbar_init();
+    uint32_t h = (blockIdx.x * 64 + id) * 2654435761u + 12345u;
+    long long tsum = 0, t_issue[4] = {0, 0, 0, 0};
+    for (int i = 0; i < iters + stages; ++i) {
+        const int s = i % stages;
+        if (i >= stages) {
+            mbar_wait(&full[s], ((i / stages) - 1) & 1);
+            tsum += clock64() - t_issue[s];
+        }
+        if (i >= iters) continue;
+        h = h * 1664525u + 1013904223u;
+        const int blk = int((h >> 8) % uint32_t(nblocks));
+        mbar_expect_tx(&full[s], 16384);
+        t_issue[s] = clock64();
+        tma_load_3d(smem + s * 16384, &tm, &full[s], 0, blk * 64, 0);
+        tma_load_3d(smem + s * 16384 + 8192, &tm, &full[s], 64, blk * 64, 0);
+    }
+    if (lat) atomicAdd(lat, (unsigned long long)(tsum / iters));
+}
+
 typedef CUresult (*EncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*,
                              CUtensorMapInterleave, CUtensorMapSwizzle, CUtensorMapL2promotion,
@@ -100,6 +131,32 @@ int main(int argc, char** argv) {
     int clk;
     cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, 0);
     printf("buffer %zu MB\n", mb);
+    if (argc > 2 && atoi(argv[2]) == 0) {  // sweep: warps x lanes x stages, 1 CTA/SM
+        for (int nw : {1, 2, 4, 8}) for (int nl : {1, 2}) for (int stages : {2, 3, 4}) {
+            const int streams = nw * nl;
+            const int smem = streams * stages * 16384 + 1024;
+            if (smem > 200 * 1024) continue;
+            const int iters = 1000;
+            cudaFuncSetAttribute(gather_sweep, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+            gather_sweep<<<148, 32 * nw, smem>>>(tm, int(rows / 64), stages, 100, nl, nullptr);
+            cudaMemset(lat, 0, 8);
+            cudaEvent_t a, b;
+            cudaEventCreate(&a);
+            cudaEventCreate(&b);
+            cudaEventRecord(a);
+            gather_sweep<<<148, 32 * nw, smem>>>(tm, int(rows / 64), stages, iters, nl, lat);
+            cudaEventRecord(b);
+            cudaEventSynchronize(b);
+            float ms;
+            cudaEventElapsedTime(&ms, a, b);
+            unsigned long long lt;
+            cudaMemcpy(&lt, lat, 8, cudaMemcpyDeviceToHost);
+            printf("warps %d lanes %d stages %d (in flight %3d KB/SM): %.2f TB/s, latency %llu (%s)\n", nw, nl,
+                   stages, streams * stages * 16, double(148) * streams * iters * 16384 / (ms * 1e-3) / 1e12,
+                   lt / (148 * streams), cudaGetErrorString(cudaGetLastError()));
+        }
+        return 0;
+    }
     // lanes-per-warp mode: argv[2] = number of issuing lanes in the one warp (each its own ring)
     if (argc > 2) {
         const int nl = atoi(argv[2]);
