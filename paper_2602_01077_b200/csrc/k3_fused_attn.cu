@@ -8,39 +8,31 @@
 //            ell_tail += p (engine.hpp:297-329)
 //   Phase 3  O = (acc + scale * ell_tail * (q . H_bar)) / ell   (engine.hpp:335-358)
 //
-// Tiling. One CTA (one per SM) owns 128 query rows = query blocks (2t, 2t+1):
-// the tcgen05 M=128 MMA is the full-rate shape (M=64 runs at half rate). The
-// CTA walks the ascending UNION of the two selections, TWO union entries (128
-// keys) per tile, so every S = Q K^T MMA is N=128 (M=128, N=64 SS MMAs are
-// shared-memory bound at 2/3 rate, tools/mma_rate.cu). A per-half flag zeroes
-// P for a 64-key group the half did not select, so executed MMA work is at most
-// two M=64 passes and about one pass when neighbouring blocks route alike.
-// Phase 2 is the same loop over ceil(N/128) centroid tiles with a per-half
-// column mask (the selection bitmask) and per-column weight n_j; Phase 3 is one
-// more MMA, Q . H_bar, into freed S columns.
+// Tiling. One CTA owns 128 query rows = query blocks (2t, 2t+1), because the
+// tcgen05 M=128 MMA is the full-rate shape (M=64 runs at half rate). The CTA
+// walks the ascending UNION of the two selections; a per-half flag masks the
+// block for the half that did not select it (its P rows are zero). Since
+// |union| <= 2k this never does more MMA work than two M=64 passes, and with
+// correlated neighbours (real DiT activations, clustered data) |union| ~ k.
+// Phase 2 is the same loop over ceil(N/64) centroid tiles, with a per-half
+// column mask (the selection bitmask) and per-column weight n_j. Phase 3 is one
+// more MMA, Q . H_bar, into the S columns of TMEM.
 //
-// Split-KV softmax. Two softmax warpgroups take alternate tiles, each with its
-// own running max / sums and its own O accumulator in TMEM (O0 | O1 | S0 | S1 =
-// 512 columns); the epilogue merges them. While warpgroup w handles tile u the
-// tensor core runs PV_{u-1} and S_{u+1} for the other warpgroup, and because
-// S_u's commit retires every earlier MMA, O_w is quiescent during the softmax
-// of tile u: the lazy rescale (only when the max grows by > 2^8) needs no wait.
-//
-// Warp roles (512 threads, one CTA per SM). TMA throughput scales with the
-// number of issuing WARPS (~24 B/clk/SM each, tools/tma_bw.cu), and a tile needs
-// 64 KB per ~1000 tensor cycles, so four warps produce: one per (tensor, 64-key
-// block of the tile).
-//   warp 0      TMA producer K, block a (+ Q once, H_bar at the end)
-//   warp 12     TMA producer K, block b
-//   warp 3      builds the union list from the two selection bitmasks, then is
-//               the TMA producer V, block a
-//   warp 13     TMA producer V, block b
-//   warp 1      tcgen05.mma issuer for warpgroup 0's tiles (elected lane issues)
-//   warp 2      TMEM allocator (512 columns), then the MMA issuer for
-//               warpgroup 1's tiles
-//   warps 4-7   softmax warpgroup 0 (even tiles), one thread per query row
-//   warps 8-11  softmax warpgroup 1 (odd tiles)
-//   warps 14-15 idle (the block is 16 warps so the four producers fit)
+// Warp roles (256 threads, two CTAs per SM so one CTA's softmax overlaps the
+// other's MMAs):
+//   warp 0     TMA producer for Q (once), K / k_bar tiles (2-stage ring), H_bar
+//   warp 1     single-thread tcgen05.mma issuer: S_t = Q K_t^T (SS, K-major),
+//              O += P_{t-1} V_{t-1} (TS: P from TMEM, V MN-major), Q H_bar
+//   warp 2     TMEM allocator (256 columns: O | S0 | S1), then TMA producer for
+//              the second 64-column half of every V / v_hat tile
+//   warp 3     builds the union list from the two selection bitmasks, then is
+//              the TMA producer for the first half of every V / v_hat tile
+//              (a TMA issue stream runs at ~32 B/clk, so two streams halve the
+//              latency of the V loads on the critical path; tools/tma_bw.cu)
+//   warps 4-7  softmax / correction / epilogue, one thread per query row
+//              (TMEM lane), exp2 with log2(e)*scale folded into one FFMA, lazy
+//              rescale of O (only when the running max grows by > 2^8), P
+//              written back to TMEM as bf16 over the S columns it came from.
 #include "kernels.h"
 #include "sm100.cuh"
 
@@ -53,32 +45,31 @@ using namespace pisa_sm100;
 
 namespace {
 
-constexpr int kThreads = 512;
-constexpr int kKStages = 3;  // K ring (freed early, right after S); V ring has 2
+constexpr int kThreads = 256;
 constexpr float kRescaleThresh = 8.0f;  // log2 units
-constexpr int kPolyEvery = 4;           // 1 in 4 softmax exponentials via ex2_poly (FMA pipe)
-// TMEM columns: O0 | O1 | S0 | S1 (128 each; O uses the first D)
-__device__ __forceinline__ constexpr uint32_t colO(int w) { return uint32_t(w) * 128u; }
-__device__ __forceinline__ constexpr uint32_t colS(int w) { return 256u + uint32_t(w) * 128u; }
+// Fraction of softmax exponentials computed by ex2_poly on the FMA pipe (FA4's
+// trick for MUFU-bound softmax): 0 = all on MUFU. With two CTAs sharing each
+// SMSP the softmax here is issue-bound, not MUFU-bound, so it is off.
+constexpr int kPolyEvery = 0;
+constexpr uint32_t kColO = 0, kColS = 128;
 
 template <int D>
 struct FusedCfg {
-    static constexpr int NH = D / 64;           // 64-column halves per row
-    static constexpr int kQ = 128 * D * 2;      // Q tile bytes
-    static constexpr int kStage = 128 * D * 2;  // one 128-key K or V stage
+    static constexpr int kQ = 128 * D * 2;  // Q tile bytes (2 halves of 128 rows for D=128)
+    static constexpr int kKV = 64 * D * 2;  // one K or V stage
     static constexpr int kOffQ = 0;
     static constexpr int kOffK = kQ;
-    static constexpr int kOffV = kQ + kKStages * kStage;
-    static constexpr int kOffBar = kOffV + 2 * kStage;
+    static constexpr int kOffV = kQ + 2 * kKV;
+    static constexpr int kOffBar = kQ + 4 * kKV;
     static constexpr int kBarBytes = 256;
-    static constexpr int kOffStat = kOffBar + kBarBytes;  // [2][128][3] fp32 epilogue merge
-    static constexpr int kOffMask = kOffStat + 2 * 128 * 3 * 4;
+    static constexpr int kOffMask = kOffBar + kBarBytes;
 };
 
 struct Bars {
     uint64_t q_full, h_full, qh_full;
-    uint64_t k_full[kKStages], k_empty[kKStages], v_full[2], v_empty[2];
+    uint64_t k_full[2], k_empty[2], v_full[2], v_empty[2];
     uint64_t s_full[2], p_full[2];
+    uint64_t o_done;
     uint32_t tmem_base;
     uint32_t n_union;
 };
@@ -94,6 +85,26 @@ __device__ __forceinline__ void trace_mark(const FusedArgs& a, int role, int t, 
 #define TRACE(role, t) ((void)0)
 #endif
 
+// max of 64 values as a 3-level tree (FMNMX3-friendly, short dependency chain)
+__device__ __forceinline__ float max64(const float* x) {
+    float m[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+        m[j] = fmaxf(fmaxf(fmaxf(x[8 * j], x[8 * j + 1]), fmaxf(x[8 * j + 2], x[8 * j + 3])),
+                     fmaxf(fmaxf(x[8 * j + 4], x[8 * j + 5]), fmaxf(x[8 * j + 6], x[8 * j + 7])));
+    return fmaxf(fmaxf(fmaxf(m[0], m[1]), fmaxf(m[2], m[3])), fmaxf(fmaxf(m[4], m[5]), fmaxf(m[6], m[7])));
+}
+
+// Writes P (bf16 pairs) over the first 32 S columns and releases the S buffer.
+__device__ __forceinline__ void publish_p(uint32_t sc, const uint32_t (&pk)[32], uint64_t* bar,
+                                          int lane) {
+    tmem_st32(sc, pk);
+    tmem_st_wait();
+    tc_fence_before();
+    __syncwarp();
+    if (lane == 0) mbar_arrive(bar);
+}
+
 template <int D>
 __device__ __forceinline__ void rescale_o(uint32_t tmem_o, float f) {
 #pragma unroll 1
@@ -107,48 +118,8 @@ __device__ __forceinline__ void rescale_o(uint32_t tmem_o, float f) {
     }
 }
 
-__device__ __forceinline__ float max64(const float* x) {
-    float m[8];
-#pragma unroll
-    for (int j = 0; j < 8; ++j)
-        m[j] = fmaxf(fmaxf(fmaxf(x[8 * j], x[8 * j + 1]), fmaxf(x[8 * j + 2], x[8 * j + 3])),
-                     fmaxf(fmaxf(x[8 * j + 4], x[8 * j + 5]), fmaxf(x[8 * j + 6], x[8 * j + 7])));
-    return fmaxf(fmaxf(fmaxf(m[0], m[1]), fmaxf(m[2], m[3])), fmaxf(fmaxf(m[4], m[5]), fmaxf(m[6], m[7])));
-}
-
-// p = 2^(x*sl2 - mm) for 64 scores, packed bf16 pairs into pk[32]; returns the sum.
-// kPoly: every kPolyEvery-th exponential goes through ex2_poly (finite x only).
-template <bool kPoly>
-__device__ __forceinline__ float exp_pack64(const float* x, float sl2, float mm, uint32_t* pk) {
-    float ps[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-    for (int i = 0; i < 64; i += 2) {
-        const float a0 = fmaf(x[i], sl2, -mm), a1 = fmaf(x[i + 1], sl2, -mm);
-        const float p0 = (kPoly && (i % kPolyEvery == kPolyEvery - 1)) ? ex2_poly(a0) : ex2(a0);
-        const float p1 = (kPoly && ((i + 1) % kPolyEvery == kPolyEvery - 1)) ? ex2_poly(a1) : ex2(a1);
-        ps[(i >> 1) & 3] += p0 + p1;
-        pk[i >> 1] = pack_bf16(p0, p1);
-    }
-    return (ps[0] + ps[1]) + (ps[2] + ps[3]);
-}
-
-// 32-score variant: p for 32 columns packed into pk[16]; returns the sum.
-template <bool kPoly>
-__device__ __forceinline__ float exp_pack32(const float* x, float sl2, float mm, uint32_t* pk) {
-    float ps[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-    for (int i = 0; i < 32; i += 2) {
-        const float a0 = fmaf(x[i], sl2, -mm), a1 = fmaf(x[i + 1], sl2, -mm);
-        const float p0 = (kPoly && (i % kPolyEvery == kPolyEvery - 1)) ? ex2_poly(a0) : ex2(a0);
-        const float p1 = (kPoly && ((i + 1) % kPolyEvery == kPolyEvery - 1)) ? ex2_poly(a1) : ex2(a1);
-        ps[(i >> 1) & 3] += p0 + p1;
-        pk[i >> 1] = pack_bf16(p0, p1);
-    }
-    return (ps[0] + ps[1]) + (ps[2] + ps[3]);
-}
-
 template <int D>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kThreads, 2)
     fused_attn_kernel(const __grid_constant__ CUtensorMap tmQ,
                       const __grid_constant__ CUtensorMap tmK,
                       const __grid_constant__ CUtensorMap tmV,
@@ -156,12 +127,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                       const __grid_constant__ CUtensorMap tmVh,
                       const __grid_constant__ CUtensorMap tmH, FusedArgs a) {
     using Cfg = FusedCfg<D>;
-    constexpr int NH = Cfg::NH;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                                ~uintptr_t(1023));
     Bars& bar = *reinterpret_cast<Bars*>(smem + Cfg::kOffBar);
-    float* stat = reinterpret_cast<float*>(smem + Cfg::kOffStat);
     uint32_t* maskA = reinterpret_cast<uint32_t*>(smem + Cfg::kOffMask);
     uint32_t* maskB = maskA + a.W;
     uint16_t* ulist = reinterpret_cast<uint16_t*>(maskB + a.W);
@@ -176,7 +145,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int b = bh / a.H, h = bh % a.H;
     const int iA = 2 * tile, iB = 2 * tile + 1;
     const bool hasB = iB < a.N;
-    const bool tail = a.variant != 0;  // Zeroth, Hybrid, GlobalCentroid
+    const bool tail = a.variant != 0;                       // Zeroth, Hybrid, GlobalCentroid
     const bool first_order = a.variant == 3 || a.variant == 4;
     const int n_last = a.L - (a.N - 1) * 64;
 
@@ -184,24 +153,23 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (threadIdx.x == 0) {
         mbar_init(&bar.q_full, 1);
         mbar_init(&bar.h_full, 1);
-        mbar_init(&bar.qh_full, 2);  // one commit per MMA warp
-        for (int s = 0; s < kKStages; ++s) {
-            mbar_init(&bar.k_full[s], 2);  // one expect_tx arrive per producer warp
-            mbar_init(&bar.k_empty[s], 1);
-        }
+        mbar_init(&bar.qh_full, 1);
         for (int s = 0; s < 2; ++s) {
-            mbar_init(&bar.v_full[s], 2);
+            mbar_init(&bar.k_full[s], 1);
+            mbar_init(&bar.k_empty[s], 1);
+            mbar_init(&bar.v_full[s], D / 64);  // one arrive per V producer (one per 64-col half)
             mbar_init(&bar.v_empty[s], 1);
             mbar_init(&bar.s_full[s], 1);
             mbar_init(&bar.p_full[s], 4);
         }
+        mbar_init(&bar.o_done, 1);
         fence_mbar_init();
         tma_prefetch(&tmQ);
         tma_prefetch(&tmK);
         tma_prefetch(&tmV);
     }
     if (warp == 2) {
-        tmem_alloc(&bar.tmem_base, 512);
+        tmem_alloc(&bar.tmem_base, 256);
         tmem_relinquish();
     }
     if (warp == 3) {
@@ -239,153 +207,141 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
-    // Producer / MMA warpgroups (warps 0-3, 12-15) hand registers to the two
-    // softmax warpgroups (warps 4-11): 2*128*64 + 2*128*184 <= 64K. Every role
-    // branch starts with its warpgroup's setmaxnreg.
     const uint32_t tmem = bar.tmem_base;
     const int U = int(bar.n_union);
-    const int T1 = (U + 1) >> 1;                        // exact tiles (2 union entries each)
-    const int T = T1 + (tail ? (a.N + 127) / 128 : 0);  // + centroid tiles (128 centroids each)
+    const int T = U + (tail ? a.nchunk2 : 0);  // key tiles: union blocks, then centroid tiles
 
-    if (warp == 0 || warp == 3 || warp == 12 || warp == 13) {
-        // ------------------------- producers: K (warps 0, 12), V (warps 3, 13) --
-        regs_dec<64>();
-        const bool isK = (warp == 0 || warp == 12);
-        const int blk = (warp >= 12) ? 1 : 0;  // which 64-key block of the tile
-        const CUtensorMap* tmx = isK ? &tmK : &tmV;
-        const CUtensorMap* tmc = isK ? &tmKb : &tmVh;
-        const int nst = isK ? kKStages : 2;
-        uint64_t* full = isK ? bar.k_full : bar.v_full;
-        uint64_t* empty = isK ? bar.k_empty : bar.v_empty;
-        uint8_t* ring = smem + (isK ? Cfg::kOffK : Cfg::kOffV);
-        if (warp == 0 && elect_one()) {
+    if (warp == 0) {
+        // ------------------------------------------------ producer: Q, K, H --
+        uint8_t* sQ = smem + Cfg::kOffQ;
+        if (elect_one()) {
             mbar_expect_tx(&bar.q_full, Cfg::kQ);
 #pragma unroll
-            for (int half = 0; half < NH; ++half)
-                tma_load_4d(smem + Cfg::kOffQ + half * 16384, &tmQ, &bar.q_full, half * 64,
-                            tile * 128, h, b);
+            for (int half = 0; half < D / 64; ++half)
+                tma_load_4d(sQ + half * 16384, &tmQ, &bar.q_full, half * 64, tile * 128, h, b);
         }
         __syncwarp();
-        // Stage layout (K-major B of S and MN-major B of PV alike): column half hh
-        // is [128 keys][128 B] at +hh*16 KB; block blk fills keys [64 blk, 64 blk + 64).
-        int s = 0, ph = 0;
-        for (int u = 0; u < T; ++u) {
-            mbar_wait(&empty[s], ph ^ 1);
-            if (lane == 0 && blk == 0) TRACE(isK ? 11 : 12, u);
-            int row;
-            if (u < T1) {
-                const int e = 2 * u + blk;
-                row = int(ulist[e < U ? e : 2 * u] & 0x3FFFu) * 64;  // odd tail: repeat (masked)
-            } else {
-                row = (u - T1) * 128 + blk * 64;
-            }
+        for (int t = 0; t < T; ++t) {
+            const int s = t & 1;
+            uint8_t* sK = smem + Cfg::kOffK + s * Cfg::kKV;
+            mbar_wait(&bar.k_empty[s], ((t >> 1) & 1) ^ 1);
+            const bool exact = t < U;
+            const int row = exact ? int(ulist[t] & 0x3FFFu) * 64 : (t - U) * 64;
             if (elect_one()) {
-                mbar_expect_tx(&full[s], Cfg::kStage / 2);
+                mbar_expect_tx(&bar.k_full[s], Cfg::kKV);
 #pragma unroll
-                for (int hh = 0; hh < NH; ++hh) {
-                    uint8_t* dst = ring + s * Cfg::kStage + hh * 16384 + blk * 8192;
-                    if (u < T1)
-                        tma_load_4d(dst, tmx, &full[s], hh * 64, row, h, b);
+                for (int half = 0; half < D / 64; ++half) {
+                    if (exact)
+                        tma_load_4d(sK + half * 8192, &tmK, &bar.k_full[s], half * 64, row, h, b);
                     else
-                        tma_load_3d(dst, tmc, &full[s], hh * 64, row, bh);
+                        tma_load_3d(sK + half * 8192, &tmKb, &bar.k_full[s], half * 64, row, bh);
                 }
-                if (blk == 0) TRACE(isK ? 0 : 1, u);
+                TRACE(0, t);
             }
             __syncwarp();
-            if (++s == nst) {
-                s = 0;
-                ph ^= 1;
-            }
         }
-        if (warp == 0 && first_order) {
-            // H_bar (D rows x D cols, MN-major B operand of Q.H_bar) into K stage 0,
-            // once every K stage has been released.
-            for (int i = 0; i < kKStages; ++i) {
-                mbar_wait(&empty[s], ph ^ 1);
-                if (++s == kKStages) {
-                    s = 0;
-                    ph ^= 1;
-                }
-            }
+        if (first_order) {
+            // H_bar (D rows) into the K ring: half c lands in K stage c.
+            for (int t = T; t < T + 2; ++t) mbar_wait(&bar.k_empty[t & 1], ((t >> 1) & 1) ^ 1);
             if (elect_one()) {
                 mbar_expect_tx(&bar.h_full, D * D * 2);
 #pragma unroll
-                for (int hh = 0; hh < NH; ++hh)
-                    tma_load_3d(smem + Cfg::kOffK + hh * 16384, &tmH, &bar.h_full, hh * 64, 0, bh);
+                for (int half = 0; half < D / 64; ++half)
+                    tma_load_3d(smem + Cfg::kOffK + half * Cfg::kKV, &tmH, &bar.h_full, half * 64, 0, bh);
             }
             __syncwarp();
         }
-    } else if (warp == 1 || warp == 2) {
-        // ------------------------------------------------------------ MMA --
-        // One issuing warp per softmax warpgroup (warp 1: even tiles -> S0/O0,
-        // warp 2: odd tiles -> S1/O1), so one warpgroup's PV never waits behind
-        // the other's S. Whole-warp loops; one elected lane issues and commits (a
-        // commit tracks the MMAs of the thread that executes it).
-        regs_dec<64>();
-        const int w = warp - 1;
-        constexpr uint32_t idS = idesc_bf16(128, 128, 0, 0);  // S = Q K^T over 128 keys
-        constexpr uint32_t idPV = idesc_bf16(128, D, 0, 1);   // O += P V (V MN-major)
-        const uint32_t qbase = smem_u32(smem + Cfg::kOffQ);
-        mbar_wait(&bar.q_full, 0);
-        for (int u = w; u < T; u += 2) {
-            const int ks_ = u % kKStages;
-            mbar_wait(&bar.k_full[ks_], (u / kKStages) & 1);
-            tc_fence_after();
-            const uint32_t kb = smem_u32(smem + Cfg::kOffK + ks_ * Cfg::kStage);
+    } else if (warp == 3 || (warp == 2 && D == 128)) {
+        // -------------------------------------------- producers: V halves --
+        // Each 64-column half of a V tile has its own issuing warp (two TMA
+        // issue streams; V is on the critical path: V_t can only load once
+        // PV_{t-2} has retired).
+        const int vh = (warp == 3) ? 0 : 1;
+        for (int t = 0; t < T; ++t) {
+            const int s = t & 1;
+            uint8_t* sV = smem + Cfg::kOffV + s * Cfg::kKV + vh * 8192;
+            mbar_wait(&bar.v_empty[s], ((t >> 1) & 1) ^ 1);
+            const bool exact = t < U;
+            const int row = exact ? int(ulist[t] & 0x3FFFu) * 64 : (t - U) * 64;
             if (elect_one()) {
-                TRACE(8, u);
-#pragma unroll
-                for (int ks = 0; ks < D / 16; ++ks) {
-                    const uint32_t hq = (ks >> 2), kq = (ks & 3) * 32;
-                    mma_ss(tmem + colS(w), sdesc_sw128(qbase + hq * 16384 + kq, 16, 1024),
-                           sdesc_sw128(kb + hq * 16384 + kq, 16, 1024), idS, ks != 0);
-                }
-                mma_commit(&bar.k_empty[ks_]);
-                mma_commit(&bar.s_full[w]);
-                TRACE(2, u);
+                mbar_expect_tx(&bar.v_full[s], 8192);
+                if (exact)
+                    tma_load_4d(sV, &tmV, &bar.v_full[s], vh * 64, row, h, b);
+                else
+                    tma_load_3d(sV, &tmVh, &bar.v_full[s], vh * 64, row, bh);
+                if (vh == 0) TRACE(1, t);
             }
             __syncwarp();
-            // PV_u once this warpgroup has published P_u (S_{u+2} reuses the buffer)
-            mbar_wait(&bar.p_full[w], (u >> 1) & 1);
-            if (lane == 0) TRACE(9, u);
-            mbar_wait(&bar.v_full[w], (u >> 1) & 1);
-            if (lane == 0) TRACE(10, u);
+        }
+    } else if (warp == 1) {
+        // ------------------------------------------------------------- MMA --
+        // Whole-warp loop, one elected lane issues (and commits: a commit
+        // tracks the MMAs of the thread that executes it).
+        constexpr uint32_t idS = idesc_bf16(128, 64, 0, 0);   // S = Q K^T
+        constexpr uint32_t idPV = idesc_bf16(128, D, 0, 1);   // O += P V (V MN-major)
+        constexpr uint32_t idQH = idesc_bf16(128, D, 0, 1);   // Q H_bar
+        const uint32_t qbase = smem_u32(smem + Cfg::kOffQ);
+        auto issue_pv = [&](int u) {
+            const int s = u & 1;
+            const uint32_t ph = (u >> 1) & 1;
+            mbar_wait(&bar.p_full[s], ph);
+            mbar_wait(&bar.v_full[s], ph);
             tc_fence_after();
-            const uint32_t vb = smem_u32(smem + Cfg::kOffV + w * Cfg::kStage);
+            const uint32_t vb = smem_u32(smem + Cfg::kOffV + s * Cfg::kKV);
             if (elect_one()) {
+                TRACE(10, u);
 #pragma unroll
-                for (int ks = 0; ks < 8; ++ks)
-                    mma_ts(tmem + colO(w), tmem + colS(w) + ks * 8,
-                           sdesc_sw128(vb + ks * 2048, 16384, 1024), idPV,
-                           (u >= 2 || ks > 0) ? 1u : 0u);
-                mma_commit(&bar.v_empty[w]);
+                for (int ks = 0; ks < 4; ++ks)
+                    mma_ts(tmem + kColO, tmem + kColS + s * 64 + ks * 8,
+                           sdesc_sw128(vb + ks * 2048, 8192, 1024), idPV, (u | ks) != 0);
+                mma_commit(&bar.v_empty[s]);
+                mma_commit(&bar.o_done);
                 TRACE(3, u);
             }
             __syncwarp();
+        };
+        mbar_wait(&bar.q_full, 0);
+        for (int t = 0; t < T; ++t) {
+            const int s = t & 1;
+            mbar_wait(&bar.k_full[s], (t >> 1) & 1);
+            tc_fence_after();
+            const uint32_t kb = smem_u32(smem + Cfg::kOffK + s * Cfg::kKV);
+            if (elect_one()) {
+                TRACE(8, t);
+#pragma unroll
+                for (int ks = 0; ks < D / 16; ++ks) {
+                    const uint32_t hq = (ks >> 2), kq = (ks & 3) * 32;
+                    mma_ss(tmem + kColS + s * 64,
+                           sdesc_sw128(qbase + hq * 16384 + kq, 16, 1024),
+                           sdesc_sw128(kb + hq * 8192 + kq, 16, 1024), idS, ks != 0);
+                }
+                mma_commit(&bar.k_empty[s]);
+                mma_commit(&bar.s_full[s]);
+                TRACE(2, t);
+            }
+            __syncwarp();
+            if (t > 0) issue_pv(t - 1);
         }
-        if (w == 0 && first_order) {
+        issue_pv(T - 1);
+        if (first_order) {
             mbar_wait(&bar.h_full, 0);
             tc_fence_after();
         }
         const uint32_t hb = smem_u32(smem + Cfg::kOffK);
         if (elect_one()) {
-            if (w == 0 && first_order) {
-                // Q.H_bar into S0, after warpgroup 0's last PV has read P from it
-                constexpr uint32_t idQH = idesc_bf16(128, D, 0, 1);
+            if (first_order) {
 #pragma unroll
                 for (int ks = 0; ks < D / 16; ++ks) {
                     const uint32_t hq = (ks >> 2), kq = (ks & 3) * 32;
-                    mma_ss(tmem + colS(0), sdesc_sw128(qbase + hq * 16384 + kq, 16, 1024),
-                           sdesc_sw128(hb + ks * 2048, 16384, 1024), idQH, ks != 0);
+                    mma_ss(tmem + kColS, sdesc_sw128(qbase + hq * 16384 + kq, 16, 1024),
+                           sdesc_sw128(hb + ks * 2048, Cfg::kKV, 1024), idQH, ks != 0);
                 }
             }
-            mma_commit(&bar.qh_full);  // both MMA warps: all their PVs (and QH) done
+            mma_commit(&bar.qh_full);  // also: every PV done
         }
         __syncwarp();
-    } else if (warp >= 4 && warp < 12) {
-        // ------------------------------------------------ softmax warpgroups --
-        regs_inc<184>();
-        const int wg = (warp - 4) >> 2;     // 0: even tiles, 1: odd tiles
+    } else if (warp >= 4) {
+        // ------------------------------------------------ softmax warpgroup --
         const int q4 = warp & 3;            // TMEM lane quadrant
         const int row = q4 * 32 + lane;     // 0..127 within the tile
         const int half = row >> 6;          // 0: block iA, 1: block iB (warp-uniform)
@@ -394,14 +350,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         const bool warp_active = __all_sync(0xffffffffu, active);
         const uint32_t* hmask = half ? maskB : maskA;
         const uint32_t lane_off = uint32_t(q4 * 32) << 16;
-        const uint32_t tO = tmem + lane_off + colO(wg);
-        const uint32_t tS = tmem + lane_off + colS(wg);
         const float sl2 = a.scale * 1.4426950408889634f;
 
         float m = -INFINITY, l = 0.f, lt = 0.f;
-        // Exponent shift for this tile; rescales O_wg only if the max grew by more
-        // than 2^8. O_wg is quiescent here: S_u's commit retired PV_{u-2}.
-        auto update_max = [&](float bm_raw) -> float {
+        // Online-softmax step shared by both phases. x: raw scores (masked = -inf).
+        // Returns the shift to exponentiate against; rescales O when needed.
+        auto update_max = [&](float bm_raw, int t) -> float {
             const float bm = bm_raw * sl2;
             float m_use = m;
             bool resc = false;
@@ -415,7 +369,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             if (__any_sync(0xffffffffu, resc)) {
                 const float f = resc ? ex2(m - m_use) : 1.f;
-                rescale_o<D>(tO, f);
+                mbar_wait(&bar.o_done, (t - 1) & 1);  // PV_{t-1} done (t >= 1 whenever resc)
+                tc_fence_after();
+                rescale_o<D>(tmem + lane_off + kColO, f);
                 l *= f;
                 lt *= f;
             }
@@ -423,238 +379,189 @@ __global__ void __launch_bounds__(kThreads, 1)
             return (m == -INFINITY) ? 0.f : m;  // all-masked row: p = 0, not NaN
         };
 
-        // 64 S columns [c0, c0 + 64) of this row -> x
-        auto load64 = [&](uint32_t c0, float* x) {
-            uint32_t r0[32], r1[32];
-            tmem_ld32(tS + c0, r0);
-            tmem_ld32(tS + c0 + 32, r1);
-            tmem_ld_wait(r0);
-            tmem_ld_wait(r1);
-#pragma unroll
-            for (int i = 0; i < 32; ++i) {
-                x[i] = __uint_as_float(r0[i]);
-                x[i + 32] = __uint_as_float(r1[i]);
-            }
-        };
-
-        for (int u = wg; u < T; u += 2) {
-            mbar_wait(&bar.s_full[wg], (u >> 1) & 1);
+        // ---- Phase 1: exact blocks of the union
+        for (int t = 0; t < U; ++t) {
+            const int s = t & 1;
+            const uint32_t sc = tmem + lane_off + kColS + s * 64;
+            const uint32_t e = ulist[t];
+            const bool use = ((e >> (14 + half)) & 1u) != 0;  // warp-uniform
+            const int nvalid = (int(e & 0x3FFFu) == a.N - 1) ? n_last : 64;
+            mbar_wait(&bar.s_full[s], (t >> 1) & 1);
             tc_fence_after();
-            if (q4 == 0) TRACE(4 + wg, u);
+            TRACE(4 + (q4 >> 1), t);
             uint32_t pk[32];
-            float x[64];
-            if (u < T1) {
-                // ---- Phase 1: two exact 64-key blocks (groups g = 0, 1)
-                const uint32_t ea = ulist[2 * u];
-                const bool hasb = 2 * u + 1 < U;
-                const uint32_t eb = hasb ? ulist[2 * u + 1] : 0u;
-                const bool use[2] = {((ea >> (14 + half)) & 1u) != 0,
-                                     hasb && ((eb >> (14 + half)) & 1u) != 0};  // warp-uniform
-                const int nv[2] = {(int(ea & 0x3FFFu) == a.N - 1) ? n_last : 64,
-                                   (int(eb & 0x3FFFu) == a.N - 1) ? n_last : 64};
-                bool fast[2];
-                float bm = -INFINITY;
+            if (use) {
+                uint32_t ra[32], rb[32];
+                tmem_ld32(sc, ra);
+                tmem_ld32(sc + 32, rb);
+                tmem_ld_wait(ra);
+                tmem_ld_wait(rb);
+                float x[64];
 #pragma unroll
-                for (int g = 0; g < 2; ++g) {  // pass 1: masked max
-                    fast[g] = warp_active && nv[g] == 64;
-                    if (!use[g]) continue;
-                    load64(g * 64, x);
-                    if (!fast[g]) {  // ragged last key block / rows past L
-#pragma unroll
-                        for (int i = 0; i < 64; ++i) x[i] = (active && i < nv[g]) ? x[i] : -INFINITY;
-                    }
-                    bm = fmaxf(bm, max64(x));
+                for (int i = 0; i < 32; ++i) {
+                    x[i] = __uint_as_float(ra[i]);
+                    x[i + 32] = __uint_as_float(rb[i]);
                 }
-                if (use[0] || use[1]) {
-                    const float mm = update_max(bm);
-                    float ps = 0.f;
+                const bool full_tile = warp_active && nvalid == 64;
+                if (!full_tile) {  // ragged last key block / rows past L
 #pragma unroll
-                    for (int g = 0; g < 2; ++g) {  // pass 2: exponentials, P over S columns
-                        if (use[g]) {
-                            load64(g * 64, x);
-                            if (fast[g]) {
-                                ps += exp_pack64<true>(x, sl2, mm, pk);
-                            } else {
+                    for (int i = 0; i < 64; ++i) x[i] = (active && i < nvalid) ? x[i] : -INFINITY;
+                }
+                const float mm = update_max(max64(x), t);
+                float ps[4] = {0.f, 0.f, 0.f, 0.f};
+                if (kPolyEvery > 0 && full_tile) {
+                    // every kPolyEvery-th exponential on the FMA pipe, the rest on MUFU
 #pragma unroll
-                                for (int i = 0; i < 64; ++i) x[i] = (active && i < nv[g]) ? x[i] : -INFINITY;
-                                ps += exp_pack64<false>(x, sl2, mm, pk);
-                            }
-                        } else {
-#pragma unroll
-                            for (int i = 0; i < 32; ++i) pk[i] = 0u;
-                        }
-                        tmem_st32(tS + g * 32, pk);
+                    for (int i = 0; i < 64; i += 2) {
+                        const float a0 = fmaf(x[i], sl2, -mm), a1 = fmaf(x[i + 1], sl2, -mm);
+                        const float p0 = (kPolyEvery > 0 && i % kPolyEvery == kPolyEvery - 1) ? ex2_poly(a0) : ex2(a0);
+                        const float p1 = (kPolyEvery > 0 && (i + 1) % kPolyEvery == kPolyEvery - 1) ? ex2_poly(a1) : ex2(a1);
+                        ps[(i >> 1) & 3] += p0 + p1;
+                        pk[i >> 1] = pack_bf16(p0, p1);
                     }
-                    l += ps;
                 } else {
 #pragma unroll
-                    for (int i = 0; i < 32; ++i) pk[i] = 0u;
-                    tmem_st32(tS, pk);
-                    tmem_st32(tS + 32, pk);
+                    for (int i = 0; i < 64; i += 2) {
+                        const float p0 = ex2(fmaf(x[i], sl2, -mm));
+                        const float p1 = ex2(fmaf(x[i + 1], sl2, -mm));
+                        ps[(i >> 1) & 3] += p0 + p1;
+                        pk[i >> 1] = pack_bf16(p0, p1);
+                    }
                 }
+                l += (ps[0] + ps[1]) + (ps[2] + ps[3]);
             } else {
-                // ---- Phase 2: 128 centroids; column mask = own selection; weight n_j
-                const int j0 = (u - T1) * 128;
-                const int nvalid = min(128, a.N - j0);
-                auto mask64 = [&](int g, float* xx) {
 #pragma unroll
-                    for (int wq = 0; wq < 2; ++wq) {
-                        const int w = (j0 >> 5) + 2 * g + wq;
-                        const uint32_t cm = w < a.W ? hmask[w] : 0xffffffffu;
-#pragma unroll
-                        for (int i = 0; i < 32; ++i) {
-                            const int col = g * 64 + wq * 32 + i;
-                            const bool ok = active && col < nvalid && !((cm >> i) & 1u);
-                            xx[wq * 32 + i] = ok ? xx[wq * 32 + i] : -INFINITY;
-                        }
-                    }
-                };
-                float bm = -INFINITY;
-#pragma unroll
-                for (int g = 0; g < 2; ++g) {
-                    load64(g * 64, x);
-                    mask64(g, x);
-                    bm = fmaxf(bm, max64(x));
-                }
-                const float mm = update_max(bm);
-                const int lc = a.N - 1 - j0;  // column of the ragged last block, if in this tile
-                float ps = 0.f, plast = 0.f;
-#pragma unroll
-                for (int c = 0; c < 4; ++c) {  // 32-column chunks
-                    uint32_t r[32];
-                    tmem_ld32(tS + c * 32, r);
-                    tmem_ld_wait(r);
-                    const int w = (j0 >> 5) + c;
-                    const uint32_t cm = w < a.W ? hmask[w] : 0xffffffffu;
-                    float xc[32];
-#pragma unroll
-                    for (int i = 0; i < 32; ++i) {
-                        const bool ok = active && (c * 32 + i) < nvalid && !((cm >> i) & 1u);
-                        xc[i] = ok ? __uint_as_float(r[i]) : -INFINITY;
-                    }
-                    uint32_t pk16[16];
-                    ps += exp_pack32<false>(xc, sl2, mm, pk16);
-                    tmem_st16(tS + c * 16, pk16);
-                    if (n_last != 64 && lc >= c * 32 && lc < c * 32 + 32) {
-#pragma unroll
-                        for (int i = 0; i < 32; ++i)
-                            if (c * 32 + i == lc) plast = ex2(fmaf(xc[i], sl2, -mm));
-                    }
-                }
-                l += 64.f * ps + (float(n_last) - 64.f) * plast;
-                lt += ps;
+                for (int i = 0; i < 32; ++i) pk[i] = 0u;
             }
-            tmem_st_wait();
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&bar.p_full[wg]);
-            if (q4 == 0) TRACE(6 + wg, u);
+            publish_p(sc, pk, &bar.p_full[s], lane);
+            TRACE(6 + (q4 >> 1), t);
+        }
+        // ---- Phase 2: centroid tiles, column mask = own selection, weight n_j
+        for (int t = U; t < T; ++t) {
+            const int s = t & 1;
+            const uint32_t sc = tmem + lane_off + kColS + s * 64;
+            const int c = t - U;
+            const uint32_t cm_lo = hmask[2 * c];
+            const uint32_t cm_hi = (2 * c + 1 < a.W) ? hmask[2 * c + 1] : 0xffffffffu;
+            const int nvalid = min(64, a.N - c * 64);
+            const bool has_last = (c == a.nchunk2 - 1) && n_last != 64;
+            mbar_wait(&bar.s_full[s], (t >> 1) & 1);
+            tc_fence_after();
+            uint32_t ra[32], rb[32];
+            tmem_ld32(sc, ra);
+            tmem_ld32(sc + 32, rb);
+            tmem_ld_wait(ra);
+            tmem_ld_wait(rb);
+            float x[64];
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+                const bool ok_lo = active && i < nvalid && !((cm_lo >> i) & 1u);
+                const bool ok_hi = active && i + 32 < nvalid && !((cm_hi >> i) & 1u);
+                x[i] = ok_lo ? __uint_as_float(ra[i]) : -INFINITY;
+                x[i + 32] = ok_hi ? __uint_as_float(rb[i]) : -INFINITY;
+            }
+            const float mm = update_max(max64(x), t);
+            uint32_t pk[32];
+            float ps0 = 0.f, ps1 = 0.f;
+#pragma unroll
+            for (int i = 0; i < 64; i += 2) {
+                const float p0 = ex2(fmaf(x[i], sl2, -mm));
+                const float p1 = ex2(fmaf(x[i + 1], sl2, -mm));
+                ps0 += p0;
+                ps1 += p1;
+                pk[i >> 1] = pack_bf16(p0, p1);
+            }
+            const float ps = ps0 + ps1;
+            float pw = 64.f * ps;
+            if (has_last) {  // the ragged last block weighs n_last, not 64
+                const int lc = a.N - 1 - c * 64;
+                float plast = 0.f;
+#pragma unroll
+                for (int i = 0; i < 64; ++i)
+                    if (i == lc) plast = ex2(fmaf(x[i], sl2, -mm));
+                pw += (float(n_last) - 64.f) * plast;
+            }
+            l += pw;
+            lt += ps;
+            publish_p(sc, pk, &bar.p_full[s], lane);
         }
 
         // ------------------------------------------------------- epilogue --
-        // Merge the two warpgroups' (m, l, lt); WG0 writes columns [0, D/2),
-        // WG1 columns [D/2, D).
-        stat[(wg * 128 + row) * 3 + 0] = m;
-        stat[(wg * 128 + row) * 3 + 1] = l;
-        stat[(wg * 128 + row) * 3 + 2] = lt;
-        asm volatile("bar.sync 1, 256;" ::: "memory");
-        const int o = 1 - wg;
-        const float m0 = wg == 0 ? m : stat[(o * 128 + row) * 3 + 0];
-        const float m1 = wg == 1 ? m : stat[(o * 128 + row) * 3 + 0];
-        const float l0 = wg == 0 ? l : stat[(o * 128 + row) * 3 + 1];
-        const float l1 = wg == 1 ? l : stat[(o * 128 + row) * 3 + 1];
-        const float lt0 = wg == 0 ? lt : stat[(o * 128 + row) * 3 + 2];
-        const float lt1 = wg == 1 ? lt : stat[(o * 128 + row) * 3 + 2];
-        float M = fmaxf(m0, m1);
-        float fa = (m0 == -INFINITY) ? 0.f : ex2(m0 - M);  // scale of O0
-        float fb = (m1 == -INFINITY) ? 0.f : ex2(m1 - M);  // scale of O1
-        float lfin = l0 * fa + l1 * fb;
-        float ltfin = lt0 * fa + lt1 * fb;
         mbar_wait(&bar.qh_full, 0);
         tc_fence_after();
         float cw = 0.f;
+        float lfin = l;
         if (a.variant == 3) {
-            cw = a.scale * ltfin;
+            cw = a.scale * lt;
             if (a.literal_phase3) cw *= (1.0f / 64.0f);
         }
+        float fo = 1.f;  // extra scale on O and l (GlobalCentroid shift)
         if (a.variant == 4 && active) {
             // slope = |U_i| exp(scale q.k_bar_global - m)   (engine.hpp:202-205)
             const uint8_t* sQ = smem + Cfg::kOffQ;
             const float* kg = a.kbar_global + size_t(bh) * D;
             float dot = 0.f;
-            for (int cc = 0; cc < D; ++cc) {
-                const uint32_t off = (cc >> 6) * 16384 + sw128_off(row, cc & 63);
-                dot = fmaf(__bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(sQ + off)), kg[cc], dot);
+            for (int c = 0; c < D; ++c) {
+                const uint32_t off = (c >> 6) * 16384 + sw128_off(row, c & 63);
+                dot = fmaf(__bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(sQ + off)), kg[c], dot);
             }
             const float gx = dot * sl2;
             const int nU = a.N - a.k;
             if (nU > 0) {
-                const float M2 = fmaxf(M, gx);
-                const float g = ex2(M - M2);
-                fa *= g;
-                fb *= g;
-                lfin *= g;
-                ltfin *= g;
-                cw = a.scale * float(nU) * ex2(gx - M2);
+                const float mm = fmaxf(m, gx);
+                fo = ex2(m - mm);
+                cw = a.scale * float(nU) * ex2(gx - mm);
                 if (a.literal_phase3) cw *= (1.0f / 64.0f);
-                M = M2;
+                m = mm;
+                lfin = l * fo;
+                lt *= fo;
             }
         }
         const float inv_l = 1.0f / lfin;
         bool bad = false;
-        const uint32_t tb = tmem + lane_off;
         char* orow = reinterpret_cast<char*>(a.out) +
                      (size_t(b) * a.os_b + size_t(h) * a.os_h + size_t(grow) * a.os_l) *
                          (a.out_f32 ? 4 : 2);
 #pragma unroll 1
-        for (int cc = wg * (D / 2); cc < (wg + 1) * (D / 2); cc += 32) {
-            uint32_t r0[32], r1[32], rq[32];
-            tmem_ld32(tb + colO(0) + cc, r0);
-            tmem_ld32(tb + colO(1) + cc, r1);
-            if (first_order) tmem_ld32(tb + colS(0) + cc, rq);
-            tmem_ld_wait(r0);
-            tmem_ld_wait(r1);
+        for (int cc = 0; cc < D; cc += 32) {
+            uint32_t ro[32], rq[32];
+            tmem_ld32(tmem + lane_off + kColO + cc, ro);
+            if (first_order) tmem_ld32(tmem + lane_off + kColS + cc, rq);
+            tmem_ld_wait(ro);
             if (first_order) tmem_ld_wait(rq);
-            float ov[32];
+            float o[32];
 #pragma unroll
             for (int i = 0; i < 32; ++i) {
-                // a warpgroup that saw no tile has f = 0 and an uninitialised O: select, not multiply
-                float acc = (fa != 0.f ? __uint_as_float(r0[i]) * fa : 0.f) +
-                            (fb != 0.f ? __uint_as_float(r1[i]) * fb : 0.f);
+                float acc = __uint_as_float(ro[i]) * fo;
                 if (first_order) acc = fmaf(cw, __uint_as_float(rq[i]), acc);
-                ov[i] = acc * inv_l;
-                bad |= active && !isfinite(ov[i]);
+                o[i] = acc * inv_l;
+                bad |= active && !isfinite(o[i]);
             }
             if (active) {
                 if (a.out_f32) {
                     float4* dst = reinterpret_cast<float4*>(orow) + cc / 4;
 #pragma unroll
-                    for (int i = 0; i < 32; i += 4)
-                        dst[i / 4] = make_float4(ov[i], ov[i + 1], ov[i + 2], ov[i + 3]);
+                    for (int i = 0; i < 32; i += 4) dst[i / 4] = make_float4(o[i], o[i + 1], o[i + 2], o[i + 3]);
                 } else {
                     uint4* dst = reinterpret_cast<uint4*>(orow + cc * 2);
 #pragma unroll
                     for (int i = 0; i < 32; i += 8)
-                        dst[i / 8] = make_uint4(pack_bf16(ov[i], ov[i + 1]), pack_bf16(ov[i + 2], ov[i + 3]),
-                                                pack_bf16(ov[i + 4], ov[i + 5]), pack_bf16(ov[i + 6], ov[i + 7]));
+                        dst[i / 8] = make_uint4(pack_bf16(o[i], o[i + 1]), pack_bf16(o[i + 2], o[i + 3]),
+                                                pack_bf16(o[i + 4], o[i + 5]), pack_bf16(o[i + 6], o[i + 7]));
                 }
             }
         }
         if (active) {
-            if (wg == 0) {
-                const size_t di = size_t(bh) * a.L + grow;
-                if (a.diag_m) a.diag_m[di] = M * 0.6931471805599453f;  // log2 units -> natural log
-                if (a.diag_l) a.diag_l[di] = lfin;
-                if (a.diag_lt) a.diag_lt[di] = ltfin;
-            }
+            const size_t di = size_t(bh) * a.L + grow;
+            if (a.diag_m) a.diag_m[di] = m * 0.6931471805599453f;  // log2 units -> natural log
+            if (a.diag_l) a.diag_l[di] = lfin;
+            if (a.diag_lt) a.diag_lt[di] = lt;
             if (bad && a.nonfinite) atomicExch(a.nonfinite, 1);
         }
-    } else {
-        regs_dec<64>();  // warps 14, 15: no role after setup
     }
     tc_fence_before();
     __syncthreads();
-    if (warp == 2) tmem_dealloc(tmem, 512);
+    if (warp == 2) tmem_dealloc(tmem, 256);
 }
 
 }  // namespace

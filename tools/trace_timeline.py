@@ -12,8 +12,8 @@ import ctypes as C  # noqa: E402
 
 import paper_2602_01077_b200 as P  # noqa: E402
 
-ROLES = ["K issued", "V issued", "S issued", "PV issued", "WG0 got S", "WG1 got S",
-         "WG0 P done", "WG1 P done", "mma K rdy", "mma P rdy", "mma V rdy", "Kslot free", "Vslot free"]
+ROLES = ["K issued", "V issued", "S issued", "PV issued", "smA got S", "smB got S",
+         "smA P done", "smB P done", "mma K rdy", "mma P rdy", "mma V rdy", "mma wait K"]
 
 
 def main():
