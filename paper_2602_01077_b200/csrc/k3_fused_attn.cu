@@ -9,30 +9,45 @@
 //   Phase 3  O = (acc + scale * ell_tail * (q . H_bar)) / ell   (engine.hpp:335-358)
 //
 // Tiling. One CTA owns 128 query rows = query blocks (2t, 2t+1), because the
-// tcgen05 M=128 MMA is the full-rate shape (M=64 runs at half rate). The CTA
-// walks the ascending UNION of the two selections; a per-half flag masks the
-// block for the half that did not select it (its P rows are zero). Since
-// |union| <= 2k this never does more MMA work than two M=64 passes, and with
-// correlated neighbours (real DiT activations, clustered data) |union| ~ k.
-// Phase 2 is the same loop over ceil(N/64) centroid tiles, with a per-half
-// column mask (the selection bitmask) and per-column weight n_j. Phase 3 is one
-// more MMA, Q . H_bar, into the S columns of TMEM.
+// tcgen05 M=128 MMA is the full-rate shape (M=64 costs the same time). The CTA
+// walks the ascending UNION of the two selections; a per-block flag masks the
+// key block for the query block that did not select it (its P rows are zero),
+// so executed MMA work <= two M=64 passes. Phase 2 is the same loop over
+// ceil(N/64) centroid tiles with a per-block column mask (the selection bitmask)
+// and per-column weight n_j. Phase 3 is one more MMA, Q . H_bar.
 //
-// Warp roles (256 threads, two CTAs per SM so one CTA's softmax overlaps the
-// other's MMAs):
-//   warp 0     TMA producer for Q (once), K / k_bar tiles (2-stage ring), H_bar
-//   warp 1     single-thread tcgen05.mma issuer: S_t = Q K_t^T (SS, K-major),
-//              O += P_{t-1} V_{t-1} (TS: P from TMEM, V MN-major), Q H_bar
-//   warp 2     TMEM allocator (256 columns: O | S0 | S1), then TMA producer for
-//              the second 64-column half of every V / v_hat tile
-//   warp 3     builds the union list from the two selection bitmasks, then is
-//              the TMA producer for the first half of every V / v_hat tile
-//              (a TMA issue stream runs at ~32 B/clk, so two streams halve the
-//              latency of the V loads on the critical path; tools/tma_bw.cu)
-//   warps 4-7  softmax / correction / epilogue, one thread per query row
-//              (TMEM lane), exp2 with log2(e)*scale folded into one FFMA, lazy
-//              rescale of O (only when the running max grows by > 2^8), P
-//              written back to TMEM as bf16 over the S columns it came from.
+// Why this shape (tools/l2_bw.cu, profiles/): the kernel streams a random
+// 16 KB K tile and a 16 KB V tile from L2 per 512 tensor cycles, ~64 B/clk/SM,
+// close to the chip's TMA delivery limit (~70 B/clk/SM), and a 16 KB TMA tile
+// takes 1300-2000 cycles under that load. Latency x bandwidth ~ 100+ KB must be
+// in flight per SM, so the design spends shared memory on K/V stages:
+//   * ONE CTA per SM, Q kept in TMEM (it is the A operand of both S = Q K^T and
+//     Q H_bar, TS-form MMAs), so shared memory holds only K/V rings:
+//     3 K + 3 V stages of two key blocks each (192 KB at d = 128);
+//   * key blocks go through the pipeline in pairs ("super-tiles" of 128 keys):
+//     S = Q [K_a; K_b]^T is one set of N=128 MMAs, and each barrier round trip,
+//     commit and softmax hand-off covers two blocks -- a single issuing thread
+//     is otherwise latency-bound on ~100 instructions per 64-key block;
+//   * TMEM (512 columns): O [0, 128) | Q [128, 192) | two S/P buffers of 128
+//     columns [256, 512) (P_g is written over the S_g columns it came from;
+//     see kSeparateP for the alternative).
+//
+// Warp roles (384 threads):
+//   warp 0     TMA producer: K / k_bar tiles (3-stage ring of pairs), H_bar at the end
+//   warp 1     single-thread tcgen05.mma issuer: S_t = Q K_t^T (TS: Q from TMEM,
+//              K K-major), O += P_u V_u (TS: P from TMEM, V MN-major), Q H_bar
+//   warp 2     TMEM allocator, then TMA producer for V columns [0, 64)
+//   warp 3     builds the union list from the two selection bitmasks, then TMA
+//              producer for V columns [64, 128) (two issue streams for V)
+//   warps 4-7  softmax / correction / epilogue of query block 2t   (warpgroup A)
+//   warps 8-11 softmax / correction / epilogue of query block 2t+1 (warpgroup B)
+// TMEM lane layout: lane q4*32 + hh*16 + r16 holds row q4*16 + r16 of query
+// block 2t + hh. Warp q4 of warpgroup hh owns those 16 lanes (16x32bx2 view:
+// thread t holds row t & 15, columns [32*(t >> 4), +32) of each 64-key half), so
+// each block's exponentials use all four SM sub-partitions (all four MUFU
+// units), and the two blocks' online softmaxes run in parallel. exp2 with
+// log2(e)*scale folded into one FFMA; lazy rescale of O (only when the running
+// max grows by > 2^8); P written back to TMEM as bf16 over its S columns.
 #include "kernels.h"
 #include "sm100.cuh"
 
@@ -45,34 +60,39 @@ using namespace pisa_sm100;
 
 namespace {
 
-constexpr int kThreads = 256;
+constexpr int kThreads = 384;
+constexpr int kSK = 3;  // K ring stages (two key blocks each)
+constexpr int kSV = 3;  // V ring stages (two key blocks each)
+constexpr int kSB = 2;  // S/P TMEM buffers (128 columns each)
 constexpr float kRescaleThresh = 8.0f;  // log2 units
-// Fraction of softmax exponentials computed by ex2_poly on the FMA pipe (FA4's
-// trick for MUFU-bound softmax): 0 = all on MUFU. With two CTAs sharing each
-// SMSP the softmax here is issue-bound, not MUFU-bound, so it is off.
-constexpr int kPolyEvery = 0;
-constexpr uint32_t kColO = 0, kColS = 128;
+constexpr uint32_t kColO = 0, kColQ = 128, kColP = 192, kColS = 256;
+// P placement. false: P_g overwrites the S_g buffer it came from (S_{g+2} is
+// issued after PV_g). true: P has its own TMEM buffer [192, 256) and S_{g+2}
+// is issued as soon as the softmax has S_g in registers -- but the single P
+// buffer then serialises softmax_g behind PV_{g-1} (measured slower: 27.4 vs
+// 25.5 ms at Wan2.1-14B).
+constexpr bool kSeparateP = false;
 
 template <int D>
 struct FusedCfg {
-    static constexpr int kQ = 128 * D * 2;  // Q tile bytes (2 halves of 128 rows for D=128)
-    static constexpr int kKV = 64 * D * 2;  // one K or V stage
-    static constexpr int kOffQ = 0;
-    static constexpr int kOffK = kQ;
-    static constexpr int kOffV = kQ + 2 * kKV;
-    static constexpr int kOffBar = kQ + 4 * kKV;
-    static constexpr int kBarBytes = 256;
+    // one K or V stage: two 64-key blocks, laid out [64-col half][128 rows] with
+    // 128-byte rows (SW128), so a stage is one N=128 (K) / K=128 (V) operand
+    static constexpr int kKV = 2 * 64 * D * 2;
+    static constexpr int kOffK = 0;
+    static constexpr int kOffV = kSK * kKV;
+    static constexpr int kOffBar = (kSK + kSV) * kKV;
+    static constexpr int kBarBytes = 512;
     static constexpr int kOffMask = kOffBar + kBarBytes;
 };
 
 struct Bars {
-    uint64_t q_full, h_full, qh_full;
-    uint64_t k_full[2], k_empty[2], v_full[2], v_empty[2];
-    uint64_t s_full[2], p_full[2];
-    uint64_t o_done;
+    uint64_t q_ready, h_full, qh_full;
+    uint64_t k_full[kSK], k_empty[kSK], v_full[kSV], v_empty[kSV];
+    uint64_t s_full[kSB], s_free[kSB], p_full[kSB], pv_done[kSB];
     uint32_t tmem_base;
     uint32_t n_union;
 };
+static_assert(sizeof(Bars) <= 512, "barrier block");
 
 #if PISA_TRACE
 // Timeline of one CTA: trace[role][t] = clock64 delta from kernel start.
@@ -85,51 +105,43 @@ __device__ __forceinline__ void trace_mark(const FusedArgs& a, int role, int t, 
 #define TRACE(role, t) ((void)0)
 #endif
 
-// max of 64 values as a 3-level tree (FMNMX3-friendly, short dependency chain)
-__device__ __forceinline__ float max64(const float* x) {
-    float m[8];
+// max of 32 values as a tree
+__device__ __forceinline__ float max32(const float* x) {
+    float m[4];
 #pragma unroll
-    for (int j = 0; j < 8; ++j)
+    for (int j = 0; j < 4; ++j)
         m[j] = fmaxf(fmaxf(fmaxf(x[8 * j], x[8 * j + 1]), fmaxf(x[8 * j + 2], x[8 * j + 3])),
                      fmaxf(fmaxf(x[8 * j + 4], x[8 * j + 5]), fmaxf(x[8 * j + 6], x[8 * j + 7])));
-    return fmaxf(fmaxf(fmaxf(m[0], m[1]), fmaxf(m[2], m[3])), fmaxf(fmaxf(m[4], m[5]), fmaxf(m[6], m[7])));
+    return fmaxf(fmaxf(m[0], m[1]), fmaxf(m[2], m[3]));
 }
 
-// Writes P (bf16 pairs) over the first 32 S columns and releases the S buffer.
-__device__ __forceinline__ void publish_p(uint32_t sc, const uint32_t (&pk)[32], uint64_t* bar,
-                                          int lane) {
-    tmem_st32(sc, pk);
-    tmem_st_wait();
-    tc_fence_before();
-    __syncwarp();
-    if (lane == 0) mbar_arrive(bar);
-}
-
+// Rescales this thread's half of the O columns of its row: 16x32bx2 view, the
+// half-warp split is D/2 columns (thread t < 16: [0, D/2), t >= 16: [D/2, D)).
 template <int D>
 __device__ __forceinline__ void rescale_o(uint32_t tmem_o, float f) {
 #pragma unroll 1
-    for (int cc = 0; cc < D; cc += 32) {
+    for (int cc = 0; cc < D / 2; cc += 32) {
         uint32_t ro[32];
-        tmem_ld32(tmem_o + cc, ro);
+        tmem_ld16x2_32<D / 2>(tmem_o + cc, ro);
         tmem_ld_wait(ro);
 #pragma unroll
         for (int i = 0; i < 32; ++i) ro[i] = __float_as_uint(__uint_as_float(ro[i]) * f);
-        tmem_st32(tmem_o + cc, ro);
+        tmem_st16x2_32<D / 2>(tmem_o + cc, ro);
     }
 }
 
 template <int D>
-__global__ void __launch_bounds__(kThreads, 2)
-    fused_attn_kernel(const __grid_constant__ CUtensorMap tmQ,
-                      const __grid_constant__ CUtensorMap tmK,
+__global__ void __launch_bounds__(kThreads, 1)
+    fused_attn_kernel(const __grid_constant__ CUtensorMap tmK,
                       const __grid_constant__ CUtensorMap tmV,
                       const __grid_constant__ CUtensorMap tmKb,
                       const __grid_constant__ CUtensorMap tmVh,
                       const __grid_constant__ CUtensorMap tmH, FusedArgs a) {
     using Cfg = FusedCfg<D>;
-    extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                               ~uintptr_t(1023));
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    // 1 KB alignment for the SW128 stages, by offset (keeps the pointer's
+    // shared-space provenance: loads of ulist / masks compile to LDS).
+    uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     Bars& bar = *reinterpret_cast<Bars*>(smem + Cfg::kOffBar);
     uint32_t* maskA = reinterpret_cast<uint32_t*>(smem + Cfg::kOffMask);
     uint32_t* maskB = maskA + a.W;
@@ -151,25 +163,31 @@ __global__ void __launch_bounds__(kThreads, 2)
 
     // ------------------------------------------------------------ setup --
     if (threadIdx.x == 0) {
-        mbar_init(&bar.q_full, 1);
+        mbar_init(&bar.q_ready, 8);  // one arrive per softmax warp
         mbar_init(&bar.h_full, 1);
         mbar_init(&bar.qh_full, 1);
-        for (int s = 0; s < 2; ++s) {
+        for (int s = 0; s < kSK; ++s) {
             mbar_init(&bar.k_full[s], 1);
             mbar_init(&bar.k_empty[s], 1);
+        }
+        for (int s = 0; s < kSV; ++s) {
             mbar_init(&bar.v_full[s], D / 64);  // one arrive per V producer (one per 64-col half)
             mbar_init(&bar.v_empty[s], 1);
-            mbar_init(&bar.s_full[s], 1);
-            mbar_init(&bar.p_full[s], 4);
         }
-        mbar_init(&bar.o_done, 1);
+        for (int s = 0; s < kSB; ++s) {
+            mbar_init(&bar.s_full[s], 1);
+            mbar_init(&bar.s_free[s], 8);  // one arrive per softmax warp
+        }
+        for (int s = 0; s < kSB; ++s) {
+            mbar_init(&bar.p_full[s], 8);
+            mbar_init(&bar.pv_done[s], 1);
+        }
         fence_mbar_init();
-        tma_prefetch(&tmQ);
         tma_prefetch(&tmK);
         tma_prefetch(&tmV);
     }
     if (warp == 2) {
-        tmem_alloc(&bar.tmem_base, 256);
+        tmem_alloc(&bar.tmem_base, 512);
         tmem_relinquish();
     }
     if (warp == 3) {
@@ -209,154 +227,228 @@ __global__ void __launch_bounds__(kThreads, 2)
     tc_fence_after();
     const uint32_t tmem = bar.tmem_base;
     const int U = int(bar.n_union);
-    const int T = U + (tail ? a.nchunk2 : 0);  // key tiles: union blocks, then centroid tiles
+    // Key tiles are processed in pairs ("super-tiles" of 128 keys): one K / V
+    // stage, one S buffer, one barrier round trip and N=128 S MMAs per pair.
+    // Phase 1 pairs consecutive union entries, Phase 2 consecutive centroid
+    // chunks; an odd tail is padded with a copy of the previous entry whose use
+    // flags are zero (fully masked: P = 0 and finite V rows).
+    const int G1 = (U + 1) >> 1;
+    const int G = G1 + (tail ? (a.nchunk2 + 1) >> 1 : 0);
+    // key-block row and use flags of sub-tile j of super-tile g (g < G1)
+    auto exact_entry = [&](int g, int j) -> uint32_t {
+        const int i = 2 * g + j;
+        return i < U ? uint32_t(ulist[i]) : (uint32_t(ulist[2 * g]) & 0x3FFFu);
+    };
+    auto tile_row = [&](int g, int j) -> int {
+        if (g < G1) return int(exact_entry(g, j) & 0x3FFFu) * 64;
+        const int c = 2 * (g - G1) + j;
+        return (c < a.nchunk2 ? c : c - 1) * 64;
+    };
 
     if (warp == 0) {
-        // ------------------------------------------------ producer: Q, K, H --
-        uint8_t* sQ = smem + Cfg::kOffQ;
-        if (elect_one()) {
-            mbar_expect_tx(&bar.q_full, Cfg::kQ);
-#pragma unroll
-            for (int half = 0; half < D / 64; ++half)
-                tma_load_4d(sQ + half * 16384, &tmQ, &bar.q_full, half * 64, tile * 128, h, b);
-        }
-        __syncwarp();
-        for (int t = 0; t < T; ++t) {
-            const int s = t & 1;
+        // ------------------------------------------------ producer: K, H --
+        int s = 0;
+        uint32_t ph = 0;
+        for (int g = 0; g < G; ++g) {
             uint8_t* sK = smem + Cfg::kOffK + s * Cfg::kKV;
-            mbar_wait(&bar.k_empty[s], ((t >> 1) & 1) ^ 1);
-            const bool exact = t < U;
-            const int row = exact ? int(ulist[t] & 0x3FFFu) * 64 : (t - U) * 64;
+            mbar_wait(&bar.k_empty[s], ph ^ 1);
+            const bool exact = g < G1;
+            const int r0 = tile_row(g, 0), r1 = tile_row(g, 1);
             if (elect_one()) {
                 mbar_expect_tx(&bar.k_full[s], Cfg::kKV);
 #pragma unroll
                 for (int half = 0; half < D / 64; ++half) {
-                    if (exact)
-                        tma_load_4d(sK + half * 8192, &tmK, &bar.k_full[s], half * 64, row, h, b);
-                    else
-                        tma_load_3d(sK + half * 8192, &tmKb, &bar.k_full[s], half * 64, row, bh);
+                    if (exact) {
+                        tma_load_4d(sK + half * 16384, &tmK, &bar.k_full[s], half * 64, r0, h, b);
+                        tma_load_4d(sK + half * 16384 + 8192, &tmK, &bar.k_full[s], half * 64, r1, h, b);
+                    } else {
+                        tma_load_3d(sK + half * 16384, &tmKb, &bar.k_full[s], half * 64, r0, bh);
+                        tma_load_3d(sK + half * 16384 + 8192, &tmKb, &bar.k_full[s], half * 64, r1, bh);
+                    }
                 }
-                TRACE(0, t);
+                TRACE(0, g);
             }
             __syncwarp();
+            if (++s == kSK) { s = 0; ph ^= 1u; }
         }
         if (first_order) {
-            // H_bar (D rows) into the K ring: half c lands in K stage c.
-            for (int t = T; t < T + 2; ++t) mbar_wait(&bar.k_empty[t & 1], ((t >> 1) & 1) ^ 1);
+            // H_bar (D x D) into K stage 0 once every S MMA is done
+            for (int i = 0; i < kSK; ++i) {
+                mbar_wait(&bar.k_empty[s], ph ^ 1);
+                if (++s == kSK) { s = 0; ph ^= 1u; }
+            }
             if (elect_one()) {
                 mbar_expect_tx(&bar.h_full, D * D * 2);
 #pragma unroll
                 for (int half = 0; half < D / 64; ++half)
-                    tma_load_3d(smem + Cfg::kOffK + half * Cfg::kKV, &tmH, &bar.h_full, half * 64, 0, bh);
+                    tma_load_3d(smem + Cfg::kOffK + half * 16384, &tmH, &bar.h_full, half * 64, 0, bh);
             }
             __syncwarp();
         }
-    } else if (warp == 3 || (warp == 2 && D == 128)) {
+    } else if (warp == 2 || (warp == 3 && D == 128)) {
         // -------------------------------------------- producers: V halves --
-        // Each 64-column half of a V tile has its own issuing warp (two TMA
-        // issue streams; V is on the critical path: V_t can only load once
-        // PV_{t-2} has retired).
-        const int vh = (warp == 3) ? 0 : 1;
-        for (int t = 0; t < T; ++t) {
-            const int s = t & 1;
-            uint8_t* sV = smem + Cfg::kOffV + s * Cfg::kKV + vh * 8192;
-            mbar_wait(&bar.v_empty[s], ((t >> 1) & 1) ^ 1);
-            const bool exact = t < U;
-            const int row = exact ? int(ulist[t] & 0x3FFFu) * 64 : (t - U) * 64;
+        const int vh = warp - 2;
+        int s = 0;
+        uint32_t ph = 0;
+        for (int g = 0; g < G; ++g) {
+            uint8_t* sV = smem + Cfg::kOffV + s * Cfg::kKV + vh * 16384;
+            mbar_wait(&bar.v_empty[s], ph ^ 1);
+            const bool exact = g < G1;
+            const int r0 = tile_row(g, 0), r1 = tile_row(g, 1);
             if (elect_one()) {
-                mbar_expect_tx(&bar.v_full[s], 8192);
-                if (exact)
-                    tma_load_4d(sV, &tmV, &bar.v_full[s], vh * 64, row, h, b);
-                else
-                    tma_load_3d(sV, &tmVh, &bar.v_full[s], vh * 64, row, bh);
-                if (vh == 0) TRACE(1, t);
+                mbar_expect_tx(&bar.v_full[s], 16384);
+                if (exact) {
+                    tma_load_4d(sV, &tmV, &bar.v_full[s], vh * 64, r0, h, b);
+                    tma_load_4d(sV + 8192, &tmV, &bar.v_full[s], vh * 64, r1, h, b);
+                } else {
+                    tma_load_3d(sV, &tmVh, &bar.v_full[s], vh * 64, r0, bh);
+                    tma_load_3d(sV + 8192, &tmVh, &bar.v_full[s], vh * 64, r1, bh);
+                }
+                if (vh == 0) TRACE(1, g);
             }
             __syncwarp();
+            if (++s == kSV) { s = 0; ph ^= 1u; }
         }
     } else if (warp == 1) {
         // ------------------------------------------------------------- MMA --
-        // Whole-warp loop, one elected lane issues (and commits: a commit
-        // tracks the MMAs of the thread that executes it).
-        constexpr uint32_t idS = idesc_bf16(128, 64, 0, 0);   // S = Q K^T
+        // Lean issue loop: shared-memory descriptors are built once and
+        // advanced by adding (byte offset >> 4) to their address field; ring
+        // positions advance incrementally (no div/mod). One elected lane issues
+        // (and commits: a commit tracks the MMAs of the thread that runs it).
+        constexpr uint32_t idS = idesc_bf16(128, 128, 0, 0);  // S = Q K^T, 128 keys (Q from TMEM)
         constexpr uint32_t idPV = idesc_bf16(128, D, 0, 1);   // O += P V (V MN-major)
         constexpr uint32_t idQH = idesc_bf16(128, D, 0, 1);   // Q H_bar
-        const uint32_t qbase = smem_u32(smem + Cfg::kOffQ);
-        auto issue_pv = [&](int u) {
-            const int s = u & 1;
-            const uint32_t ph = (u >> 1) & 1;
-            mbar_wait(&bar.p_full[s], ph);
-            mbar_wait(&bar.v_full[s], ph);
+        const uint64_t kdesc0 = sdesc_sw128(smem_u32(smem + Cfg::kOffK), 16, 1024);
+        const uint64_t vdesc0 = sdesc_sw128(smem_u32(smem + Cfg::kOffV), 16384, 1024);
+        const uint64_t hdesc0 = sdesc_sw128(smem_u32(smem + Cfg::kOffK), 16384, 1024);
+        const uint32_t tS = tmem + kColS, tQ = tmem + kColQ, tO = tmem + kColO, tP = tmem + kColP;
+        int sk = 0;                     // K stage of the next S
+        uint32_t phk = 0;               // its k_full parity
+        int sv = 0;                     // V stage of the next PV
+        uint32_t phv = 0;               // its v_full parity
+        auto issue_s = [&](int g) {     // S_g into S buffer g & 1
+            mbar_wait<true>(&bar.k_full[sk], phk);
             tc_fence_after();
-            const uint32_t vb = smem_u32(smem + Cfg::kOffV + s * Cfg::kKV);
             if (elect_one()) {
-                TRACE(10, u);
+                TRACE(8, g);
+                const uint64_t kd = kdesc0 + uint64_t(sk * (Cfg::kKV >> 4));
+                const uint32_t d = tS + uint32_t(g & 1) * 128;
 #pragma unroll
-                for (int ks = 0; ks < 4; ++ks)
-                    mma_ts(tmem + kColO, tmem + kColS + s * 64 + ks * 8,
-                           sdesc_sw128(vb + ks * 2048, 8192, 1024), idPV, (u | ks) != 0);
-                mma_commit(&bar.v_empty[s]);
-                mma_commit(&bar.o_done);
-                TRACE(3, u);
+                for (int ks = 0; ks < D / 16; ++ks)
+                    mma_ts(d, tQ + ks * 8, kd + uint64_t(((ks >> 2) * 16384 + (ks & 3) * 32) >> 4), idS, ks != 0);
+                mma_commit(&bar.k_empty[sk]);
+                mma_commit(&bar.s_full[g & 1]);
+                TRACE(2, g);
             }
             __syncwarp();
+            if (++sk == kSK) { sk = 0; phk ^= 1u; }
         };
-        mbar_wait(&bar.q_full, 0);
-        for (int t = 0; t < T; ++t) {
-            const int s = t & 1;
-            mbar_wait(&bar.k_full[s], (t >> 1) & 1);
+        auto issue_pv = [&](int g) {    // O += P_g V_g
+            mbar_wait<true>(&bar.p_full[g & 1], uint32_t((g >> 1) & 1));
+            TRACE(9, g);
+            mbar_wait<true>(&bar.v_full[sv], phv);
             tc_fence_after();
-            const uint32_t kb = smem_u32(smem + Cfg::kOffK + s * Cfg::kKV);
             if (elect_one()) {
-                TRACE(8, t);
+                TRACE(10, g);
+                const uint64_t vd = vdesc0 + uint64_t(sv * (Cfg::kKV >> 4));
 #pragma unroll
-                for (int ks = 0; ks < D / 16; ++ks) {
-                    const uint32_t hq = (ks >> 2), kq = (ks & 3) * 32;
-                    mma_ss(tmem + kColS + s * 64,
-                           sdesc_sw128(qbase + hq * 16384 + kq, 16, 1024),
-                           sdesc_sw128(kb + hq * 8192 + kq, 16, 1024), idS, ks != 0);
+                for (int ks = 0; ks < 8; ++ks) {
+                    const uint32_t pa = kSeparateP ? tP + (ks >> 2) * 32 + (ks & 3) * 8
+                                                   : tS + uint32_t(g & 1) * 128 + (ks >> 2) * 64 + (ks & 3) * 8;
+                    mma_ts(tO, pa, vd + uint64_t((ks * 2048) >> 4), idPV, (g == 0 && ks == 0) ? 0u : 1u);
                 }
-                mma_commit(&bar.k_empty[s]);
-                mma_commit(&bar.s_full[s]);
-                TRACE(2, t);
+                mma_commit(&bar.v_empty[sv]);
+                mma_commit(&bar.pv_done[g & 1]);
+                TRACE(3, g);
             }
             __syncwarp();
-            if (t > 0) issue_pv(t - 1);
+            if (++sv == kSV) { sv = 0; phv ^= 1u; }
+        };
+        static_assert(kSB == 2, "two S buffers");
+        mbar_wait<true>(&bar.q_ready, 0);
+        tc_fence_after();
+        for (int g = 0; g < kSB && g < G; ++g) issue_s(g);
+        for (int g = 0; g < G; ++g) {
+            if (kSeparateP) {
+                // S_{g+2} as soon as the softmax has S_g in registers (it
+                // overlaps the softmax of g), then PV_g once P_g is in TMEM
+                if (g + kSB < G) {
+                    mbar_wait<true>(&bar.s_free[g & 1], uint32_t((g >> 1) & 1));
+                    issue_s(g + kSB);
+                }
+                issue_pv(g);
+            } else {
+                issue_pv(g);  // in-order tensor pipe: S_{g+2} below overwrites P_g after PV_g read it
+                if (g + kSB < G) issue_s(g + kSB);
+            }
         }
-        issue_pv(T - 1);
         if (first_order) {
-            mbar_wait(&bar.h_full, 0);
+            mbar_wait<true>(&bar.h_full, 0);
             tc_fence_after();
         }
-        const uint32_t hb = smem_u32(smem + Cfg::kOffK);
         if (elect_one()) {
             if (first_order) {
 #pragma unroll
-                for (int ks = 0; ks < D / 16; ++ks) {
-                    const uint32_t hq = (ks >> 2), kq = (ks & 3) * 32;
-                    mma_ss(tmem + kColS, sdesc_sw128(qbase + hq * 16384 + kq, 16, 1024),
-                           sdesc_sw128(hb + ks * 2048, Cfg::kKV, 1024), idQH, ks != 0);
-                }
+                for (int ks = 0; ks < D / 16; ++ks)
+                    mma_ts(tS, tQ + ks * 8, hdesc0 + uint64_t((ks * 2048) >> 4), idQH, ks != 0);
             }
             mma_commit(&bar.qh_full);  // also: every PV done
         }
         __syncwarp();
     } else if (warp >= 4) {
-        // ------------------------------------------------ softmax warpgroup --
-        const int q4 = warp & 3;            // TMEM lane quadrant
-        const int row = q4 * 32 + lane;     // 0..127 within the tile
-        const int half = row >> 6;          // 0: block iA, 1: block iB (warp-uniform)
-        const int grow = tile * 128 + row;  // query row within the sequence
-        const bool active = grow < a.L;
-        const bool warp_active = __all_sync(0xffffffffu, active);
-        const uint32_t* hmask = half ? maskB : maskA;
-        const uint32_t lane_off = uint32_t(q4 * 32) << 16;
+        // ------------------------------------------------ softmax warpgroups --
+        const int hh = (warp - 4) >> 2;  // query block 2*tile + hh
+        const int q4 = warp & 3;         // TMEM lane quadrant
+        const int r16 = lane & 15;
+        const int ch = lane >> 4;        // column half of a 64-key sub-tile
         const float sl2 = a.scale * 1.4426950408889634f;
+        const uint32_t lbase = tmem + (uint32_t(q4 * 32 + hh * 16) << 16);
+        const int grow = (2 * tile + hh) * 64 + q4 * 16 + r16;
+        const bool active = grow < a.L;
+        const bool wact = __all_sync(0xffffffffu, active);
+        const uint32_t* hmask = hh ? maskB : maskA;
+        const __nv_bfloat16* qrow = a.q + size_t(b) * a.qs_b + size_t(h) * a.qs_h + size_t(grow) * a.qs_l;
 
-        float m = -INFINITY, l = 0.f, lt = 0.f;
-        // Online-softmax step shared by both phases. x: raw scores (masked = -inf).
-        // Returns the shift to exponentiate against; rescales O when needed.
-        auto update_max = [&](float bm_raw, int t) -> float {
-            const float bm = bm_raw * sl2;
+        // Q -> TMEM (bf16 pairs, lane = row): this thread's row, packed columns
+        // [ch * D/4, ch * D/4 + D/4).
+        {
+            uint32_t qr[32];
+            const uint4* src = reinterpret_cast<const uint4*>(qrow) + ch * (D / 16);
+#pragma unroll
+            for (int i = 0; i < D / 16; ++i) {
+                const uint4 v = active ? src[i] : make_uint4(0u, 0u, 0u, 0u);
+                qr[4 * i] = v.x;
+                qr[4 * i + 1] = v.y;
+                qr[4 * i + 2] = v.z;
+                qr[4 * i + 3] = v.w;
+            }
+            if constexpr (D == 128) {
+                tmem_st16x2_32<32>(lbase + kColQ, qr);
+            } else {
+                tmem_st16x2_16<16>(lbase + kColQ, reinterpret_cast<const uint32_t(&)[16]>(qr));
+            }
+            tmem_st_wait();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&bar.q_ready);
+        }
+
+        float m = -INFINITY, l = 0.f, lt = 0.f;  // l, lt: this thread's partial sums
+
+        // Online-softmax step over one 128-key super-tile: bm_loc = max of this
+        // thread's live scores (masked = -inf). Returns the shift to
+        // exponentiate against (log2 units); rescales O lazily when the max
+        // grows by > 2^8 (after PV_{g-1}: O must be quiescent).
+        auto wait_pv_prev = [&](int g) {  // PV_{g-1} done
+            if (g > 0) {
+                // PV_{g-3} is known done (S_g, or P_{g-1}, came after it), so
+                // the parity names PV_{g-1} unambiguously
+                mbar_wait<true>(&bar.pv_done[(g - 1) & 1], uint32_t(((g - 1) >> 1) & 1));
+                tc_fence_after();
+            }
+        };
+        auto update_max = [&](float bm_loc, int g) -> float {
+            const float bm = fmaxf(bm_loc, __shfl_xor_sync(0xffffffffu, bm_loc, 16)) * sl2;
             float m_use = m;
             bool resc = false;
             if (bm > -INFINITY) {
@@ -369,152 +461,179 @@ __global__ void __launch_bounds__(kThreads, 2)
             }
             if (__any_sync(0xffffffffu, resc)) {
                 const float f = resc ? ex2(m - m_use) : 1.f;
-                mbar_wait(&bar.o_done, (t - 1) & 1);  // PV_{t-1} done (t >= 1 whenever resc)
-                tc_fence_after();
-                rescale_o<D>(tmem + lane_off + kColO, f);
+                wait_pv_prev(g);
+                rescale_o<D>(lbase + kColO, f);
                 l *= f;
                 lt *= f;
             }
             m = m_use;
-            return (m == -INFINITY) ? 0.f : m;  // all-masked row: p = 0, not NaN
+            return (m_use == -INFINITY) ? 0.f : m_use;  // all-masked row: p = 0, not NaN
         };
-
-        // ---- Phase 1: exact blocks of the union
-        for (int t = 0; t < U; ++t) {
-            const int s = t & 1;
-            const uint32_t sc = tmem + lane_off + kColS + s * 64;
-            const uint32_t e = ulist[t];
-            const bool use = ((e >> (14 + half)) & 1u) != 0;  // warp-uniform
-            const int nvalid = (int(e & 0x3FFFu) == a.N - 1) ? n_last : 64;
-            mbar_wait(&bar.s_full[s], (t >> 1) & 1);
-            tc_fence_after();
-            TRACE(4 + (q4 >> 1), t);
-            uint32_t pk[32];
-            if (use) {
-                uint32_t ra[32], rb[32];
-                tmem_ld32(sc, ra);
-                tmem_ld32(sc + 32, rb);
-                tmem_ld_wait(ra);
-                tmem_ld_wait(rb);
-                float x[64];
-#pragma unroll
-                for (int i = 0; i < 32; ++i) {
-                    x[i] = __uint_as_float(ra[i]);
-                    x[i + 32] = __uint_as_float(rb[i]);
-                }
-                const bool full_tile = warp_active && nvalid == 64;
-                if (!full_tile) {  // ragged last key block / rows past L
-#pragma unroll
-                    for (int i = 0; i < 64; ++i) x[i] = (active && i < nvalid) ? x[i] : -INFINITY;
-                }
-                const float mm = update_max(max64(x), t);
-                float ps[4] = {0.f, 0.f, 0.f, 0.f};
-                if (kPolyEvery > 0 && full_tile) {
-                    // every kPolyEvery-th exponential on the FMA pipe, the rest on MUFU
-#pragma unroll
-                    for (int i = 0; i < 64; i += 2) {
-                        const float a0 = fmaf(x[i], sl2, -mm), a1 = fmaf(x[i + 1], sl2, -mm);
-                        const float p0 = (kPolyEvery > 0 && i % kPolyEvery == kPolyEvery - 1) ? ex2_poly(a0) : ex2(a0);
-                        const float p1 = (kPolyEvery > 0 && (i + 1) % kPolyEvery == kPolyEvery - 1) ? ex2_poly(a1) : ex2(a1);
-                        ps[(i >> 1) & 3] += p0 + p1;
-                        pk[i >> 1] = pack_bf16(p0, p1);
-                    }
-                } else {
-#pragma unroll
-                    for (int i = 0; i < 64; i += 2) {
-                        const float p0 = ex2(fmaf(x[i], sl2, -mm));
-                        const float p1 = ex2(fmaf(x[i + 1], sl2, -mm));
-                        ps[(i >> 1) & 3] += p0 + p1;
-                        pk[i >> 1] = pack_bf16(p0, p1);
-                    }
-                }
-                l += (ps[0] + ps[1]) + (ps[2] + ps[3]);
-            } else {
-#pragma unroll
-                for (int i = 0; i < 32; ++i) pk[i] = 0u;
+        // S_g is in registers: its TMEM buffer may take S_{g+2}
+        auto free_s = [&](int g) {
+            if (kSeparateP) {
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&bar.s_free[g & 1]);
             }
-            publish_p(sc, pk, &bar.p_full[s], lane);
-            TRACE(6 + (q4 >> 1), t);
-        }
-        // ---- Phase 2: centroid tiles, column mask = own selection, weight n_j
-        for (int t = U; t < T; ++t) {
-            const int s = t & 1;
-            const uint32_t sc = tmem + lane_off + kColS + s * 64;
-            const int c = t - U;
-            const uint32_t cm_lo = hmask[2 * c];
-            const uint32_t cm_hi = (2 * c + 1 < a.W) ? hmask[2 * c + 1] : 0xffffffffu;
-            const int nvalid = min(64, a.N - c * 64);
-            const bool has_last = (c == a.nchunk2 - 1) && n_last != 64;
-            mbar_wait(&bar.s_full[s], (t >> 1) & 1);
+        };
+        auto publish_p = [&](int g) {
+            tmem_st_wait();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&bar.p_full[g & 1]);
+        };
+        // P of sub-tile j of super-tile g: own buffer, or over the S columns
+        auto p_addr = [&](int g, int j) -> uint32_t {
+            return kSeparateP ? lbase + kColP + 32 * j : lbase + kColS + (g & 1) * 128 + 64 * j;
+        };
+        const uint32_t kZero16[16] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
+
+        // ---- Phase 1: exact blocks of the union, two per super-tile
+        for (int g = 0; g < G1; ++g) {
+            const uint32_t e0 = ulist[2 * g];
+            const uint32_t e1 = (2 * g + 1 < U) ? uint32_t(ulist[2 * g + 1]) : 0u;  // pad: unused
+            const bool use0 = (e0 >> (14 + hh)) & 1u, use1 = (e1 >> (14 + hh)) & 1u;  // warp-uniform
+            const int nv0 = (int(e0 & 0x3FFFu) == a.N - 1) ? n_last : 64;
+            const int nv1 = (int(e1 & 0x3FFFu) == a.N - 1) ? n_last : 64;
+            const uint32_t sc = lbase + kColS + (g & 1) * 128;
+            mbar_wait<true>(&bar.s_full[g & 1], uint32_t((g >> 1) & 1));
             tc_fence_after();
-            uint32_t ra[32], rb[32];
-            tmem_ld32(sc, ra);
-            tmem_ld32(sc + 32, rb);
-            tmem_ld_wait(ra);
-            tmem_ld_wait(rb);
-            float x[64];
+            if (q4 == 0) TRACE(4 + hh, g);
+            if (use0 || use1) {
+                // scores as raw bits, masked in place (only the ragged last key
+                // block / rows past L need masks); loads only of the selected
+                // sub-tiles
+                uint32_t r0[32], r1[32];
+                if (use0) tmem_ld16x2_32<32>(sc, r0);
+                if (use1) tmem_ld16x2_32<32>(sc + 64, r1);
+                tmem_ld_wait(r0);
+                tmem_ld_wait(r1);
+                free_s(g);
+                if (!(wact && nv0 == 64 && nv1 == 64)) {
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) {
+                        const int col = ch * 32 + i;
+                        if (!(active && col < nv0)) r0[i] = 0xff800000u;  // -inf
+                        if (!(active && col < nv1)) r1[i] = 0xff800000u;
+                    }
+                }
+                float bm_loc = -INFINITY;
+                if (use0) bm_loc = max32(reinterpret_cast<const float*>(r0));
+                if (use1) bm_loc = fmaxf(bm_loc, max32(reinterpret_cast<const float*>(r1)));
+                const float mm = update_max(bm_loc, g);
+                // exponentials only for the selected sub-tiles (warp-uniform)
+                auto expo_store = [&](const uint32_t (&r)[32], uint32_t addr) {
+                    uint32_t pk[16];
+                    float ps[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+                    for (int i = 0; i < 32; i += 2) {
+                        const float p0 = ex2(fmaf(__uint_as_float(r[i]), sl2, -mm));
+                        const float p1 = ex2(fmaf(__uint_as_float(r[i + 1]), sl2, -mm));
+                        ps[(i >> 1) & 3] += p0 + p1;
+                        pk[i >> 1] = pack_bf16(p0, p1);
+                    }
+                    l += (ps[0] + ps[1]) + (ps[2] + ps[3]);
+                    tmem_st16x2_16<16>(addr, pk);  // P (bf16 pairs)
+                };
+                if (kSeparateP) wait_pv_prev(g);  // the P buffer is free once PV_{g-1} read it
+                if (use0) expo_store(r0, p_addr(g, 0)); else tmem_st16x2_16<16>(p_addr(g, 0), kZero16);
+                if (use1) expo_store(r1, p_addr(g, 1)); else tmem_st16x2_16<16>(p_addr(g, 1), kZero16);
+            } else {
+                free_s(g);
+                if (kSeparateP) wait_pv_prev(g);
+                tmem_st16x2_16<16>(p_addr(g, 0), kZero16);
+                tmem_st16x2_16<16>(p_addr(g, 1), kZero16);
+            }
+            publish_p(g);
+            if (q4 == 0) TRACE(6 + hh, g);
+        }
+        // ---- Phase 2: centroid chunks, two per super-tile; column mask = own
+        // selection, weight n_j (the ragged last block weighs n_last)
+        for (int g = G1; g < G; ++g) {
+            const int c0 = 2 * (g - G1);
+            const uint32_t sc = lbase + kColS + (g & 1) * 128;
+            // this thread's 32 columns of chunk c: blocks c*64 + ch*32 + i
+            auto colmask = [&](int c) -> uint32_t {
+                const int w = 2 * c + ch;
+                return (c < a.nchunk2 && w < a.W) ? hmask[w] : 0xffffffffu;
+            };
+            const uint32_t cm0 = colmask(c0), cm1 = colmask(c0 + 1);
+            const int nv0 = min(64, a.N - c0 * 64), nv1 = min(64, a.N - (c0 + 1) * 64);
+            mbar_wait<true>(&bar.s_full[g & 1], uint32_t((g >> 1) & 1));
+            tc_fence_after();
+            uint32_t r0[32], r1[32];
+            tmem_ld16x2_32<32>(sc, r0);
+            tmem_ld16x2_32<32>(sc + 64, r1);
+            tmem_ld_wait(r0);
+            tmem_ld_wait(r1);
+            free_s(g);
 #pragma unroll
             for (int i = 0; i < 32; ++i) {
-                const bool ok_lo = active && i < nvalid && !((cm_lo >> i) & 1u);
-                const bool ok_hi = active && i + 32 < nvalid && !((cm_hi >> i) & 1u);
-                x[i] = ok_lo ? __uint_as_float(ra[i]) : -INFINITY;
-                x[i + 32] = ok_hi ? __uint_as_float(rb[i]) : -INFINITY;
+                const int col = ch * 32 + i;
+                if (!(active && col < nv0 && !((cm0 >> i) & 1u))) r0[i] = 0xff800000u;
+                if (!(active && col < nv1 && !((cm1 >> i) & 1u))) r1[i] = 0xff800000u;
             }
-            const float mm = update_max(max64(x), t);
-            uint32_t pk[32];
-            float ps0 = 0.f, ps1 = 0.f;
+            const float mm = update_max(fmaxf(max32(reinterpret_cast<const float*>(r0)),
+                                              max32(reinterpret_cast<const float*>(r1))), g);
+            // column (within this thread's 32) of the ragged last block, if here
+            const int lb = a.N - 1 - c0 * 64 - ch * 32;  // 0..31 -> sub-tile 0, 64..95 -> sub-tile 1
+            const bool ragged = n_last != 64;
+            float ps = 0.f, plast = 0.f;
+            auto expo_store = [&](const uint32_t (&r)[32], uint32_t addr, int lbo) {
+                uint32_t pk[16];
+                float q0 = 0.f, q1 = 0.f;
 #pragma unroll
-            for (int i = 0; i < 64; i += 2) {
-                const float p0 = ex2(fmaf(x[i], sl2, -mm));
-                const float p1 = ex2(fmaf(x[i + 1], sl2, -mm));
-                ps0 += p0;
-                ps1 += p1;
-                pk[i >> 1] = pack_bf16(p0, p1);
-            }
-            const float ps = ps0 + ps1;
-            float pw = 64.f * ps;
-            if (has_last) {  // the ragged last block weighs n_last, not 64
-                const int lc = a.N - 1 - c * 64;
-                float plast = 0.f;
-#pragma unroll
-                for (int i = 0; i < 64; ++i)
-                    if (i == lc) plast = ex2(fmaf(x[i], sl2, -mm));
-                pw += (float(n_last) - 64.f) * plast;
-            }
-            l += pw;
+                for (int i = 0; i < 32; i += 2) {
+                    const float p0 = ex2(fmaf(__uint_as_float(r[i]), sl2, -mm));
+                    const float p1 = ex2(fmaf(__uint_as_float(r[i + 1]), sl2, -mm));
+                    q0 += p0;
+                    q1 += p1;
+                    if (ragged) plast += (lbo == i ? p0 : 0.f) + (lbo == i + 1 ? p1 : 0.f);
+                    pk[i >> 1] = pack_bf16(p0, p1);
+                }
+                ps += q0 + q1;
+                tmem_st16x2_16<16>(addr, pk);
+            };
+            if (kSeparateP) wait_pv_prev(g);
+            expo_store(r0, p_addr(g, 0), lb);
+            expo_store(r1, p_addr(g, 1), lb - 64);
+            l += 64.f * ps + (float(n_last) - 64.f) * plast;
             lt += ps;
-            publish_p(sc, pk, &bar.p_full[s], lane);
+            publish_p(g);
         }
 
         // ------------------------------------------------------- epilogue --
         mbar_wait(&bar.qh_full, 0);
         tc_fence_after();
+        float mrow = m;
+        float lfin = l + __shfl_xor_sync(0xffffffffu, l, 16);
+        float ltot = lt + __shfl_xor_sync(0xffffffffu, lt, 16);
         float cw = 0.f;
-        float lfin = l;
         if (a.variant == 3) {
-            cw = a.scale * lt;
+            cw = a.scale * ltot;
             if (a.literal_phase3) cw *= (1.0f / 64.0f);
         }
         float fo = 1.f;  // extra scale on O and l (GlobalCentroid shift)
-        if (a.variant == 4 && active) {
+        if (a.variant == 4) {
             // slope = |U_i| exp(scale q.k_bar_global - m)   (engine.hpp:202-205)
-            const uint8_t* sQ = smem + Cfg::kOffQ;
             const float* kg = a.kbar_global + size_t(bh) * D;
             float dot = 0.f;
-            for (int c = 0; c < D; ++c) {
-                const uint32_t off = (c >> 6) * 16384 + sw128_off(row, c & 63);
-                dot = fmaf(__bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(sQ + off)), kg[c], dot);
+            if (active) {
+                for (int c = ch * (D / 2); c < (ch + 1) * (D / 2); ++c)
+                    dot = fmaf(__bfloat162float(qrow[c]), kg[c], dot);
             }
+            dot += __shfl_xor_sync(0xffffffffu, dot, 16);
             const float gx = dot * sl2;
             const int nU = a.N - a.k;
-            if (nU > 0) {
-                const float mm = fmaxf(m, gx);
-                fo = ex2(m - mm);
+            if (active && nU > 0) {
+                const float mm = fmaxf(mrow, gx);
+                fo = ex2(mrow - mm);
                 cw = a.scale * float(nU) * ex2(gx - mm);
                 if (a.literal_phase3) cw *= (1.0f / 64.0f);
-                m = mm;
-                lfin = l * fo;
-                lt *= fo;
+                mrow = mm;
+                lfin *= fo;
+                ltot *= fo;
             }
         }
         const float inv_l = 1.0f / lfin;
@@ -523,10 +642,10 @@ __global__ void __launch_bounds__(kThreads, 2)
                      (size_t(b) * a.os_b + size_t(h) * a.os_h + size_t(grow) * a.os_l) *
                          (a.out_f32 ? 4 : 2);
 #pragma unroll 1
-        for (int cc = 0; cc < D; cc += 32) {
+        for (int cc = 0; cc < D / 2; cc += 32) {
             uint32_t ro[32], rq[32];
-            tmem_ld32(tmem + lane_off + kColO + cc, ro);
-            if (first_order) tmem_ld32(tmem + lane_off + kColS + cc, rq);
+            tmem_ld16x2_32<D / 2>(lbase + kColO + cc, ro);
+            if (first_order) tmem_ld16x2_32<D / 2>(lbase + kColS + cc, rq);
             tmem_ld_wait(ro);
             if (first_order) tmem_ld_wait(rq);
             float o[32];
@@ -537,13 +656,14 @@ __global__ void __launch_bounds__(kThreads, 2)
                 o[i] = acc * inv_l;
                 bad |= active && !isfinite(o[i]);
             }
+            const int col = ch * (D / 2) + cc;
             if (active) {
                 if (a.out_f32) {
-                    float4* dst = reinterpret_cast<float4*>(orow) + cc / 4;
+                    float4* dst = reinterpret_cast<float4*>(orow) + col / 4;
 #pragma unroll
                     for (int i = 0; i < 32; i += 4) dst[i / 4] = make_float4(o[i], o[i + 1], o[i + 2], o[i + 3]);
                 } else {
-                    uint4* dst = reinterpret_cast<uint4*>(orow + cc * 2);
+                    uint4* dst = reinterpret_cast<uint4*>(orow + col * 2);
 #pragma unroll
                     for (int i = 0; i < 32; i += 8)
                         dst[i / 8] = make_uint4(pack_bf16(o[i], o[i + 1]), pack_bf16(o[i + 2], o[i + 3]),
@@ -553,15 +673,17 @@ __global__ void __launch_bounds__(kThreads, 2)
         }
         if (active) {
             const size_t di = size_t(bh) * a.L + grow;
-            if (a.diag_m) a.diag_m[di] = m * 0.6931471805599453f;  // log2 units -> natural log
-            if (a.diag_l) a.diag_l[di] = lfin;
-            if (a.diag_lt) a.diag_lt[di] = lt;
+            if (ch == 0) {
+                if (a.diag_m) a.diag_m[di] = mrow * 0.6931471805599453f;  // log2 units -> natural log
+                if (a.diag_l) a.diag_l[di] = lfin;
+                if (a.diag_lt) a.diag_lt[di] = ltot;
+            }
             if (bad && a.nonfinite) atomicExch(a.nonfinite, 1);
         }
     }
     tc_fence_before();
     __syncthreads();
-    if (warp == 2) tmem_dealloc(tmem, 256);
+    if (warp == 2) tmem_dealloc(tmem, 512);
 }
 
 }  // namespace
@@ -571,20 +693,19 @@ size_t fused_smem_bytes(int D, int N, int W) {
     return 1024 + core + size_t(2 * W) * 4 + size_t(N) * 2 + 16;
 }
 
-cudaError_t launch_fused(int D, const CUtensorMap& tmQ, const CUtensorMap& tmK,
-                         const CUtensorMap& tmV, const CUtensorMap& tmKb,
-                         const CUtensorMap& tmVh, const CUtensorMap& tmH, const FusedArgs& a,
-                         int BH, cudaStream_t s) {
+cudaError_t launch_fused(int D, const CUtensorMap& tmK, const CUtensorMap& tmV,
+                         const CUtensorMap& tmKb, const CUtensorMap& tmVh, const CUtensorMap& tmH,
+                         const FusedArgs& a, int BH, cudaStream_t s) {
     const size_t smem = fused_smem_bytes(D, a.N, a.W);
     dim3 grid((a.N + 1) / 2, BH);
     if (D == 128) {
         auto k = fused_attn_kernel<128>;
         cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-        k<<<grid, kThreads, smem, s>>>(tmQ, tmK, tmV, tmKb, tmVh, tmH, a);
+        k<<<grid, kThreads, smem, s>>>(tmK, tmV, tmKb, tmVh, tmH, a);
     } else {
         auto k = fused_attn_kernel<64>;
         cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-        k<<<grid, kThreads, smem, s>>>(tmQ, tmK, tmV, tmKb, tmVh, tmH, a);
+        k<<<grid, kThreads, smem, s>>>(tmK, tmV, tmKb, tmVh, tmH, a);
     }
     return cudaGetLastError();
 }

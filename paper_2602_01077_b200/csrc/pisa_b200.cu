@@ -188,7 +188,8 @@ pisa_status resolve(pisa_ctx* ctx, const pisa_attn_desc* d, Plan* p) {
     if (d->router != PISA_ROUTER_PLAIN)
         return fail(ctx, PISA_ERR_UNSUPPORTED, "only the Plain router runs on the GPU path");
     const int64_t N = (d->seq_len + 63) / 64;
-    if (N > 8192) return fail(ctx, PISA_ERR_UNSUPPORTED, "more than 8192 key blocks");
+    if (N > 4096)  // the fused kernel keeps the union list and masks in shared memory
+        return fail(ctx, PISA_ERR_UNSUPPORTED, "more than 4096 key blocks (seq_len > 262144)");
     int64_t k = d->topk;
     if (k <= 0) {
         if (k < 0) return fail(ctx, PISA_ERR_INVALID_SPARSITY, "k must lie in [1, N]");
@@ -310,15 +311,18 @@ pisa_status run_select(pisa_ctx* ctx, const pisa_attn_desc& d, const Plan& p, co
 pisa_status run_fused(pisa_ctx* ctx, const pisa_attn_desc& d, const Plan& p, const Work& w,
                       const void* q, const void* k, const void* v, void* o, const pisa_diag* diag,
                       cudaStream_t s) {
-    CUtensorMap tq, tk, tv, tkb, tvh, th;
-    if (!make_qkv_map(&tq, q, d, d.q_strides, 128) || !make_qkv_map(&tk, k, d, d.k_strides, 64) ||
-        !make_qkv_map(&tv, v, d, d.v_strides, 64))
+    CUtensorMap tk, tv, tkb, tvh, th;
+    if (!make_qkv_map(&tk, k, d, d.k_strides, 64) || !make_qkv_map(&tv, v, d, d.v_strides, 64))
         return fail(ctx, PISA_ERR_INVALID_DIMENSION, "TMA descriptor rejected the q/k/v layout");
     if (!make_3d_map(&tkb, w.kbar_bf, p.D, p.Npad, p.BH, 64) ||
         !make_3d_map(&tvh, w.vhat_bf, p.D, p.Npad, p.BH, 64) ||
         !make_3d_map(&th, w.hbar_bf, p.D, p.D, p.BH, uint32_t(p.D)))
         return fail(ctx, PISA_ERR_CUDA, "TMA descriptor creation failed");
     FusedArgs a{};
+    a.q = static_cast<const __nv_bfloat16*>(q);
+    a.qs_b = d.q_strides[0];
+    a.qs_h = d.q_strides[1];
+    a.qs_l = d.q_strides[2];
     a.mask = w.mask;
     a.kbar_global = w.kglob;
     a.out = o;
@@ -348,7 +352,7 @@ pisa_status run_fused(pisa_ctx* ctx, const pisa_attn_desc& d, const Plan& p, con
     cudaError_t e;
     {
         ProfScope ps(ctx, kK3, s);
-        e = launch_fused(int(p.D), tq, tk, tv, tkb, tvh, th, a, int(p.BH), s);
+        e = launch_fused(int(p.D), tk, tv, tkb, tvh, th, a, int(p.BH), s);
     }
     if (e != cudaSuccess) return cuda_fail(ctx, e, "fused launch");
     ctx->launches += 1;

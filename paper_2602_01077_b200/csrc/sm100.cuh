@@ -53,19 +53,37 @@ __device__ __forceinline__ uint64_t global_ns() {
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     return t;
 }
-// Blocks until the phase with the given parity has completed. With the
-// watchdog on, a wait still pending after ~4 s traps instead of hanging the GPU
-// (the timer is only read on the slow path).
+// try_wait without a suspend hint: SYNCS.PHASECHK.TRYWAIT polls for a short
+// hardware window and returns; no NANOSLEEP, so the caller sees the phase flip
+// within tens of cycles (for latency-critical waiters: MMA issuer, softmax).
+__device__ __forceinline__ bool mbar_try_wait_spin(uint32_t addr, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(addr), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+// Blocks until the phase with the given parity has completed. Spin = false
+// suspends the thread in hardware between polls (frees issue slots; wake-up can
+// lag by hundreds of cycles), Spin = true polls. With the watchdog on, a wait
+// still pending after ~4 s traps instead of hanging the GPU (the timer is only
+// read on the slow path).
+template <bool Spin = false>
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     const uint32_t addr = smem_u32(bar);
-    if (mbar_try_wait(addr, parity)) return;
+    auto poll = [&]() { return Spin ? mbar_try_wait_spin(addr, parity) : mbar_try_wait(addr, parity); };
+    if (poll()) return;
 #if PISA_WATCHDOG
     const uint64_t t0 = global_ns();
-    while (!mbar_try_wait(addr, parity)) {
+    while (!poll()) {
         if (global_ns() - t0 > 4000000000ull) __trap();
     }
 #else
-    while (!mbar_try_wait(addr, parity)) {
+    while (!poll()) {
     }
 #endif
 }
@@ -185,6 +203,40 @@ __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32
         "%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(
             taddr),
         PISA_S8(0), PISA_S8(8), PISA_S8(16), PISA_S8(24)
+        : "memory");
+}
+#undef PISA_S8
+// 16 lanes x 32 bit, split by half-warp: thread t (t < 16) reads lane base+t,
+// columns [c, c+32); thread t+16 reads the same lane, columns [c+OFF, c+OFF+32).
+// Lets one warp spread the 16 rows of one query block over all 32 threads.
+#define PISA_R8(i) "=r"(r[i]), "=r"(r[i + 1]), "=r"(r[i + 2]), "=r"(r[i + 3]), "=r"(r[i + 4]), \
+                   "=r"(r[i + 5]), "=r"(r[i + 6]), "=r"(r[i + 7])
+template <int OFF>
+__device__ __forceinline__ void tmem_ld16x2_32(uint32_t taddr, uint32_t (&r)[32]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.16x32bx2.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,"
+        "%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32], %33;"
+        : PISA_R8(0), PISA_R8(8), PISA_R8(16), PISA_R8(24)
+        : "r"(taddr), "n"(OFF));
+}
+#undef PISA_R8
+#define PISA_S8(i) "r"(r[i]), "r"(r[i + 1]), "r"(r[i + 2]), "r"(r[i + 3]), "r"(r[i + 4]), \
+                   "r"(r[i + 5]), "r"(r[i + 6]), "r"(r[i + 7])
+template <int OFF>
+__device__ __forceinline__ void tmem_st16x2_16(uint32_t taddr, const uint32_t (&r)[16]) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.16x32bx2.x16.b32 [%0], %1, {%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,"
+        "%12,%13,%14,%15,%16,%17};" ::"r"(taddr),
+        "n"(OFF), PISA_S8(0), PISA_S8(8)
+        : "memory");
+}
+template <int OFF>
+__device__ __forceinline__ void tmem_st16x2_32(uint32_t taddr, const uint32_t (&r)[32]) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.16x32bx2.x32.b32 [%0], %1, {%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,"
+        "%12,%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32,"
+        "%33};" ::"r"(taddr),
+        "n"(OFF), PISA_S8(0), PISA_S8(8), PISA_S8(16), PISA_S8(24)
         : "memory");
 }
 #undef PISA_S8
