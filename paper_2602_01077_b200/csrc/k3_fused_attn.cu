@@ -21,21 +21,24 @@
 // close to the chip's TMA delivery limit (~70 B/clk/SM), and a 16 KB TMA tile
 // takes 1300-2000 cycles under that load. Latency x bandwidth ~ 100+ KB must be
 // in flight per SM, so the design spends shared memory on K/V stages:
-//   * ONE CTA per SM, Q kept in TMEM (it is the A operand of both S = Q K^T and
-//     Q H_bar, TS-form MMAs), so shared memory holds only K/V rings:
-//     3 K + 3 V stages of two key blocks each (192 KB at d = 128);
+//   * ONE CTA per SM: Q (32 KB) + 2 K + 3 V stages of two key blocks each
+//     (192 KB at d = 128) in shared memory;
 //   * key blocks go through the pipeline in pairs ("super-tiles" of 128 keys):
 //     S = Q [K_a; K_b]^T is one set of N=128 MMAs, and each barrier round trip,
 //     commit and softmax hand-off covers two blocks -- a single issuing thread
 //     is otherwise latency-bound on ~100 instructions per 64-key block;
-//   * TMEM (512 columns): O [0, 128) | Q [128, 192) | two S/P buffers of 128
-//     columns [256, 512) (P_g is written over the S_g columns it came from;
-//     see kSeparateP for the alternative).
+//   * TMEM (512 columns): O [0, 128) | three S/P buffers of 128 columns (P_g is
+//     written over the S_g columns it came from), so the chain
+//     S_g -> softmax_g -> PV_g -> S_{g+3} spans three super-tiles and the
+//     tensor pipe stays fed while one super-tile is in the softmax.
+//     (Q in TMEM, TS-form S MMAs, would free shared memory but leave room for
+//     only two S buffers: measured 24.7 ms vs the three-buffer design.)
 //
 // Warp roles (384 threads):
-//   warp 0     TMA producer: K / k_bar tiles (3-stage ring of pairs), H_bar at the end
-//   warp 1     single-thread tcgen05.mma issuer: S_t = Q K_t^T (TS: Q from TMEM,
-//              K K-major), O += P_u V_u (TS: P from TMEM, V MN-major), Q H_bar
+//   warp 0     TMA producer: Q (once), K / k_bar tiles (3-stage ring of pairs),
+//              H_bar at the end
+//   warp 1     single-thread tcgen05.mma issuer: S_g = Q K_g^T (SS, K-major),
+//              O += P_g V_g (TS: P from TMEM, V MN-major), Q H_bar (SS)
 //   warp 2     TMEM allocator, then TMA producer for V columns [0, 64)
 //   warp 3     builds the union list from the two selection bitmasks, then TMA
 //              producer for V columns [64, 128) (two issue streams for V)
@@ -61,34 +64,47 @@ using namespace pisa_sm100;
 namespace {
 
 constexpr int kThreads = 384;
-constexpr int kSK = 3;  // K ring stages (two key blocks each)
-constexpr int kSV = 3;  // V ring stages (two key blocks each)
-constexpr int kSB = 2;  // S/P TMEM buffers (128 columns each)
+#ifndef PISA_KSTAGES
+#define PISA_KSTAGES 2
+#endif
+#ifndef PISA_VSTAGES
+#define PISA_VSTAGES 3
+#endif
+constexpr int kSK = PISA_KSTAGES;  // K ring stages (two key blocks each)
+constexpr int kSV = PISA_VSTAGES;  // V ring stages (two key blocks each)
+constexpr int kSB = 3;  // S/P TMEM buffers (128 columns each)
 constexpr float kRescaleThresh = 8.0f;  // log2 units
-constexpr uint32_t kColO = 0, kColQ = 128, kColP = 192, kColS = 256;
-// P placement. false: P_g overwrites the S_g buffer it came from (S_{g+2} is
-// issued after PV_g). true: P has its own TMEM buffer [192, 256) and S_{g+2}
-// is issued as soon as the softmax has S_g in registers -- but the single P
-// buffer then serialises softmax_g behind PV_{g-1} (measured slower: 27.4 vs
-// 25.5 ms at Wan2.1-14B).
-constexpr bool kSeparateP = false;
+constexpr uint32_t kColO = 0, kColS = 128;  // O | three S/P buffers (P_g over the S_g columns)
+// Exponentials of the softmax: element i of each pair-unrolled 32-column row
+// chunk goes to ex2_poly (FMA pipe) when bit (i % 8) of kPolyMask is set, else
+// to MUFU.EX2 (FA4's split of exp2 across pipes; measured slower here: the
+// softmax is issue-bound, not MUFU-bound, so the default is all-MUFU).
+#ifndef PISA_POLY_MASK
+#define PISA_POLY_MASK 0x00
+#endif
+constexpr uint32_t kPolyMask = PISA_POLY_MASK;
+__device__ __forceinline__ float ex2_mix(float x, int i) {
+    return ((kPolyMask >> (i & 7)) & 1u) ? ex2_poly(x) : ex2(x);
+}
 
 template <int D>
 struct FusedCfg {
+    static constexpr int kQ = 128 * D * 2;  // Q tile: [64-col half][128 rows], rows interleaved
     // one K or V stage: two 64-key blocks, laid out [64-col half][128 rows] with
     // 128-byte rows (SW128), so a stage is one N=128 (K) / K=128 (V) operand
     static constexpr int kKV = 2 * 64 * D * 2;
-    static constexpr int kOffK = 0;
-    static constexpr int kOffV = kSK * kKV;
-    static constexpr int kOffBar = (kSK + kSV) * kKV;
+    static constexpr int kOffQ = 0;
+    static constexpr int kOffK = kQ;
+    static constexpr int kOffV = kQ + kSK * kKV;
+    static constexpr int kOffBar = kQ + (kSK + kSV) * kKV;
     static constexpr int kBarBytes = 512;
     static constexpr int kOffMask = kOffBar + kBarBytes;
 };
 
 struct Bars {
-    uint64_t q_ready, h_full, qh_full;
-    uint64_t k_full[kSK], k_empty[kSK], v_full[kSV], v_empty[kSV];
-    uint64_t s_full[kSB], s_free[kSB], p_full[kSB], pv_done[kSB];
+    uint64_t q_full, h_full, qh_full;
+    uint64_t k_full[kSK], v_full[kSV], v_empty[kSV];
+    uint64_t s_full[kSB], p_full[kSB];
     uint32_t tmem_base;
     uint32_t n_union;
 };
@@ -132,7 +148,8 @@ __device__ __forceinline__ void rescale_o(uint32_t tmem_o, float f) {
 
 template <int D>
 __global__ void __launch_bounds__(kThreads, 1)
-    fused_attn_kernel(const __grid_constant__ CUtensorMap tmK,
+    fused_attn_kernel(const __grid_constant__ CUtensorMap tmQ,
+                      const __grid_constant__ CUtensorMap tmK,
                       const __grid_constant__ CUtensorMap tmV,
                       const __grid_constant__ CUtensorMap tmKb,
                       const __grid_constant__ CUtensorMap tmVh,
@@ -163,26 +180,20 @@ __global__ void __launch_bounds__(kThreads, 1)
 
     // ------------------------------------------------------------ setup --
     if (threadIdx.x == 0) {
-        mbar_init(&bar.q_ready, 8);  // one arrive per softmax warp
+        mbar_init(&bar.q_full, 1);
         mbar_init(&bar.h_full, 1);
         mbar_init(&bar.qh_full, 1);
-        for (int s = 0; s < kSK; ++s) {
-            mbar_init(&bar.k_full[s], 1);
-            mbar_init(&bar.k_empty[s], 1);
-        }
+        for (int s = 0; s < kSK; ++s) mbar_init(&bar.k_full[s], 1);
         for (int s = 0; s < kSV; ++s) {
             mbar_init(&bar.v_full[s], D / 64);  // one arrive per V producer (one per 64-col half)
             mbar_init(&bar.v_empty[s], 1);
         }
         for (int s = 0; s < kSB; ++s) {
             mbar_init(&bar.s_full[s], 1);
-            mbar_init(&bar.s_free[s], 8);  // one arrive per softmax warp
-        }
-        for (int s = 0; s < kSB; ++s) {
-            mbar_init(&bar.p_full[s], 8);
-            mbar_init(&bar.pv_done[s], 1);
+            mbar_init(&bar.p_full[s], 8);  // one arrive per softmax warp
         }
         fence_mbar_init();
+        tma_prefetch(&tmQ);
         tma_prefetch(&tmK);
         tma_prefetch(&tmV);
     }
@@ -246,12 +257,29 @@ __global__ void __launch_bounds__(kThreads, 1)
     };
 
     if (warp == 0) {
-        // ------------------------------------------------ producer: K, H --
+        // ------------------------------------------------ producer: Q, K, H --
+        if (elect_one()) {
+            // Interleaved row order: the 16-row chunk (quadrant q4, block hh) of
+            // the tile lands at shared-memory / TMEM rows q4*32 + hh*16.
+            mbar_expect_tx(&bar.q_full, Cfg::kQ);
+#pragma unroll
+            for (int half = 0; half < D / 64; ++half)
+#pragma unroll
+                for (int c = 0; c < 8; ++c)
+                    tma_load_4d(smem + Cfg::kOffQ + half * 16384 + c * 2048, &tmQ, &bar.q_full, half * 64,
+                                tile * 128 + (c & 1) * 64 + (c >> 1) * 16, h, b);
+        }
+        __syncwarp();
+        // K stage of S_g is free once S_{g-kSK} is done: s_full of that S
+        // (no separate "empty" commit; S_{g-kSK+3} cannot complete before K_g is
+        // loaded, so the parity is unambiguous)
+        auto wait_s_done = [&](int j) {
+            if (j >= 0) mbar_wait(&bar.s_full[j % kSB], uint32_t((j / kSB) & 1));
+        };
         int s = 0;
-        uint32_t ph = 0;
         for (int g = 0; g < G; ++g) {
             uint8_t* sK = smem + Cfg::kOffK + s * Cfg::kKV;
-            mbar_wait(&bar.k_empty[s], ph ^ 1);
+            wait_s_done(g - kSK);
             const bool exact = g < G1;
             const int r0 = tile_row(g, 0), r1 = tile_row(g, 1);
             if (elect_one()) {
@@ -269,14 +297,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                 TRACE(0, g);
             }
             __syncwarp();
-            if (++s == kSK) { s = 0; ph ^= 1u; }
+            if (++s == kSK) s = 0;
         }
         if (first_order) {
-            // H_bar (D x D) into K stage 0 once every S MMA is done
-            for (int i = 0; i < kSK; ++i) {
-                mbar_wait(&bar.k_empty[s], ph ^ 1);
-                if (++s == kSK) { s = 0; ph ^= 1u; }
-            }
+            // H_bar (D x D = one stage) into K stage 0 once every S MMA is done
+            for (int j = G - kSK; j < G; ++j) wait_s_done(j);
             if (elect_one()) {
                 mbar_expect_tx(&bar.h_full, D * D * 2);
 #pragma unroll
@@ -315,72 +340,78 @@ __global__ void __launch_bounds__(kThreads, 1)
         // advanced by adding (byte offset >> 4) to their address field; ring
         // positions advance incrementally (no div/mod). One elected lane issues
         // (and commits: a commit tracks the MMAs of the thread that runs it).
-        constexpr uint32_t idS = idesc_bf16(128, 128, 0, 0);  // S = Q K^T, 128 keys (Q from TMEM)
-        constexpr uint32_t idPV = idesc_bf16(128, D, 0, 1);   // O += P V (V MN-major)
+        constexpr uint32_t idS = idesc_bf16(128, 128, 0, 0);  // S = Q K^T, 128 keys
+        constexpr uint32_t idPV = idesc_bf16(128, D, 0, 1);   // O += P V (P from TMEM, V MN-major)
         constexpr uint32_t idQH = idesc_bf16(128, D, 0, 1);   // Q H_bar
+        const uint64_t qdesc0 = sdesc_sw128(smem_u32(smem + Cfg::kOffQ), 16, 1024);
         const uint64_t kdesc0 = sdesc_sw128(smem_u32(smem + Cfg::kOffK), 16, 1024);
         const uint64_t vdesc0 = sdesc_sw128(smem_u32(smem + Cfg::kOffV), 16384, 1024);
         const uint64_t hdesc0 = sdesc_sw128(smem_u32(smem + Cfg::kOffK), 16384, 1024);
-        const uint32_t tS = tmem + kColS, tQ = tmem + kColQ, tO = tmem + kColO, tP = tmem + kColP;
-        int sk = 0;                     // K stage of the next S
+        const uint32_t tS = tmem + kColS, tO = tmem + kColO;
+        int sk = 0, sbk = 0;            // K stage and S buffer of the next S
         uint32_t phk = 0;               // its k_full parity
-        int sv = 0;                     // V stage of the next PV
-        uint32_t phv = 0;               // its v_full parity
-        auto issue_s = [&](int g) {     // S_g into S buffer g & 1
+        int sv = 0, sbv = 0;            // V stage and S/P buffer of the next PV
+        uint32_t phv = 0, php = 0;      // v_full / p_full parities
+        // MMAs of S_g into S buffer g % 3 (SS: Q and K from shared memory);
+        // commit: s_full (the softmax's "S ready" and the K producer's "stage free")
+        auto mma_s = [&](int g) {
+            TRACE(8, g);
+            const uint64_t kd = kdesc0 + uint64_t(sk * (Cfg::kKV >> 4));
+            const uint32_t d = tS + uint32_t(sbk) * 128;
+#pragma unroll
+            for (int ks = 0; ks < D / 16; ++ks) {
+                const uint64_t off = uint64_t(((ks >> 2) * 16384 + (ks & 3) * 32) >> 4);
+                mma_ss(d, qdesc0 + off, kd + off, idS, ks != 0);
+            }
+            mma_commit(&bar.s_full[sbk]);
+            TRACE(2, g);
+        };
+        auto advance_s = [&]() {
+            if (++sk == kSK) { sk = 0; phk ^= 1u; }
+            if (++sbk == kSB) sbk = 0;
+        };
+        // MMAs of O += P_g V_g, P_g over the S_g columns; commit: v_empty (the V
+        // producer's "stage free" and the softmax's "PV_g done")
+        auto mma_pv = [&](int g) {
+            TRACE(10, g);
+            const uint64_t vd = vdesc0 + uint64_t(sv * (Cfg::kKV >> 4));
+            const uint32_t pa = tS + uint32_t(sbv) * 128;
+#pragma unroll
+            for (int ks = 0; ks < 8; ++ks)
+                mma_ts(tO, pa + (ks >> 2) * 64 + (ks & 3) * 8, vd + uint64_t((ks * 2048) >> 4), idPV,
+                       (g == 0 && ks == 0) ? 0u : 1u);
+            mma_commit(&bar.v_empty[sv]);
+            TRACE(3, g);
+        };
+        auto advance_pv = [&]() {
+            if (++sv == kSV) { sv = 0; phv ^= 1u; }
+            if (++sbv == kSB) { sbv = 0; php ^= 1u; }
+        };
+        mbar_wait<true>(&bar.q_full, 0);
+        tc_fence_after();
+        for (int g = 0; g < kSB && g < G; ++g) {
             mbar_wait<true>(&bar.k_full[sk], phk);
             tc_fence_after();
-            if (elect_one()) {
-                TRACE(8, g);
-                const uint64_t kd = kdesc0 + uint64_t(sk * (Cfg::kKV >> 4));
-                const uint32_t d = tS + uint32_t(g & 1) * 128;
-#pragma unroll
-                for (int ks = 0; ks < D / 16; ++ks)
-                    mma_ts(d, tQ + ks * 8, kd + uint64_t(((ks >> 2) * 16384 + (ks & 3) * 32) >> 4), idS, ks != 0);
-                mma_commit(&bar.k_empty[sk]);
-                mma_commit(&bar.s_full[g & 1]);
-                TRACE(2, g);
-            }
+            if (elect_one()) mma_s(g);
             __syncwarp();
-            if (++sk == kSK) { sk = 0; phk ^= 1u; }
-        };
-        auto issue_pv = [&](int g) {    // O += P_g V_g
-            mbar_wait<true>(&bar.p_full[g & 1], uint32_t((g >> 1) & 1));
+            advance_s();
+        }
+        for (int g = 0; g < G; ++g) {
+            // PV_g, then S_{g+3} (in-order tensor pipe: S_{g+3} overwrites P_g
+            // after PV_g read it); all waits first, one elected issue block
+            const bool more = g + kSB < G;
+            mbar_wait<true>(&bar.p_full[sbv], php);
             TRACE(9, g);
             mbar_wait<true>(&bar.v_full[sv], phv);
+            if (more) mbar_wait<true>(&bar.k_full[sk], phk);
             tc_fence_after();
             if (elect_one()) {
-                TRACE(10, g);
-                const uint64_t vd = vdesc0 + uint64_t(sv * (Cfg::kKV >> 4));
-#pragma unroll
-                for (int ks = 0; ks < 8; ++ks) {
-                    const uint32_t pa = kSeparateP ? tP + (ks >> 2) * 32 + (ks & 3) * 8
-                                                   : tS + uint32_t(g & 1) * 128 + (ks >> 2) * 64 + (ks & 3) * 8;
-                    mma_ts(tO, pa, vd + uint64_t((ks * 2048) >> 4), idPV, (g == 0 && ks == 0) ? 0u : 1u);
-                }
-                mma_commit(&bar.v_empty[sv]);
-                mma_commit(&bar.pv_done[g & 1]);
-                TRACE(3, g);
+                mma_pv(g);
+                if (more) mma_s(g + kSB);
             }
             __syncwarp();
-            if (++sv == kSV) { sv = 0; phv ^= 1u; }
-        };
-        static_assert(kSB == 2, "two S buffers");
-        mbar_wait<true>(&bar.q_ready, 0);
-        tc_fence_after();
-        for (int g = 0; g < kSB && g < G; ++g) issue_s(g);
-        for (int g = 0; g < G; ++g) {
-            if (kSeparateP) {
-                // S_{g+2} as soon as the softmax has S_g in registers (it
-                // overlaps the softmax of g), then PV_g once P_g is in TMEM
-                if (g + kSB < G) {
-                    mbar_wait<true>(&bar.s_free[g & 1], uint32_t((g >> 1) & 1));
-                    issue_s(g + kSB);
-                }
-                issue_pv(g);
-            } else {
-                issue_pv(g);  // in-order tensor pipe: S_{g+2} below overwrites P_g after PV_g read it
-                if (g + kSB < G) issue_s(g + kSB);
-            }
+            advance_pv();
+            if (more) advance_s();
         }
         if (first_order) {
             mbar_wait<true>(&bar.h_full, 0);
@@ -390,7 +421,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (first_order) {
 #pragma unroll
                 for (int ks = 0; ks < D / 16; ++ks)
-                    mma_ts(tS, tQ + ks * 8, hdesc0 + uint64_t((ks * 2048) >> 4), idQH, ks != 0);
+                    mma_ss(tS, qdesc0 + uint64_t(((ks >> 2) * 16384 + (ks & 3) * 32) >> 4),
+                           hdesc0 + uint64_t((ks * 2048) >> 4), idQH, ks != 0);
             }
             mma_commit(&bar.qh_full);  // also: every PV done
         }
@@ -409,43 +441,26 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t* hmask = hh ? maskB : maskA;
         const __nv_bfloat16* qrow = a.q + size_t(b) * a.qs_b + size_t(h) * a.qs_h + size_t(grow) * a.qs_l;
 
-        // Q -> TMEM (bf16 pairs, lane = row): this thread's row, packed columns
-        // [ch * D/4, ch * D/4 + D/4).
-        {
-            uint32_t qr[32];
-            const uint4* src = reinterpret_cast<const uint4*>(qrow) + ch * (D / 16);
-#pragma unroll
-            for (int i = 0; i < D / 16; ++i) {
-                const uint4 v = active ? src[i] : make_uint4(0u, 0u, 0u, 0u);
-                qr[4 * i] = v.x;
-                qr[4 * i + 1] = v.y;
-                qr[4 * i + 2] = v.z;
-                qr[4 * i + 3] = v.w;
-            }
-            if constexpr (D == 128) {
-                tmem_st16x2_32<32>(lbase + kColQ, qr);
-            } else {
-                tmem_st16x2_16<16>(lbase + kColQ, reinterpret_cast<const uint32_t(&)[16]>(qr));
-            }
-            tmem_st_wait();
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&bar.q_ready);
-        }
-
         float m = -INFINITY, l = 0.f, lt = 0.f;  // l, lt: this thread's partial sums
 
         // Online-softmax step over one 128-key super-tile: bm_loc = max of this
         // thread's live scores (masked = -inf). Returns the shift to
         // exponentiate against (log2 units); rescales O lazily when the max
         // grows by > 2^8 (after PV_{g-1}: O must be quiescent).
-        auto wait_pv_prev = [&](int g) {  // PV_{g-1} done
+        // S/P buffer ring: super-tile g uses buffer sb = g % 3, phase parity phs
+        int sb = 0;
+        uint32_t phs = 0;
+        auto wait_pv_prev = [&](int g) {  // PV_{g-1} done = its V stage released
             if (g > 0) {
-                // PV_{g-3} is known done (S_g, or P_{g-1}, came after it), so
+                // PV_{g-1-kSV} is known done (S_g was issued after PV_{g-3}), so
                 // the parity names PV_{g-1} unambiguously
-                mbar_wait<true>(&bar.pv_done[(g - 1) & 1], uint32_t(((g - 1) >> 1) & 1));
+                const int j = g - 1;
+                mbar_wait<true>(&bar.v_empty[j % kSV], uint32_t((j / kSV) & 1));
                 tc_fence_after();
             }
+        };
+        auto advance = [&]() {
+            if (++sb == kSB) { sb = 0; phs ^= 1u; }
         };
         auto update_max = [&](float bm_loc, int g) -> float {
             const float bm = fmaxf(bm_loc, __shfl_xor_sync(0xffffffffu, bm_loc, 16)) * sl2;
@@ -469,23 +484,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             m = m_use;
             return (m_use == -INFINITY) ? 0.f : m_use;  // all-masked row: p = 0, not NaN
         };
-        // S_g is in registers: its TMEM buffer may take S_{g+2}
-        auto free_s = [&](int g) {
-            if (kSeparateP) {
-                tc_fence_before();
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&bar.s_free[g & 1]);
-            }
-        };
-        auto publish_p = [&](int g) {
+        auto publish_p = [&]() {
             tmem_st_wait();
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(&bar.p_full[g & 1]);
-        };
-        // P of sub-tile j of super-tile g: own buffer, or over the S columns
-        auto p_addr = [&](int g, int j) -> uint32_t {
-            return kSeparateP ? lbase + kColP + 32 * j : lbase + kColS + (g & 1) * 128 + 64 * j;
+            if (lane == 0) mbar_arrive(&bar.p_full[sb]);
         };
         const uint32_t kZero16[16] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
 
@@ -496,8 +499,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             const bool use0 = (e0 >> (14 + hh)) & 1u, use1 = (e1 >> (14 + hh)) & 1u;  // warp-uniform
             const int nv0 = (int(e0 & 0x3FFFu) == a.N - 1) ? n_last : 64;
             const int nv1 = (int(e1 & 0x3FFFu) == a.N - 1) ? n_last : 64;
-            const uint32_t sc = lbase + kColS + (g & 1) * 128;
-            mbar_wait<true>(&bar.s_full[g & 1], uint32_t((g >> 1) & 1));
+            const uint32_t sc = lbase + kColS + sb * 128;
+            mbar_wait<true>(&bar.s_full[sb], phs);
             tc_fence_after();
             if (q4 == 0) TRACE(4 + hh, g);
             if (use0 || use1) {
@@ -509,7 +512,6 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (use1) tmem_ld16x2_32<32>(sc + 64, r1);
                 tmem_ld_wait(r0);
                 tmem_ld_wait(r1);
-                free_s(g);
                 if (!(wact && nv0 == 64 && nv1 == 64)) {
 #pragma unroll
                     for (int i = 0; i < 32; ++i) {
@@ -528,31 +530,29 @@ __global__ void __launch_bounds__(kThreads, 1)
                     float ps[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
                     for (int i = 0; i < 32; i += 2) {
-                        const float p0 = ex2(fmaf(__uint_as_float(r[i]), sl2, -mm));
-                        const float p1 = ex2(fmaf(__uint_as_float(r[i + 1]), sl2, -mm));
+                        const float p0 = ex2_mix(fmaf(__uint_as_float(r[i]), sl2, -mm), i);
+                        const float p1 = ex2_mix(fmaf(__uint_as_float(r[i + 1]), sl2, -mm), i + 1);
                         ps[(i >> 1) & 3] += p0 + p1;
                         pk[i >> 1] = pack_bf16(p0, p1);
                     }
                     l += (ps[0] + ps[1]) + (ps[2] + ps[3]);
                     tmem_st16x2_16<16>(addr, pk);  // P (bf16 pairs)
                 };
-                if (kSeparateP) wait_pv_prev(g);  // the P buffer is free once PV_{g-1} read it
-                if (use0) expo_store(r0, p_addr(g, 0)); else tmem_st16x2_16<16>(p_addr(g, 0), kZero16);
-                if (use1) expo_store(r1, p_addr(g, 1)); else tmem_st16x2_16<16>(p_addr(g, 1), kZero16);
+                if (use0) expo_store(r0, sc); else tmem_st16x2_16<16>(sc, kZero16);
+                if (use1) expo_store(r1, sc + 64); else tmem_st16x2_16<16>(sc + 64, kZero16);
             } else {
-                free_s(g);
-                if (kSeparateP) wait_pv_prev(g);
-                tmem_st16x2_16<16>(p_addr(g, 0), kZero16);
-                tmem_st16x2_16<16>(p_addr(g, 1), kZero16);
+                tmem_st16x2_16<16>(sc, kZero16);
+                tmem_st16x2_16<16>(sc + 64, kZero16);
             }
-            publish_p(g);
+            publish_p();
+            advance();
             if (q4 == 0) TRACE(6 + hh, g);
         }
         // ---- Phase 2: centroid chunks, two per super-tile; column mask = own
         // selection, weight n_j (the ragged last block weighs n_last)
         for (int g = G1; g < G; ++g) {
             const int c0 = 2 * (g - G1);
-            const uint32_t sc = lbase + kColS + (g & 1) * 128;
+            const uint32_t sc = lbase + kColS + sb * 128;
             // this thread's 32 columns of chunk c: blocks c*64 + ch*32 + i
             auto colmask = [&](int c) -> uint32_t {
                 const int w = 2 * c + ch;
@@ -560,14 +560,13 @@ __global__ void __launch_bounds__(kThreads, 1)
             };
             const uint32_t cm0 = colmask(c0), cm1 = colmask(c0 + 1);
             const int nv0 = min(64, a.N - c0 * 64), nv1 = min(64, a.N - (c0 + 1) * 64);
-            mbar_wait<true>(&bar.s_full[g & 1], uint32_t((g >> 1) & 1));
+            mbar_wait<true>(&bar.s_full[sb], phs);
             tc_fence_after();
             uint32_t r0[32], r1[32];
             tmem_ld16x2_32<32>(sc, r0);
             tmem_ld16x2_32<32>(sc + 64, r1);
             tmem_ld_wait(r0);
             tmem_ld_wait(r1);
-            free_s(g);
 #pragma unroll
             for (int i = 0; i < 32; ++i) {
                 const int col = ch * 32 + i;
@@ -585,8 +584,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                 float q0 = 0.f, q1 = 0.f;
 #pragma unroll
                 for (int i = 0; i < 32; i += 2) {
-                    const float p0 = ex2(fmaf(__uint_as_float(r[i]), sl2, -mm));
-                    const float p1 = ex2(fmaf(__uint_as_float(r[i + 1]), sl2, -mm));
+                    const float p0 = ex2_mix(fmaf(__uint_as_float(r[i]), sl2, -mm), i);
+                    const float p1 = ex2_mix(fmaf(__uint_as_float(r[i + 1]), sl2, -mm), i + 1);
                     q0 += p0;
                     q1 += p1;
                     if (ragged) plast += (lbo == i ? p0 : 0.f) + (lbo == i + 1 ? p1 : 0.f);
@@ -595,12 +594,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                 ps += q0 + q1;
                 tmem_st16x2_16<16>(addr, pk);
             };
-            if (kSeparateP) wait_pv_prev(g);
-            expo_store(r0, p_addr(g, 0), lb);
-            expo_store(r1, p_addr(g, 1), lb - 64);
+            expo_store(r0, sc, lb);
+            expo_store(r1, sc + 64, lb - 64);
             l += 64.f * ps + (float(n_last) - 64.f) * plast;
             lt += ps;
-            publish_p(g);
+            publish_p();
+            advance();
         }
 
         // ------------------------------------------------------- epilogue --
@@ -693,7 +692,7 @@ size_t fused_smem_bytes(int D, int N, int W) {
     return 1024 + core + size_t(2 * W) * 4 + size_t(N) * 2 + 16;
 }
 
-cudaError_t launch_fused(int D, const CUtensorMap& tmK, const CUtensorMap& tmV,
+cudaError_t launch_fused(int D, const CUtensorMap& tmQ, const CUtensorMap& tmK, const CUtensorMap& tmV,
                          const CUtensorMap& tmKb, const CUtensorMap& tmVh, const CUtensorMap& tmH,
                          const FusedArgs& a, int BH, cudaStream_t s) {
     const size_t smem = fused_smem_bytes(D, a.N, a.W);
@@ -701,11 +700,11 @@ cudaError_t launch_fused(int D, const CUtensorMap& tmK, const CUtensorMap& tmV,
     if (D == 128) {
         auto k = fused_attn_kernel<128>;
         cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-        k<<<grid, kThreads, smem, s>>>(tmK, tmV, tmKb, tmVh, tmH, a);
+        k<<<grid, kThreads, smem, s>>>(tmQ, tmK, tmV, tmKb, tmVh, tmH, a);
     } else {
         auto k = fused_attn_kernel<64>;
         cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-        k<<<grid, kThreads, smem, s>>>(tmK, tmV, tmKb, tmVh, tmH, a);
+        k<<<grid, kThreads, smem, s>>>(tmQ, tmK, tmV, tmKb, tmVh, tmH, a);
     }
     return cudaGetLastError();
 }

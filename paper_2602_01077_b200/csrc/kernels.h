@@ -59,7 +59,7 @@ cudaError_t launch_plan_to_mask(const int32_t* selected, int N, int k, int W, ui
 // K3: fused piecewise attention (Phase 1 exact over S_i, Phase 2 centroid tail,
 // Phase 3 global first-order correction), one CTA (one SM) per pair of query blocks.
 struct FusedArgs {
-    const __nv_bfloat16* q;    // queries (loaded into TMEM by the softmax warps)
+    const __nv_bfloat16* q;    // queries (GlobalCentroid slope reads rows directly)
     int64_t qs_b, qs_h, qs_l;  // element strides of q
     const uint32_t* mask;      // [BH][N][W]
     const float* kbar_global;  // [BH][D] (GlobalCentroid) or null
@@ -74,7 +74,7 @@ struct FusedArgs {
     unsigned long long* trace;  // PISA_TRACE builds only: [8][1024] clock deltas
     int trace_tile;
 };
-cudaError_t launch_fused(int D, const CUtensorMap& tmK, const CUtensorMap& tmV,
+cudaError_t launch_fused(int D, const CUtensorMap& tmQ, const CUtensorMap& tmK, const CUtensorMap& tmV,
                          const CUtensorMap& tmKb, const CUtensorMap& tmVh, const CUtensorMap& tmH,
                          const FusedArgs& a, int BH, cudaStream_t s);
 size_t fused_smem_bytes(int D, int N, int W);

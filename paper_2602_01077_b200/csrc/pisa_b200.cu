@@ -311,8 +311,9 @@ pisa_status run_select(pisa_ctx* ctx, const pisa_attn_desc& d, const Plan& p, co
 pisa_status run_fused(pisa_ctx* ctx, const pisa_attn_desc& d, const Plan& p, const Work& w,
                       const void* q, const void* k, const void* v, void* o, const pisa_diag* diag,
                       cudaStream_t s) {
-    CUtensorMap tk, tv, tkb, tvh, th;
-    if (!make_qkv_map(&tk, k, d, d.k_strides, 64) || !make_qkv_map(&tv, v, d, d.v_strides, 64))
+    CUtensorMap tq, tk, tv, tkb, tvh, th;
+    if (!make_qkv_map(&tq, q, d, d.q_strides, 16) || !make_qkv_map(&tk, k, d, d.k_strides, 64) ||
+        !make_qkv_map(&tv, v, d, d.v_strides, 64))
         return fail(ctx, PISA_ERR_INVALID_DIMENSION, "TMA descriptor rejected the q/k/v layout");
     if (!make_3d_map(&tkb, w.kbar_bf, p.D, p.Npad, p.BH, 64) ||
         !make_3d_map(&tvh, w.vhat_bf, p.D, p.Npad, p.BH, 64) ||
@@ -352,7 +353,7 @@ pisa_status run_fused(pisa_ctx* ctx, const pisa_attn_desc& d, const Plan& p, con
     cudaError_t e;
     {
         ProfScope ps(ctx, kK3, s);
-        e = launch_fused(int(p.D), tk, tv, tkb, tvh, th, a, int(p.BH), s);
+        e = launch_fused(int(p.D), tq, tk, tv, tkb, tvh, th, a, int(p.BH), s);
     }
     if (e != cudaSuccess) return cuda_fail(ctx, e, "fused launch");
     ctx->launches += 1;

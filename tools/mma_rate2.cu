@@ -44,7 +44,7 @@ __global__ void __launch_bounds__(384, 1) rate(int mode_in, int iters, unsigned 
     const int base_mode0 = 0; (void)base_mode0;
     const bool commits = mode >= 36;
     if (commits) mode -= 36;
-    const bool tmem_noise = mode >= 9 && mode != 18, tma_noise = mode >= 18;
+    const bool tmem_noise = (mode >= 9 && mode < 18) || mode >= 27, tma_noise = mode >= 18 && mode < 36;
     const int base_mode = (mode >= 45) ? mode - 36 : mode % 9;
     if (warp >= 4 && tmem_noise) {
         // softmax-like TMEM traffic: 16x32bx2 loads of 32 columns + stores of 16, lanes of this warp
@@ -70,7 +70,8 @@ __global__ void __launch_bounds__(384, 1) rate(int mode_in, int iters, unsigned 
         }
         __syncwarp();
         uint32_t hsh = blockIdx.x * 2654435761u + 7u;
-        for (int i = 0; *stop == 0; ++i) {
+        int i = 0;
+        for (; *stop == 0; ++i) {
             const int s2 = i % 5;
             if (i >= 5) mbar_wait(&fb[s2], ((i / 5) - 1) & 1);
             hsh = hsh * 1664525u + 1013904223u;
@@ -82,7 +83,8 @@ __global__ void __launch_bounds__(384, 1) rate(int mode_in, int iters, unsigned 
             }
             __syncwarp();
         }
-        for (int s2 = 0; s2 < 5; ++s2) mbar_wait(&fb[s2], 0);  // drain (approximate)
+        for (int j = i - 5; j < i; ++j)  // drain the last (up to) 5 loads
+            if (j >= 0) mbar_wait(&fb[j % 5], (j / 5) & 1);
     }
     if (warp == 0) {
         const int mode = base_mode;
@@ -204,7 +206,7 @@ int main() {
                                CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     }
-    for (int mode : {0, 1, 45, 46, 47, 48}) {
+    for (int mode : {6, 6 + 9, 6 + 18, 6 + 27, 7, 7 + 18}) {
         const int iters = 2048;
         rate<<<148, 384, smem>>>(mode, 16, d, tm);
         cudaMemset(d, 0, 16);
@@ -222,7 +224,7 @@ int main() {
         }
         printf("%s", mode >= 36 ? "[4 commits/tile] " : "");
         printf("%-36s %-22s %.1f cyc/iter -> %.0f MAC/clk/SM (%.0f%% of 4096)  %s\n", names[bm],
-               (mode % 36) >= 9 ? "+TMEM ld/st (8 warps)" : "",
+               mode >= 27 ? "+TMEM +TMA" : mode >= 18 ? "+TMA ring" : mode >= 9 ? "+TMEM ld/st (8 warps)" : "",
                total, macs[bm] / total, 100.0 * macs[bm] / total / 4096.0, cudaGetErrorString(cudaGetLastError()));
         if (tiles[bm] > 0) printf("   -> %.1f cycles per 64-key tile (tensor floor 512)\n", total / tiles[bm]);
     }
