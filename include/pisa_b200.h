@@ -27,7 +27,7 @@
 extern "C" {
 #endif
 
-#define PISA_B200_ABI_VERSION 1
+#define PISA_B200_ABI_VERSION 2
 
 /* Status codes. Reference class in brackets (errors.hpp line). */
 typedef enum pisa_status {
@@ -79,13 +79,16 @@ typedef struct pisa_attn_desc {
     double sparsity;        /* r in [0,1): fraction of key blocks approximated (router.hpp:80) */
     int64_t topk;           /* > 0 overrides r with an explicit k in [1, N] */
     int32_t variant;        /* pisa_variant */
-    int32_t router;         /* pisa_router; only PLAIN on the GPU path */
+    int32_t router;         /* pisa_router (RouterOptions::strategy, engine.hpp:386) */
     int32_t force_diagonal; /* RouterOptions::force_diagonal (router.hpp:146-148) */
     int32_t literal_phase3; /* AttentionConfig::literal_phase3 (engine.hpp:346) */
     int32_t ragged;         /* 1: allow L % 64 != 0 (documented extension); 0: BLOCK_DIVISIBILITY */
     int32_t out_dtype;      /* pisa_dtype of O */
     int32_t check_finite;   /* 1: synchronize and report NUMERICAL_OVERFLOW (engine.hpp:83-93) */
-    int32_t reserved;
+    int32_t row_level;      /* RouterOptions::row_level (engine.hpp:389): not on the GPU path
+                               (UNSUPPORTED); must be 0 */
+    double epsilon;         /* RouterOptions::epsilon (engine.hpp:387), default 1e-6; the
+                               covariance router requires > 0 (INVALID_EPSILON) */
 } pisa_attn_desc;
 
 /* Optional per-row diagnostics (PisaOutput, engine.hpp:43-57), fp32, [batch][heads][seq_len].
@@ -118,7 +121,8 @@ pisa_status pisa_b200_resolve(const pisa_attn_desc* desc, int64_t* num_blocks, i
                               double* scale);
 
 /* ---- the hot path -------------------------------------------------------- */
-/* Full forward: K1 block statistics -> K2 fp32 scoring + top-k -> K3 fused
+/* Full forward: K1 block statistics [-> K1c spectral norms, covariance router]
+ * -> K2 fp32 scoring + top-k -> K3 fused
  * piecewise attention, stream-ordered, no host synchronisation (unless
  * desc->check_finite). Replaces pisa_multihead(..., use_streaming=true). */
 pisa_status pisa_b200_fwd(pisa_ctx* ctx, const pisa_attn_desc* desc, const void* q,
@@ -143,9 +147,21 @@ pisa_status pisa_b200_block_stats(pisa_ctx* ctx, const pisa_attn_desc* desc, con
 
 /* Select (select_topk_plain): fp32 scores scale*<q_bar_i, k_bar_j>, top-k by
  * (score desc, index asc), ascending output. Inputs fp32 [B*H][N][d];
- * selected int32 [B*H][N][k]; mask (optional) uint32 [B*H][N][ceil(N/32)]. */
+ * selected int32 [B*H][N][k]; mask (optional) uint32 [B*H][N][ceil(N/32)].
+ * desc->router must be PLAIN. */
 pisa_status pisa_b200_select(pisa_ctx* ctx, const pisa_attn_desc* desc, const float* q_bar,
                              const float* k_bar, int32_t* selected, uint32_t* mask, void* stream);
+/* Spectral deviation norms M_j = ||H_j - H_bar||_2 per key block
+ * (compute_global_stats(.., compute_norms=true), block_stats.hpp:207-241), fp32
+ * [B*H][N], computed from Q/K/V like pisa_b200_block_stats (Lanczos on
+ * (H_j - H_bar)^T (H_j - H_bar); the reference uses an exact Jacobi solve). */
+pisa_status pisa_b200_block_norms(pisa_ctx* ctx, const pisa_attn_desc* desc, const void* q,
+                                  const void* k, const void* v, float* m, void* stream);
+/* Covariance-aware select (select_topk_covariance, router.hpp:157-193): scores
+ * scale*<q_bar_i, k_bar_j> + log(M_j + desc->epsilon); m fp32 [B*H][N]. */
+pisa_status pisa_b200_select_cov(pisa_ctx* ctx, const pisa_attn_desc* desc, const float* q_bar,
+                                 const float* k_bar, const float* m, int32_t* selected,
+                                 uint32_t* mask, void* stream);
 
 /* Attention (pisa_streaming / pisa_reference) for a GIVEN plan and prepare
  * products (device, as produced above): selected int32 [B*H][N][k] ascending,

@@ -234,7 +234,9 @@ MultiheadResult<T> pisa_multihead(const TensorBundle<T>& bundle, double r,
     desc.scale = cfg.scale;
     desc.sparsity = r;
     desc.variant = int32_t(variant);
-    desc.router = router.row_level ? -1 : int32_t(router.strategy);
+    desc.router = int32_t(router.strategy);
+    desc.epsilon = router.epsilon;
+    desc.row_level = router.row_level;
     desc.force_diagonal = router.force_diagonal;
     desc.literal_phase3 = cfg.literal_phase3;
     desc.ragged = cfg.ragged;

@@ -58,6 +58,11 @@ def lib():
         L.oracle_query_means.argtypes = [_f32p, i64, i64, i64, _f64p]
         L.oracle_select_plain.argtypes = [_f64p, _f64p, i64, i64, i64, i64, C.c_double, C.c_int,
                                           _i32p, C.c_void_p]
+        L.oracle_select_cov.argtypes = [_f64p, _f64p, _f64p, i64, i64, i64, i64, C.c_double,
+                                        C.c_double, C.c_int, _i32p, C.c_void_p]
+        L.oracle_select_rowmax.argtypes = [_f32p, _f64p, C.c_void_p, i64, i64, i64, i64, i64,
+                                           C.c_double, C.c_double, _i32p, C.c_void_p]
+        L.oracle_block_norms.argtypes = [_f32p, _f32p, i64, i64, i64, _f64p, C.c_void_p, C.c_int]
         L.oracle_pisa_attention.argtypes = [_f32p, _f32p, _f32p, i64, i64, i64, _i32p, i64, _f64p,
                                             _f64p, _f64p, _f64p, C.c_double, C.c_int, C.c_int,
                                             i64, i64, C.c_int, _f64p, _f64p, _f64p, _f64p]
@@ -91,6 +96,11 @@ def ref():
         R.ref_block_stats.argtypes = [_f32p, _f32p, _f32p, i64, i64, i64, _f64p, _f64p, _f64p,
                                       _f64p, _f64p]
         R.ref_select_plain.argtypes = [_f64p, _f64p, i64, i64, i64, i64, C.c_double, C.c_int, _i32p]
+        R.ref_block_norms.argtypes = [_f32p, _f32p, i64, i64, i64, _f64p, C.c_void_p]
+        R.ref_select_cov.argtypes = [_f64p, _f64p, _f64p, i64, i64, i64, i64, C.c_double, C.c_double,
+                                     C.c_int, _i32p]
+        R.ref_select_rowmax.argtypes = [_f32p, _f64p, C.c_void_p, i64, i64, i64, i64, i64, C.c_double,
+                                        C.c_double, _i32p]
         R.ref_multihead.argtypes = [_f32p, _f32p, _f32p, i64, i64, i64, C.c_double, C.c_int,
                                     C.c_int, i64, i64, C.c_double, C.c_int, C.c_int, C.c_int,
                                     C.c_uint, _f32p, C.c_void_p, C.c_void_p, C.c_void_p,
@@ -178,6 +188,50 @@ def select_plain(qbar, kbar, k: int, scale: float, force_diagonal: bool = False,
     return (sel, scores) if return_scores else sel
 
 
+def block_norms(k: np.ndarray, v: np.ndarray, B: int = 64, threads: int = 0):
+    """M_j = ||H_j - H_bar||_2 per key block (compute_global_stats with norms,
+    block_stats.hpp:207-241; Jacobi spectral norm, :42-94). Ragged-aware."""
+    L, d = k.shape
+    N = (L + B - 1) // B
+    m = np.empty(N)
+    _check(lib().oracle_block_norms(np.ascontiguousarray(k, np.float32),
+                                    np.ascontiguousarray(v, np.float32), L, d, B, m, None, threads),
+           "block_norms")
+    return m
+
+
+def select_cov(qbar, kbar, m, k: int, scale: float, eps: float = 1e-6, force_diagonal=False,
+               return_scores: bool = False):
+    """select_topk_covariance (router.hpp:157-193)."""
+    nq, d = qbar.shape
+    n = kbar.shape[0]
+    sel = np.empty((nq, k), np.int32)
+    scores = np.empty((nq, n)) if return_scores else None
+    _check(lib().oracle_select_cov(np.ascontiguousarray(qbar), np.ascontiguousarray(kbar),
+                                   np.ascontiguousarray(m, np.float64), nq, n, d, k, scale, eps,
+                                   int(force_diagonal), sel,
+                                   scores.ctypes.data if scores is not None else None),
+           "select_cov")
+    return (sel, scores) if return_scores else sel
+
+
+def select_rowmax(q, kbar, k: int, scale: float, m=None, eps: float = 1e-6, B: int = 64,
+                  return_scores: bool = False):
+    """select_topk_rowmax (router.hpp:198-233); m = None for the plain score."""
+    L, d = q.shape
+    n = kbar.shape[0]
+    nq = (L + B - 1) // B
+    sel = np.empty((nq, k), np.int32)
+    scores = np.empty((nq, n)) if return_scores else None
+    mm = None if m is None else np.ascontiguousarray(m, np.float64)
+    _check(lib().oracle_select_rowmax(np.ascontiguousarray(q, np.float32), np.ascontiguousarray(kbar),
+                                      mm.ctypes.data if mm is not None else None, L, n, d, B, k,
+                                      scale, eps, sel,
+                                      scores.ctypes.data if scores is not None else None),
+           "select_rowmax")
+    return (sel, scores) if return_scores else sel
+
+
 VARIANTS = {"sparse_only": 0, "zeroth": 1, "block_first": 2, "hybrid": 3, "global_centroid": 4}
 
 
@@ -254,8 +308,39 @@ def ref_select_plain(qbar, kbar, k: int, scale: float, force_diagonal=False):
     return sel
 
 
+def ref_block_norms(k, v, B: int = 64):
+    L, d = k.shape
+    m = np.empty(L // B)
+    _check(ref().ref_block_norms(np.ascontiguousarray(k, np.float32),
+                                 np.ascontiguousarray(v, np.float32), L, d, B, m, None),
+           "ref_block_norms")
+    return m
+
+
+def ref_select_cov(qbar, kbar, m, k: int, scale: float, eps=1e-6, force_diagonal=False):
+    nq, d = qbar.shape
+    sel = np.empty((nq, k), np.int32)
+    _check(ref().ref_select_cov(np.ascontiguousarray(qbar), np.ascontiguousarray(kbar),
+                                np.ascontiguousarray(m, np.float64), nq, kbar.shape[0], d, k, scale,
+                                eps, int(force_diagonal), sel), "ref_select_cov")
+    return sel
+
+
+def ref_select_rowmax(q, kbar, k: int, scale: float, m=None, eps=1e-6, B: int = 64):
+    L, d = q.shape
+    sel = np.empty((L // B, k), np.int32)
+    mm = None if m is None else np.ascontiguousarray(m, np.float64)
+    _check(ref().ref_select_rowmax(np.ascontiguousarray(q, np.float32), np.ascontiguousarray(kbar),
+                                   mm.ctypes.data if mm is not None else None, L, kbar.shape[0], d,
+                                   B, k, scale, eps, sel), "ref_select_rowmax")
+    return sel
+
+
 def ref_multihead(q, k, v, r=0.875, variant="hybrid", force_diagonal=False, B=64, group=8,
-                  scale=0.0, accum_f64=True, streaming=True, literal_phase3=False, threads=0):
+                  scale=0.0, accum_f64=True, streaming=True, literal_phase3=False, threads=0,
+                  router="plain", row_level=False):
+    """pisa_multihead of the unmodified reference; router "plain" | "covariance"
+    (RouterOptions, engine.hpp:385-390, epsilon 1e-6)."""
     H, L, d = q.shape
     N = L // B
     kk, _ = sparsity_to_k(r, N)
@@ -267,7 +352,8 @@ def ref_multihead(q, k, v, r=0.875, variant="hybrid", force_diagonal=False, B=64
     _check(ref().ref_multihead(np.ascontiguousarray(q, np.float32),
                                np.ascontiguousarray(k, np.float32),
                                np.ascontiguousarray(v, np.float32), H, L, d, r, VARIANTS[variant],
-                               int(force_diagonal), B, group, scale, int(accum_f64),
+                               int(force_diagonal) | (2 if router == "covariance" else 0)
+                               | (4 if row_level else 0), B, group, scale, int(accum_f64),
                                int(streaming), int(literal_phase3), threads, out,
                                sel.ctypes.data, denom.ctypes.data, tm.ctypes.data, et.ctypes.data,
                                rm.ctypes.data, times.ctypes.data, C.byref(kout)), "ref_multihead")

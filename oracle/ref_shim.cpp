@@ -125,6 +125,52 @@ int ref_select_plain(const double* qbar, const double* kbar, int64_t nq, int64_t
     });
 }
 
+// Spectral deviation norms M_j = ||H_j - H_bar||_2 (compute_global_stats with
+// compute_norms = true, block_stats.hpp:207-241, SpectralMethod::Exact as
+// pisa_multihead uses it, engine.hpp:439). m: [N].
+int ref_block_norms(const float* k, const float* v, int64_t L, int64_t d, int64_t B, double* m,
+                    double* m_max) {
+    return guarded([&] {
+        pisa::ConstView<float> kv(k, std::size_t(L), std::size_t(d));
+        pisa::ConstView<float> vv(v, std::size_t(L), std::size_t(d));
+        auto st = pisa::compute_block_stats(kv, vv, std::size_t(B));
+        pisa::compute_global_stats(st, pisa::SpectralMethod::Exact, true);
+        std::memcpy(m, st.m.data(), st.m.size() * sizeof(double));
+        if (m_max) *m_max = st.m_max;
+    });
+}
+
+// select_topk_covariance (router.hpp:157-193).
+int ref_select_cov(const double* qbar, const double* kbar, const double* m, int64_t nq, int64_t n,
+                   int64_t d, int64_t k, double scale, double eps, int force_diagonal,
+                   int32_t* selected) {
+    return guarded([&] {
+        pisa::ConstView<double> qb(qbar, std::size_t(nq), std::size_t(d));
+        pisa::ConstView<double> kb(kbar, std::size_t(n), std::size_t(d));
+        const std::vector<double> mv(m, m + n);
+        const auto plan = pisa::select_topk_covariance(qb, kb, mv, eps, std::size_t(k), scale,
+                                                       force_diagonal != 0);
+        for (int64_t i = 0; i < nq; ++i)
+            for (int64_t p = 0; p < k; ++p) selected[i * k + p] = int32_t(plan.selected[i][p]);
+    });
+}
+
+// select_topk_rowmax (router.hpp:198-233) on float queries [L][d]; m may be NULL.
+int ref_select_rowmax(const float* q, const double* kbar, const double* m, int64_t L, int64_t n,
+                      int64_t d, int64_t B, int64_t k, double scale, double eps, int32_t* selected) {
+    return guarded([&] {
+        pisa::ConstView<float> qv(q, std::size_t(L), std::size_t(d));
+        pisa::ConstView<double> kb(kbar, std::size_t(n), std::size_t(d));
+        std::vector<double> mv;
+        if (m) mv.assign(m, m + n);
+        const auto plan = pisa::select_topk_rowmax<float>(qv, kb, std::size_t(B), std::size_t(k), scale,
+                                                         m ? &mv : nullptr, eps);
+        const int64_t nq = L / B;
+        for (int64_t i = 0; i < nq; ++i)
+            for (int64_t p = 0; p < k; ++p) selected[i * k + p] = int32_t(plan.selected[i][p]);
+    });
+}
+
 // pisa_multihead (engine.hpp:408-470) on a [H][L][d] float bundle, Plain router.
 // out: [H][L][d] float; selected: [H][N][k]; diagnostics [H][L] doubles
 // (optional); times_ms[3] = prepare, select, attention (optional).
@@ -144,8 +190,12 @@ int ref_multihead(const float* q, const float* k, const float* v, int64_t H, int
         b.k.assign(k, k + n);
         b.v.assign(v, v + n);
         const auto cfg = make_cfg(block, group, scale, accum_f64, literal_phase3, threads);
+        // force_diagonal carries RouterOptions flags: bit 0 force_diagonal,
+        // bit 1 CovarianceAware strategy, bit 2 row_level (epsilon stays 1e-6)
         pisa::RouterOptions router;
-        router.force_diagonal = force_diagonal != 0;
+        router.force_diagonal = (force_diagonal & 1) != 0;
+        if (force_diagonal & 2) router.strategy = pisa::RouterStrategy::CovarianceAware;
+        router.row_level = (force_diagonal & 4) != 0;
         const auto res = pisa::pisa_multihead(b, r, router, pisa::PisaVariant(variant), cfg,
                                               streaming != 0);
         const std::size_t nb = res.num_blocks, kk = res.k;

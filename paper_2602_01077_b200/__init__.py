@@ -11,6 +11,7 @@ from .pisa import (  # noqa: F401
     RouterOptions, RouterStrategy, SelectionPlan, SparsityResolution, TensorBundle,
     Unsupported, compute_prepare, fwd, fwd_host, kernel_names, make_desc, pisa_attention,
     pisa_multihead, pisa_reference, pisa_streaming, resolve, select_topk_plain, selftest_mma,
+    block_norms, select_topk_covariance,
     sparsity_to_k, variant_name,
 )
 

@@ -23,7 +23,7 @@ class AttnDesc(C.Structure):
         ("scale", C.c_double), ("sparsity", C.c_double), ("topk", i64),
         ("variant", C.c_int32), ("router", C.c_int32), ("force_diagonal", C.c_int32),
         ("literal_phase3", C.c_int32), ("ragged", C.c_int32), ("out_dtype", C.c_int32),
-        ("check_finite", C.c_int32), ("reserved", C.c_int32),
+        ("check_finite", C.c_int32), ("row_level", C.c_int32), ("epsilon", C.c_double),
     ]
 
 
@@ -36,7 +36,8 @@ class Diag(C.Structure):
 EXPORTED = [
     "pisa_b200_create", "pisa_b200_destroy", "pisa_b200_last_error", "pisa_b200_abi_version",
     "pisa_b200_sparsity_to_k", "pisa_b200_resolve", "pisa_b200_fwd", "pisa_b200_fwd_host",
-    "pisa_b200_block_stats", "pisa_b200_select", "pisa_b200_attention",
+    "pisa_b200_block_stats", "pisa_b200_select", "pisa_b200_block_norms",
+    "pisa_b200_select_cov", "pisa_b200_attention",
     "pisa_b200_last_launch_count", "pisa_b200_kernel_name", "pisa_b200_selftest_mma",
     "pisa_b200_set_profiling", "pisa_b200_read_profile", "pisa_b200_debug_trace",
 ]
@@ -74,6 +75,8 @@ def load(build_if_missing: bool = False):
     L.pisa_b200_fwd_host.argtypes = [vp, C.POINTER(AttnDesc), vp, vp, vp, vp, C.POINTER(Diag)]
     L.pisa_b200_block_stats.argtypes = [vp, C.POINTER(AttnDesc), vp, vp, vp, vp, vp, vp, vp, vp]
     L.pisa_b200_select.argtypes = [vp, C.POINTER(AttnDesc), vp, vp, vp, vp, vp]
+    L.pisa_b200_block_norms.argtypes = [vp, C.POINTER(AttnDesc), vp, vp, vp, vp, vp]
+    L.pisa_b200_select_cov.argtypes = [vp, C.POINTER(AttnDesc), vp, vp, vp, vp, vp, vp]
     L.pisa_b200_attention.argtypes = [vp, C.POINTER(AttnDesc), vp, vp, vp, vp, vp, vp, vp, vp,
                                       C.POINTER(Diag), vp]
     L.pisa_b200_last_launch_count.argtypes = [vp]
@@ -87,7 +90,8 @@ def load(build_if_missing: bool = False):
     L.pisa_b200_read_profile.argtypes = [vp, C.POINTER(C.c_double), C.POINTER(i64)]
     for name in ("pisa_b200_set_profiling", "pisa_b200_read_profile", "pisa_b200_create", "pisa_b200_sparsity_to_k", "pisa_b200_resolve",
                  "pisa_b200_fwd", "pisa_b200_fwd_host", "pisa_b200_block_stats",
-                 "pisa_b200_select", "pisa_b200_attention", "pisa_b200_selftest_mma"):
+                 "pisa_b200_select", "pisa_b200_block_norms", "pisa_b200_select_cov",
+                 "pisa_b200_attention", "pisa_b200_selftest_mma"):
         getattr(L, name).restype = C.c_int
     _lib = L
     return L

@@ -31,9 +31,12 @@ __device__ __forceinline__ uint32_t order_key(float f) {
 // same order as the reference's dot_d loop), so results are reproducible.
 constexpr int kTile = 64, kAK = 32;
 
+// rect (covariance router, router.hpp:176-183): per key block log(M_j + eps),
+// added after the scaled dot product; null for the plain router.
 template <int D>
 __global__ void __launch_bounds__(256) score_kernel(const float* __restrict__ qbar,
                                                     const float* __restrict__ kbar,
+                                                    const float* __restrict__ rect,
                                                     uint32_t* __restrict__ keys, int N,
                                                     float scale) {
     __shared__ float As[kAK][kTile + 4];
@@ -71,7 +74,11 @@ __global__ void __launch_bounds__(256) score_kernel(const float* __restrict__ qb
 #pragma unroll
         for (int w = 0; w < 4; ++w) {
             const int j = j0 + tx * 4 + w;
-            if (j < N) keys[(size_t(bh) * N + i) * N + j] = order_key(scale * acc[u][w]);
+            if (j < N) {
+                float sc = scale * acc[u][w];
+                if (rect) sc += rect[size_t(bh) * N + j];
+                keys[(size_t(bh) * N + i) * N + j] = order_key(sc);
+            }
         }
     }
 }
@@ -212,9 +219,9 @@ cudaError_t launch_select(int D, const SelectArgs& a, int BH, uint32_t* keys, cu
     const int nt = (a.N + kTile - 1) / kTile;
     dim3 g1(nt, nt, BH);
     if (D == 128)
-        score_kernel<128><<<g1, 256, 0, s>>>(a.qbar, a.kbar, keys, a.N, a.scale);
+        score_kernel<128><<<g1, 256, 0, s>>>(a.qbar, a.kbar, a.rect, keys, a.N, a.scale);
     else
-        score_kernel<64><<<g1, 256, 0, s>>>(a.qbar, a.kbar, keys, a.N, a.scale);
+        score_kernel<64><<<g1, 256, 0, s>>>(a.qbar, a.kbar, a.rect, keys, a.N, a.scale);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     const size_t smem = sizeof(uint32_t) * size_t(kRowsPerCta) * (a.N + 256);
@@ -226,6 +233,18 @@ cudaError_t launch_select(int D, const SelectArgs& a, int BH, uint32_t* keys, cu
 cudaError_t launch_plan_to_mask(const int32_t* selected, int N, int k, int W, uint32_t* mask,
                                 int* bad, int BH, cudaStream_t s) {
     plan_to_mask_kernel<<<dim3(N, BH), 128, 0, s>>>(selected, N, k, W, mask, bad);
+    return cudaGetLastError();
+}
+
+namespace {
+__global__ void rectifier_kernel(const float* __restrict__ m, double eps, float* __restrict__ rect, int n) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) rect[i] = float(log(double(m[i]) + eps));
+}
+}  // namespace
+
+cudaError_t launch_rectifier(const float* m, double eps, float* rect, int n, cudaStream_t s) {
+    rectifier_kernel<<<(n + 255) / 256, 256, 0, s>>>(m, eps, rect, n);
     return cudaGetLastError();
 }
 

@@ -39,15 +39,32 @@ cudaError_t launch_stats_to_bf16(int D, const float* kbar, const float* vhat, co
                                  __nv_bfloat16* hbar_bf, float* kbar_global, int BH,
                                  cudaStream_t s);
 
+// K1c: spectral deviation norms M_j = ||H_j - H_bar||_2 (covariance router).
+struct NormArgs {
+    const float* kbar;  // [BH][N][D]
+    const float* hbar;  // [BH][D][D]
+    float* m;           // [BH][N]
+    float* rect;        // [BH][N] log(M_j + eps), or null
+    double eps;
+    int L, N, H;
+    int64_t ks_b, ks_h, ks_l, vs_b, vs_h, vs_l;  // element strides of k / v
+};
+cudaError_t launch_block_norms(int D, const __nv_bfloat16* k, const __nv_bfloat16* v,
+                               const NormArgs& a, int BH, cudaStream_t s);
+size_t block_norms_smem_bytes(int D);
+
 // K2: fp32 block scoring + top-k (score desc, index asc) per query block.
 struct SelectArgs {
     const float* qbar;  // [BH][N][D]
     const float* kbar;  // [BH][N][D]
+    const float* rect;  // [BH][N] covariance rectifier log(M_j + eps) added to scores, or null
     int32_t* selected;  // [BH][N][k]  (may be null)
     uint32_t* mask;     // [BH][N][W]
     int N, W, k, force_diagonal;
     float scale;
 };
+// rect[i] = log(m[i] + eps) (covariance rectifier from caller-supplied norms)
+cudaError_t launch_rectifier(const float* m, double eps, float* rect, int n, cudaStream_t s);
 // keys: scratch uint32 [BH][N][N]
 cudaError_t launch_select(int D, const SelectArgs& a, int BH, uint32_t* keys, cudaStream_t s);
 

@@ -47,8 +47,8 @@ namespace {
 
 const char* kKernelNames[] = {"block_stats_kernel", "hbar_reduce_kernel", "select_kernels",
                               "fused_attn_kernel",  "plan_to_mask_kernel", "stats_to_bf16_kernel",
-                              nullptr};
-enum KernelId { kK1 = 0, kK1b = 1, kK2 = 2, kK3 = 3, kPlan = 4, kToBf16 = 5 };
+                              "block_norms_kernel", nullptr};
+enum KernelId { kK1 = 0, kK1b = 1, kK2 = 2, kK3 = 3, kPlan = 4, kToBf16 = 5, kK1c = 6 };
 
 cudaEvent_t pooled_event(pisa_ctx* c) {
     if (!c->pool.empty()) {
@@ -185,8 +185,13 @@ pisa_status resolve(pisa_ctx* ctx, const pisa_attn_desc* d, Plan* p) {
         return fail(ctx, PISA_ERR_INVALID_DIMENSION, "unknown variant");
     if (d->variant == PISA_BLOCK_FIRST)
         return fail(ctx, PISA_ERR_UNSUPPORTED, "BlockFirst is not on the GPU path");
-    if (d->router != PISA_ROUTER_PLAIN)
-        return fail(ctx, PISA_ERR_UNSUPPORTED, "only the Plain router runs on the GPU path");
+    if (d->router != PISA_ROUTER_PLAIN && d->router != PISA_ROUTER_COVARIANCE)
+        return fail(ctx, PISA_ERR_INVALID_DIMENSION, "unknown router");
+    if (d->router == PISA_ROUTER_COVARIANCE && !(d->epsilon > 0.0))  // router.hpp:164-166
+        return fail(ctx, PISA_ERR_INVALID_EPSILON,
+                    "epsilon must be > 0, got " + std::to_string(d->epsilon));
+    if (d->row_level)
+        return fail(ctx, PISA_ERR_UNSUPPORTED, "row-level routing is not on the GPU path");
     const int64_t N = (d->seq_len + 63) / 64;
     if (N > 4096)  // the fused kernel keeps the union list and masks in shared memory
         return fail(ctx, PISA_ERR_UNSUPPORTED, "more than 4096 key blocks (seq_len > 262144)");
@@ -224,7 +229,7 @@ pisa_status resolve(pisa_ctx* ctx, const pisa_attn_desc* d, Plan* p) {
 
 // ------------------------------------------------------------ workspace --
 struct Work {
-    float *kbar, *vhat, *qbar, *hpart, *hbar, *kglob;
+    float *kbar, *vhat, *qbar, *hpart, *hbar, *kglob, *norms, *rect;
     __nv_bfloat16 *kbar_bf, *vhat_bf, *hbar_bf;
     int32_t* selected;
     uint32_t* mask;
@@ -248,7 +253,7 @@ pisa_status workspace(pisa_ctx* ctx, const Plan& p, Work* w) {
                  o_kbf = take(BH * p.Npad * D * 2), o_vbf = take(BH * p.Npad * D * 2),
                  o_hbf = take(BH * D * D * 2), o_sel = take(BH * N * p.k * 4),
                  o_mask = take(BH * N * p.W * 4), o_keys = take(BH * N * N * 4),
-                 o_flag = take(16);
+                 o_norms = take(BH * N * 4), o_rect = take(BH * N * 4), o_flag = take(16);
     if (off > ctx->arena_bytes) {
         if (ctx->arena) cudaFree(ctx->arena);
         ctx->arena = nullptr;
@@ -264,6 +269,8 @@ pisa_status workspace(pisa_ctx* ctx, const Plan& p, Work* w) {
     w->hpart = reinterpret_cast<float*>(b + o_hpart);
     w->hbar = reinterpret_cast<float*>(b + o_hbar);
     w->kglob = reinterpret_cast<float*>(b + o_kglob);
+    w->norms = reinterpret_cast<float*>(b + o_norms);
+    w->rect = reinterpret_cast<float*>(b + o_rect);
     w->kbar_bf = reinterpret_cast<__nv_bfloat16*>(b + o_kbf);
     w->vhat_bf = reinterpret_cast<__nv_bfloat16*>(b + o_vbf);
     w->hbar_bf = reinterpret_cast<__nv_bfloat16*>(b + o_hbf);
@@ -296,10 +303,25 @@ pisa_status run_stats(pisa_ctx* ctx, const pisa_attn_desc& d, const Plan& p, con
     return PISA_OK;
 }
 
+// K1c: M_j = ||H_j - H_bar||_2 and the rectifier log(M_j + eps) (covariance router),
+// after run_stats (needs k_bar and H_bar in the workspace).
+pisa_status run_norms(pisa_ctx* ctx, const pisa_attn_desc& d, const Plan& p, const Work& w,
+                      const void* k, const void* v, cudaStream_t s) {
+    NormArgs a{w.kbar,      w.hbar,        w.norms,       w.rect,        d.epsilon,
+               int(p.L),    int(p.N),      int(d.heads),  d.k_strides[0], d.k_strides[1],
+               d.k_strides[2], d.v_strides[0], d.v_strides[1], d.v_strides[2]};
+    ProfScope ps(ctx, kK1c, s);
+    const cudaError_t e = launch_block_norms(int(p.D), static_cast<const __nv_bfloat16*>(k),
+                                             static_cast<const __nv_bfloat16*>(v), a, int(p.BH), s);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "block_norms launch");
+    ctx->launches += 1;
+    return PISA_OK;
+}
+
 pisa_status run_select(pisa_ctx* ctx, const pisa_attn_desc& d, const Plan& p, const float* qbar,
-                       const float* kbar, int32_t* selected, uint32_t* mask, uint32_t* keys,
-                       cudaStream_t s) {
-    SelectArgs a{qbar, kbar, selected, mask, int(p.N), int(p.W), int(p.k), d.force_diagonal,
+                       const float* kbar, const float* rect, int32_t* selected, uint32_t* mask,
+                       uint32_t* keys, cudaStream_t s) {
+    SelectArgs a{qbar, kbar, rect, selected, mask, int(p.N), int(p.W), int(p.k), d.force_diagonal,
                  float(p.scale)};
     ProfScope ps(ctx, kK2, s);
     const cudaError_t e = launch_select(int(p.D), a, int(p.BH), keys, s);
@@ -437,7 +459,7 @@ const char* pisa_b200_last_error(const pisa_ctx* c) { return c ? c->last_error.c
 int64_t pisa_b200_last_launch_count(const pisa_ctx* c) { return c ? c->launches : 0; }
 
 const char* pisa_b200_kernel_name(int i) {
-    if (i < 0 || i >= 6) return nullptr;
+    if (i < 0 || i >= 7) return nullptr;
     return kKernelNames[i];
 }
 
@@ -510,8 +532,12 @@ pisa_status pisa_b200_fwd(pisa_ctx* ctx, const pisa_attn_desc* d, const void* q,
     Work w;
     if ((st = workspace(ctx, p, &w)) != PISA_OK) return st;
     if ((st = run_stats(ctx, *d, p, w, q, k, v, s)) != PISA_OK) return st;
+    const bool cov = d->router == PISA_ROUTER_COVARIANCE;
+    if (cov && (st = run_norms(ctx, *d, p, w, k, v, s)) != PISA_OK) return st;
     int32_t* sel = (diag && diag->selected) ? diag->selected : nullptr;
-    if ((st = run_select(ctx, *d, p, w.qbar, w.kbar, sel, w.mask, w.keys, s)) != PISA_OK) return st;
+    if ((st = run_select(ctx, *d, p, w.qbar, w.kbar, cov ? w.rect : nullptr, sel, w.mask, w.keys, s)) !=
+        PISA_OK)
+        return st;
     return run_fused(ctx, *d, p, w, q, k, v, o, diag, s);
 }
 
@@ -552,7 +578,53 @@ pisa_status pisa_b200_select(pisa_ctx* ctx, const pisa_attn_desc* d, const float
     const cudaStream_t s = static_cast<cudaStream_t>(stream);
     Work w;
     if ((st = workspace(ctx, p, &w)) != PISA_OK) return st;
-    return run_select(ctx, *d, p, q_bar, k_bar, selected, mask ? mask : w.mask, w.keys, s);
+    if (d->router != PISA_ROUTER_PLAIN)
+        return fail(ctx, PISA_ERR_INVALID_DIMENSION, "covariance routing: use pisa_b200_select_cov");
+    return run_select(ctx, *d, p, q_bar, k_bar, nullptr, selected, mask ? mask : w.mask, w.keys, s);
+}
+
+pisa_status pisa_b200_block_norms(pisa_ctx* ctx, const pisa_attn_desc* d, const void* q,
+                                  const void* k, const void* v, float* m, void* stream) {
+    if (!ctx) return PISA_ERR_INVALID_DIMENSION;
+    ctx->launches = 0;
+    Plan p;
+    pisa_status st = resolve(ctx, d, &p);
+    if (st != PISA_OK) return st;
+    if (!q || !k || !v || !m) return fail(ctx, PISA_ERR_INVALID_DIMENSION, "null pointer");
+    DeviceGuard g(ctx->device);
+    const cudaStream_t s = static_cast<cudaStream_t>(stream);
+    Work w;
+    if ((st = workspace(ctx, p, &w)) != PISA_OK) return st;
+    if ((st = run_stats(ctx, *d, p, w, q, k, v, s)) != PISA_OK) return st;
+    pisa_attn_desc dd = *d;
+    if (!(dd.epsilon > 0.0)) dd.epsilon = 1e-6;  // M_j itself does not depend on eps
+    if ((st = run_norms(ctx, dd, p, w, k, v, s)) != PISA_OK) return st;
+    const cudaError_t e =
+        cudaMemcpyAsync(m, w.norms, size_t(p.BH) * p.N * 4, cudaMemcpyDeviceToDevice, s);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "block_norms copy-out");
+    return PISA_OK;
+}
+
+pisa_status pisa_b200_select_cov(pisa_ctx* ctx, const pisa_attn_desc* d, const float* q_bar,
+                                 const float* k_bar, const float* m, int32_t* selected,
+                                 uint32_t* mask, void* stream) {
+    if (!ctx) return PISA_ERR_INVALID_DIMENSION;
+    ctx->launches = 0;
+    Plan p;
+    pisa_status st = resolve(ctx, d, &p);
+    if (st != PISA_OK) return st;
+    if (!(d->epsilon > 0.0))  // router.hpp:164-166
+        return fail(ctx, PISA_ERR_INVALID_EPSILON, "epsilon must be > 0, got " + std::to_string(d->epsilon));
+    if (!q_bar || !k_bar || !m || (!selected && !mask))
+        return fail(ctx, PISA_ERR_INVALID_DIMENSION, "null pointer");
+    DeviceGuard g(ctx->device);
+    const cudaStream_t s = static_cast<cudaStream_t>(stream);
+    Work w;
+    if ((st = workspace(ctx, p, &w)) != PISA_OK) return st;
+    cudaError_t e = launch_rectifier(m, d->epsilon, w.rect, int(p.BH) * int(p.N), s);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "rectifier launch");
+    ctx->launches += 1;
+    return run_select(ctx, *d, p, q_bar, k_bar, w.rect, selected, mask ? mask : w.mask, w.keys, s);
 }
 
 pisa_status pisa_b200_attention(pisa_ctx* ctx, const pisa_attn_desc* d, const void* q,

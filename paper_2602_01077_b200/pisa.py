@@ -282,7 +282,7 @@ def _strides_bhld(t: torch.Tensor, layout: str):
 def make_desc(q, k, v, o, *, layout="bhld", block_size=64, group_size=8, scale=0.0,
               sparsity=0.875, topk=0, variant=PisaVariant.Hybrid,
               router=RouterStrategy.Plain, force_diagonal=False, literal_phase3=False,
-              ragged=True, check_finite=False) -> _abi.AttnDesc:
+              ragged=True, check_finite=False, epsilon=1e-6, row_level=False) -> _abi.AttnDesc:
     if q.dim() != 4:
         raise InvalidDimension("InvalidDimension: expected 4-D tensors")
     if layout == "bhld":
@@ -305,6 +305,8 @@ def make_desc(q, k, v, o, *, layout="bhld", block_size=64, group_size=8, scale=0
     desc.topk = int(topk)
     desc.variant = int(variant)
     desc.router = int(router)
+    desc.epsilon = float(epsilon)
+    desc.row_level = int(row_level)
     desc.force_diagonal = int(force_diagonal)
     desc.literal_phase3 = int(literal_phase3)
     desc.ragged = int(ragged)
@@ -431,6 +433,56 @@ def select_topk_plain(q_bar: torch.Tensor, k_bar: torch.Tensor, k: int, scale: f
     return sel
 
 
+def block_norms(q, k, v, block_size: int = 64, ragged: bool = True) -> torch.Tensor:
+    """M_j = ||H_j - H_bar||_2 per key block (compute_global_stats with
+    compute_norms, block_stats.hpp:207-241): fp32 [..][N]. q/k/v [H][L][d] or
+    [B][H][L][d] bf16 device tensors."""
+    q4, k4, v4 = _bundle4(q), _bundle4(k), _bundle4(v)
+    _check_inputs(q4, k4, v4)
+    ctx = Context.get(q4.device.index)
+    desc = make_desc(q4, k4, v4, q4, block_size=block_size, ragged=ragged)
+    B, H, L = desc.batch, desc.heads, desc.seq_len
+    N = -(-L // block_size)
+    m = torch.empty((B, H, N), dtype=torch.float32, device=q4.device)
+    _raise(ctx.lib.pisa_b200_block_norms(ctx.handle, C.byref(desc), _ptr(q4), _ptr(k4), _ptr(v4),
+                                         _ptr(m), _stream()), ctx.handle)
+    return m.reshape(*q.shape[:-2], N)
+
+
+def select_topk_covariance(q_bar: torch.Tensor, k_bar: torch.Tensor, m: torch.Tensor,
+                           epsilon: float, k: int, scale: float, force_diagonal: bool = False,
+                           return_mask: bool = False):
+    """select_topk_covariance (router.hpp:157-193): scores scale * <q_bar_i, k_bar_j>
+    + log(M_j + epsilon) on fp32 device tensors q_bar/k_bar [..][N][d], m [..][N]."""
+    q4 = q_bar.reshape(-1, 1, *q_bar.shape[-2:]).contiguous()
+    k4 = k_bar.reshape(-1, 1, *k_bar.shape[-2:]).contiguous()
+    BH, _, N, d = q4.shape
+    if not epsilon > 0.0:
+        raise InvalidEpsilon(f"InvalidEpsilon: epsilon must be > 0, got {epsilon}")
+    if m.numel() != BH * N:
+        raise InvalidDimension("InvalidDimension: M has wrong length")
+    if k < 1 or k > N:
+        raise InvalidSparsity(f"InvalidSparsity: k must lie in [1, N], got {k} for N = {N}")
+    ctx = Context.get(q4.device.index)
+    desc = _abi.AttnDesc()
+    desc.batch, desc.heads, desc.seq_len, desc.head_dim = BH, 1, N * 64, d
+    for nm in ("q_strides", "k_strides", "v_strides", "o_strides"):
+        getattr(desc, nm)[:] = (N * 64 * d, N * 64 * d, d)
+    desc.block_size, desc.group_size, desc.scale, desc.topk = 64, 8, float(scale), int(k)
+    desc.variant, desc.force_diagonal, desc.ragged = 3, int(force_diagonal), 1
+    desc.router, desc.epsilon = int(RouterStrategy.CovarianceAware), float(epsilon)
+    sel = torch.empty((BH, N, k), dtype=torch.int32, device=q4.device)
+    W = (N + 31) // 32
+    mask = torch.empty((BH, N, W), dtype=torch.int32, device=q4.device)
+    st = ctx.lib.pisa_b200_select_cov(ctx.handle, C.byref(desc), _ptr(q4), _ptr(k4),
+                                      _ptr(m.contiguous().float()), _ptr(sel), _ptr(mask), _stream())
+    _raise(st, ctx.handle)
+    sel = sel.reshape(*q_bar.shape[:-2], N, k)
+    if return_mask:
+        return sel, mask.reshape(*q_bar.shape[:-2], N, W)
+    return sel
+
+
 def pisa_attention(q, k, v, selected: torch.Tensor, stats: BlockStatistics,
                    cfg: AttentionConfig = AttentionConfig(), variant=PisaVariant.Hybrid,
                    out_dtype=torch.bfloat16, diagnostics=True, ragged=True):
@@ -485,8 +537,8 @@ def pisa_multihead(bundle: TensorBundle, r: float, router: RouterOptions = Route
     streaming and reference formulations are the same kernel (they agree to
     1e-10 in the reference, test_engine.cpp:137-150), so ``use_streaming`` only
     selects which variant set is legal, as in the reference (:460)."""
-    if router.strategy != RouterStrategy.Plain or router.row_level:
-        raise Unsupported("Unsupported: only the Plain block-mean router runs on the GPU path")
+    if router.row_level:
+        raise Unsupported("Unsupported: row-level routing is not on the GPU path")
     cfg.check(bundle.seq_len, ragged=ragged)
     L = bundle.seq_len
     n = -(-L // cfg.block_size)
@@ -496,7 +548,8 @@ def pisa_multihead(bundle: TensorBundle, r: float, router: RouterOptions = Route
     out, ex = fwd(q4, k4, v4, out_dtype=out_dtype, diagnostics=diagnostics, return_plan=True,
                   block_size=cfg.block_size, group_size=cfg.group_size, scale=cfg.scale,
                   sparsity=r, variant=variant, force_diagonal=router.force_diagonal,
-                  literal_phase3=cfg.literal_phase3, ragged=ragged)
+                  literal_phase3=cfg.literal_phase3, ragged=ragged, router=router.strategy,
+                  epsilon=router.epsilon)
     torch.cuda.current_stream().synchronize()
     ms = (time.perf_counter() - t0) * 1e3
     res = MultiheadResult(k=res_k.k, num_blocks=n, sparsity_requested=r,

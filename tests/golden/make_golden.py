@@ -6,7 +6,8 @@ Run in the dev container (where /root/reference exists):
 The fixtures travel with the repo, so the GPU box can pin the oracle without
 /root/reference. Each case stores the bf16-rounded inputs, the reference plan,
 prepare products and outputs of pisa_multihead (Hybrid / Zeroth / SparseOnly /
-GlobalCentroid, streaming where the reference offers it).
+GlobalCentroid, streaming where the reference offers it), and the covariance-aware
+router's norms M_j, plan and Hybrid output.
 """
 import os
 import sys
@@ -38,6 +39,12 @@ def main():
             rec[f"ell_tail_{variant}"] = res["ell_tail"]
             rec["selected"] = res["selected"]
             rec["topk"] = np.int64(res["k"])
+        # covariance-aware router (select_topk_covariance + spectral norms)
+        res = O.ref_multihead(q, k, v, r=r, variant="hybrid", force_diagonal=fd, accum_f64=True,
+                              streaming=True, router="covariance")
+        rec["out_hybrid_cov"] = res["out"]
+        rec["selected_cov"] = res["selected"]
+        rec["m_norms"] = np.stack([O.ref_block_norms(k[h], v[h]) for h in range(H)])
         stats = [O.ref_block_stats(q[h], k[h], v[h]) for h in range(H)]
         rec["k_bar"] = np.stack([s[0] for s in stats])
         rec["v_hat"] = np.stack([s[1] for s in stats])

@@ -33,7 +33,7 @@ def test_exports_every_declared_symbol(lib):
 
 
 def test_abi_version(lib):
-    assert lib.pisa_b200_abi_version() == 1
+    assert lib.pisa_b200_abi_version() == 2  # v2: RouterOptions epsilon / row_level in the descriptor
 
 
 def test_kernel_names(lib):
@@ -69,6 +69,7 @@ def _desc(**kw):
     d.block_size, d.group_size = kw.get("block", 64), kw.get("group", 8)
     d.scale, d.sparsity, d.topk = kw.get("scale", 0.0), kw.get("r", 0.875), kw.get("topk", 0)
     d.variant, d.router = kw.get("variant", 3), kw.get("router", 0)
+    d.epsilon, d.row_level = kw.get("eps", 1e-6), kw.get("row_level", 0)
     d.ragged = kw.get("ragged", 1)
     return d
 
@@ -93,13 +94,21 @@ def test_resolve_wan14b(lib):
     (dict(r=1.0), 3),                     # InvalidSparsity (router.hpp:81-84)
     (dict(topk=65, L=4096), 3),           # k > N
     (dict(variant=2), 8),                 # BlockFirst: not on the GPU path
-    (dict(router=1), 8),                  # covariance router: not on the GPU path
+    (dict(router=1, eps=0.0), 4),         # InvalidEpsilon (router.hpp:164-166)
+    (dict(router=1, eps=-1.0), 4),
+    (dict(router=2), 1),                  # unknown router
+    (dict(row_level=1), 8),               # row-level routing: not on the GPU path
     (dict(block=32), 8),
     (dict(D=96), 8),
     (dict(L=0), 1),
 ])
 def test_resolve_errors(lib, kw, status):
     assert _resolve(lib, _desc(**kw))[0] == status
+
+
+def test_covariance_router_resolves(lib):
+    st, n, k, _ = _resolve(lib, _desc(router=1, eps=1e-6, L=1000))
+    assert (st, n, k) == (0, 16, 2)
 
 
 def test_explicit_topk_and_scale(lib):

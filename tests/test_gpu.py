@@ -117,6 +117,90 @@ def test_select_index_sets_exact(P, oracle_mod, kind, L, d, r, fd):
     assert nbad <= max(1, N // 1000), f"{nbad} near-tie rows"
 
 
+# ------------------------------------------- covariance-aware router (§8f #1) --
+@pytest.mark.parametrize("kind,H,L,d", [("gaussian", 1, 1024, 64), ("clustered", 2, 1000, 128),
+                                        ("gaussian", 1, 4096, 128)])
+def test_block_norms_match_oracle(P, oracle_mod, kind, H, L, d):
+    """M_j = ||H_j - H_bar||_2 (Lanczos, fp32) against the fp64 Jacobi oracle
+    (pinned to the reference's compute_global_stats in test_oracle.py)."""
+    O = oracle_mod
+    q, k, v = O.gen(kind, 2, H, L, d)
+    m = P.block_norms(dev_bf16(q, False), dev_bf16(k, False), dev_bf16(v, False)).cpu().numpy()
+    for h in range(H):
+        ref = O.block_norms(k[h], v[h])
+        rel = np.abs(m[h] - ref) / np.maximum(ref, 1e-30)
+        assert rel.max() <= 2e-5, f"head {h}: max rel err {rel.max():.3e}"
+
+
+def _cov_swaps(O, qb64, kb64, m64, sel_gpu, k, scale, fd):
+    ref, sc = O.select_cov(qb64, kb64, m64, k, scale, 1e-6, fd, return_scores=True)
+    bad = np.where((sel_gpu != ref).any(1))[0]
+    non_tie = []
+    for i in bad:
+        kth = np.sort(sc[i])[::-1][k - 1]
+        diff = set(sel_gpu[i]) ^ set(ref[i])
+        # GPU scores carry the fp32 rectifier (M_j ~1e-6 relative) on top of fp32 dots
+        if any(abs(sc[i][j] - kth) > 1e-5 * max(1.0, abs(kth)) for j in diff):
+            non_tie.append(int(i))
+    return len(bad), non_tie
+
+
+@pytest.mark.parametrize("kind,L,d,r,fd", [("gaussian", 4096, 128, 0.875, False),
+                                           ("clustered", 3000, 128, 0.75, True)])
+def test_covariance_select_index_sets(P, oracle_mod, kind, L, d, r, fd):
+    import torch
+    O = oracle_mod
+    q, k, v = O.gen(kind, 3, 1, L, d)
+    N = (L + 63) // 64
+    kk = O.sparsity_to_k(r, N)[0]
+    scale = d ** -0.5
+    qd, kd, vd = dev_bf16(q, False), dev_bf16(k, False), dev_bf16(v, False)
+    st = P.compute_prepare(qd, kd, vd)
+    m_gpu = P.block_norms(qd, kd, vd)
+    sel = P.select_topk_covariance(st.q_bar[0, 0], st.k_bar[0, 0], m_gpu[0], 1e-6, kk, scale,
+                                   force_diagonal=fd).cpu().numpy()
+    okb = O.block_stats(k[0], v[0])[0]
+    oqb = O.query_means(q[0])
+    om = O.block_norms(k[0], v[0])
+    nbad, non_tie = _cov_swaps(O, oqb, okb, om, sel, kk, scale, fd)
+    assert not non_tie, f"index sets differ beyond near-ties in rows {non_tie}"
+    assert nbad <= max(1, N // 200), f"{nbad} near-tie rows"
+    # the fused forward with the covariance router routes identically
+    out, ex = P.fwd(qd.unsqueeze(0), kd.unsqueeze(0), vd.unsqueeze(0), return_plan=True,
+                    sparsity=r, force_diagonal=fd, router=P.RouterStrategy.CovarianceAware,
+                    epsilon=1e-6)
+    torch.cuda.synchronize()
+    assert np.array_equal(ex["selected"][0, 0].cpu().numpy(), sel)
+
+
+@pytest.mark.parametrize("path", sorted(glob.glob(os.path.join(GOLDEN, "*_h*_l*.npz"))),
+                         ids=lambda p: os.path.basename(p)[:-4])
+def test_covariance_router_matches_reference_golden(P, path):
+    """pisa_multihead with RouterOptions{CovarianceAware}: plan and Hybrid output
+    against the unmodified reference's (fixtures from oracle/_ref)."""
+    f = np.load(path)
+    out, ex = run_fwd(P, f["q"], f["k"], f["v"], sparsity=float(f["r"]),
+                      variant=P.PisaVariant.Hybrid, force_diagonal=bool(f["force_diagonal"]),
+                      router=P.RouterStrategy.CovarianceAware, epsilon=1e-6)
+    assert np.array_equal(ex["selected"], f["selected_cov"])
+    check_close(out, f["out_hybrid_cov"].astype(np.float64))
+
+
+def test_covariance_multihead_api(P):
+    import torch
+    H, L, d = 2, 768, 64
+    g = torch.Generator().manual_seed(0)
+    x = [torch.randn(H, L, d, generator=g).to(torch.bfloat16).cuda() for _ in range(3)]
+    res = P.pisa_multihead(P.TensorBundle(*x), 0.75,
+                           P.RouterOptions(strategy=P.RouterStrategy.CovarianceAware), P.PisaVariant.Hybrid,
+                           P.AttentionConfig(), True)
+    assert len(res.plans) == H and res.k == 3
+    with pytest.raises(P.InvalidEpsilon):
+        P.pisa_multihead(P.TensorBundle(*x), 0.75,
+                         P.RouterOptions(strategy=P.RouterStrategy.CovarianceAware, epsilon=0.0),
+                         P.PisaVariant.Hybrid, P.AttentionConfig(), True)
+
+
 def test_select_edge_cases(P):
     import torch
     import torch.nn.functional as F

@@ -129,6 +129,72 @@ def test_oracle_matches_live_reference(oracle_mod, ref_available, kind, seed, H,
     np.testing.assert_allclose(res["ell_tail"] * np.exp(res["row_max"]), ref["ell_tail"], rtol=1e-9)
 
 
+# --------------------------------------- covariance-aware / row-level router --
+@pytest.mark.parametrize("path", _fixtures(), ids=lambda p: os.path.basename(p)[:-4])
+def test_covariance_router_matches_reference_fixture(oracle_mod, path):
+    """M_j (Jacobi spectral norms) 1e-10, covariance plan bit-exact, Hybrid output
+    with that plan within fp32 rounding of the reference's pisa_multihead with
+    RouterOptions{CovarianceAware} (engine.hpp:439-453)."""
+    O = oracle_mod
+    f = np.load(path)
+    q, k, v = f["q"], f["k"], f["v"]
+    H, L, d = q.shape
+    fd = bool(f["force_diagonal"])
+    kk, scale = int(f["topk"]), 1.0 / np.sqrt(d)
+    for h in range(H):
+        m = O.block_norms(k[h], v[h])
+        np.testing.assert_allclose(m, f["m_norms"][h], rtol=1e-10)
+        st = O.block_stats(k[h], v[h])
+        sel = O.select_cov(O.query_means(q[h]), st[0], m, kk, scale, 1e-6, fd)
+        assert np.array_equal(sel, f["selected_cov"][h])
+        out = O.pisa_attention(q[h], k[h], v[h], sel, st, scale, "hybrid")[0]
+        ref = f["out_hybrid_cov"][h].astype(np.float64)
+        assert np.abs(out - ref).max() <= 2e-6 * max(1.0, np.abs(ref).max())
+
+
+@pytest.mark.parametrize("kind,seed,L,d", [("gaussian", 7, 1024, 64), ("clustered", 8, 768, 128),
+                                           ("clustered", 9, 512, 16)])
+def test_router_variants_match_live_reference(oracle_mod, ref_available, kind, seed, L, d):
+    """select_topk_covariance / select_topk_rowmax (plain and rectified) and the
+    spectral norms against the unmodified reference (router.hpp:157-233)."""
+    if not ref_available:
+        pytest.skip("oracle/_ref not built (reference sources absent)")
+    O = oracle_mod
+    q, k, v = (x[0] for x in O.gen(kind, seed, 1, L, d))
+    m = O.block_norms(k, v)
+    np.testing.assert_allclose(m, O.ref_block_norms(k, v), rtol=1e-12)
+    kb = O.block_stats(k, v)[0]
+    qb = O.query_means(q)
+    N, scale = kb.shape[0], 1.0 / np.sqrt(d)
+    for kk in (1, N // 4, N - 1):
+        for fd in (False, True):
+            assert np.array_equal(O.select_cov(qb, kb, m, kk, scale, 1e-6, fd),
+                                  O.ref_select_cov(qb, kb, m, kk, scale, 1e-6, fd))
+        for eps in (1e-6, 0.5):
+            assert np.array_equal(O.select_rowmax(q, kb, kk, scale, m=m, eps=eps),
+                                  O.ref_select_rowmax(q, kb, kk, scale, m=m, eps=eps))
+        assert np.array_equal(O.select_rowmax(q, kb, kk, scale), O.ref_select_rowmax(q, kb, kk, scale))
+
+
+def test_covariance_router_rejects_epsilon(oracle_mod):
+    # router.hpp:164-166: epsilon must be > 0 -> InvalidEpsilon
+    O = oracle_mod
+    with pytest.raises(O.OracleError) as e:
+        O.select_cov(np.zeros((2, 4)), np.zeros((2, 4)), np.ones(2), 1, 1.0, 0.0)
+    assert e.value.status == 4
+
+
+def test_block_norms_of_identical_blocks_vanish(oracle_mod):
+    # every block equal -> H_j == H_bar -> M_j == 0 (the all-zero matrix path of
+    # spectral_norm_exact, block_stats.hpp:58-60)
+    O = oracle_mod
+    rng = np.random.default_rng(0)
+    kb = rng.standard_normal((64, 32)).astype(np.float32)
+    vb = rng.standard_normal((64, 32)).astype(np.float32)
+    m = O.block_norms(np.tile(kb, (4, 1)), np.tile(vb, (4, 1)))
+    assert np.all(m == 0.0)
+
+
 # ------------------------------------------------ invariants of the math --
 def test_full_coverage_equals_dense(oracle_mod):
     # test_engine.cpp:52-66 (r = 0: every variant = dense), incl. a ragged L
