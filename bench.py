@@ -171,19 +171,11 @@ def cpu_reference_sample(wl, steps, warmup, log):
 
 
 # ---------------------------------------------------------- GPU arm ----
-def union_executed_flops(sel, N, d, C2, first_order=True):
-    """Executed MMA FLOPs of the fused kernel: per 128-row tile the union of the two
-    query blocks' selections plus the centroid tiles plus Q.H_bar."""
-    import torch
-    Hr = sel.shape[0]
-    k = sel.shape[-1]
-    m = torch.zeros((Hr, N, N), dtype=torch.bool, device=sel.device)
-    m.scatter_(2, sel.long(), True)
-    if N % 2:
-        m = torch.cat([m, torch.zeros((Hr, 1, N), dtype=torch.bool, device=sel.device)], 1)
-    u = (m[:, 0::2] | m[:, 1::2]).sum(-1).double()  # [Hr][tiles]
-    per_tile = (u + C2) * (4.0 * 128 * 64 * d) + (2.0 * 128 * d * d if first_order else 0.0)
-    return float(per_tile.sum().item()), float(u.mean().item()) / k
+def executed_flops(tiles, ctas, d, first_order=True):
+    """Executed MMA FLOPs of the fused kernel from its device tile counter: every
+    64-key tile (union block or centroid chunk, pair padding included) is an
+    S = Q K^T and a P V over 128 query rows, plus one Q.H_bar per CTA."""
+    return tiles * (4.0 * 128 * 64 * d) + (ctas * 2.0 * 128 * d * d if first_order else 0.0)
 
 
 def main():
@@ -269,7 +261,6 @@ def main():
     for _ in range(warmup - 1):
         P.fwd(q, kk, v, out, **kw)
     torch.cuda.synchronize()
-    exec_flops, union_ratio = union_executed_flops(ex["selected"][0], N, d, C2)
     del ex
 
     # timed region
@@ -293,6 +284,10 @@ def main():
             dist.barrier()
     ctx.set_profiling(False)
     prof = ctx.read_profile()
+    tiles = ctx.fused_tiles() / args.steps  # per launch
+    ctas = Hr * B * (-(-N // 2))
+    exec_flops = executed_flops(tiles, ctas, d)
+    union_ratio = (tiles / ctas - 2 * (-(-C2 // 2))) / k  # union blocks (incl. pair padding) per tile / k
     t_ms = e0.elapsed_time(e1) / args.steps
     t = torch.tensor([t_ms], device=dev, dtype=torch.float64)
     if world > 1:

@@ -186,6 +186,10 @@ pisa_status pisa_b200_set_profiling(pisa_ctx* ctx, int enable);
  * libraries built with -DPISA_TRACE=1 write it. dev_buf: 16*1024 u64 (device). */
 pisa_status pisa_b200_debug_trace(pisa_ctx* ctx, unsigned long long* dev_buf, int tile);
 pisa_status pisa_b200_read_profile(pisa_ctx* ctx, double* ms, int64_t* launches);
+/* 64-key tiles (union blocks + centroid chunks, including pair padding) the
+ * fused kernel processed while profiling was enabled, summed over launches;
+ * synchronises and resets the counter. bench.py derives executed MMA FLOPs from it. */
+pisa_status pisa_b200_fused_tiles(pisa_ctx* ctx, int64_t* tiles);
 
 /* Standalone tensor-core self test: runs the three tcgen05 operand modes the fused
  * kernel uses (K-major SS, MN-major SS, TMEM-A TS) on small tiles and writes the

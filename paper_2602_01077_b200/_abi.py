@@ -39,7 +39,8 @@ EXPORTED = [
     "pisa_b200_block_stats", "pisa_b200_select", "pisa_b200_block_norms",
     "pisa_b200_select_cov", "pisa_b200_attention",
     "pisa_b200_last_launch_count", "pisa_b200_kernel_name", "pisa_b200_selftest_mma",
-    "pisa_b200_set_profiling", "pisa_b200_read_profile", "pisa_b200_debug_trace",
+    "pisa_b200_set_profiling", "pisa_b200_read_profile", "pisa_b200_fused_tiles",
+    "pisa_b200_debug_trace",
 ]
 
 _lib = None
@@ -88,6 +89,8 @@ def load(build_if_missing: bool = False):
     L.pisa_b200_debug_trace.argtypes = [vp, vp, C.c_int]
     L.pisa_b200_debug_trace.restype = C.c_int
     L.pisa_b200_read_profile.argtypes = [vp, C.POINTER(C.c_double), C.POINTER(i64)]
+    L.pisa_b200_fused_tiles.argtypes = [vp, C.POINTER(i64)]
+    L.pisa_b200_fused_tiles.restype = C.c_int
     for name in ("pisa_b200_set_profiling", "pisa_b200_read_profile", "pisa_b200_create", "pisa_b200_sparsity_to_k", "pisa_b200_resolve",
                  "pisa_b200_fwd", "pisa_b200_fwd_host", "pisa_b200_block_stats",
                  "pisa_b200_select", "pisa_b200_block_norms", "pisa_b200_select_cov",

@@ -1,0 +1,162 @@
+// K2c / K2d: query-block pairing for the fused kernel (no reference
+// counterpart: it only reorders work, every query block's result is unchanged).
+//
+// K3 runs two query blocks per CTA over the UNION of their selections, so its
+// executed work is proportional to sum over pairs |S_a U S_b|. Pairing
+// consecutive blocks (2t, 2t+1) is what a spatially coherent DiT sequence wants,
+// but not in general: on independent (gaussian) routing the union of two
+// neighbours is 1.87 k, and on multi-cluster data blocks that route alike can
+// be far apart. Here:
+//   K2c pair_candidates_kernel: warp per query block i, overlap
+//       o(i, j) = popcount(mask_i & mask_j) for j within +-kWindow of i, keeps
+//       the best kCand partners (overlap desc, index asc);
+//   K2d pair_match_kernel: one CTA per (batch, head), locally-dominant matching
+//       on the candidate graph (the parallel form of greedy max-weight
+//       matching, a 1/2-approximation): every unmatched block proposes its best
+//       unmatched candidate, mutual proposals match, repeat; the blocks left
+//       over are paired in index order. Deterministic (ties -> lower index).
+// Output pairs[bh][t] = (a, b), a < b, b = -1 for a lone last block; the fused
+// kernel's tile t processes query blocks a and b.
+#include "kernels.h"
+
+namespace pisa_b200 {
+namespace {
+
+constexpr int kCand = 8;
+// Candidate partners of block i are the blocks within +-kWindow of it: full
+// O(N^2 W) search costs ~2.5 ms at Wan2.1-14B for a further ~2 % fewer union
+// tiles (simulated: gaussian union/k 1.871 -> 1.77 windowed vs 1.735 full;
+// multi-cluster 1.856 -> 1.06 vs 1.02).
+constexpr int kWindow = 48;
+
+// candidate (overlap, index) ordering: higher overlap first, then lower index
+__device__ __forceinline__ bool better(int ov, int j, int ov2, int j2) {
+    return ov > ov2 || (ov == ov2 && j < j2);
+}
+
+__global__ void __launch_bounds__(256) pair_candidates_kernel(const uint32_t* __restrict__ mask, int N,
+                                                             int W, int* __restrict__ cand) {
+    extern __shared__ uint32_t mrow[];  // [8 warps][W]
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int bh = blockIdx.y;
+    const int i = blockIdx.x * 8 + warp;
+    uint32_t* mi = mrow + warp * W;
+    const uint32_t* M = mask + size_t(bh) * N * W;
+    if (i < N)
+        for (int w = lane; w < W; w += 32) mi[w] = M[size_t(i) * W + w];
+    __syncwarp();
+    if (i >= N) return;
+    int bo[kCand], bj[kCand];
+#pragma unroll
+    for (int c = 0; c < kCand; ++c) {
+        bo[c] = -1;
+        bj[c] = 0x7fffffff;
+    }
+    const int j0 = max(0, i - kWindow), j1 = min(N, i + kWindow + 1);
+    for (int j = j0 + lane; j < j1; j += 32) {
+        if (j == i) continue;
+        const uint32_t* mj = M + size_t(j) * W;
+        int ov = 0;
+        for (int w = 0; w < W; ++w) ov += __popc(mi[w] & mj[w]);
+        if (better(ov, j, bo[kCand - 1], bj[kCand - 1])) {  // insert into the sorted list
+            int c = kCand - 1;
+            while (c > 0 && better(ov, j, bo[c - 1], bj[c - 1])) {
+                bo[c] = bo[c - 1];
+                bj[c] = bj[c - 1];
+                --c;
+            }
+            bo[c] = ov;
+            bj[c] = j;
+        }
+    }
+    // warp merge: kCand rounds of arg-best over the lanes' list heads
+    int head = 0;
+    for (int c = 0; c < kCand; ++c) {
+        const int myo = head < kCand ? bo[head] : -1, myj = head < kCand ? bj[head] : 0x7fffffff;
+        int o = myo, jj = myj;
+#pragma unroll
+        for (int s = 16; s > 0; s >>= 1) {
+            const int o2 = __shfl_xor_sync(0xffffffffu, o, s), j2 = __shfl_xor_sync(0xffffffffu, jj, s);
+            if (better(o2, j2, o, jj)) {
+                o = o2;
+                jj = j2;
+            }
+        }
+        if (myj == jj && myo == o && head < kCand) ++head;  // the winner pops its head
+        if (lane == 0) cand[(size_t(bh) * N + i) * kCand + c] = jj < N ? jj : -1;
+    }
+}
+
+__global__ void __launch_bounds__(1024) pair_match_kernel(const int* __restrict__ cand, int N,
+                                                          int2* __restrict__ pairs) {
+    extern __shared__ int partner[];  // [N], then prop [N]
+    int* prop = partner + N;
+    __shared__ int progress;
+    const int bh = blockIdx.x;
+    const int* C = cand + size_t(bh) * N * kCand;
+    for (int i = threadIdx.x; i < N; i += blockDim.x) partner[i] = -1;
+    __syncthreads();
+    for (int round = 0; round < 64; ++round) {
+        // every unmatched block proposes its best unmatched candidate
+        for (int i = threadIdx.x; i < N; i += blockDim.x) {
+            int p = -1;
+            if (partner[i] < 0) {
+                for (int c = 0; c < kCand; ++c) {
+                    const int j = C[size_t(i) * kCand + c];
+                    if (j >= 0 && partner[j] < 0) {
+                        p = j;
+                        break;
+                    }
+                }
+            }
+            prop[i] = p;
+        }
+        if (threadIdx.x == 0) progress = 0;
+        __syncthreads();
+        for (int i = threadIdx.x; i < N; i += blockDim.x) {
+            const int j = prop[i];
+            if (j >= 0 && prop[j] == i) {  // mutual: both sides record it
+                partner[i] = j;
+                progress = 1;
+            }
+        }
+        __syncthreads();
+        if (!progress) break;
+        __syncthreads();
+    }
+    // emit pairs in order of the lower index; leftovers paired in index order
+    if (threadIdx.x == 0) {
+        int t = 0, pending = -1;
+        for (int i = 0; i < N; ++i) {
+            const int j = partner[i];
+            if (j > i) {
+                pairs[size_t(bh) * ((N + 1) / 2) + t++] = make_int2(i, j);
+            } else if (j < 0) {
+                if (pending < 0) {
+                    pending = i;
+                } else {
+                    pairs[size_t(bh) * ((N + 1) / 2) + t++] = make_int2(pending, i);
+                    pending = -1;
+                }
+            }
+        }
+        if (pending >= 0) pairs[size_t(bh) * ((N + 1) / 2) + t++] = make_int2(pending, -1);
+    }
+}
+
+}  // namespace
+
+cudaError_t launch_pairing(const uint32_t* mask, int N, int W, int BH, int* cand, int2* pairs,
+                           cudaStream_t s) {
+    const size_t sm1 = size_t(8) * W * 4;
+    cudaFuncSetAttribute(pair_candidates_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm1));
+    pair_candidates_kernel<<<dim3((N + 7) / 8, BH), 256, sm1, s>>>(mask, N, W, cand);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    const size_t sm2 = size_t(2) * N * 4;
+    cudaFuncSetAttribute(pair_match_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm2));
+    pair_match_kernel<<<BH, 1024, sm2, s>>>(cand, N, pairs);
+    return cudaGetLastError();
+}
+
+}  // namespace pisa_b200

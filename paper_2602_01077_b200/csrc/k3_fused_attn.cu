@@ -172,8 +172,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int tile = blockIdx.x;
     const int bh = blockIdx.y;
     const int b = bh / a.H, h = bh % a.H;
-    const int iA = 2 * tile, iB = 2 * tile + 1;
-    const bool hasB = iB < a.N;
+    // query blocks of this tile: the pairing kernel's choice, or (2t, 2t+1)
+    int iA = 2 * tile, iB = 2 * tile + 1;
+    if (a.pairs) {
+        const int2 pr = a.pairs[size_t(bh) * ((a.N + 1) / 2) + tile];
+        iA = pr.x;
+        iB = pr.y;
+    }
+    const bool hasB = iB >= 0 && iB < a.N;
     const bool tail = a.variant != 0;                       // Zeroth, Hybrid, GlobalCentroid
     const bool first_order = a.variant == 3 || a.variant == 4;
     const int n_last = a.L - (a.N - 1) * 64;
@@ -267,7 +273,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                 for (int c = 0; c < 8; ++c)
                     tma_load_4d(smem + Cfg::kOffQ + half * 16384 + c * 2048, &tmQ, &bar.q_full, half * 64,
-                                tile * 128 + (c & 1) * 64 + (c >> 1) * 16, h, b);
+                                ((c & 1) && hasB ? iB : iA) * 64 + (c >> 1) * 16, h, b);
         }
         __syncwarp();
         // K stage of S_g is free once S_{g-kSK} is done: s_full of that S
@@ -387,6 +393,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (++sv == kSV) { sv = 0; phv ^= 1u; }
             if (++sbv == kSB) { sbv = 0; php ^= 1u; }
         };
+        if (a.tile_count && lane == 0) atomicAdd(a.tile_count, (unsigned long long)(2 * G));
         mbar_wait<true>(&bar.q_full, 0);
         tc_fence_after();
         for (int g = 0; g < kSB && g < G; ++g) {
@@ -435,8 +442,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int ch = lane >> 4;        // column half of a 64-key sub-tile
         const float sl2 = a.scale * 1.4426950408889634f;
         const uint32_t lbase = tmem + (uint32_t(q4 * 32 + hh * 16) << 16);
-        const int grow = (2 * tile + hh) * 64 + q4 * 16 + r16;
-        const bool active = grow < a.L;
+        const int qblk = hh ? iB : iA;  // iB < 0: lone last block, its half is idle
+        const int grow = qblk * 64 + q4 * 16 + r16;
+        const bool active = qblk >= 0 && grow < a.L;
         const bool wact = __all_sync(0xffffffffu, active);
         const uint32_t* hmask = hh ? maskB : maskA;
         const __nv_bfloat16* qrow = a.q + size_t(b) * a.qs_b + size_t(h) * a.qs_h + size_t(grow) * a.qs_l;

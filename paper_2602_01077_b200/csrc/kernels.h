@@ -68,6 +68,11 @@ cudaError_t launch_rectifier(const float* m, double eps, float* rect, int n, cud
 // keys: scratch uint32 [BH][N][N]
 cudaError_t launch_select(int D, const SelectArgs& a, int BH, uint32_t* keys, cudaStream_t s);
 
+// K2c/K2d: overlap-aware pairing of query blocks for the fused kernel.
+// cand: scratch int [BH][N][8]; pairs: int2 [BH][ceil(N/2)].
+cudaError_t launch_pairing(const uint32_t* mask, int N, int W, int BH, int* cand, int2* pairs,
+                           cudaStream_t s);
+
 // Plan (ascending lists) -> bitmask, with SelectionPlan::validate semantics
 // (router.hpp:50-70): sets *bad = 1 on out-of-range / non-ascending entries.
 cudaError_t launch_plan_to_mask(const int32_t* selected, int N, int k, int W, uint32_t* mask,
@@ -76,6 +81,7 @@ cudaError_t launch_plan_to_mask(const int32_t* selected, int N, int k, int W, ui
 // K3: fused piecewise attention (Phase 1 exact over S_i, Phase 2 centroid tail,
 // Phase 3 global first-order correction), one CTA (one SM) per pair of query blocks.
 struct FusedArgs {
+    const int2* pairs;         // [BH][ceil(N/2)] query blocks per tile (K2d), or null: (2t, 2t+1)
     const __nv_bfloat16* q;    // queries (GlobalCentroid slope reads rows directly)
     int64_t qs_b, qs_h, qs_l;  // element strides of q
     const uint32_t* mask;      // [BH][N][W]
@@ -89,6 +95,7 @@ struct FusedArgs {
     int L, N, H, W, nchunk2, variant, literal_phase3, out_f32, k;
     float scale;
     unsigned long long* trace;  // PISA_TRACE builds only: [8][1024] clock deltas
+    unsigned long long* tile_count;  // instrumentation: += 64-key tiles processed (incl. padding), or null
     int trace_tile;
 };
 cudaError_t launch_fused(int D, const CUtensorMap& tmQ, const CUtensorMap& tmK, const CUtensorMap& tmV,

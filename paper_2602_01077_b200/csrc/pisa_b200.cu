@@ -10,6 +10,7 @@
 #include <cstdio>
 #include <cstring>
 #include <mutex>
+#include <cstdlib>
 #include <string>
 #include <vector>
 
@@ -41,14 +42,16 @@ struct pisa_ctx {
     std::vector<cudaEvent_t> pool;
     unsigned long long* trace = nullptr;  // debug timeline (PISA_TRACE builds)
     int trace_tile = 0;
+    bool pairing = true;  // overlap-aware query-block pairing (env PISA_B200_PAIRING=0: off)
+    unsigned long long* tiles_dev = nullptr;  // fused-kernel tile counter (profiling only)
 };
 
 namespace {
 
 const char* kKernelNames[] = {"block_stats_kernel", "hbar_reduce_kernel", "select_kernels",
                               "fused_attn_kernel",  "plan_to_mask_kernel", "stats_to_bf16_kernel",
-                              "block_norms_kernel", nullptr};
-enum KernelId { kK1 = 0, kK1b = 1, kK2 = 2, kK3 = 3, kPlan = 4, kToBf16 = 5, kK1c = 6 };
+                              "block_norms_kernel", "pairing_kernels",    nullptr};
+enum KernelId { kK1 = 0, kK1b = 1, kK2 = 2, kK3 = 3, kPlan = 4, kToBf16 = 5, kK1c = 6, kPair = 7 };
 
 cudaEvent_t pooled_event(pisa_ctx* c) {
     if (!c->pool.empty()) {
@@ -230,6 +233,8 @@ pisa_status resolve(pisa_ctx* ctx, const pisa_attn_desc* d, Plan* p) {
 // ------------------------------------------------------------ workspace --
 struct Work {
     float *kbar, *vhat, *qbar, *hpart, *hbar, *kglob, *norms, *rect;
+    int* cand;
+    int2* pairs;
     __nv_bfloat16 *kbar_bf, *vhat_bf, *hbar_bf;
     int32_t* selected;
     uint32_t* mask;
@@ -253,7 +258,8 @@ pisa_status workspace(pisa_ctx* ctx, const Plan& p, Work* w) {
                  o_kbf = take(BH * p.Npad * D * 2), o_vbf = take(BH * p.Npad * D * 2),
                  o_hbf = take(BH * D * D * 2), o_sel = take(BH * N * p.k * 4),
                  o_mask = take(BH * N * p.W * 4), o_keys = take(BH * N * N * 4),
-                 o_norms = take(BH * N * 4), o_rect = take(BH * N * 4), o_flag = take(16);
+                 o_norms = take(BH * N * 4), o_rect = take(BH * N * 4),
+                 o_cand = take(BH * N * 8 * 4), o_pairs = take(BH * ((N + 1) / 2) * 8), o_flag = take(16);
     if (off > ctx->arena_bytes) {
         if (ctx->arena) cudaFree(ctx->arena);
         ctx->arena = nullptr;
@@ -271,6 +277,8 @@ pisa_status workspace(pisa_ctx* ctx, const Plan& p, Work* w) {
     w->kglob = reinterpret_cast<float*>(b + o_kglob);
     w->norms = reinterpret_cast<float*>(b + o_norms);
     w->rect = reinterpret_cast<float*>(b + o_rect);
+    w->cand = reinterpret_cast<int*>(b + o_cand);
+    w->pairs = reinterpret_cast<int2*>(b + o_pairs);
     w->kbar_bf = reinterpret_cast<__nv_bfloat16*>(b + o_kbf);
     w->vhat_bf = reinterpret_cast<__nv_bfloat16*>(b + o_vbf);
     w->hbar_bf = reinterpret_cast<__nv_bfloat16*>(b + o_hbf);
@@ -341,7 +349,16 @@ pisa_status run_fused(pisa_ctx* ctx, const pisa_attn_desc& d, const Plan& p, con
         !make_3d_map(&tvh, w.vhat_bf, p.D, p.Npad, p.BH, 64) ||
         !make_3d_map(&th, w.hbar_bf, p.D, p.D, p.BH, uint32_t(p.D)))
         return fail(ctx, PISA_ERR_CUDA, "TMA descriptor creation failed");
+    // overlap-aware pairing of query blocks (K2c/K2d); PISA_B200_PAIRING=0 keeps (2t, 2t+1)
+    const bool pairing = ctx->pairing && p.N > 2;
+    if (pairing) {
+        ProfScope ps(ctx, kPair, s);
+        const cudaError_t e = launch_pairing(w.mask, int(p.N), int(p.W), int(p.BH), w.cand, w.pairs, s);
+        if (e != cudaSuccess) return cuda_fail(ctx, e, "pairing launch");
+        ctx->launches += 2;
+    }
     FusedArgs a{};
+    a.pairs = pairing ? w.pairs : nullptr;
     a.q = static_cast<const __nv_bfloat16*>(q);
     a.qs_b = d.q_strides[0];
     a.qs_h = d.q_strides[1];
@@ -367,6 +384,7 @@ pisa_status run_fused(pisa_ctx* ctx, const pisa_attn_desc& d, const Plan& p, con
     a.k = int(p.k);
     a.scale = float(p.scale);
     a.trace = ctx->trace;
+    a.tile_count = ctx->prof ? ctx->tiles_dev : nullptr;
     a.trace_tile = ctx->trace_tile;
     if (d.check_finite) {
         const cudaError_t e = cudaMemsetAsync(w.flag, 0, sizeof(int), s);
@@ -422,6 +440,7 @@ pisa_status pisa_b200_create(pisa_ctx** out, int device) {
     if (prop.major != 10) return PISA_ERR_UNSUPPORTED;  // sm_100a kernels only
     pisa_ctx* c = new pisa_ctx;
     c->device = device;
+    if (const char* ev = std::getenv("PISA_B200_PAIRING")) c->pairing = std::atoi(ev) != 0;
     DeviceGuard g(device);
     if (cudaMallocHost(&c->flag_host, sizeof(int)) != cudaSuccess) {
         delete c;
@@ -432,6 +451,7 @@ pisa_status pisa_b200_create(pisa_ctx** out, int device) {
 }
 
 void pisa_b200_destroy(pisa_ctx* c) {
+    if (c && c->tiles_dev) cudaFree(c->tiles_dev);
     if (!c) return;
     DeviceGuard g(c->device);
     cudaDeviceSynchronize();
@@ -459,8 +479,22 @@ const char* pisa_b200_last_error(const pisa_ctx* c) { return c ? c->last_error.c
 int64_t pisa_b200_last_launch_count(const pisa_ctx* c) { return c ? c->launches : 0; }
 
 const char* pisa_b200_kernel_name(int i) {
-    if (i < 0 || i >= 7) return nullptr;
+    if (i < 0 || i >= 8) return nullptr;
     return kKernelNames[i];
+}
+
+pisa_status pisa_b200_fused_tiles(pisa_ctx* c, int64_t* tiles) {
+    if (!c || !tiles) return PISA_ERR_INVALID_DIMENSION;
+    DeviceGuard g(c->device);
+    unsigned long long h = 0;
+    cudaError_t e = cudaSuccess;
+    if (c->tiles_dev) {
+        e = cudaMemcpy(&h, c->tiles_dev, sizeof(h), cudaMemcpyDeviceToHost);
+        if (e == cudaSuccess) e = cudaMemset(c->tiles_dev, 0, sizeof(h));
+    }
+    if (e != cudaSuccess) return cuda_fail(c, e, "fused_tiles");
+    *tiles = int64_t(h);
+    return PISA_OK;
 }
 
 pisa_status pisa_b200_debug_trace(pisa_ctx* c, unsigned long long* dev_buf, int tile) {
@@ -473,6 +507,12 @@ pisa_status pisa_b200_debug_trace(pisa_ctx* c, unsigned long long* dev_buf, int 
 pisa_status pisa_b200_set_profiling(pisa_ctx* c, int enable) {
     if (!c) return PISA_ERR_INVALID_DIMENSION;
     c->prof = enable != 0;
+    if (c->prof && !c->tiles_dev) {
+        DeviceGuard g(c->device);
+        cudaError_t e = cudaMalloc(&c->tiles_dev, sizeof(unsigned long long));
+        if (e == cudaSuccess) e = cudaMemset(c->tiles_dev, 0, sizeof(unsigned long long));
+        if (e != cudaSuccess) return cuda_fail(c, e, "profiling counter");
+    }
     return PISA_OK;
 }
 

@@ -266,6 +266,12 @@ class Context:
         names = kernel_names()
         return {names[i]: (ms[i], n[i]) for i in range(len(names)) if n[i] > 0}
 
+    def fused_tiles(self) -> int:
+        """64-key tiles the fused kernel processed while profiling (resets)."""
+        t = _abi.i64()
+        _raise(self.lib.pisa_b200_fused_tiles(self.handle, C.byref(t)), self.handle)
+        return t.value
+
 
 def _strides_bhld(t: torch.Tensor, layout: str):
     """Element strides (b, h, l) of a 4-D tensor in 'bhld' or 'blhd' order."""

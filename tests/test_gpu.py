@@ -389,8 +389,8 @@ def test_multihead_api_mirror(P, oracle_mod):
     with pytest.raises(P.BlockDivisibility):
         P.pisa_multihead(P.TensorBundle(*(t[:, :1000] for t in (b.q, b.k, b.v))), 0.75,
                          ragged=False)
-    with pytest.raises(P.Unsupported):
-        P.pisa_multihead(b, 0.75, P.RouterOptions(strategy=P.RouterStrategy.CovarianceAware))
+    with pytest.raises(P.Unsupported):  # row-level routing stays off the GPU path
+        P.pisa_multihead(b, 0.75, P.RouterOptions(row_level=True))
 
 
 # ------------------------------------------------------- full-size shapes ---
