@@ -101,6 +101,10 @@ def ref():
                                      C.c_int, _i32p]
         R.ref_select_rowmax.argtypes = [_f32p, _f64p, C.c_void_p, i64, i64, i64, i64, i64, C.c_double,
                                         C.c_double, _i32p]
+        R.ref_pqkv_write.argtypes = [C.c_char_p, C.c_int, _f64p, _f64p, _f64p, i64, i64, i64,
+                                     C.POINTER(i64)]
+        R.ref_pqkv_read.argtypes = [C.c_char_p, C.POINTER(i64), C.c_void_p, i64, C.c_char_p, i64]
+        R.ref_flop_model.argtypes = [i64, i64, i64, i64, C.c_int, _f64p]
         R.ref_multihead.argtypes = [_f32p, _f32p, _f32p, i64, i64, i64, C.c_double, C.c_int,
                                     C.c_int, i64, i64, C.c_double, C.c_int, C.c_int, C.c_int,
                                     C.c_uint, _f32p, C.c_void_p, C.c_void_p, C.c_void_p,
@@ -334,6 +338,41 @@ def ref_select_rowmax(q, kbar, k: int, scale: float, m=None, eps=1e-6, B: int = 
                                    mm.ctypes.data if mm is not None else None, L, kbar.shape[0], d,
                                    B, k, scale, eps, sel), "ref_select_rowmax")
     return sel
+
+
+def ref_pqkv_write(path: str, q, k, v, dtype: str = "f32") -> int:
+    """The reference's write_bundle_file (io.hpp:102-126) on [H][L][d] arrays."""
+    H, L, d = q.shape
+    nb = i64()
+    _check(ref().ref_pqkv_write(path.encode(), 1 if dtype == "f32" else 2,
+                                *(np.ascontiguousarray(x, np.float64) for x in (q, k, v)), H, L, d,
+                                C.byref(nb)), "ref_pqkv_write")
+    return nb.value
+
+
+def ref_pqkv_read(path: str):
+    """The reference's read_bundle_file (io.hpp:180-221): (q, k, v, dtype_tag) or
+    raises OracleError whose message starts with the reference error class."""
+    sd = (i64 * 4)()
+    err = C.create_string_buffer(512)
+    st = ref().ref_pqkv_read(path.encode(), sd, None, 0, err, 512)
+    if st != 0:
+        e = OracleError(st, err.value.decode())
+        e.message = err.value.decode()
+        raise e
+    H, L, d, tag = (int(x) for x in sd)
+    buf = np.empty(3 * H * L * d)
+    st = ref().ref_pqkv_read(path.encode(), sd, buf.ctypes.data, buf.size, err, 512)
+    _check(st, "ref_pqkv_read")
+    buf = buf.reshape(3, H, L, d)
+    return buf[0], buf[1], buf[2], tag
+
+
+def ref_flop_model(L, d, b, k, variant="hybrid"):
+    out = np.empty(6)
+    _check(ref().ref_flop_model(L, d, b, k, VARIANTS[variant], out), "ref_flop_model")
+    return dict(zip(["dense_flops", "sparse_flops", "pisa_flops", "sparse_ratio", "pisa_ratio",
+                     "overhead_ratio"], out.tolist()))
 
 
 def ref_multihead(q, k, v, r=0.875, variant="hybrid", force_diagonal=False, B=64, group=8,

@@ -14,6 +14,7 @@
 #include <cstdint>
 #include <cstring>
 #include <exception>
+#include <variant>
 
 #include "pisa/pisa.hpp"
 
@@ -168,6 +169,76 @@ int ref_select_rowmax(const float* q, const double* kbar, const double* m, int64
         const int64_t nq = L / B;
         for (int64_t i = 0; i < nq; ++i)
             for (int64_t p = 0; p < k; ++p) selected[i * k + p] = int32_t(plan.selected[i][p]);
+    });
+}
+
+// PQKV (io.hpp): write a bundle through the reference writer (dtype 1 = f32,
+// 2 = f64; values given as doubles), and read one back: header fields and the
+// payload converted to double. read status != 0 carries the reference's Io
+// error class (status_of maps ErrorKind::Io to 3).
+int ref_pqkv_write(const char* path, int dtype, const double* q, const double* k, const double* v,
+                   int64_t H, int64_t L, int64_t d, int64_t* bytes) {
+    return guarded([&] {
+        const std::size_t n = std::size_t(H * L * d);
+        auto fill = [&](auto& b) {
+            b.num_heads = std::size_t(H);
+            b.seq_len = std::size_t(L);
+            b.head_dim = std::size_t(d);
+            b.q.assign(q, q + n);
+            b.k.assign(k, k + n);
+            b.v.assign(v, v + n);
+        };
+        if (dtype == 1) {
+            pisa::TensorBundle<float> b;
+            fill(b);
+            *bytes = int64_t(pisa::write_bundle_file(pisa::AnyBundle(b), path));
+        } else {
+            pisa::TensorBundle<double> b;
+            fill(b);
+            *bytes = int64_t(pisa::write_bundle_file(pisa::AnyBundle(b), path));
+        }
+    });
+}
+
+int ref_pqkv_read(const char* path, int64_t* shape_dtype, double* qkv, int64_t cap,
+                  char* err, int64_t err_cap) {
+    try {
+        const auto any = pisa::read_bundle_file(path);
+        std::visit([&](const auto& b) {
+            shape_dtype[0] = int64_t(b.num_heads);
+            shape_dtype[1] = int64_t(b.seq_len);
+            shape_dtype[2] = int64_t(b.head_dim);
+            shape_dtype[3] = int64_t(pisa::dtype_of<typename std::decay_t<decltype(b)>::value_type>());
+            const std::size_t n = b.total_elems();
+            if (int64_t(3 * n) <= cap)
+                for (std::size_t i = 0; i < n; ++i) {
+                    qkv[i] = double(b.q[i]);
+                    qkv[n + i] = double(b.k[i]);
+                    qkv[2 * n + i] = double(b.v[i]);
+                }
+        }, any);
+        return 0;
+    } catch (const std::exception& e) {
+        if (err && err_cap > 0) {
+            std::strncpy(err, e.what(), std::size_t(err_cap - 1));
+            err[err_cap - 1] = 0;
+        }
+        return status_of(e);
+    }
+}
+
+// flop_model (analysis.hpp:309-355): out = dense, sparse, pisa, sparse_ratio,
+// pisa_ratio, overhead_ratio.
+int ref_flop_model(int64_t L, int64_t d, int64_t b, int64_t k, int variant, double* out) {
+    return guarded([&] {
+        const auto r = pisa::flop_model(std::size_t(L), std::size_t(d), std::size_t(b), std::size_t(k),
+                                        pisa::PisaVariant(variant));
+        out[0] = r.dense_flops;
+        out[1] = r.sparse_flops;
+        out[2] = r.pisa_flops;
+        out[3] = r.sparse_ratio;
+        out[4] = r.pisa_ratio;
+        out[5] = r.overhead_ratio;
     });
 }
 

@@ -11,8 +11,13 @@ from .pisa import (  # noqa: F401
     RouterOptions, RouterStrategy, SelectionPlan, SparsityResolution, TensorBundle,
     Unsupported, compute_prepare, fwd, fwd_host, kernel_names, make_desc, pisa_attention,
     pisa_multihead, pisa_reference, pisa_streaming, resolve, select_topk_plain, selftest_mma,
-    block_norms, select_topk_covariance,
+    block_norms, select_topk_covariance, BadMagic, IoError, IoFailure, MalformedFile,
+    NonFiniteValue, UnsupportedDtype, UnsupportedVersion,
     sparsity_to_k, variant_name,
 )
+
+from . import dit  # noqa: F401,E402  (DiT integration surface: warmup policy, joint attention)
+from .dit import PRESETS, PisaAttention, WarmupPolicy  # noqa: F401,E402
+from . import pqkv  # noqa: F401,E402  (PQKV tensor files, io.hpp)
 
 __all__ = [n for n in dir() if not n.startswith("_")]

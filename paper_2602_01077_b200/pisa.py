@@ -93,6 +93,34 @@ class CudaError(Error):
     kind = ErrorKind.Invariant
 
 
+class IoFailure(Error):  # base of the PQKV / file errors (errors.hpp:52-80, ErrorKind::Io)
+    kind = ErrorKind.Io
+
+
+class BadMagic(IoFailure):
+    pass
+
+
+class UnsupportedVersion(IoFailure):
+    pass
+
+
+class UnsupportedDtype(IoFailure):
+    pass
+
+
+class MalformedFile(IoFailure):
+    pass
+
+
+class NonFiniteValue(IoFailure):
+    pass
+
+
+class IoError(IoFailure):
+    pass
+
+
 _STATUS = {1: InvalidDimension, 2: BlockDivisibility, 3: InvalidSparsity, 4: InvalidEpsilon,
            5: EmptySelection, 6: NumericalOverflow, 7: DegenerateScale, 8: Unsupported,
            9: CudaError}
