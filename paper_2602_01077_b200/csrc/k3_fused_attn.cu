@@ -21,8 +21,10 @@
 // close to the chip's TMA delivery limit (~70 B/clk/SM), and a 16 KB TMA tile
 // takes 1300-2000 cycles under that load. Latency x bandwidth ~ 100+ KB must be
 // in flight per SM, so the design spends shared memory on K/V stages:
-//   * ONE CTA per SM: Q (32 KB) + 2 K + 3 V stages of two key blocks each
-//     (192 KB at d = 128) in shared memory;
+//   * ONE CTA per SM: Q (32 KB) + 3 K + 3 V stages of two key blocks each
+//     (224 KB at d = 128) in shared memory (no per-CTA union list: every
+//     consumer walks maskA | maskB with its own cursor); with two K stages the
+//     K load for S_{g+3} could only start after S_{g+1} and arrived late;
 //   * key blocks go through the pipeline in pairs ("super-tiles" of 128 keys):
 //     S = Q [K_a; K_b]^T is one set of N=128 MMAs, and each barrier round trip,
 //     commit and softmax hand-off covers two blocks -- a single issuing thread
@@ -65,7 +67,7 @@ namespace {
 
 constexpr int kThreads = 384;
 #ifndef PISA_KSTAGES
-#define PISA_KSTAGES 2
+#define PISA_KSTAGES 3
 #endif
 #ifndef PISA_VSTAGES
 #define PISA_VSTAGES 3
@@ -157,12 +159,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     using Cfg = FusedCfg<D>;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     // 1 KB alignment for the SW128 stages, by offset (keeps the pointer's
-    // shared-space provenance: loads of ulist / masks compile to LDS).
+    // shared-space provenance: loads of the masks compile to LDS).
     uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     Bars& bar = *reinterpret_cast<Bars*>(smem + Cfg::kOffBar);
     uint32_t* maskA = reinterpret_cast<uint32_t*>(smem + Cfg::kOffMask);
     uint32_t* maskB = maskA + a.W;
-    uint16_t* ulist = reinterpret_cast<uint16_t*>(maskB + a.W);
 #if PISA_TRACE
     const long long tstart = clock64();
 #endif
@@ -208,36 +209,22 @@ __global__ void __launch_bounds__(kThreads, 1)
         tmem_relinquish();
     }
     if (warp == 3) {
-        // selection bitmasks of the two query blocks -> ascending union with flags
+        // selection bitmasks of the two query blocks into shared memory, and the
+        // size U of their union (every consumer walks the union itself, in
+        // ascending order, with a UnionCursor)
         const uint32_t* mA = a.mask + (size_t(bh) * a.N + iA) * a.W;
         const uint32_t* mB = a.mask + (size_t(bh) * a.N + iB) * a.W;
-        uint32_t base = 0;
-        for (int w0 = 0; w0 < a.W; w0 += 32) {
-            const int w = w0 + lane;
-            const uint32_t wa = w < a.W ? mA[w] : 0u;
-            const uint32_t wb = (w < a.W && hasB) ? mB[w] : 0u;
-            if (w < a.W) {
-                maskA[w] = wa;
-                maskB[w] = hasB ? wb : 0xffffffffu;
-            }
-            uint32_t bits = wa | wb;
-            const uint32_t cnt = __popc(bits);
-            uint32_t incl = cnt;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
-                if (lane >= o) incl += v;
-            }
-            uint32_t pos = base + incl - cnt;
-            while (bits) {
-                const int bit = __ffs(bits) - 1;
-                bits &= bits - 1;
-                const uint32_t j = uint32_t(w * 32 + bit);
-                ulist[pos++] = uint16_t(j | (((wa >> bit) & 1u) << 14) | (((wb >> bit) & 1u) << 15));
-            }
-            base += __shfl_sync(0xffffffffu, incl, 31);
+        uint32_t cnt = 0;
+        for (int w = lane; w < a.W; w += 32) {
+            const uint32_t wa = mA[w];
+            const uint32_t wb = hasB ? mB[w] : 0u;
+            maskA[w] = wa;
+            maskB[w] = wb;
+            cnt += __popc(wa | wb);
         }
-        if (lane == 0) bar.n_union = base;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+        if (lane == 0) bar.n_union = cnt;
     }
     tc_fence_before();
     __syncthreads();
@@ -251,15 +238,36 @@ __global__ void __launch_bounds__(kThreads, 1)
     // flags are zero (fully masked: P = 0 and finite V rows).
     const int G1 = (U + 1) >> 1;
     const int G = G1 + (tail ? (a.nchunk2 + 1) >> 1 : 0);
-    // key-block row and use flags of sub-tile j of super-tile g (g < G1)
-    auto exact_entry = [&](int g, int j) -> uint32_t {
-        const int i = 2 * g + j;
-        return i < U ? uint32_t(ulist[i]) : (uint32_t(ulist[2 * g]) & 0x3FFFu);
+    // The ascending union of the two selections, walked by each consumer in
+    // order: entry = block index | (selected by 2t) << 14 | (by 2t+1) << 15.
+    struct UnionCursor {
+        const uint32_t* ma;
+        const uint32_t* mb;
+        int w = -1;
+        uint32_t bits = 0;
+        __device__ __forceinline__ uint32_t next() {
+            while (bits == 0) {
+                ++w;
+                bits = ma[w] | mb[w];
+            }
+            const int b = __ffs(bits) - 1;
+            bits &= bits - 1;
+            return uint32_t(w * 32 + b) | (((ma[w] >> b) & 1u) << 14) | (((mb[w] >> b) & 1u) << 15);
+        }
     };
-    auto tile_row = [&](int g, int j) -> int {
-        if (g < G1) return int(exact_entry(g, j) & 0x3FFFu) * 64;
-        const int c = 2 * (g - G1) + j;
-        return (c < a.nchunk2 ? c : c - 1) * 64;
+    // key rows of the two sub-tiles of super-tile g: union entries (the odd
+    // tail repeats the previous entry, fully masked), then centroid chunks
+    auto tile_rows = [&](UnionCursor& cur, int g, int& r0, int& r1) {
+        if (g < G1) {
+            const uint32_t e0 = cur.next();
+            const uint32_t e1 = (2 * g + 1 < U) ? cur.next() : e0;
+            r0 = int(e0 & 0x3FFFu) * 64;
+            r1 = int(e1 & 0x3FFFu) * 64;
+        } else {
+            const int c = 2 * (g - G1);
+            r0 = c * 64;
+            r1 = (c + 1 < a.nchunk2 ? c + 1 : c) * 64;
+        }
     };
 
     if (warp == 0) {
@@ -283,11 +291,13 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (j >= 0) mbar_wait(&bar.s_full[j % kSB], uint32_t((j / kSB) & 1));
         };
         int s = 0;
+        UnionCursor cur{maskA, maskB};
         for (int g = 0; g < G; ++g) {
             uint8_t* sK = smem + Cfg::kOffK + s * Cfg::kKV;
             wait_s_done(g - kSK);
             const bool exact = g < G1;
-            const int r0 = tile_row(g, 0), r1 = tile_row(g, 1);
+            int r0, r1;
+            tile_rows(cur, g, r0, r1);
             if (elect_one()) {
                 mbar_expect_tx(&bar.k_full[s], Cfg::kKV);
 #pragma unroll
@@ -321,11 +331,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int vh = warp - 2;
         int s = 0;
         uint32_t ph = 0;
+        UnionCursor cur{maskA, maskB};
         for (int g = 0; g < G; ++g) {
             uint8_t* sV = smem + Cfg::kOffV + s * Cfg::kKV + vh * 16384;
             mbar_wait(&bar.v_empty[s], ph ^ 1);
             const bool exact = g < G1;
-            const int r0 = tile_row(g, 0), r1 = tile_row(g, 1);
+            int r0, r1;
+            tile_rows(cur, g, r0, r1);
             if (elect_one()) {
                 mbar_expect_tx(&bar.v_full[s], 16384);
                 if (exact) {
@@ -404,21 +416,23 @@ __global__ void __launch_bounds__(kThreads, 1)
             advance_s();
         }
         for (int g = 0; g < G; ++g) {
-            // PV_g, then S_{g+3} (in-order tensor pipe: S_{g+3} overwrites P_g
-            // after PV_g read it); all waits first, one elected issue block
-            const bool more = g + kSB < G;
+            // PV_g as soon as P_g and V_g are in, then S_{g+3} once K_{g+3} is
+            // (in-order tensor pipe: S_{g+3} overwrites P_g after PV_g read it);
+            // a late K tile never holds back PV_g
             mbar_wait<true>(&bar.p_full[sbv], php);
             TRACE(9, g);
             mbar_wait<true>(&bar.v_full[sv], phv);
-            if (more) mbar_wait<true>(&bar.k_full[sk], phk);
             tc_fence_after();
-            if (elect_one()) {
-                mma_pv(g);
-                if (more) mma_s(g + kSB);
-            }
+            if (elect_one()) mma_pv(g);
             __syncwarp();
             advance_pv();
-            if (more) advance_s();
+            if (g + kSB < G) {
+                mbar_wait<true>(&bar.k_full[sk], phk);
+                tc_fence_after();
+                if (elect_one()) mma_s(g + kSB);
+                __syncwarp();
+                advance_s();
+            }
         }
         if (first_order) {
             mbar_wait<true>(&bar.h_full, 0);
@@ -501,9 +515,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t kZero16[16] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
 
         // ---- Phase 1: exact blocks of the union, two per super-tile
+        UnionCursor cur{maskA, maskB};
         for (int g = 0; g < G1; ++g) {
-            const uint32_t e0 = ulist[2 * g];
-            const uint32_t e1 = (2 * g + 1 < U) ? uint32_t(ulist[2 * g + 1]) : 0u;  // pad: unused
+            const uint32_t e0 = cur.next();
+            const uint32_t e1 = (2 * g + 1 < U) ? cur.next() : 0u;  // pad: unused
             const bool use0 = (e0 >> (14 + hh)) & 1u, use1 = (e1 >> (14 + hh)) & 1u;  // warp-uniform
             const int nv0 = (int(e0 & 0x3FFFu) == a.N - 1) ? n_last : 64;
             const int nv1 = (int(e1 & 0x3FFFu) == a.N - 1) ? n_last : 64;
@@ -697,7 +712,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 size_t fused_smem_bytes(int D, int N, int W) {
     const size_t core = (D == 128) ? size_t(FusedCfg<128>::kOffMask) : size_t(FusedCfg<64>::kOffMask);
-    return 1024 + core + size_t(2 * W) * 4 + size_t(N) * 2 + 16;
+    (void)N;
+    return 1024 + core + size_t(2 * W) * 4 + 16;
 }
 
 cudaError_t launch_fused(int D, const CUtensorMap& tmQ, const CUtensorMap& tmK, const CUtensorMap& tmV,
