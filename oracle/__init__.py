@@ -105,6 +105,7 @@ def ref():
                                      C.POINTER(i64)]
         R.ref_pqkv_read.argtypes = [C.c_char_p, C.POINTER(i64), C.c_void_p, i64, C.c_char_p, i64]
         R.ref_flop_model.argtypes = [i64, i64, i64, i64, C.c_int, _f64p]
+        R.ref_theorem1.argtypes = [_f32p, _f32p, _f32p, i64, i64, i64, i64, _i32p, _f64p, _f64p]
         R.ref_multihead.argtypes = [_f32p, _f32p, _f32p, i64, i64, i64, C.c_double, C.c_int,
                                     C.c_int, i64, i64, C.c_double, C.c_int, C.c_int, C.c_int,
                                     C.c_uint, _f32p, C.c_void_p, C.c_void_p, C.c_void_p,
@@ -373,6 +374,22 @@ def ref_flop_model(L, d, b, k, variant="hybrid"):
     _check(ref().ref_flop_model(L, d, b, k, VARIANTS[variant], out), "ref_flop_model")
     return dict(zip(["dense_flops", "sparse_flops", "pisa_flops", "sparse_ratio", "pisa_ratio",
                      "overhead_ratio"], out.tolist()))
+
+
+def ref_theorem1(q, k, v, ksel: int, B: int = 64):
+    """The reference's theorem1_check + jensen_check (analysis.hpp:86-223) for one
+    head (Plain router, norms by the exact solver): dict with the plan, per-row
+    arrays and the report scalars."""
+    L, d = q.shape
+    N = L // B
+    plan = np.empty((N, ksel), np.int32)
+    rows = np.empty((5, L))
+    scal = np.empty(6)
+    _check(ref().ref_theorem1(*(np.ascontiguousarray(x, np.float32) for x in (q, k, v)), L, d, B, ksel,
+                              plan, rows, scal), "ref_theorem1")
+    return dict(plan=plan, actual_err=rows[0], bound=rows[1], rho=rows[2], alpha_sum=rows[3],
+                jensen_rhs=rows[4], c_q=scal[0], m_max=scal[1], violations=int(scal[2]),
+                jensen_violations=int(scal[3]), max_slack_ratio=scal[4], jensen_check=int(scal[5]))
 
 
 def ref_multihead(q, k, v, r=0.875, variant="hybrid", force_diagonal=False, B=64, group=8,

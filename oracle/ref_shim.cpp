@@ -242,6 +242,46 @@ int ref_flop_model(int64_t L, int64_t d, int64_t b, int64_t k, int variant, doub
     });
 }
 
+// theorem1_check + jensen_check (analysis.hpp:86-223) for one head with the
+// Plain router at k selected blocks: plan out [N][k]; rows[5][L] = actual_err,
+// bound, rho, alpha_sum, jensen_rhs; scal[6] = c_q, m_max, violations,
+// jensen_violations, max_slack_ratio, jensen_check violations.
+int ref_theorem1(const float* q, const float* k, const float* v, int64_t L, int64_t d, int64_t B,
+                 int64_t ksel, int32_t* plan_out, double* rows, double* scal) {
+    return guarded([&] {
+        pisa::ConstView<float> qv(q, std::size_t(L), std::size_t(d));
+        pisa::ConstView<float> kv(k, std::size_t(L), std::size_t(d));
+        pisa::ConstView<float> vv(v, std::size_t(L), std::size_t(d));
+        auto st = pisa::compute_block_stats(kv, vv, std::size_t(B));
+        pisa::compute_global_stats(st, pisa::SpectralMethod::Exact, true);
+        const auto qb = pisa::query_block_means(qv, std::size_t(B));
+        pisa::AttentionConfig cfg;
+        cfg.block_size = std::size_t(B);
+        const double scale = cfg.resolved_scale(std::size_t(d));
+        const auto plan = pisa::select_topk_plain(pisa::ConstView<double>(qb.data.data(), qb.rows, qb.cols),
+                                                  pisa::ConstView<double>(st.k_bar.data.data(), st.k_bar.rows,
+                                                                          st.k_bar.cols),
+                                                  std::size_t(ksel), scale, false);
+        const int64_t N = L / B;
+        for (int64_t i = 0; i < N; ++i)
+            for (int64_t p = 0; p < ksel; ++p) plan_out[i * ksel + p] = int32_t(plan.selected[i][p]);
+        const auto rep = pisa::theorem1_check(qv, kv, vv, plan, st, cfg);
+        for (int64_t t = 0; t < L; ++t) {
+            rows[t] = rep.rows[t].actual_err;
+            rows[L + t] = rep.rows[t].bound;
+            rows[2 * L + t] = rep.rows[t].rho;
+            rows[3 * L + t] = rep.rows[t].alpha_sum;
+            rows[4 * L + t] = rep.rows[t].jensen_rhs;
+        }
+        scal[0] = rep.c_q;
+        scal[1] = rep.m_max;
+        scal[2] = double(rep.violations);
+        scal[3] = double(rep.jensen_violations);
+        scal[4] = rep.max_slack_ratio;
+        scal[5] = double(pisa::jensen_check(qv, kv, plan, std::size_t(B), scale));
+    });
+}
+
 // pisa_multihead (engine.hpp:408-470) on a [H][L][d] float bundle, Plain router.
 // out: [H][L][d] float; selected: [H][N][k]; diagnostics [H][L] doubles
 // (optional); times_ms[3] = prepare, select, attention (optional).

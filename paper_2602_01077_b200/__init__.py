@@ -19,5 +19,6 @@ from .pisa import (  # noqa: F401
 from . import dit  # noqa: F401,E402  (DiT integration surface: warmup policy, joint attention)
 from .dit import PRESETS, PisaAttention, WarmupPolicy  # noqa: F401,E402
 from . import pqkv  # noqa: F401,E402  (PQKV tensor files, io.hpp)
+from . import analysis  # noqa: F401,E402  (theory checks on GPU outputs, analysis.hpp)
 
 __all__ = [n for n in dir() if not n.startswith("_")]
