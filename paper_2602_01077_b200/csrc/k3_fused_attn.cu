@@ -85,6 +85,13 @@ constexpr uint32_t kColO = 0, kColS = 128;  // O | three S/P buffers (P_g over t
 #define PISA_POLY_MASK 0x00
 #endif
 constexpr uint32_t kPolyMask = PISA_POLY_MASK;
+// The softmax warps' wait for S: spin (poll) or suspend in hardware between
+// polls. Polling steals issue slots from the other warpgroup's warps on the
+// same sub-partitions while one warpgroup runs ahead.
+#ifndef PISA_SOFTMAX_SPIN
+#define PISA_SOFTMAX_SPIN 1
+#endif
+constexpr bool kSoftmaxSpin = PISA_SOFTMAX_SPIN != 0;
 __device__ __forceinline__ float ex2_mix(float x, int i) {
     return ((kPolyMask >> (i & 7)) & 1u) ? ex2_poly(x) : ex2(x);
 }
@@ -523,7 +530,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int nv0 = (int(e0 & 0x3FFFu) == a.N - 1) ? n_last : 64;
             const int nv1 = (int(e1 & 0x3FFFu) == a.N - 1) ? n_last : 64;
             const uint32_t sc = lbase + kColS + sb * 128;
-            mbar_wait<true>(&bar.s_full[sb], phs);
+            mbar_wait<kSoftmaxSpin>(&bar.s_full[sb], phs);
             tc_fence_after();
             if (q4 == 0) TRACE(4 + hh, g);
             if (use0 || use1) {
@@ -583,7 +590,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             };
             const uint32_t cm0 = colmask(c0), cm1 = colmask(c0 + 1);
             const int nv0 = min(64, a.N - c0 * 64), nv1 = min(64, a.N - (c0 + 1) * 64);
-            mbar_wait<true>(&bar.s_full[sb], phs);
+            mbar_wait<kSoftmaxSpin>(&bar.s_full[sb], phs);
             tc_fence_after();
             uint32_t r0[32], r1[32];
             tmem_ld16x2_32<32>(sc, r0);
