@@ -92,6 +92,17 @@ constexpr uint32_t kPolyMask = PISA_POLY_MASK;
 #define PISA_SOFTMAX_SPIN 1
 #endif
 constexpr bool kSoftmaxSpin = PISA_SOFTMAX_SPIN != 0;
+// Phase-1 block order. 0: the ascending union (default). 1: balanced (A&B
+// pairs, then (A-only, B-only) pairs: equal softmax work per warpgroup in every
+// super-tile). 2: grouped (A&B pairs, then alternating (A, A) / (B, B) pairs:
+// each warpgroup active in the fewest super-tiles). Measured on one B200
+// (Wan2.1-14B, gaussian / clustered): ascending 24.7-25.1 / 19.2-19.3 ms,
+// balanced 26.5 / 19.7 ms, grouped 25.4 / 20.0 ms -- the per-super-tile fixed
+// softmax cost penalises balancing, and scrambling the order costs the L2
+// reuse between neighbouring CTAs walking similar selections in step.
+#ifndef PISA_BALANCED
+#define PISA_BALANCED 0
+#endif
 __device__ __forceinline__ float ex2_mix(float x, int i) {
     return ((kPolyMask >> (i & 7)) & 1u) ? ex2_poly(x) : ex2(x);
 }
@@ -115,7 +126,7 @@ struct Bars {
     uint64_t k_full[kSK], v_full[kSV], v_empty[kSV];
     uint64_t s_full[kSB], p_full[kSB];
     uint32_t tmem_base;
-    uint32_t n_union;
+    uint32_t n_ab, n_a, n_b;
 };
 static_assert(sizeof(Bars) <= 512, "barrier block");
 
@@ -217,57 +228,141 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     if (warp == 3) {
         // selection bitmasks of the two query blocks into shared memory, and the
-        // size U of their union (every consumer walks the union itself, in
-        // ascending order, with a UnionCursor)
+        // sizes of the three parts of their union (A&B, A only, B only; every
+        // consumer walks them itself with a UnionCursor)
         const uint32_t* mA = a.mask + (size_t(bh) * a.N + iA) * a.W;
         const uint32_t* mB = a.mask + (size_t(bh) * a.N + iB) * a.W;
-        uint32_t cnt = 0;
+        uint32_t nab = 0, na = 0, nb = 0;
         for (int w = lane; w < a.W; w += 32) {
             const uint32_t wa = mA[w];
             const uint32_t wb = hasB ? mB[w] : 0u;
             maskA[w] = wa;
             maskB[w] = wb;
-            cnt += __popc(wa | wb);
+            nab += __popc(wa & wb);
+            na += __popc(wa & ~wb);
+            nb += __popc(wb & ~wa);
         }
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
-        if (lane == 0) bar.n_union = cnt;
+        for (int o = 16; o > 0; o >>= 1) {
+            nab += __shfl_xor_sync(0xffffffffu, nab, o);
+            na += __shfl_xor_sync(0xffffffffu, na, o);
+            nb += __shfl_xor_sync(0xffffffffu, nb, o);
+        }
+        if (lane == 0) {
+            bar.n_ab = nab;
+            bar.n_a = na;
+            bar.n_b = nb;
+        }
     }
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = bar.tmem_base;
-    const int U = int(bar.n_union);
+    const int nAB = int(bar.n_ab), nAo = int(bar.n_a), nBo = int(bar.n_b);
     // Key tiles are processed in pairs ("super-tiles" of 128 keys): one K / V
     // stage, one S buffer, one barrier round trip and N=128 S MMAs per pair.
-    // Phase 1 pairs consecutive union entries, Phase 2 consecutive centroid
-    // chunks; an odd tail is padded with a copy of the previous entry whose use
-    // flags are zero (fully masked: P = 0 and finite V rows).
-    const int G1 = (U + 1) >> 1;
+    // Phase 1 walks the union of the two selections in the order PISA_BALANCED
+    // picks (the online softmax is order-independent up to rounding; default:
+    // ascending). The balanced / grouped orders use the split A&B, A-only,
+    // B-only (|A-only| == |B-only| since both select k). An odd tail is padded
+    // with a copy of the previous entry whose use flags are zero (fully
+    // masked: P = 0 and finite V rows).
+    // Phase 2 pairs consecutive centroid chunks.
+    const int gAB = (nAB + 1) >> 1;
+    const int nX = min(nAo, nBo);
+    const int nR = max(nAo, nBo) - nX;
+#if PISA_BALANCED == 2
+    const int gA = (nAo + 1) >> 1, gB = (nBo + 1) >> 1;
+    const int G1 = gAB + gA + gB;
+#elif PISA_BALANCED
+    const int G1 = gAB + nX + ((nR + 1) >> 1);
+#else
+    const int nU = nAB + nAo + nBo;
+    const int G1 = (nU + 1) >> 1;
+#endif
     const int G = G1 + (tail ? (a.nchunk2 + 1) >> 1 : 0);
-    // The ascending union of the two selections, walked by each consumer in
-    // order: entry = block index | (selected by 2t) << 14 | (by 2t+1) << 15.
-    struct UnionCursor {
+    // entry = block index | (selected by query block A) << 14 | (by B) << 15
+    struct BitStream {
         const uint32_t* ma;
         const uint32_t* mb;
-        int w = -1;
-        uint32_t bits = 0;
+        int kind;  // 0: A&B, 1: A only, 2: B only, 3: A|B (with use flags)
+        int w;
+        uint32_t bits;
         __device__ __forceinline__ uint32_t next() {
             while (bits == 0) {
                 ++w;
-                bits = ma[w] | mb[w];
+                const uint32_t x = ma[w], y = mb[w];
+                bits = kind == 0 ? (x & y) : kind == 1 ? (x & ~y) : kind == 2 ? (y & ~x) : (x | y);
             }
             const int b = __ffs(bits) - 1;
             bits &= bits - 1;
-            return uint32_t(w * 32 + b) | (((ma[w] >> b) & 1u) << 14) | (((mb[w] >> b) & 1u) << 15);
+            const uint32_t f = kind == 3 ? ((((ma[w] >> b) & 1u) << 14) | (((mb[w] >> b) & 1u) << 15)) : 0u;
+            return uint32_t(w * 32 + b) | f;
         }
     };
-    // key rows of the two sub-tiles of super-tile g: union entries (the odd
-    // tail repeats the previous entry, fully masked), then centroid chunks
+    struct UnionCursor {
+        BitStream ab, ao, bo;
+        __device__ __forceinline__ UnionCursor(const uint32_t* ma, const uint32_t* mb)
+            : ab{ma, mb, PISA_BALANCED ? 0 : 3, -1, 0u}, ao{ma, mb, 1, -1, 0u}, bo{ma, mb, 2, -1, 0u} {}
+        // the two entries of super-tile g (called for g = 0, 1, ... in order)
+        __device__ __forceinline__ void pair(int g, int gAB, int nAB, int nX, int nR, bool restA, uint32_t& e0,
+                                             uint32_t& e1) {
+#if !PISA_BALANCED
+            // ascending union order (kept as a build variant for A/B timing)
+            if (true) {
+                BitStream& u = ab;  // constructed with kind 3 in this build
+                e0 = u.next();
+                e1 = (2 * g + 1 < nAB) ? u.next() : (e0 & 0x3FFFu);
+                return;
+            }
+#endif
+#if PISA_BALANCED == 2
+            // grouped: (A&B, A&B), then alternating (A, A) / (B, B) pairs so
+            // each warpgroup has a used sub-tile in as few super-tiles as
+            // possible (the other skips ahead on zero P)
+            if (g >= gAB) {
+                const int j = g - gAB;
+                const int gA = (nX + 1) >> 1, gB = (nR + 1) >> 1;  // here nX = |A only|, nR = |B only|
+                const int m2 = 2 * min(gA, gB);
+                const bool useA = j < m2 ? !(j & 1) : gA > gB;
+                const int i = j < m2 ? (j >> 1) : (min(gA, gB) + j - m2);
+                BitStream& r = useA ? ao : bo;
+                const uint32_t f = useA ? (1u << 14) : (2u << 14);
+                e0 = r.next() | f;
+                e1 = (2 * i + 1 < (useA ? nX : nR)) ? (r.next() | f) : (e0 & 0x3FFFu);
+                return;
+            }
+#endif
+            if (g < gAB) {
+                e0 = ab.next() | (3u << 14);
+                e1 = (2 * g + 1 < nAB) ? (ab.next() | (3u << 14)) : (e0 & 0x3FFFu);
+            } else if (g < gAB + nX) {
+                e0 = ao.next() | (1u << 14);
+                e1 = bo.next() | (2u << 14);
+            } else {
+                const int j = g - gAB - nX;
+                BitStream& r = restA ? ao : bo;
+                const uint32_t f = restA ? (1u << 14) : (2u << 14);
+                e0 = r.next() | f;
+                e1 = (2 * j + 1 < nR) ? (r.next() | f) : (e0 & 0x3FFFu);
+            }
+        }
+    };
+    const bool restA = nAo > nBo;
+#if PISA_BALANCED == 2
+    const int kPairX = nAo, kPairR = nBo;
+#else
+    const int kPairX = nX, kPairR = nR;
+#endif
+#if !PISA_BALANCED
+    const int nPair = nU;  // the union cursor's count (pair() reads it as nAB)
+#else
+    const int nPair = nAB;
+#endif
     auto tile_rows = [&](UnionCursor& cur, int g, int& r0, int& r1) {
         if (g < G1) {
-            const uint32_t e0 = cur.next();
-            const uint32_t e1 = (2 * g + 1 < U) ? cur.next() : e0;
+            uint32_t e0, e1;
+            cur.pair(g, gAB, nPair, kPairX, kPairR, restA, e0, e1);
             r0 = int(e0 & 0x3FFFu) * 64;
             r1 = int(e1 & 0x3FFFu) * 64;
         } else {
@@ -298,7 +393,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (j >= 0) mbar_wait(&bar.s_full[j % kSB], uint32_t((j / kSB) & 1));
         };
         int s = 0;
-        UnionCursor cur{maskA, maskB};
+        UnionCursor cur(maskA, maskB);
         for (int g = 0; g < G; ++g) {
             uint8_t* sK = smem + Cfg::kOffK + s * Cfg::kKV;
             wait_s_done(g - kSK);
@@ -338,7 +433,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int vh = warp - 2;
         int s = 0;
         uint32_t ph = 0;
-        UnionCursor cur{maskA, maskB};
+        UnionCursor cur(maskA, maskB);
         for (int g = 0; g < G; ++g) {
             uint8_t* sV = smem + Cfg::kOffV + s * Cfg::kKV + vh * 16384;
             mbar_wait(&bar.v_empty[s], ph ^ 1);
@@ -522,10 +617,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t kZero16[16] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
 
         // ---- Phase 1: exact blocks of the union, two per super-tile
-        UnionCursor cur{maskA, maskB};
+        UnionCursor cur(maskA, maskB);
         for (int g = 0; g < G1; ++g) {
-            const uint32_t e0 = cur.next();
-            const uint32_t e1 = (2 * g + 1 < U) ? cur.next() : 0u;  // pad: unused
+            uint32_t e0, e1;
+            cur.pair(g, gAB, nPair, kPairX, kPairR, restA, e0, e1);  // pad: use flags 0
             const bool use0 = (e0 >> (14 + hh)) & 1u, use1 = (e1 >> (14 + hh)) & 1u;  // warp-uniform
             const int nv0 = (int(e0 & 0x3FFFu) == a.N - 1) ? n_last : 64;
             const int nv1 = (int(e1 & 0x3FFFu) == a.N - 1) ? n_last : 64;
