@@ -2,29 +2,76 @@
 // covariance-aware router's rectifier (compute_global_stats with compute_norms,
 // block_stats.hpp:207-241; select_topk_covariance, router.hpp:157-193).
 //
-// One CTA (256 threads) per (key block j, batch*head):
-//   1. centred keys kc = K_j - k_bar_j and V_j into shared memory (fp32; the
-//      ragged last block has n < 64 rows, the rest are zero),
-//   2. H_j = kc^T V_j (each thread an 8 x 8 tile, fp32, fixed order over rows),
-//      D = H_j - H_bar (H_bar from K1b),
-//   3. sigma_max(D)^2 = lambda_max(D^T D) by kLanczos steps of Lanczos on D^T D
-//      from the normalised all-ones start (the reference's power-iteration
-//      start, block_stats.hpp:98);
-//      the extreme Ritz value of the kLanczos-step tridiagonal is found by a
-//      warp-parallel multisection on its Sturm sequence.
-// The reference uses the exact Jacobi eigen-solve in fp64 (block_stats.hpp:42-94);
-// the extreme eigenvalue of D^T D is well separated after a few dozen Lanczos
-// steps, so M_j agrees to fp32 rounding (~1e-6 relative, measured in the tests).
+// sigma_max(D)^2 = lambda_max(D^T D), D = H_j - H_bar, by kLanczos steps of
+// Lanczos from the normalised all-ones start (the reference's power-iteration
+// start, block_stats.hpp:98); the extreme Ritz value of the tridiagonal is found
+// by a warp-parallel multisection on its Sturm sequence. The reference uses the
+// exact Jacobi eigen-solve in fp64 (block_stats.hpp:42-94); the extreme
+// eigenvalue of D^T D is well separated after a few dozen Lanczos steps, so M_j
+// agrees to fp32 rounding (~1e-6 relative, measured in the tests).
 // Outputs m[bh][j] (fp32) and rect[bh][j] = log(M_j + eps) (computed in fp64).
+//
+// Two kernels:
+//   * block_norms_tc_kernel (D = 128, the hot configuration): H_j and
+//     G = D^T D on the tensor cores, Lanczos on G from registers;
+//   * block_norms_kernel<64>: CUDA-core H_j and Lanczos on D^T D as two
+//     matvecs per step (D = 64 is 8x less work per block).
 #include "kernels.h"
 #include "sm100.cuh"
 
 namespace pisa_b200 {
+using namespace pisa_sm100;
+
 namespace {
 
 constexpr int kNormThreads = 256;
 constexpr int kLanczos = 24;  // fp32-converged (<5e-8 rel.) on gaussian / clustered blocks
 
+// Largest eigenvalue of the m x m Lanczos tridiagonal (alpha = ab[0..m),
+// beta = ab[kLanczos..]) by a 32-way multisection on its Sturm count (the
+// number of eigenvalues below x, from the LDL^T pivots); each round shrinks the
+// bracket 33x (fp32 is the precision M_j is delivered in). One warp; lane 0
+// stores M_j = sqrt(lambda_max) and the rectifier log(M_j + eps) (fp64).
+__device__ __forceinline__ void ritz_max_and_store(const float* ab, int m, int lane, const NormArgs& a, size_t o) {
+    float hi = 0.f;
+    for (int i = 0; i < m; ++i) {
+        const float r = fabsf(ab[i]) + (i > 0 ? fabsf(ab[kLanczos + i - 1]) : 0.f) +
+                        (i + 1 < m ? fabsf(ab[kLanczos + i]) : 0.f);
+        hi = fmaxf(hi, r);  // Gershgorin bound
+    }
+    float lo = 0.f;  // D^T D is positive semi-definite
+    for (int round = 0; round < 7 && hi > lo; ++round) {
+        const float x = lo + (hi - lo) * float(lane + 1) * (1.0f / 33.0f);
+        int c = 0;
+        float q = 1.f;
+        for (int i = 0; i < m; ++i) {
+            const float bb = i > 0 ? ab[kLanczos + i - 1] : 0.f;
+            q = (ab[i] - x) - (i > 0 ? bb * bb / q : 0.f);
+            if (q == 0.f) q = -1e-30f;
+            c += q < 0.f;
+        }
+        const unsigned all_below = __ballot_sync(0xffffffffu, c >= m);  // lambda_max < x
+        const int f = all_below ? __ffs(all_below) - 1 : 32;
+        const float xf = __shfl_sync(0xffffffffu, x, f < 32 ? f : 31);
+        const float xp = __shfl_sync(0xffffffffu, x, f > 0 ? f - 1 : 0);
+        const float nlo = f > 0 ? xp : lo, nhi = f < 32 ? xf : hi;
+        lo = nlo;
+        hi = nhi;
+    }
+    if (lane == 0) {
+        const double sigma = sqrt(fmax(0.0, double(0.5f * (lo + hi))));
+        a.m[o] = float(sigma);
+        if (a.rect) a.rect[o] = float(log(sigma + a.eps));
+    }
+}
+
+// ---------------------------------------------------------------------------
+// D = 64: one CTA (256 threads) per (key block j, batch*head):
+//   1. centred keys kc = K_j - k_bar_j and V_j into shared memory (fp32; the
+//      ragged last block has n < 64 rows, the rest are zero),
+//   2. H_j = kc^T V_j (each thread an 8 x 8 tile, fp32, fixed order over rows),
+//      D = H_j - H_bar (H_bar from K1b),
+//   3. Lanczos on D^T D, two matvecs per step, two threads per row / column.
 template <int D>
 __global__ void __launch_bounds__(kNormThreads) block_norms_kernel(const __nv_bfloat16* __restrict__ k,
                                                                    const __nv_bfloat16* __restrict__ v,
@@ -192,47 +239,272 @@ __global__ void __launch_bounds__(kNormThreads) block_norms_kernel(const __nv_bf
         __syncthreads();
     }
     __syncthreads();
+    if (warp == 0) ritz_max_and_store(ab, m, lane, a, size_t(bh) * a.N + j);
+}
+
+// ---------------------------------------------------------------------------
+// D = 128 (the hot configuration): everything GEMM-shaped on the tensor cores.
+// One CTA (4 warps) per (key block j, batch*head), three CTAs per SM:
+//   1. TMA: K_j and V_j (bf16, 128B-swizzled 64-row tiles, rows >= L zero-filled),
+//   2. centring kc = K_j - k_bar_j in fp32 and an exact-to-fp32 split
+//      kc = hi + mid + lo into three bf16 tiles (in place of K and behind it),
+//   3. tcgen05: TMEM[a][c] = sum_rows (lo + mid + hi)[r][a] V[r][c] (12 MMAs,
+//      M = N = 128, both operands MN-major; bf16 products are exact, fp32
+//      accumulation) -- H_j to fp32 accuracy without the cancellation of the
+//      uncentred identity,
+//   4. thread a reads row a of H_j and subtracts H_bar: row a of D,
+//   5. G = D^T D on the tensor cores from the same kind of split of D
+//      (hi/mid/lo, the six products above 2^-26 relative), written to shared
+//      memory 64 rows at a time (two passes, 24 MMAs each; the buffer of the
+//      K split is reused and G overwrites H_j in TMEM),
+//   6. thread a holds row a of G in registers; Lanczos on G needs one matvec
+//      per step against the broadcast Lanczos vector (packed FFMA2).
+// Measured (Wan2.1-14B shape, 40 heads): 5.35 ms, from 13.6 ms for the CUDA-core
+// H_j + two-matvec Lanczos. The bound is now the latency of the 24 dependent
+// Lanczos steps (two block reductions each) with only three blocks resident per
+// SM (each block's G is 64 KB of registers); a register-blocked G (4 rows x 32
+// columns per thread, 4x less vector traffic) measured the same.
+constexpr int kTcThreads = 128;
+struct TcCfg {
+    static constexpr int kTile = 64 * 128 * 2;            // one 64-row bf16 tile (two 64-column SW128 halves)
+    static constexpr int kOffV = 3 * kTile;               // hi | mid | lo | V
+    static constexpr int kOffVec = 4 * kTile;             // Lanczos vector [128]
+    static constexpr int kOffKb = kOffVec + 128 * 4;      // k_bar_j [128]
+    static constexpr int kOffRed = kOffKb + 128 * 4;      // [2][4] reduction scratch, alpha / beta
+    static constexpr int kOffBar = (kOffRed + (8 + 2 * kLanczos) * 4 + 7) & ~7;
+    static constexpr int kSmem = 1024 + kOffBar + 48;
+};
+
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
+    uint64_t r;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;"
+        : "=l"(r)
+        : "l"(*reinterpret_cast<uint64_t*>(&a)), "l"(*reinterpret_cast<uint64_t*>(&b)),
+          "l"(*reinterpret_cast<uint64_t*>(&c)));
+    return *reinterpret_cast<float2*>(&r);
+}
+
+// x = hi + mid + lo, each a bf16 pair (exact to 2^-27 relative)
+__device__ __forceinline__ void split3(float x0, float x1, uint32_t& h, uint32_t& m, uint32_t& l) {
+    const __nv_bfloat162 h2 = __floats2bfloat162_rn(x0, x1);
+    const float2 hf = __bfloat1622float2(h2);
+    const float y0 = x0 - hf.x, y1 = x1 - hf.y;  // exact
+    const __nv_bfloat162 m2 = __floats2bfloat162_rn(y0, y1);
+    const float2 mf = __bfloat1622float2(m2);
+    const __nv_bfloat162 l2 = __floats2bfloat162_rn(y0 - mf.x, y1 - mf.y);
+    h = *reinterpret_cast<const uint32_t*>(&h2);
+    m = *reinterpret_cast<const uint32_t*>(&m2);
+    l = *reinterpret_cast<const uint32_t*>(&l2);
+}
+
+// TMEM row (lane) of the issuing warp's quadrant, 128 fp32 columns
+__device__ __forceinline__ void tmem_row128(uint32_t taddr, float (&x)[128]) {
+#pragma unroll
+    for (int cc = 0; cc < 4; ++cc) {
+        uint32_t r[32];
+        tmem_ld32(taddr + cc * 32, r);
+        tmem_ld_wait(r);
+#pragma unroll
+        for (int i = 0; i < 32; ++i) x[cc * 32 + i] = __uint_as_float(r[i]);
+    }
+}
+
+__global__ void __launch_bounds__(kTcThreads, 3)
+    block_norms_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
+                          NormArgs a) {
+    using Cfg = TcCfg;
+    constexpr int D = 128;
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+    float* vs = reinterpret_cast<float*>(smem + Cfg::kOffVec);
+    float* kb = reinterpret_cast<float*>(smem + Cfg::kOffKb);
+    float* red = reinterpret_cast<float*>(smem + Cfg::kOffRed);
+    float* ab = red + 8;
+    // [0] tiles landed, [1] H_j MMAs done, [2] / [3] G passes done
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + Cfg::kOffBar);
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 4);
+    const int j = blockIdx.x, bh = blockIdx.y;
+    const int b = bh / a.H, h = bh % a.H;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int n = min(64, a.L - j * 64);
+
+    if (tid == 0) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) mbar_init(&bar[i], 1);
+        fence_mbar_init();
+    }
     if (warp == 0) {
-        // largest eigenvalue of the m x m tridiagonal (alpha, beta): 32-way
-        // multisection on the Sturm count (number of eigenvalues below x from
-        // the LDL^T pivots), each round shrinks the bracket 33x (fp32 is the
-        // precision M_j is delivered in)
-        float hi = 0.f;
-        for (int i = 0; i < m; ++i) {
-            const float r = fabsf(ab[i]) + (i > 0 ? fabsf(ab[kLanczos + i - 1]) : 0.f) +
-                            (i + 1 < m ? fabsf(ab[kLanczos + i]) : 0.f);
-            hi = fmaxf(hi, r);  // Gershgorin bound
-        }
-        float lo = 0.f;  // D^T D is positive semi-definite
-        for (int round = 0; round < 7 && hi > lo; ++round) {
-            const float x = lo + (hi - lo) * float(lane + 1) * (1.0f / 33.0f);
-            int c = 0;
-            float q = 1.f;
-            for (int i = 0; i < m; ++i) {
-                const float bb = i > 0 ? ab[kLanczos + i - 1] : 0.f;
-                q = (ab[i] - x) - (i > 0 ? bb * bb / q : 0.f);
-                if (q == 0.f) q = -1e-30f;
-                c += q < 0.f;
+        tmem_alloc(tslot, 128);
+        tmem_relinquish();
+    }
+    kb[tid] = a.kbar[(size_t(bh) * a.N + j) * D + tid];
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tslot;
+    const uint32_t trow = tmem + (uint32_t(warp * 32) << 16);  // this thread's TMEM lane = tid
+    if (warp == 0) {
+        if (elect_one()) {
+            mbar_expect_tx(&bar[0], 2 * Cfg::kTile);
+#pragma unroll
+            for (int half = 0; half < 2; ++half) {
+                tma_load_4d(smem + half * 8192, &tmK, &bar[0], half * 64, j * 64, h, b);
+                tma_load_4d(smem + Cfg::kOffV + half * 8192, &tmV, &bar[0], half * 64, j * 64, h, b);
             }
-            const unsigned all_below = __ballot_sync(0xffffffffu, c >= m);  // lambda_max < x
-            const int f = all_below ? __ffs(all_below) - 1 : 32;
-            const float xf = __shfl_sync(0xffffffffu, x, f < 32 ? f : 31);
-            const float xp = __shfl_sync(0xffffffffu, x, f > 0 ? f - 1 : 0);
-            const float nlo = f > 0 ? xp : lo, nhi = f < 32 ? xf : hi;
-            lo = nlo;
-            hi = nhi;
         }
-        if (lane == 0) {
-            const double sigma = sqrt(fmax(0.0, double(0.5f * (lo + hi))));
-            a.m[size_t(bh) * a.N + j] = float(sigma);
-            if (a.rect) a.rect[size_t(bh) * a.N + j] = float(log(sigma + a.eps));
+        __syncwarp();
+    }
+    mbar_wait(&bar[0], 0);
+
+    // ---- 2. centre and split, one 16-byte chunk (8 keys of one row) at a time
+#pragma unroll 2
+    for (int i = 0; i < 8; ++i) {
+        const int ci = tid + kTcThreads * i;
+        const int r = (ci >> 3) & 63;
+        const int d0 = (ci >> 9) * 64 + (((ci & 7) ^ (r & 7)) << 3);  // undo the 128B swizzle
+        uint4 w = *reinterpret_cast<const uint4*>(smem + ci * 16);
+        const __nv_bfloat162* k2 = reinterpret_cast<const __nv_bfloat162*>(&w);
+        uint4 hw, mw, lw;
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+            const float2 kf = __bfloat1622float2(k2[t]);
+            const float x0 = r < n ? kf.x - kb[d0 + 2 * t] : 0.f;
+            const float x1 = r < n ? kf.y - kb[d0 + 2 * t + 1] : 0.f;
+            split3(x0, x1, (&hw.x)[t], (&mw.x)[t], (&lw.x)[t]);
+        }
+        *reinterpret_cast<uint4*>(smem + ci * 16) = hw;
+        *reinterpret_cast<uint4*>(smem + Cfg::kTile + ci * 16) = mw;
+        *reinterpret_cast<uint4*>(smem + 2 * Cfg::kTile + ci * 16) = lw;
+    }
+    fence_proxy_async();  // generic-proxy tile writes -> tcgen05 operand reads
+    __syncthreads();
+
+    constexpr uint32_t idesc = idesc_bf16(128, 128, 1, 1);
+    const uint32_t base = smem_u32(smem);
+    auto desc = [&](int tile, int ks) { return sdesc_sw128(base + tile * Cfg::kTile + ks * 2048, 8192, 1024); };
+    // ---- 3. H_j = kc^T V: small parts first
+    if (warp == 0) {
+        tc_fence_after();
+        if (elect_one()) {
+#pragma unroll
+            for (int part = 2; part >= 0; --part)
+#pragma unroll
+                for (int ks = 0; ks < 4; ++ks) mma_ss(tmem, desc(part, ks), desc(3, ks), idesc, part != 2 || ks != 0);
+            mma_commit(&bar[1]);
+        }
+        __syncwarp();
+    }
+    mbar_wait(&bar[1], 0);
+    tc_fence_after();
+
+    // ---- 4. row a = tid of D = H_j - H_bar
+    float x[D];
+    tmem_row128(trow, x);
+    {
+        const float4* hb = reinterpret_cast<const float4*>(a.hbar + (size_t(bh) * D + tid) * D);
+#pragma unroll
+        for (int i = 0; i < D / 4; ++i) {
+            const float4 hv = __ldg(hb + i);
+            x[4 * i] -= hv.x;
+            x[4 * i + 1] -= hv.y;
+            x[4 * i + 2] -= hv.z;
+            x[4 * i + 3] -= hv.w;
         }
     }
+    // ---- 5. G = D^T D, rows of D 64 at a time through the split tiles
+#pragma unroll
+    for (int pass = 0; pass < 2; ++pass) {
+        if ((tid >> 6) == pass) {
+            const int r = tid & 63;
+#pragma unroll
+            for (int c8 = 0; c8 < D / 8; ++c8) {  // 16-byte chunk of row r, swizzled
+                const uint32_t off = uint32_t((c8 >> 3) * 8192 + r * 128 + (((c8 & 7) ^ (r & 7)) << 4));
+                uint4 hw, mw, lw;
+#pragma unroll
+                for (int t = 0; t < 4; ++t)
+                    split3(x[c8 * 8 + 2 * t], x[c8 * 8 + 2 * t + 1], (&hw.x)[t], (&mw.x)[t], (&lw.x)[t]);
+                *reinterpret_cast<uint4*>(smem + off) = hw;
+                *reinterpret_cast<uint4*>(smem + Cfg::kTile + off) = mw;
+                *reinterpret_cast<uint4*>(smem + 2 * Cfg::kTile + off) = lw;
+            }
+        }
+        fence_proxy_async();
+        tc_fence_before();  // pass 0: every H_j row is read out of TMEM before G overwrites it
+        __syncthreads();
+        if (warp == 0) {
+            tc_fence_after();
+            if (elect_one()) {
+                // (lo,hi) (hi,lo) (mid,mid) (mid,hi) (hi,mid) (hi,hi); tiles 0 = hi, 1 = mid, 2 = lo
+                constexpr int kA[6] = {2, 0, 1, 1, 0, 0}, kB[6] = {0, 2, 1, 0, 1, 0};
+#pragma unroll
+                for (int p = 0; p < 6; ++p)
+#pragma unroll
+                    for (int ks = 0; ks < 4; ++ks)
+                        mma_ss(tmem, desc(kA[p], ks), desc(kB[p], ks), idesc, pass != 0 || p != 0 || ks != 0);
+                mma_commit(&bar[2 + pass]);
+            }
+            __syncwarp();
+        }
+        mbar_wait(&bar[2 + pass], 0);  // the tiles are rewritten by the next pass
+        tc_fence_after();
+    }
+    // ---- 6. row a of G into registers; Lanczos on G
+    tmem_row128(trow, x);
+    float vcur = rsqrtf(float(D)), vprev = 0.f, beta_prev = 0.f;
+    vs[tid] = vcur;
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) tmem_dealloc(tmem, 128);
+
+    int par = 0;
+    auto block_sum = [&](float v) -> float {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (lane == 0) red[par * 4 + warp] = v;
+        __syncthreads();
+        const float s = (red[par * 4] + red[par * 4 + 1]) + (red[par * 4 + 2] + red[par * 4 + 3]);
+        par ^= 1;
+        return s;
+    };
+    int m = 0;
+    for (; m < kLanczos; ++m) {
+        // y_a = G[a] . v (v broadcast from shared memory)
+        float2 y0 = make_float2(0.f, 0.f), y1 = y0, y2 = y0, y3 = y0;
+#pragma unroll
+        for (int c = 0; c < D; c += 8) {
+            const float4 v4 = *reinterpret_cast<const float4*>(vs + c);
+            const float4 w4 = *reinterpret_cast<const float4*>(vs + c + 4);
+            y0 = ffma2(make_float2(x[c], x[c + 1]), make_float2(v4.x, v4.y), y0);
+            y1 = ffma2(make_float2(x[c + 2], x[c + 3]), make_float2(v4.z, v4.w), y1);
+            y2 = ffma2(make_float2(x[c + 4], x[c + 5]), make_float2(w4.x, w4.y), y2);
+            y3 = ffma2(make_float2(x[c + 6], x[c + 7]), make_float2(w4.z, w4.w), y3);
+        }
+        float y = ((y0.x + y0.y) + (y1.x + y1.y)) + ((y2.x + y2.y) + (y3.x + y3.y));
+        const float alpha = block_sum(vcur * y);
+        y -= alpha * vcur + beta_prev * vprev;
+        const float beta = sqrtf(block_sum(y * y));
+        if (tid == 0) {
+            ab[m] = alpha;
+            ab[kLanczos + m] = beta;
+        }
+        if (!(beta > 1e-30f * fmaxf(1.f, fabsf(alpha)))) {  // invariant subspace (or D == 0)
+            ++m;
+            break;
+        }
+        vprev = vcur;
+        vcur = y / beta;
+        vs[tid] = vcur;  // every read of v for this step preceded the first barrier above
+        beta_prev = beta;
+        __syncthreads();
+    }
+    __syncthreads();
+    if (warp == 0) ritz_max_and_store(ab, m, lane, a, size_t(bh) * a.N + j);
 }
 
 }  // namespace
 
 size_t block_norms_smem_bytes(int D) {
+    if (D == 128) return TcCfg::kSmem;
     // phase 1 (centred K and V, 2 x 64 x D floats) and phases 2-3 (D, Lanczos
     // basis, scratch) share the buffer
     const size_t p1 = size_t(2) * 64 * D * 4;
@@ -240,14 +512,13 @@ size_t block_norms_smem_bytes(int D) {
     return p1 > p3 ? p1 : p3;
 }
 
-cudaError_t launch_block_norms(int D, const __nv_bfloat16* k, const __nv_bfloat16* v, const NormArgs& a,
-                               int BH, cudaStream_t s) {
+cudaError_t launch_block_norms(int D, const CUtensorMap& tmK, const CUtensorMap& tmV, const __nv_bfloat16* k,
+                               const __nv_bfloat16* v, const NormArgs& a, int BH, cudaStream_t s) {
     const size_t smem = block_norms_smem_bytes(D);
     dim3 grid(a.N, BH);
     if (D == 128) {
-        auto kern = block_norms_kernel<128>;
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-        kern<<<grid, kNormThreads, smem, s>>>(k, v, a);
+        cudaFuncSetAttribute(block_norms_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        block_norms_tc_kernel<<<grid, kTcThreads, smem, s>>>(tmK, tmV, a);
     } else {
         auto kern = block_norms_kernel<64>;
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));

@@ -318,8 +318,11 @@ pisa_status run_norms(pisa_ctx* ctx, const pisa_attn_desc& d, const Plan& p, con
     NormArgs a{w.kbar,      w.hbar,        w.norms,       w.rect,        d.epsilon,
                int(p.L),    int(p.N),      int(d.heads),  d.k_strides[0], d.k_strides[1],
                d.k_strides[2], d.v_strides[0], d.v_strides[1], d.v_strides[2]};
+    CUtensorMap tk, tv;
+    if (!make_qkv_map(&tk, k, d, d.k_strides, 64) || !make_qkv_map(&tv, v, d, d.v_strides, 64))
+        return fail(ctx, PISA_ERR_INVALID_DIMENSION, "TMA descriptor rejected the k/v layout");
     ProfScope ps(ctx, kK1c, s);
-    const cudaError_t e = launch_block_norms(int(p.D), static_cast<const __nv_bfloat16*>(k),
+    const cudaError_t e = launch_block_norms(int(p.D), tk, tv, static_cast<const __nv_bfloat16*>(k),
                                              static_cast<const __nv_bfloat16*>(v), a, int(p.BH), s);
     if (e != cudaSuccess) return cuda_fail(ctx, e, "block_norms launch");
     ctx->launches += 1;

@@ -132,6 +132,22 @@ def test_block_norms_match_oracle(P, oracle_mod, kind, H, L, d):
         assert rel.max() <= 2e-5, f"head {h}: max rel err {rel.max():.3e}"
 
 
+@pytest.mark.parametrize("d", [64, 128])
+def test_block_norms_keys_with_large_mean(P, oracle_mod, d):
+    """Keys with a large common offset (|mean| >> spread, as real key
+    projections often have): the deviation norms are computed from centred keys,
+    so no precision is lost to cancellation."""
+    import torch
+    O = oracle_mod
+    q, k, v = O.gen("gaussian", 4, 1, 2048, d)
+    off = np.linspace(-12.0, 12.0, d)[None, None, :]
+    k = torch.from_numpy(k + off).to(torch.bfloat16).float().numpy()  # bf16-exact inputs
+    m = P.block_norms(dev_bf16(q, False), dev_bf16(k, False), dev_bf16(v, False)).cpu().numpy()
+    ref = O.block_norms(k[0].astype(np.float64), v[0])
+    rel = np.abs(m[0] - ref) / np.maximum(ref, 1e-30)
+    assert rel.max() <= 2e-5, f"max rel err {rel.max():.3e}"
+
+
 def _cov_swaps(O, qb64, kb64, m64, sel_gpu, k, scale, fd):
     ref, sc = O.select_cov(qb64, kb64, m64, k, scale, 1e-6, fd, return_scores=True)
     bad = np.where((sel_gpu != ref).any(1))[0]
