@@ -187,6 +187,8 @@ def main():
     ap.add_argument("--workload", default="wan14b", choices=list(WORKLOADS))
     ap.add_argument("--data", default="gaussian", choices=["gaussian", "clustered"])
     ap.add_argument("--density", type=float, default=None)
+    ap.add_argument("--router", default="plain", choices=["plain", "covariance"],
+                    help="routing strategy (the headline is plain; covariance adds K1c)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-dense", action="store_true")
@@ -255,6 +257,8 @@ def main():
     out = torch.empty(shape, device=dev, dtype=torch.bfloat16)
     ctx = P.Context.get(local_rank)
     kw = dict(sparsity=1.0 - density, variant=P.PisaVariant.Hybrid)
+    if args.router == "covariance":
+        kw["router"] = P.RouterStrategy.CovarianceAware
 
     # warmup (+ the plan, for executed-FLOP accounting)
     _, ex = P.fwd(q, kk, v, out, return_plan=True, **kw)
@@ -375,7 +379,7 @@ def main():
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
             "data": f"synthetic {args.data} (torch RNG on device), bf16",
             "config": {"workload": cfg_name, "B": B, "H": H, "L": L, "d": d, "N": N, "k": k,
-                       "density": density, "block": 64, "variant": "hybrid", "router": "plain",
+                       "density": density, "block": 64, "variant": "hybrid", "router": args.router,
                        "parallelism": f"head-sharded x{world}", "heads_per_gpu": Hr,
                        "l2": "inputs 2.3 GB > 126 MB L2, no flush"},
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",

@@ -43,6 +43,7 @@ struct pisa_ctx {
     unsigned long long* trace = nullptr;  // debug timeline (PISA_TRACE builds)
     int trace_tile = 0;
     bool pairing = true;  // overlap-aware query-block pairing (env PISA_B200_PAIRING=0: off)
+    int host_chunks = 16;  // head chunks of the host path's copy/compute pipeline (env PISA_B200_HOST_CHUNKS)
     unsigned long long* tiles_dev = nullptr;  // fused-kernel tile counter (profiling only)
 };
 
@@ -444,6 +445,7 @@ pisa_status pisa_b200_create(pisa_ctx** out, int device) {
     pisa_ctx* c = new pisa_ctx;
     c->device = device;
     if (const char* ev = std::getenv("PISA_B200_PAIRING")) c->pairing = std::atoi(ev) != 0;
+    if (const char* ev = std::getenv("PISA_B200_HOST_CHUNKS")) c->host_chunks = std::max(1, std::atoi(ev));
     DeviceGuard g(device);
     if (cudaMallocHost(&c->flag_host, sizeof(int)) != cudaSuccess) {
         delete c;
@@ -721,7 +723,7 @@ pisa_status pisa_b200_fwd_host(pisa_ctx* ctx, const pisa_attn_desc* d, const voi
     const int64_t BH = p.BH, L = p.L, D = p.D;
     const size_t in_bytes = size_t(L) * D * 2;
     const size_t out_bytes = size_t(L) * D * (d->out_dtype == PISA_DTYPE_F32 ? 4 : 2);
-    const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(BH, (BH + 7) / 8));
+    const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(BH, (BH + ctx->host_chunks - 1) / ctx->host_chunks));
     const bool want_diag = hdiag && (hdiag->row_max || hdiag->ell || hdiag->ell_tail || hdiag->selected);
     const size_t diag_bytes = want_diag ? size_t(L) * 4 * 3 + size_t(p.N) * p.k * 4 : 0;
     const size_t set_bytes = size_t(chunk) * (3 * in_bytes + out_bytes + diag_bytes);
