@@ -229,13 +229,22 @@ def main():
     dev = torch.device("cuda", local_rank)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
-    # (batch x head) sharding: contiguous head ranges per rank
-    h0 = rank * H // world
-    h1 = (rank + 1) * H // world
-    Hr = h1 - h0
+    from paper_2602_01077_b200.sharding import Piece, unit_qblock_pieces
+
     N = -(-L // 64)
     k = P.sparsity_to_k(1.0 - density, N).k
     C2 = -(-N // 64)
+    # (batch x head) sharding: contiguous head ranges per rank; when the heads do
+    # not divide over the ranks, (head x query-block range) units
+    even = (B * H) % world == 0
+    if even:
+        h0, h1 = rank * H // world, (rank + 1) * H // world
+        pieces = [Piece(0, h0, h1, 0, N)]
+    else:
+        assert B == 1, "query-block sharding in bench.py assumes B == 1"
+        pieces = unit_qblock_pieces(B, H, N, world, rank)
+        h0, h1 = min(p.h0 for p in pieces), max(p.h1 for p in pieces)
+    Hr = h1 - h0  # heads whose Q/K/V this rank holds
 
     g = torch.Generator(device=dev)
     g.manual_seed(1234 + rank)
@@ -260,12 +269,18 @@ def main():
     if args.router == "covariance":
         kw["router"] = P.RouterStrategy.CovarianceAware
 
-    # warmup (+ the plan, for executed-FLOP accounting)
-    _, ex = P.fwd(q, kk, v, out, return_plan=True, **kw)
-    for _ in range(warmup - 1):
-        P.fwd(q, kk, v, out, **kw)
+    def step():
+        n = 0
+        for pc in pieces:
+            sl = (slice(None), slice(pc.h0 - h0, pc.h1 - h0))
+            rng = None if (pc.qb0, pc.qb1) == (0, N) else (pc.qb0, pc.qb1)
+            P.fwd(q[sl], kk[sl], v[sl], out[sl], q_blocks=rng, **kw)
+            n += ctx.last_launch_count()
+        return n
+
+    for _ in range(warmup):
+        step()
     torch.cuda.synchronize()
-    del ex
 
     # timed region
     stream = torch.cuda.current_stream()
@@ -280,16 +295,15 @@ def main():
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         for _ in range(args.steps):
-            P.fwd(q, kk, v, out, **kw)
-            launches += ctx.last_launch_count()
+            launches += step()
         e1.record(stream)
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
     ctx.set_profiling(False)
     prof = ctx.read_profile()
-    tiles = ctx.fused_tiles() / args.steps  # per launch
-    ctas = Hr * B * (-(-N // 2))
+    tiles = ctx.fused_tiles() / args.steps  # per step (all pieces)
+    ctas = B * sum((p.h1 - p.h0) * (-(-(p.qb1 - p.qb0) // 2)) for p in pieces)
     exec_flops = executed_flops(tiles, ctas, d)
     union_ratio = (tiles / ctas - 2 * (-(-C2 // 2))) / k  # union blocks (incl. pair padding) per tile / k
     t_ms = e0.elapsed_time(e1) / args.steps
@@ -305,9 +319,10 @@ def main():
     peak, peak_sus, hbm, peak_src = load_peaks()
     fused_ms, fused_n = prof.get("fused_attn_kernel", (0.0, 0))
     fused_avg = fused_ms / max(1, fused_n)
-    alg = Hr * B * flops_fused(L, d, N, k)
-    achieved = alg / (fused_avg * 1e-3) / 1e12 if fused_avg > 0 else None
-    executed = exec_flops / (fused_avg * 1e-3) / 1e12 if fused_avg > 0 else None
+    fused_step = fused_ms / args.steps  # one launch per piece, pieces per step
+    alg = B * flops_fused(L, d, N, k) * sum((p.h1 - p.h0) * (p.qb1 - p.qb0) for p in pieces) / N
+    achieved = alg / (fused_step * 1e-3) / 1e12 if fused_step > 0 else None
+    executed = exec_flops / (fused_step * 1e-3) / 1e12 if fused_step > 0 else None
     traffic = None
     tp = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tp):
@@ -357,11 +372,14 @@ def main():
         if world > 1:
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         te = float(tt.item())
-        nb = 2 * B * Hr * L * d
+        hs = torch.tensor([Hr], device=dev, dtype=torch.float64)
+        if world > 1:
+            dist.all_reduce(hs)
+        nb = 2 * B * int(hs.item()) * L * d  # bytes of one tensor over all ranks
         e2e = {"value": total_dense / (te * 1e-3) / 1e12, "unit": "TFLOPS (dense-equivalent)",
-               "ms_per_step": te, "h2d_bytes_per_step": 3 * nb * world,
-               "d2h_bytes_per_step": nb * world,
-               "path": "pisa_b200_fwd_host (pinned host Q/K/V/O; H2D, compute, D2H overlapped per head chunk)"}
+               "ms_per_step": te, "h2d_bytes_per_step": 3 * nb, "d2h_bytes_per_step": nb,
+               "path": "pisa_b200_fwd_host (pinned host Q/K/V/O; H2D, compute, D2H overlapped per head chunk)"
+                       + ("" if even else "; whole heads of each rank's span (partial heads computed in full)")}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -380,7 +398,9 @@ def main():
             "data": f"synthetic {args.data} (torch RNG on device), bf16",
             "config": {"workload": cfg_name, "B": B, "H": H, "L": L, "d": d, "N": N, "k": k,
                        "density": density, "block": 64, "variant": "hybrid", "router": args.router,
-                       "parallelism": f"head-sharded x{world}", "heads_per_gpu": Hr,
+                       "parallelism": (f"head-sharded x{world}" if even
+                                       else f"head x query-block sharded x{world}"),
+                       "heads_per_gpu": Hr, "pieces_rank0": [list(p) for p in pieces],
                        "l2": "inputs 2.3 GB > 126 MB L2, no flush"},
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                          "frac": (achieved / peak) if achieved else None, "traffic": traffic,

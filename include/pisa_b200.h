@@ -128,6 +128,16 @@ pisa_status pisa_b200_resolve(const pisa_attn_desc* desc, int64_t* num_blocks, i
 pisa_status pisa_b200_fwd(pisa_ctx* ctx, const pisa_attn_desc* desc, const void* q,
                           const void* k, const void* v, void* o, const pisa_diag* diag,
                           void* stream);
+/* The forward restricted to query blocks [qb_begin, qb_end) of every (b, h):
+ * the unit of (head x query-block range) sharding when heads do
+ * not divide evenly over ranks. Statistics and routing use the full K / V
+ * (pisa_multihead's per-head prepare, engine.hpp:437-441); output rows (and
+ * diag rows) outside the range are not written. Every query block's result is
+ * bitwise identical to the full call's. qb_end = -1 means N. A range outside
+ * [0, N) -> PISA_ERR_INVALID_DIMENSION. */
+pisa_status pisa_b200_fwd_qrange(pisa_ctx* ctx, const pisa_attn_desc* desc, const void* q,
+                                 const void* k, const void* v, void* o, int64_t qb_begin,
+                                 int64_t qb_end, const pisa_diag* diag, void* stream);
 
 /* Same, with Q/K/V/O in (ideally pinned) HOST memory: the ctx stages heads through
  * device buffers on its own streams, overlapping H2D copy, compute and D2H copy.

@@ -16,7 +16,9 @@
 //       unmatched candidate, mutual proposals match, repeat; the blocks left
 //       over are paired in index order. Deterministic (ties -> lower index).
 // Output pairs[bh][t] = (a, b), a < b, b = -1 for a lone last block; the fused
-// kernel's tile t processes query blocks a and b.
+// kernel's tile t processes query blocks a and b. Only query blocks in
+// [qb0, qb1) take part (a rank's share of a head under (head x query-block
+// range) sharding); t counts from 0.
 #include "kernels.h"
 
 namespace pisa_b200 {
@@ -35,24 +37,24 @@ __device__ __forceinline__ bool better(int ov, int j, int ov2, int j2) {
 }
 
 __global__ void __launch_bounds__(256) pair_candidates_kernel(const uint32_t* __restrict__ mask, int N,
-                                                             int W, int* __restrict__ cand) {
+                                                             int W, int qb0, int qb1, int* __restrict__ cand) {
     extern __shared__ uint32_t mrow[];  // [8 warps][W]
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int bh = blockIdx.y;
-    const int i = blockIdx.x * 8 + warp;
+    const int i = qb0 + blockIdx.x * 8 + warp;
     uint32_t* mi = mrow + warp * W;
     const uint32_t* M = mask + size_t(bh) * N * W;
-    if (i < N)
+    if (i < qb1)
         for (int w = lane; w < W; w += 32) mi[w] = M[size_t(i) * W + w];
     __syncwarp();
-    if (i >= N) return;
+    if (i >= qb1) return;
     int bo[kCand], bj[kCand];
 #pragma unroll
     for (int c = 0; c < kCand; ++c) {
         bo[c] = -1;
         bj[c] = 0x7fffffff;
     }
-    const int j0 = max(0, i - kWindow), j1 = min(N, i + kWindow + 1);
+    const int j0 = max(qb0, i - kWindow), j1 = min(qb1, i + kWindow + 1);
     for (int j = j0 + lane; j < j1; j += 32) {
         if (j == i) continue;
         const uint32_t* mj = M + size_t(j) * W;
@@ -87,18 +89,18 @@ __global__ void __launch_bounds__(256) pair_candidates_kernel(const uint32_t* __
     }
 }
 
-__global__ void __launch_bounds__(1024) pair_match_kernel(const int* __restrict__ cand, int N,
-                                                          int2* __restrict__ pairs) {
+__global__ void __launch_bounds__(1024) pair_match_kernel(const int* __restrict__ cand, int N, int qb0,
+                                                          int qb1, int2* __restrict__ pairs) {
     extern __shared__ int partner[];  // [N], then prop [N]
     int* prop = partner + N;
     __shared__ int progress;
     const int bh = blockIdx.x;
     const int* C = cand + size_t(bh) * N * kCand;
-    for (int i = threadIdx.x; i < N; i += blockDim.x) partner[i] = -1;
+    for (int i = qb0 + threadIdx.x; i < qb1; i += blockDim.x) partner[i] = -1;
     __syncthreads();
     for (int round = 0; round < 64; ++round) {
         // every unmatched block proposes its best unmatched candidate
-        for (int i = threadIdx.x; i < N; i += blockDim.x) {
+        for (int i = qb0 + threadIdx.x; i < qb1; i += blockDim.x) {
             int p = -1;
             if (partner[i] < 0) {
                 for (int c = 0; c < kCand; ++c) {
@@ -113,7 +115,7 @@ __global__ void __launch_bounds__(1024) pair_match_kernel(const int* __restrict_
         }
         if (threadIdx.x == 0) progress = 0;
         __syncthreads();
-        for (int i = threadIdx.x; i < N; i += blockDim.x) {
+        for (int i = qb0 + threadIdx.x; i < qb1; i += blockDim.x) {
             const int j = prop[i];
             if (j >= 0 && prop[j] == i) {  // mutual: both sides record it
                 partner[i] = j;
@@ -127,7 +129,7 @@ __global__ void __launch_bounds__(1024) pair_match_kernel(const int* __restrict_
     // emit pairs in order of the lower index; leftovers paired in index order
     if (threadIdx.x == 0) {
         int t = 0, pending = -1;
-        for (int i = 0; i < N; ++i) {
+        for (int i = qb0; i < qb1; ++i) {
             const int j = partner[i];
             if (j > i) {
                 pairs[size_t(bh) * ((N + 1) / 2) + t++] = make_int2(i, j);
@@ -146,16 +148,16 @@ __global__ void __launch_bounds__(1024) pair_match_kernel(const int* __restrict_
 
 }  // namespace
 
-cudaError_t launch_pairing(const uint32_t* mask, int N, int W, int BH, int* cand, int2* pairs,
-                           cudaStream_t s) {
+cudaError_t launch_pairing(const uint32_t* mask, int N, int W, int qb0, int qb1, int BH, int* cand,
+                           int2* pairs, cudaStream_t s) {
     const size_t sm1 = size_t(8) * W * 4;
     cudaFuncSetAttribute(pair_candidates_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm1));
-    pair_candidates_kernel<<<dim3((N + 7) / 8, BH), 256, sm1, s>>>(mask, N, W, cand);
+    pair_candidates_kernel<<<dim3((qb1 - qb0 + 7) / 8, BH), 256, sm1, s>>>(mask, N, W, qb0, qb1, cand);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     const size_t sm2 = size_t(2) * N * 4;
     cudaFuncSetAttribute(pair_match_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm2));
-    pair_match_kernel<<<BH, 1024, sm2, s>>>(cand, N, pairs);
+    pair_match_kernel<<<BH, 1024, sm2, s>>>(cand, N, qb0, qb1, pairs);
     return cudaGetLastError();
 }
 

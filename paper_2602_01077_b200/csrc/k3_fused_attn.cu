@@ -191,14 +191,15 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int tile = blockIdx.x;
     const int bh = blockIdx.y;
     const int b = bh / a.H, h = bh % a.H;
-    // query blocks of this tile: the pairing kernel's choice, or (2t, 2t+1)
-    int iA = 2 * tile, iB = 2 * tile + 1;
+    // query blocks of this tile (within the range [qb0, qb1)): the pairing
+    // kernel's choice, or consecutive blocks
+    int iA = a.qb0 + 2 * tile, iB = iA + 1;
     if (a.pairs) {
         const int2 pr = a.pairs[size_t(bh) * ((a.N + 1) / 2) + tile];
         iA = pr.x;
         iB = pr.y;
     }
-    const bool hasB = iB >= 0 && iB < a.N;
+    const bool hasB = iB >= 0 && iB < a.qb1;
     const bool tail = a.variant != 0;                       // Zeroth, Hybrid, GlobalCentroid
     const bool first_order = a.variant == 3 || a.variant == 4;
     const int n_last = a.L - (a.N - 1) * 64;
@@ -822,7 +823,7 @@ cudaError_t launch_fused(int D, const CUtensorMap& tmQ, const CUtensorMap& tmK, 
                          const CUtensorMap& tmKb, const CUtensorMap& tmVh, const CUtensorMap& tmH,
                          const FusedArgs& a, int BH, cudaStream_t s) {
     const size_t smem = fused_smem_bytes(D, a.N, a.W);
-    dim3 grid((a.N + 1) / 2, BH);
+    dim3 grid((a.qb1 - a.qb0 + 1) / 2, BH);
     if (D == 128) {
         auto k = fused_attn_kernel<128>;
         cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));

@@ -71,7 +71,7 @@ cudaError_t launch_select(int D, const SelectArgs& a, int BH, uint32_t* keys, cu
 
 // K2c/K2d: overlap-aware pairing of query blocks for the fused kernel.
 // cand: scratch int [BH][N][8]; pairs: int2 [BH][ceil(N/2)].
-cudaError_t launch_pairing(const uint32_t* mask, int N, int W, int BH, int* cand, int2* pairs,
+cudaError_t launch_pairing(const uint32_t* mask, int N, int W, int qb0, int qb1, int BH, int* cand, int2* pairs,
                            cudaStream_t s);
 
 // Plan (ascending lists) -> bitmask, with SelectionPlan::validate semantics
@@ -94,6 +94,7 @@ struct FusedArgs {
     float* diag_lt;
     int* nonfinite;  // device flag or null
     int L, N, H, W, nchunk2, variant, literal_phase3, out_f32, k;
+    int qb0, qb1;  // query blocks [qb0, qb1) are computed (the rest of O is untouched)
     float scale;
     unsigned long long* trace;  // PISA_TRACE builds only: [8][1024] clock deltas
     unsigned long long* tile_count;  // instrumentation: += 64-key tiles processed (incl. padding), or null

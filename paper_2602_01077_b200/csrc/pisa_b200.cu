@@ -168,6 +168,7 @@ bool make_3d_map(CUtensorMap* m, const void* base, uint64_t D, uint64_t rows, ui
 struct Plan {
     int64_t BH, L, D, N, Npad, W, k, nchunk1, nchunk2;
     double scale;
+    int64_t qb0 = 0, qb1 = 0;  // query-block range of the fused step ([0, N) unless restricted)
 };
 
 pisa_status resolve(pisa_ctx* ctx, const pisa_attn_desc* d, Plan* p) {
@@ -354,10 +355,11 @@ pisa_status run_fused(pisa_ctx* ctx, const pisa_attn_desc& d, const Plan& p, con
         !make_3d_map(&th, w.hbar_bf, p.D, p.D, p.BH, uint32_t(p.D)))
         return fail(ctx, PISA_ERR_CUDA, "TMA descriptor creation failed");
     // overlap-aware pairing of query blocks (K2c/K2d); PISA_B200_PAIRING=0 keeps (2t, 2t+1)
-    const bool pairing = ctx->pairing && p.N > 2;
+    const int qb0 = int(p.qb0), qb1 = int(p.qb1 > 0 ? p.qb1 : p.N);
+    const bool pairing = ctx->pairing && qb1 - qb0 > 2;
     if (pairing) {
         ProfScope ps(ctx, kPair, s);
-        const cudaError_t e = launch_pairing(w.mask, int(p.N), int(p.W), int(p.BH), w.cand, w.pairs, s);
+        const cudaError_t e = launch_pairing(w.mask, int(p.N), int(p.W), qb0, qb1, int(p.BH), w.cand, w.pairs, s);
         if (e != cudaSuccess) return cuda_fail(ctx, e, "pairing launch");
         ctx->launches += 2;
     }
@@ -386,6 +388,8 @@ pisa_status run_fused(pisa_ctx* ctx, const pisa_attn_desc& d, const Plan& p, con
     a.literal_phase3 = d.literal_phase3;
     a.out_f32 = d.out_dtype == PISA_DTYPE_F32;
     a.k = int(p.k);
+    a.qb0 = qb0;
+    a.qb1 = qb1;
     a.scale = float(p.scale);
     a.trace = ctx->trace;
     a.tile_count = ctx->prof ? ctx->tiles_dev : nullptr;
@@ -563,13 +567,21 @@ pisa_status pisa_b200_resolve(const pisa_attn_desc* d, int64_t* num_blocks, int6
     return PISA_OK;
 }
 
-pisa_status pisa_b200_fwd(pisa_ctx* ctx, const pisa_attn_desc* d, const void* q, const void* k,
-                          const void* v, void* o, const pisa_diag* diag, void* stream) {
+namespace {
+pisa_status fwd_range(pisa_ctx* ctx, const pisa_attn_desc* d, const void* q, const void* k, const void* v,
+                      void* o, int64_t qb_begin, int64_t qb_end, const pisa_diag* diag, void* stream) {
     if (!ctx) return PISA_ERR_INVALID_DIMENSION;
     ctx->launches = 0;
     Plan p;
     pisa_status st = resolve(ctx, d, &p);
     if (st != PISA_OK) return st;
+    if (qb_end < 0) qb_end = p.N;
+    if (qb_begin < 0 || qb_begin >= qb_end || qb_end > p.N)
+        return fail(ctx, PISA_ERR_INVALID_DIMENSION,
+                    "query-block range [" + std::to_string(qb_begin) + ", " + std::to_string(qb_end) +
+                        ") outside [0, " + std::to_string(p.N) + ")");
+    p.qb0 = qb_begin;
+    p.qb1 = qb_end;
     if (!q || !k || !v || !o) return fail(ctx, PISA_ERR_INVALID_DIMENSION, "null tensor pointer");
     if (!out_dtype_ok(d)) return fail(ctx, PISA_ERR_UNSUPPORTED, "output dtype");
     DeviceGuard g(ctx->device);
@@ -584,6 +596,18 @@ pisa_status pisa_b200_fwd(pisa_ctx* ctx, const pisa_attn_desc* d, const void* q,
         PISA_OK)
         return st;
     return run_fused(ctx, *d, p, w, q, k, v, o, diag, s);
+}
+}  // namespace
+
+pisa_status pisa_b200_fwd(pisa_ctx* ctx, const pisa_attn_desc* d, const void* q, const void* k,
+                          const void* v, void* o, const pisa_diag* diag, void* stream) {
+    return fwd_range(ctx, d, q, k, v, o, 0, -1, diag, stream);
+}
+
+pisa_status pisa_b200_fwd_qrange(pisa_ctx* ctx, const pisa_attn_desc* d, const void* q, const void* k,
+                                 const void* v, void* o, int64_t qb_begin, int64_t qb_end,
+                                 const pisa_diag* diag, void* stream) {
+    return fwd_range(ctx, d, q, k, v, o, qb_begin, qb_end, diag, stream);
 }
 
 pisa_status pisa_b200_block_stats(pisa_ctx* ctx, const pisa_attn_desc* d, const void* q,

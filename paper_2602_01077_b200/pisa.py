@@ -376,9 +376,12 @@ def resolve(desc: _abi.AttnDesc):
 
 
 def fwd(q, k, v, out=None, *, layout="bhld", out_dtype=torch.bfloat16, diagnostics=False,
-        return_plan=False, ctx: Optional[Context] = None, **kw):
+        return_plan=False, ctx: Optional[Context] = None, q_blocks=None, **kw):
     """The fused forward (pisa_b200_fwd) on 4-D device tensors.
 
+    ``q_blocks=(begin, end)`` restricts the fused step to those query blocks of
+    every head (pisa_b200_fwd_qrange; rows outside are left as they are in
+    ``out``) -- the unit of (head x query-block range) sharding.
     Returns ``out`` or ``(out, extras)`` where extras holds row_max / ell / ell_tail
     ([B][H][L] fp32) and the plan ([B][H][N][k] int32) when requested."""
     _check_inputs(q, k, v)
@@ -399,8 +402,13 @@ def fwd(q, k, v, out=None, *, layout="bhld", out_dtype=torch.bfloat16, diagnosti
         if return_plan:
             extras["selected"] = torch.empty((B, H, N, kk), dtype=torch.int32, device=q.device)
             diag.selected = extras["selected"].data_ptr()
-    st = ctx.lib.pisa_b200_fwd(ctx.handle, C.byref(desc), _ptr(q), _ptr(k), _ptr(v), _ptr(out),
-                               C.byref(diag) if diag is not None else None, _stream())
+    dp = C.byref(diag) if diag is not None else None
+    if q_blocks is None:
+        st = ctx.lib.pisa_b200_fwd(ctx.handle, C.byref(desc), _ptr(q), _ptr(k), _ptr(v), _ptr(out), dp,
+                                   _stream())
+    else:
+        st = ctx.lib.pisa_b200_fwd_qrange(ctx.handle, C.byref(desc), _ptr(q), _ptr(k), _ptr(v), _ptr(out),
+                                          int(q_blocks[0]), int(q_blocks[1]), dp, _stream())
     _raise(st, ctx.handle)
     return (out, extras) if extras else out
 

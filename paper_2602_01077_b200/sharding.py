@@ -3,10 +3,16 @@ path needs: heads are independent in pisa_multihead
 (engine.hpp:432-468), so each rank runs the full K1 -> K2 -> K3 sequence on a
 contiguous range of (b, h) units with no data-path collective. The optional
 final gather of O is one all_gather over NCCL (NVLink/NVSwitch) or gloo.
+
+When the units do not divide evenly (Wan2.1-1.3B: 12 heads on 8 GPUs), the
+work is split in (unit x query-block) space instead: query blocks of a head are
+independent too (engine.hpp:272), so a rank may own a range of query blocks of
+a head, computed by pisa_b200_fwd_qrange (statistics and routing still see the
+head's full K / V, recomputed by every rank that touches the head).
 """
 from __future__ import annotations
 
-from typing import Tuple
+from typing import List, NamedTuple, Tuple
 
 import torch
 
@@ -41,3 +47,47 @@ def gather_heads(local: torch.Tensor, units: int, world: int, group=None) -> tor
     bufs = [torch.empty_like(pad) for _ in range(world)]
     dist.all_gather(bufs, pad, group=group)
     return torch.cat([b[: hi - lo] for b, (lo, hi) in zip(bufs, shares)], 0)
+
+
+class Piece(NamedTuple):
+    """Units [u0, u1) of one batch index b (heads h0 = u0 % H ...), query blocks [qb0, qb1)."""
+    b: int
+    h0: int
+    h1: int
+    qb0: int
+    qb1: int
+
+
+def unit_qblock_pieces(B: int, H: int, N: int, world: int, rank: int) -> List[Piece]:
+    """This rank's share of the B*H*N query blocks (balanced to +-1 block), as
+    at most a few (batch, head range, query-block range) calls: a partial first
+    head, whole heads, a partial last head (split again at batch boundaries)."""
+    total = B * H * N
+    lo, hi = unit_range(total, world, rank)
+    pieces: List[Piece] = []
+    x = lo
+    while x < hi:
+        u, qb = divmod(x, N)
+        b, h = divmod(u, H)
+        if qb != 0 or hi - x < N:  # partial head
+            end = min(hi, (u + 1) * N)
+            pieces.append(Piece(b, h, h + 1, qb, end - u * N))
+            x = end
+        else:  # whole heads up to the end of this batch index or of the share
+            nh = min((hi - x) // N, H - h)
+            pieces.append(Piece(b, h, h + nh, 0, N))
+            x += nh * N
+    return pieces
+
+
+def fwd_pieces(q, k, v, out, pieces: List[Piece], **kw):
+    """Runs this rank's pieces on [B][H][L][d] device tensors (views per piece,
+    no copies); rows of `out` outside the pieces are not written."""
+    from . import pisa as P
+
+    for pc in pieces:
+        sl = (slice(pc.b, pc.b + 1), slice(pc.h0, pc.h1))
+        N = -(-q.shape[2] // 64)
+        rng = None if (pc.qb0, pc.qb1) == (0, N) else (pc.qb0, pc.qb1)
+        P.fwd(q[sl], k[sl], v[sl], out[sl], q_blocks=rng, **kw)
+    return out

@@ -469,3 +469,36 @@ def test_cpp_shim_drop_in(P, oracle_mod, tmp_path):
     assert np.array_equal(plan, ref["selected"])
     for h in range(H):
         check_close(out[h], ref["out"][h])
+
+
+# ----------------------------------- (head x query-block range) sharding (§8e) --
+def test_qrange_pieces_reassemble_bitwise(P, oracle_mod):
+    """Eight simulated ranks over 3 heads (ragged L = 1000, N = 16): each runs
+    pisa_b200_fwd_qrange on its (head, query-block range) pieces; the assembled
+    output, diagnostics and plan equal the full call's bit for bit."""
+    import torch
+
+    from paper_2602_01077_b200.sharding import fwd_pieces, unit_qblock_pieces
+    q, k, v = (dev_bf16(x) for x in oracle_mod.gen("clustered", 21, 3, 1000, 128))
+    kw = dict(sparsity=0.75)
+    full = P.fwd(q, k, v, **kw)
+    out = torch.full_like(full, float("nan"))
+    for r in range(8):
+        fwd_pieces(q, k, v, out, unit_qblock_pieces(1, 3, 16, 8, r), **kw)
+    torch.cuda.synchronize()
+    assert torch.equal(out, full)
+    # a single range: rows outside it are untouched, rows inside equal the full call
+    part = torch.zeros_like(full)
+    P.fwd(q, k, v, part, q_blocks=(5, 11), **kw)
+    torch.cuda.synchronize()
+    assert torch.equal(part[:, :, 5 * 64:11 * 64], full[:, :, 5 * 64:11 * 64])
+    assert not part[:, :, :5 * 64].any() and not part[:, :, 11 * 64:].any()
+    # the ragged last block alone, and a lone first block
+    for rng in ((15, 16), (0, 1)):
+        part.zero_()
+        P.fwd(q, k, v, part, q_blocks=rng, **kw)
+        torch.cuda.synchronize()
+        assert torch.equal(part[:, :, rng[0] * 64:rng[1] * 64], full[:, :, rng[0] * 64:rng[1] * 64])
+    for bad in ((3, 3), (-1, 4), (0, 17), (12, 5)):
+        with pytest.raises(P.InvalidDimension):
+            P.fwd(q, k, v, part, q_blocks=bad, **kw)

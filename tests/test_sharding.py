@@ -8,7 +8,7 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_2602_01077_b200.sharding import gather_heads, shard_heads, unit_range
+from paper_2602_01077_b200.sharding import gather_heads, shard_heads, unit_qblock_pieces, unit_range
 
 
 @pytest.mark.parametrize("units,world", [(40, 1), (40, 2), (40, 8), (12, 8), (24, 5), (3, 4)])
@@ -20,6 +20,27 @@ def test_unit_range_partitions(units, world):
         seen += list(range(lo, hi))
     assert seen == list(range(units))
     sizes = [unit_range(units, world, r)[1] - unit_range(units, world, r)[0] for r in range(world)]
+    assert max(sizes) - min(sizes) <= 1
+
+
+@pytest.mark.parametrize("B,H,N,world", [(1, 12, 512, 8), (1, 40, 1182, 8), (2, 3, 10, 4), (1, 1, 7, 3),
+                                         (1, 24, 72, 5), (3, 2, 1, 4)])
+def test_unit_qblock_pieces_partition(B, H, N, world):
+    """(unit x query-block) sharding: every query block of every
+    (b, h) on exactly one rank, shares balanced to one block, at most three
+    calls per rank and batch index."""
+    cover, sizes = [], []
+    for r in range(world):
+        ps = unit_qblock_pieces(B, H, N, world, r)
+        n = 0
+        for p in ps:
+            assert 0 <= p.b < B and 0 <= p.h0 < p.h1 <= H and 0 <= p.qb0 < p.qb1 <= N
+            assert p.h1 - p.h0 == 1 or (p.qb0, p.qb1) == (0, N)  # a partial range covers one head
+            cover += [(p.b, h, qb) for h in range(p.h0, p.h1) for qb in range(p.qb0, p.qb1)]
+            n += (p.h1 - p.h0) * (p.qb1 - p.qb0)
+        sizes.append(n)
+        assert len(ps) <= 3 * B
+    assert sorted(cover) == [(b, h, q) for b in range(B) for h in range(H) for q in range(N)]
     assert max(sizes) - min(sizes) <= 1
 
 
