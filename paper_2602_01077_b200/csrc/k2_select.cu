@@ -25,62 +25,155 @@ __device__ __forceinline__ uint32_t order_key(float f) {
     return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
 }
 
-// K2a: score tile. keys[bh][i][j] = order_key(scale * <q_bar_i, k_bar_j>) for a
-// 64 x 64 tile of (query block, key block) pairs; 256 threads, 4 x 4 outputs
-// each. Every output accumulates a = 0 .. D-1 in order with fp32 FMA (the
-// same order as the reference's dot_d loop), so results are reproducible.
-constexpr int kTile = 64, kAK = 32;
+// K2a: score tile on the tensor cores. keys[bh][i][j] = order_key(scale *
+// <q_bar_i, k_bar_j> [+ rect_j]) for a 128 x 128 tile of (query block, key
+// block) pairs. q_bar / k_bar (fp32) are split exactly (to 2^-27 relative) into
+// bf16 hi + mid + lo parts; the six cross products above 2^-26 run as tcgen05
+// MMAs (bf16 products are exact, fp32 accumulation), so the scores carry fp32
+// accuracy (at least that of the reference-order fp32 dot product) and are
+// deterministic. 256 threads: all split, warp 0 issues, all eight read TMEM
+// (warp w: lane quadrant w % 4, columns (w / 4) * 64 ..).
+constexpr int kTile = 128;
+constexpr int kScoreThreads = 256;
+
+template <int D>
+struct ScoreCfg {
+    static constexpr int kPart = kTile * D * 2;  // one bf16 operand part (K-major, SW128 halves of 64)
+    static constexpr int kOffB = 3 * kPart;      // A: hi | mid | lo, then B: hi | mid | lo
+    static constexpr int kSmem = 1024 + 6 * kPart + 64;
+};
+
+// x = hi + mid + lo, each a bf16 pair (exact to 2^-27 relative)
+__device__ __forceinline__ void split3(float x0, float x1, uint32_t& h, uint32_t& m, uint32_t& l) {
+    const __nv_bfloat162 h2 = __floats2bfloat162_rn(x0, x1);
+    const float2 hf = __bfloat1622float2(h2);
+    const float y0 = x0 - hf.x, y1 = x1 - hf.y;  // exact
+    const __nv_bfloat162 m2 = __floats2bfloat162_rn(y0, y1);
+    const float2 mf = __bfloat1622float2(m2);
+    const __nv_bfloat162 l2 = __floats2bfloat162_rn(y0 - mf.x, y1 - mf.y);
+    h = *reinterpret_cast<const uint32_t*>(&h2);
+    m = *reinterpret_cast<const uint32_t*>(&m2);
+    l = *reinterpret_cast<const uint32_t*>(&l2);
+}
 
 // rect (covariance router, router.hpp:176-183): per key block log(M_j + eps),
 // added after the scaled dot product; null for the plain router.
 template <int D>
-__global__ void __launch_bounds__(256) score_kernel(const float* __restrict__ qbar,
-                                                    const float* __restrict__ kbar,
-                                                    const float* __restrict__ rect,
-                                                    uint32_t* __restrict__ keys, int N,
-                                                    float scale) {
-    __shared__ float As[kAK][kTile + 4];
-    __shared__ float Bs[kAK][kTile + 4];
+__global__ void __launch_bounds__(kScoreThreads, 1) score_kernel(const float* __restrict__ qbar,
+                                                                 const float* __restrict__ kbar,
+                                                                 const float* __restrict__ rect,
+                                                                 uint32_t* __restrict__ keys, int N,
+                                                                 float scale) {
+    using Cfg = ScoreCfg<D>;
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+    uint64_t* done = reinterpret_cast<uint64_t*>(smem + 6 * Cfg::kPart);
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(done + 1);
     const int bh = blockIdx.z;
     const int i0 = blockIdx.y * kTile, j0 = blockIdx.x * kTile;
-    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    if (tid == 0) {
+        mbar_init(done, 1);
+        fence_mbar_init();
+    }
+    if (warp == 0) {
+        tmem_alloc(tslot, 128);
+        tmem_relinquish();
+    }
+    // split q_bar rows i0.. (A) and k_bar rows j0.. (B), 4 fp32 per step, into
+    // the 128B-swizzled K-major bf16 parts
+    constexpr int kQ4 = D / 4;  // float4 per row
     const float* qb = qbar + size_t(bh) * N * D;
     const float* kb = kbar + size_t(bh) * N * D;
-    float acc[4][4] = {};
-    for (int a0 = 0; a0 < D; a0 += kAK) {
-        __syncthreads();
-        for (int e = threadIdx.x; e < kTile * kAK; e += 256) {
-            const int r = e / kAK, c = e % kAK;
-            As[c][r] = (i0 + r < N) ? qb[size_t(i0 + r) * D + a0 + c] : 0.f;
-            Bs[c][r] = (j0 + r < N) ? kb[size_t(j0 + r) * D + a0 + c] : 0.f;
+    // 16 independent 16-byte loads in flight per thread (one CTA per SM: the
+    // load phase is latency-bound otherwise)
+    constexpr int kPer = 2 * kTile * kQ4 / kScoreThreads;  // float4 per thread (32 / 16)
+    constexpr int kBatch = 16;
+#pragma unroll
+    for (int b0 = 0; b0 < kPer; b0 += kBatch) {
+        float4 x[kBatch];
+#pragma unroll
+        for (int t = 0; t < kBatch; ++t) {
+            const int e = tid + (b0 + t) * kScoreThreads;
+            const int op = e / (kTile * kQ4), r = (e / kQ4) % kTile, c = (e % kQ4) * 4;
+            const int row = (op ? j0 : i0) + r;
+            x[t] = row < N ? __ldg(reinterpret_cast<const float4*>((op ? kb : qb) + size_t(row) * D + c))
+                           : make_float4(0.f, 0.f, 0.f, 0.f);
         }
-        __syncthreads();
-#pragma unroll 8
-        for (int c = 0; c < kAK; ++c) {
-            const float4 av = *reinterpret_cast<const float4*>(&As[c][ty * 4]);
-            const float4 bv = *reinterpret_cast<const float4*>(&Bs[c][tx * 4]);
-            const float ar[4] = {av.x, av.y, av.z, av.w};
-            const float br[4] = {bv.x, bv.y, bv.z, bv.w};
 #pragma unroll
-            for (int u = 0; u < 4; ++u)
-#pragma unroll
-                for (int w = 0; w < 4; ++w) acc[u][w] = fmaf(ar[u], br[w], acc[u][w]);
-        }
-    }
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-        const int i = i0 + ty * 4 + u;
-        if (i >= N) continue;
-#pragma unroll
-        for (int w = 0; w < 4; ++w) {
-            const int j = j0 + tx * 4 + w;
-            if (j < N) {
-                float sc = scale * acc[u][w];
-                if (rect) sc += rect[size_t(bh) * N + j];
-                keys[(size_t(bh) * N + i) * N + j] = order_key(sc);
-            }
+        for (int t = 0; t < kBatch; ++t) {
+            const int e = tid + (b0 + t) * kScoreThreads;
+            const int op = e / (kTile * kQ4), r = (e / kQ4) % kTile, c = (e % kQ4) * 4;
+            uint2 h, m, l;
+            split3(x[t].x, x[t].y, h.x, m.x, l.x);
+            split3(x[t].z, x[t].w, h.y, m.y, l.y);
+            const uint32_t off = uint32_t(op * Cfg::kOffB + (c >> 6) * (kTile * 128)) + sw128_off(r, c & 63);
+            *reinterpret_cast<uint2*>(smem + off) = h;
+            *reinterpret_cast<uint2*>(smem + off + Cfg::kPart) = m;
+            *reinterpret_cast<uint2*>(smem + off + 2 * Cfg::kPart) = l;
         }
     }
+    fence_proxy_async();
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tslot;
+    if (warp == 0) {
+        if (elect_one()) {
+            constexpr uint32_t idesc = idesc_bf16(128, 128, 0, 0);
+            const uint32_t base = smem_u32(smem);
+            // (lo,hi) (hi,lo) (mid,mid) (mid,hi) (hi,mid) (hi,hi): small terms first
+            constexpr int kA[6] = {2, 0, 1, 1, 0, 0}, kB[6] = {0, 2, 1, 0, 1, 0};
+#pragma unroll
+            for (int p = 0; p < 6; ++p)
+#pragma unroll
+                for (int ks = 0; ks < D / 16; ++ks) {
+                    const uint32_t off = uint32_t((ks >> 2) * (kTile * 128) + (ks & 3) * 32);
+                    mma_ss(tmem, sdesc_sw128(base + kA[p] * Cfg::kPart + off, 16, 1024),
+                           sdesc_sw128(base + Cfg::kOffB + kB[p] * Cfg::kPart + off, 16, 1024), idesc,
+                           p != 0 || ks != 0);
+                }
+            mma_commit(done);
+        }
+        __syncwarp();
+    }
+    mbar_wait(done, 0);
+    tc_fence_after();
+    // epilogue: keys of row i (TMEM lane), 64 columns per warp, staged through
+    // shared memory (the operand parts are dead) so that each row leaves as
+    // coalesced 128-byte warp stores (rows of `keys` are N * 4 bytes apart,
+    // generally not 16-byte aligned)
+    constexpr int kTS = kTile + 1;  // padded row: conflict-free row writes and column reads
+    uint32_t* T = reinterpret_cast<uint32_t*>(smem);
+    const int q = warp & 3, ch = warp >> 2;
+    const int rl = q * 32 + lane;  // local row
+    const float* rc = rect ? rect + size_t(bh) * N + j0 : nullptr;
+#pragma unroll
+    for (int cc = 0; cc < 2; ++cc) {
+        uint32_t r[32];
+        tmem_ld32(tmem + (uint32_t(q * 32) << 16) + ch * 64 + cc * 32, r);
+        tmem_ld_wait(r);
+        const int cb = ch * 64 + cc * 32;
+#pragma unroll
+        for (int t = 0; t < 32; ++t) {
+            float v = scale * __uint_as_float(r[t]);
+            if (rc && j0 + cb + t < N) v += rc[cb + t];
+            T[rl * kTS + cb + t] = order_key(v);
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    for (int rr = warp; rr < kTile; rr += kScoreThreads / 32) {
+        const int i = i0 + rr;
+        if (i >= N) break;
+        uint32_t* krow = keys + (size_t(bh) * N + i) * N + j0;
+#pragma unroll
+        for (int m = 0; m < kTile / 32; ++m) {
+            const int c = m * 32 + lane;
+            if (j0 + c < N) krow[c] = T[rr * kTS + c];
+        }
+    }
+    if (warp == 0) tmem_dealloc(tmem, 128);
 }
 
 // K2b: per query block, radix-select the k-th largest key (8-bit digits from the
@@ -218,10 +311,13 @@ __global__ void plan_to_mask_kernel(const int32_t* __restrict__ selected, int N,
 cudaError_t launch_select(int D, const SelectArgs& a, int BH, uint32_t* keys, cudaStream_t s) {
     const int nt = (a.N + kTile - 1) / kTile;
     dim3 g1(nt, nt, BH);
-    if (D == 128)
-        score_kernel<128><<<g1, 256, 0, s>>>(a.qbar, a.kbar, a.rect, keys, a.N, a.scale);
-    else
-        score_kernel<64><<<g1, 256, 0, s>>>(a.qbar, a.kbar, a.rect, keys, a.N, a.scale);
+    if (D == 128) {
+        cudaFuncSetAttribute(score_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, ScoreCfg<128>::kSmem);
+        score_kernel<128><<<g1, kScoreThreads, ScoreCfg<128>::kSmem, s>>>(a.qbar, a.kbar, a.rect, keys, a.N, a.scale);
+    } else {
+        cudaFuncSetAttribute(score_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, ScoreCfg<64>::kSmem);
+        score_kernel<64><<<g1, kScoreThreads, ScoreCfg<64>::kSmem, s>>>(a.qbar, a.kbar, a.rect, keys, a.N, a.scale);
+    }
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     const size_t smem = sizeof(uint32_t) * size_t(kRowsPerCta) * (a.N + 256);
