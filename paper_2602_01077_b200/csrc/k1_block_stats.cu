@@ -30,7 +30,8 @@ struct StatsCfg {
     static constexpr int kStage = 3 * kTile;        // K | V | Q
     static constexpr int kRing = kStages * kStage;
     static constexpr int kKbS = kStatsG * D * 4;    // k_bar of the chunk (fp32)
-    static constexpr int kSmem = 1024 + kRing + 2 * kKbS + 256;
+    static constexpr int kRed = 2 * 4 * 3 * D * 4;  // column-sum partials, double-buffered
+    static constexpr int kSmem = 1024 + kRing + 2 * kKbS + kRed + 256;
 };
 
 template <int D>
@@ -45,7 +46,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint8_t* ring = smem;
     float* kb_s = reinterpret_cast<float*>(smem + Cfg::kRing);
     float* vh_s = kb_s + kStatsG * D;
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Cfg::kRing + 2 * Cfg::kKbS);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Cfg::kRing + 2 * Cfg::kKbS + Cfg::kRed);
     uint64_t* full = bars;               // [kStages]
     uint64_t* empty = bars + kStages;    // [kStages]
     uint64_t* done = bars + 2 * kStages;
@@ -121,28 +122,75 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (elect_one()) mma_commit(done);
         __syncwarp();
     } else {
-        // Column warps: column c == TMEM lane this thread reads in the epilogue.
+        // Column warps. Sums over the 64 rows: thread (row group rg, 16-byte
+        // column chunk cg) adds D/16 rows of 8 columns of K, V and Q (24
+        // independent fp32 accumulators, 16-byte loads), the row groups are
+        // combined by shuffles and through shared memory (double-buffered by
+        // block parity), then thread c owns column c. Rows past L are TMA
+        // zero-fill, so they add nothing.
         const int q = warp & 3;
         const int c = q * 32 + lane;
         const bool has_col = c < D;
-        const float* kcol_unused = nullptr;
-        (void)kcol_unused;
+        const int t = threadIdx.x - 64;           // 0..127 over the four column warps
+        constexpr int kCh = D / 8;                // 16-byte chunks per row
+        constexpr int kRows = 64 * kCh / 128;     // rows per row group (8 / 4)
+        const int cg = t % kCh, rg = t / kCh;
+        float* red = vh_s + kStatsG * D;          // [2][4 warps][3][D]
         for (int jl = 0; jl < nb; ++jl) {
             const int s = jl % kStages;
             mbar_wait(&full[s], (jl / kStages) & 1);
             const int j = j0 + jl;
             const int nrow = min(64, a.L - j * 64);
+            const uint8_t* st = ring + s * Cfg::kStage;
+            float acc[3][8];
+#pragma unroll
+            for (int m = 0; m < 3; ++m)
+#pragma unroll
+                for (int e = 0; e < 8; ++e) acc[m][e] = 0.f;
+#pragma unroll
+            for (int rr = 0; rr < kRows; ++rr) {
+                const int r = rg * kRows + rr;
+                const uint32_t off = uint32_t((cg >> 3) * 8192 + r * 128 + (((cg & 7) ^ (r & 7)) << 4));
+#pragma unroll
+                for (int m = 0; m < 3; ++m) {
+                    const uint4 w = *reinterpret_cast<const uint4*>(st + m * Cfg::kTile + off);
+                    const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&w);
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        const float2 f = __bfloat1622float2(b2[e]);
+                        acc[m][2 * e] += f.x;
+                        acc[m][2 * e + 1] += f.y;
+                    }
+                }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[s]);  // the tile is read
+            // row groups inside the warp: lanes kCh apart
+#pragma unroll
+            for (int o = kCh; o < 32; o <<= 1)
+#pragma unroll
+                for (int m = 0; m < 3; ++m)
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) acc[m][e] += __shfl_xor_sync(0xffffffffu, acc[m][e], o);
+            float* rb = red + (jl & 1) * (4 * 3 * D) + q * (3 * D);
+            if (lane < kCh) {
+#pragma unroll
+                for (int m = 0; m < 3; ++m) {
+                    *reinterpret_cast<float4*>(rb + m * D + cg * 8) =
+                        make_float4(acc[m][0], acc[m][1], acc[m][2], acc[m][3]);
+                    *reinterpret_cast<float4*>(rb + m * D + cg * 8 + 4) =
+                        make_float4(acc[m][4], acc[m][5], acc[m][6], acc[m][7]);
+                }
+            }
+            asm volatile("bar.sync 2, 128;" ::: "memory");
             if (has_col) {
-                const uint8_t* st = ring + s * Cfg::kStage;
-                const uint32_t coff = (c >> 6) * 8192;
+                const float* rb0 = red + (jl & 1) * (4 * 3 * D);
                 float sk = 0.f, sv = 0.f, sq = 0.f;
-                for (int r = 0; r < nrow; ++r) {
-                    const uint32_t off = coff + sw128_off(r, c & 63);
-                    sk += __bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(st + off));
-                    sv += __bfloat162float(
-                        *reinterpret_cast<const __nv_bfloat16*>(st + Cfg::kTile + off));
-                    sq += __bfloat162float(
-                        *reinterpret_cast<const __nv_bfloat16*>(st + 2 * Cfg::kTile + off));
+#pragma unroll
+                for (int w = 0; w < 4; ++w) {
+                    sk += rb0[w * 3 * D + c];
+                    sv += rb0[w * 3 * D + D + c];
+                    sq += rb0[w * 3 * D + 2 * D + c];
                 }
                 const float inv = 1.0f / float(nrow);
                 const float kbv = sk * inv;
@@ -156,8 +204,6 @@ __global__ void __launch_bounds__(kThreads, 1)
                 kb_s[jl * D + c] = kbv;
                 vh_s[jl * D + c] = sv;
             }
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&empty[s]);
         }
         // Zero the bf16 padding rows [N, Npad) once per (b, h).
         if (has_col && j0 + nb == a.N) {
