@@ -88,10 +88,43 @@ constexpr uint32_t kPolyMask = PISA_POLY_MASK;
 // The softmax warps' wait for S: spin (poll) or suspend in hardware between
 // polls. Polling steals issue slots from the other warpgroup's warps on the
 // same sub-partitions while one warpgroup runs ahead.
+// 2: poll with a PISA_SOFTMAX_NS nanosleep between polls.
 #ifndef PISA_SOFTMAX_SPIN
 #define PISA_SOFTMAX_SPIN 1
 #endif
+#ifndef PISA_SOFTMAX_NS
+#define PISA_SOFTMAX_NS 32
+#endif
 constexpr bool kSoftmaxSpin = PISA_SOFTMAX_SPIN != 0;
+__device__ __forceinline__ void softmax_wait(uint64_t* bar, uint32_t parity) {
+#if PISA_SOFTMAX_SPIN == 2
+    mbar_wait_backoff<PISA_SOFTMAX_NS>(bar, parity);
+#else
+    mbar_wait<kSoftmaxSpin>(bar, parity);
+#endif
+}
+// PISA_MMA_WAIT 1: the MMA warp polls its barriers with a short nanosleep
+// (instead of a pure spin that takes issue slots from the two softmax warps on
+// its sub-partition). PISA_PSPLIT 1: P is published per 64-key sub-tile and
+// the MMA warp issues PV of the first sub-tile while the softmax computes the
+// second.
+#ifndef PISA_MMA_WAIT
+#define PISA_MMA_WAIT 0
+#endif
+#ifndef PISA_MMA_NS
+#define PISA_MMA_NS 20
+#endif
+#ifndef PISA_PSPLIT
+#define PISA_PSPLIT 0
+#endif
+__device__ __forceinline__ void mma_wait(uint64_t* bar, uint32_t parity) {
+#if PISA_MMA_WAIT
+    mbar_wait_backoff<PISA_MMA_NS>(bar, parity);
+#else
+    mbar_wait<true>(bar, parity);
+#endif
+}
+
 // Phase-1 block order. 0: the ascending union (default). 1: balanced (A&B
 // pairs, then (A-only, B-only) pairs: equal softmax work per warpgroup in every
 // super-tile). 2: grouped (A&B pairs, then alternating (A, A) / (B, B) pairs:
@@ -124,7 +157,7 @@ struct FusedCfg {
 struct Bars {
     uint64_t q_full, h_full, qh_full;
     uint64_t k_full[kSK], v_full[kSV], v_empty[kSV];
-    uint64_t s_full[kSB], p_full[kSB];
+    uint64_t s_full[kSB], p_full[kSB], p_half[kSB];
     uint32_t tmem_base;
     uint32_t n_ab, n_a, n_b;
 };
@@ -217,6 +250,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int s = 0; s < kSB; ++s) {
             mbar_init(&bar.s_full[s], 1);
             mbar_init(&bar.p_full[s], 8);  // one arrive per softmax warp
+            mbar_init(&bar.p_half[s], 8);  // (PISA_PSPLIT) first sub-tile of P
         }
         fence_mbar_init();
         tma_prefetch(&tmQ);
@@ -493,15 +527,17 @@ __global__ void __launch_bounds__(kThreads, 1)
         };
         // MMAs of O += P_g V_g, P_g over the S_g columns; commit: v_empty (the V
         // producer's "stage free" and the softmax's "PV_g done")
-        auto mma_pv = [&](int g) {
+        // PV of sub-tiles [k0, k1) of super-tile g (4 MMAs of 16 keys each);
+        // the last one commits the V stage
+        auto mma_pv = [&](int g, int k0, int k1) {
             TRACE(10, g);
             const uint64_t vd = vdesc0 + uint64_t(sv * (Cfg::kKV >> 4));
             const uint32_t pa = tS + uint32_t(sbv) * 128;
 #pragma unroll
-            for (int ks = 0; ks < 8; ++ks)
+            for (int ks = 4 * k0; ks < 4 * k1; ++ks)
                 mma_ts(tO, pa + (ks >> 2) * 64 + (ks & 3) * 8, vd + uint64_t((ks * 2048) >> 4), idPV,
                        (g == 0 && ks == 0) ? 0u : 1u);
-            mma_commit(&bar.v_empty[sv]);
+            if (k1 == 2) mma_commit(&bar.v_empty[sv]);
             TRACE(3, g);
         };
         auto advance_pv = [&]() {
@@ -509,10 +545,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (++sbv == kSB) { sbv = 0; php ^= 1u; }
         };
         if (a.tile_count && lane == 0) atomicAdd(a.tile_count, (unsigned long long)(2 * G));
-        mbar_wait<true>(&bar.q_full, 0);
+        mma_wait(&bar.q_full, 0);
         tc_fence_after();
         for (int g = 0; g < kSB && g < G; ++g) {
-            mbar_wait<true>(&bar.k_full[sk], phk);
+            mma_wait(&bar.k_full[sk], phk);
             tc_fence_after();
             if (elect_one()) mma_s(g);
             __syncwarp();
@@ -522,15 +558,28 @@ __global__ void __launch_bounds__(kThreads, 1)
             // PV_g as soon as P_g and V_g are in, then S_{g+3} once K_{g+3} is
             // (in-order tensor pipe: S_{g+3} overwrites P_g after PV_g read it);
             // a late K tile never holds back PV_g
-            mbar_wait<true>(&bar.p_full[sbv], php);
-            TRACE(9, g);
-            mbar_wait<true>(&bar.v_full[sv], phv);
+#if PISA_PSPLIT
+            mma_wait(&bar.p_half[sbv], php);
+            mma_wait(&bar.v_full[sv], phv);
             tc_fence_after();
-            if (elect_one()) mma_pv(g);
+            if (elect_one()) mma_pv(g, 0, 1);
             __syncwarp();
+            mma_wait(&bar.p_full[sbv], php);
+            TRACE(9, g);
+            tc_fence_after();
+            if (elect_one()) mma_pv(g, 1, 2);
+            __syncwarp();
+#else
+            mma_wait(&bar.p_full[sbv], php);
+            TRACE(9, g);
+            mma_wait(&bar.v_full[sv], phv);
+            tc_fence_after();
+            if (elect_one()) mma_pv(g, 0, 2);
+            __syncwarp();
+#endif
             advance_pv();
             if (g + kSB < G) {
-                mbar_wait<true>(&bar.k_full[sk], phk);
+                mma_wait(&bar.k_full[sk], phk);
                 tc_fence_after();
                 if (elect_one()) mma_s(g + kSB);
                 __syncwarp();
@@ -538,7 +587,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
         }
         if (first_order) {
-            mbar_wait<true>(&bar.h_full, 0);
+            mma_wait(&bar.h_full, 0);
             tc_fence_after();
         }
         if (elect_one()) {
@@ -602,6 +651,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (__any_sync(0xffffffffu, resc)) {
                 const float f = resc ? ex2(m - m_use) : 1.f;
                 wait_pv_prev(g);
+                TRACE(24 + hh * 4 + q4, g);  // (trace builds) rescale of this warp's rows
                 rescale_o<D>(lbase + kColO, f);
                 l *= f;
                 lt *= f;
@@ -609,11 +659,20 @@ __global__ void __launch_bounds__(kThreads, 1)
             m = m_use;
             return (m_use == -INFINITY) ? 0.f : m_use;  // all-masked row: p = 0, not NaN
         };
-        auto publish_p = [&]() {
+        auto publish_half = [&]() {  // first sub-tile of P stored (PISA_PSPLIT)
+#if PISA_PSPLIT
+            tmem_st_wait();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&bar.p_half[sb]);
+#endif
+        };
+        auto publish_p = [&](int g_cur) {
             tmem_st_wait();
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&bar.p_full[sb]);
+            TRACE(16 + hh * 4 + q4, g_cur);  // (trace builds) every warp's P publish
         };
         const uint32_t kZero16[16] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
 
@@ -626,7 +685,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int nv0 = (int(e0 & 0x3FFFu) == a.N - 1) ? n_last : 64;
             const int nv1 = (int(e1 & 0x3FFFu) == a.N - 1) ? n_last : 64;
             const uint32_t sc = lbase + kColS + sb * 128;
-            mbar_wait<kSoftmaxSpin>(&bar.s_full[sb], phs);
+            softmax_wait(&bar.s_full[sb], phs);
             tc_fence_after();
             if (q4 == 0) TRACE(4 + hh, g);
             if (use0 || use1) {
@@ -665,12 +724,14 @@ __global__ void __launch_bounds__(kThreads, 1)
                     tmem_st16x2_16<16>(addr, pk);  // P (bf16 pairs)
                 };
                 if (use0) expo_store(r0, sc); else tmem_st16x2_16<16>(sc, kZero16);
+                publish_half();
                 if (use1) expo_store(r1, sc + 64); else tmem_st16x2_16<16>(sc + 64, kZero16);
             } else {
                 tmem_st16x2_16<16>(sc, kZero16);
+                publish_half();
                 tmem_st16x2_16<16>(sc + 64, kZero16);
             }
-            publish_p();
+            publish_p(g);
             advance();
             if (q4 == 0) TRACE(6 + hh, g);
         }
@@ -686,7 +747,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             };
             const uint32_t cm0 = colmask(c0), cm1 = colmask(c0 + 1);
             const int nv0 = min(64, a.N - c0 * 64), nv1 = min(64, a.N - (c0 + 1) * 64);
-            mbar_wait<kSoftmaxSpin>(&bar.s_full[sb], phs);
+            softmax_wait(&bar.s_full[sb], phs);
             tc_fence_after();
             uint32_t r0[32], r1[32];
             tmem_ld16x2_32<32>(sc, r0);
@@ -721,10 +782,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                 tmem_st16x2_16<16>(addr, pk);
             };
             expo_store(r0, sc, lb);
+            publish_half();
             expo_store(r1, sc + 64, lb - 64);
             l += 64.f * ps + (float(n_last) - 64.f) * plast;
             lt += ps;
-            publish_p();
+            publish_p(g);
             advance();
         }
 

@@ -67,6 +67,24 @@ __device__ __forceinline__ bool mbar_try_wait_spin(uint32_t addr, uint32_t parit
         : "memory");
     return ok != 0;
 }
+// Polls with a short nanosleep between polls: prompt wake-up (<~2 x ns) while a
+// warp that runs ahead gives its issue slots to the warps sharing its
+// sub-partition instead of polling continuously.
+template <int kNs>
+__device__ __forceinline__ void mbar_wait_backoff(uint64_t* bar, uint32_t parity) {
+    const uint32_t addr = smem_u32(bar);
+    if (mbar_try_wait_spin(addr, parity)) return;
+#if PISA_WATCHDOG
+    const uint64_t t0 = global_ns();
+#endif
+    do {
+        __nanosleep(kNs);
+#if PISA_WATCHDOG
+        if (global_ns() - t0 > 4000000000ull) __trap();
+#endif
+    } while (!mbar_try_wait_spin(addr, parity));
+}
+
 // Blocks until the phase with the given parity has completed. Spin = false
 // suspends the thread in hardware between polls (frees issue slots; wake-up can
 // lag by hundreds of cycles), Spin = true polls. With the watchdog on, a wait

@@ -22,13 +22,13 @@ def main():
     dev = torch.device("cuda", 0)
     q, k, v = (torch.randn((1, H, L, d), device=dev, dtype=torch.bfloat16) for _ in range(3))
     ctx = P.Context.get(0)
-    buf = torch.zeros(16 * 1024, dtype=torch.int64, device=dev)
+    buf = torch.zeros(32 * 1024, dtype=torch.int64, device=dev)
     for _ in range(2):
         P.fwd(q, k, v, sparsity=0.875)
     ctx.lib.pisa_b200_debug_trace(ctx.handle, C.c_void_p(buf.data_ptr()), tile)
     P.fwd(q, k, v, sparsity=0.875)
     torch.cuda.synchronize()
-    tr = buf.view(16, 1024).cpu().tolist()
+    tr = buf.view(32, 1024).cpu().tolist()
     n = max(i for i in range(1024) if tr[2][i] or i == 0) + 1
     print("t  " + " ".join(f"{r:>11s}" for r in ROLES))
     for t in range(n):
@@ -36,6 +36,16 @@ def main():
     # per-tile deltas in steady state
     ds = [tr[2][t + 1] - tr[2][t] for t in range(20, n - 30)]
     print("median S-issue period (cycles):", sorted(ds)[len(ds) // 2] if ds else None)
+    # per-warp P publish (roles 16..23: warpgroup A warps q4 = 0..3, then B) and
+    # rescales (roles 24..31), relative to the warpgroup's q4 = 0 warp
+    print("\nper-warp P publish - q4=0 warp (A: q4=1..3 | B: q4=1..3), rescale marks R")
+    for t in range(n):
+        row = []
+        for hh in range(2):
+            base = tr[16 + hh * 4][t]
+            row.append(" ".join(f"{tr[16 + hh * 4 + w][t] - base:6d}" for w in range(1, 4)))
+            row.append("".join("R" if tr[24 + hh * 4 + w][t] else "." for w in range(4)))
+        print(f"{t:3d}  A {row[0]} {row[1]}   B {row[2]} {row[3]}   mmaP-lastP {tr[9][t] - max(tr[16 + i][t] for i in range(8)):6d}")
 
 
 if __name__ == "__main__":
