@@ -128,12 +128,22 @@ pisa_status pisa_b200_resolve(const pisa_attn_desc* desc, int64_t* num_blocks, i
 pisa_status pisa_b200_fwd(pisa_ctx* ctx, const pisa_attn_desc* desc, const void* q,
                           const void* k, const void* v, void* o, const pisa_diag* diag,
                           void* stream);
+/* Query-block pairing for the fused kernel (which query blocks share a CTA):
+ * 0 = consecutive blocks, 1 = auto
+ * (overlap-aware pairing when >= 768 query blocks are computed, the default),
+ * 2 = always overlap-aware. Env PISA_B200_PAIRING sets the initial mode. The
+ * plan does not depend on it; outputs agree to rounding (the grouping of a
+ * block's key blocks into super-tiles moves its lazy-rescale points). */
+pisa_status pisa_b200_set_pairing(pisa_ctx* ctx, int mode);
+
 /* The forward restricted to query blocks [qb_begin, qb_end) of every (b, h):
  * the unit of (head x query-block range) sharding when heads do
  * not divide evenly over ranks. Statistics and routing use the full K / V
  * (pisa_multihead's per-head prepare, engine.hpp:437-441); output rows (and
- * diag rows) outside the range are not written. Every query block's result is
- * bitwise identical to the full call's. qb_end = -1 means N. A range outside
+ * diag rows) outside the range are not written. Every query block's result
+ * equals the full call's to rounding (query blocks may be paired differently,
+ * which moves the online softmax's lazy-rescale points; the plan is identical).
+ * qb_end = -1 means N. A range outside
  * [0, N) -> PISA_ERR_INVALID_DIMENSION. */
 pisa_status pisa_b200_fwd_qrange(pisa_ctx* ctx, const pisa_attn_desc* desc, const void* q,
                                  const void* k, const void* v, void* o, int64_t qb_begin,

@@ -36,7 +36,7 @@ class Diag(C.Structure):
 EXPORTED = [
     "pisa_b200_create", "pisa_b200_destroy", "pisa_b200_last_error", "pisa_b200_abi_version",
     "pisa_b200_sparsity_to_k", "pisa_b200_resolve", "pisa_b200_fwd", "pisa_b200_fwd_host",
-    "pisa_b200_fwd_qrange", "pisa_b200_block_stats", "pisa_b200_select", "pisa_b200_block_norms",
+    "pisa_b200_fwd_qrange", "pisa_b200_set_pairing", "pisa_b200_block_stats", "pisa_b200_select", "pisa_b200_block_norms",
     "pisa_b200_select_cov", "pisa_b200_attention",
     "pisa_b200_last_launch_count", "pisa_b200_kernel_name", "pisa_b200_selftest_mma",
     "pisa_b200_set_profiling", "pisa_b200_read_profile", "pisa_b200_fused_tiles",
@@ -75,6 +75,7 @@ def load(build_if_missing: bool = False):
     L.pisa_b200_fwd.argtypes = [vp, C.POINTER(AttnDesc), vp, vp, vp, vp, C.POINTER(Diag), vp]
     L.pisa_b200_fwd_host.argtypes = [vp, C.POINTER(AttnDesc), vp, vp, vp, vp, C.POINTER(Diag)]
     L.pisa_b200_fwd_qrange.argtypes = [vp, C.POINTER(AttnDesc), vp, vp, vp, vp, i64, i64, C.POINTER(Diag), vp]
+    L.pisa_b200_set_pairing.argtypes = [vp, C.c_int]
     L.pisa_b200_block_stats.argtypes = [vp, C.POINTER(AttnDesc), vp, vp, vp, vp, vp, vp, vp, vp]
     L.pisa_b200_select.argtypes = [vp, C.POINTER(AttnDesc), vp, vp, vp, vp, vp]
     L.pisa_b200_block_norms.argtypes = [vp, C.POINTER(AttnDesc), vp, vp, vp, vp, vp]
@@ -93,8 +94,8 @@ def load(build_if_missing: bool = False):
     L.pisa_b200_fused_tiles.argtypes = [vp, C.POINTER(i64)]
     L.pisa_b200_fused_tiles.restype = C.c_int
     for name in ("pisa_b200_set_profiling", "pisa_b200_read_profile", "pisa_b200_create", "pisa_b200_sparsity_to_k", "pisa_b200_resolve",
-                 "pisa_b200_fwd", "pisa_b200_fwd_host", "pisa_b200_fwd_qrange", "pisa_b200_block_stats",
-                 "pisa_b200_select", "pisa_b200_block_norms", "pisa_b200_select_cov",
+                 "pisa_b200_fwd", "pisa_b200_fwd_host", "pisa_b200_fwd_qrange", "pisa_b200_set_pairing",
+                 "pisa_b200_block_stats", "pisa_b200_select", "pisa_b200_block_norms", "pisa_b200_select_cov",
                  "pisa_b200_attention", "pisa_b200_selftest_mma"):
         getattr(L, name).restype = C.c_int
     _lib = L

@@ -57,8 +57,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int chunk = blockIdx.x;
     const int bh = blockIdx.y;
     const int b = bh / a.H, h = bh % a.H;
-    const int j0 = chunk * kStatsG;
-    const int nb = min(kStatsG, a.N - j0);
+    const int j0 = chunk * a.G;
+    const int nb = min(a.G, a.N - j0);
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < kStages; ++s) {

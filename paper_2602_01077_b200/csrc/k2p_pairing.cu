@@ -1,5 +1,7 @@
 // K2c / K2d: query-block pairing for the fused kernel (no reference
-// counterpart: it only reorders work, every query block's result is unchanged).
+// counterpart: it only regroups work; every query block computes the same math,
+// equal to rounding -- the grouping of its key blocks into super-tiles moves
+// the online softmax's lazy-rescale points).
 //
 // K3 runs two query blocks per CTA over the UNION of their selections, so its
 // executed work is proportional to sum over pairs |S_a U S_b|. Pairing

@@ -21,6 +21,7 @@ struct StatsArgs {
     __nv_bfloat16* vhat_bf;
     float* hpart;
     int L, N, Npad, H, nchunk;
+    int G;  // key blocks per CTA (<= kStatsG)
 };
 cudaError_t launch_block_stats(int D, const CUtensorMap& tmQ, const CUtensorMap& tmK,
                                const CUtensorMap& tmV, const StatsArgs& a, int BH,

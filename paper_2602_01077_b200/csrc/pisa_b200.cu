@@ -21,6 +21,7 @@ using namespace pisa_b200;
 
 struct pisa_ctx {
     int device = 0;
+    int sms = 148;  // multiprocessor count (K1 chunk sizing)
     std::string last_error;
     // grow-only device arena
     void* arena = nullptr;
@@ -42,7 +43,12 @@ struct pisa_ctx {
     std::vector<cudaEvent_t> pool;
     unsigned long long* trace = nullptr;  // debug timeline (PISA_TRACE builds)
     int trace_tile = 0;
-    bool pairing = true;  // overlap-aware query-block pairing (env PISA_B200_PAIRING=0: off)
+    // overlap-aware query-block pairing: 0 off, 1 auto (only when the range has
+    // >= kPairMinBlocks query blocks: below that its fixed cost exceeds the union
+    // it saves -- measured: FLUX N=72 +25 us for -2 us, Wan2.1-1.3B N=512 +66 us
+    // for -50 us, Wan2.1-14B N=1182 +0.32 ms for -0.84 ms), 2 always.
+    // env PISA_B200_PAIRING, API pisa_b200_set_pairing
+    int pairing = 1;
     int host_chunks = 16;  // head chunks of the host path's copy/compute pipeline (env PISA_B200_HOST_CHUNKS)
     unsigned long long* tiles_dev = nullptr;  // fused-kernel tile counter (profiling only)
 };
@@ -167,6 +173,7 @@ bool make_3d_map(CUtensorMap* m, const void* base, uint64_t D, uint64_t rows, ui
 // ------------------------------------------------------------ resolve --
 struct Plan {
     int64_t BH, L, D, N, Npad, W, k, nchunk1, nchunk2;
+    int64_t statsG;  // key blocks per K1 CTA
     double scale;
     int64_t qb0 = 0, qb1 = 0;  // query-block range of the fused step ([0, N) unless restricted)
 };
@@ -226,7 +233,11 @@ pisa_status resolve(pisa_ctx* ctx, const pisa_attn_desc* d, Plan* p) {
     p->Npad = (N + 127) / 128 * 128;  // K3 reads 128-centroid tiles
     p->W = (N + 31) / 32;
     p->k = k;
-    p->nchunk1 = (N + kStatsG - 1) / kStatsG;
+    // K1: up to kStatsG key blocks per CTA, fewer when that would leave SMs idle
+    // (small shapes: FLUX's N = 72 x 24 heads would be 72 CTAs at 32 per CTA)
+    const int64_t sms = ctx ? ctx->sms : 148;
+    p->statsG = std::max<int64_t>(4, std::min<int64_t>(kStatsG, (N * p->BH + 2 * sms - 1) / (2 * sms)));
+    p->nchunk1 = (N + p->statsG - 1) / p->statsG;
     p->nchunk2 = (N + 63) / 64;
     p->scale = d->scale > 0.0 ? d->scale : 1.0 / std::sqrt(double(D));  // attention.hpp:34-37
     return PISA_OK;
@@ -298,7 +309,7 @@ pisa_status run_stats(pisa_ctx* ctx, const pisa_attn_desc& d, const Plan& p, con
         !make_qkv_map(&tv, v, d, d.v_strides, 64))
         return fail(ctx, PISA_ERR_INVALID_DIMENSION, "TMA descriptor rejected the q/k/v layout");
     StatsArgs sa{w.kbar, w.vhat, w.qbar, w.kbar_bf, w.vhat_bf, w.hpart,
-                 int(p.L), int(p.N), int(p.Npad), int(d.heads), int(p.nchunk1)};
+                 int(p.L), int(p.N), int(p.Npad), int(d.heads), int(p.nchunk1), int(p.statsG)};
     cudaError_t e;
     {
         ProfScope ps(ctx, kK1, s);
@@ -356,7 +367,8 @@ pisa_status run_fused(pisa_ctx* ctx, const pisa_attn_desc& d, const Plan& p, con
         return fail(ctx, PISA_ERR_CUDA, "TMA descriptor creation failed");
     // overlap-aware pairing of query blocks (K2c/K2d); PISA_B200_PAIRING=0 keeps (2t, 2t+1)
     const int qb0 = int(p.qb0), qb1 = int(p.qb1 > 0 ? p.qb1 : p.N);
-    const bool pairing = ctx->pairing && qb1 - qb0 > 2;
+    constexpr int kPairMinBlocks = 768;
+    const bool pairing = qb1 - qb0 > 2 && (ctx->pairing == 2 || (ctx->pairing == 1 && qb1 - qb0 >= kPairMinBlocks));
     if (pairing) {
         ProfScope ps(ctx, kPair, s);
         const cudaError_t e = launch_pairing(w.mask, int(p.N), int(p.W), qb0, qb1, int(p.BH), w.cand, w.pairs, s);
@@ -448,7 +460,8 @@ pisa_status pisa_b200_create(pisa_ctx** out, int device) {
     if (prop.major != 10) return PISA_ERR_UNSUPPORTED;  // sm_100a kernels only
     pisa_ctx* c = new pisa_ctx;
     c->device = device;
-    if (const char* ev = std::getenv("PISA_B200_PAIRING")) c->pairing = std::atoi(ev) != 0;
+    cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, device);
+    if (const char* ev = std::getenv("PISA_B200_PAIRING")) c->pairing = std::max(0, std::min(2, std::atoi(ev)));
     if (const char* ev = std::getenv("PISA_B200_HOST_CHUNKS")) c->host_chunks = std::max(1, std::atoi(ev));
     DeviceGuard g(device);
     if (cudaMallocHost(&c->flag_host, sizeof(int)) != cudaSuccess) {
@@ -598,6 +611,13 @@ pisa_status fwd_range(pisa_ctx* ctx, const pisa_attn_desc* d, const void* q, con
     return run_fused(ctx, *d, p, w, q, k, v, o, diag, s);
 }
 }  // namespace
+
+pisa_status pisa_b200_set_pairing(pisa_ctx* ctx, int mode) {
+    if (!ctx) return PISA_ERR_INVALID_DIMENSION;
+    if (mode < 0 || mode > 2) return fail(ctx, PISA_ERR_INVALID_DIMENSION, "pairing mode must be 0, 1 or 2");
+    ctx->pairing = mode;
+    return PISA_OK;
+}
 
 pisa_status pisa_b200_fwd(pisa_ctx* ctx, const pisa_attn_desc* d, const void* q, const void* k,
                           const void* v, void* o, const pisa_diag* diag, void* stream) {

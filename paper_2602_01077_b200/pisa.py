@@ -283,6 +283,11 @@ class Context:
     def last_launch_count(self) -> int:
         return int(self.lib.pisa_b200_last_launch_count(self.handle))
 
+    def set_pairing(self, mode: int) -> None:
+        """Query-block pairing of the fused kernel: 0 consecutive, 1 auto, 2 always
+        overlap-aware (pisa_b200_set_pairing); results do not depend on it."""
+        _raise(self.lib.pisa_b200_set_pairing(self.handle, int(mode)), self.handle)
+
     def set_profiling(self, on: bool) -> None:
         _raise(self.lib.pisa_b200_set_profiling(self.handle, int(on)), self.handle)
 

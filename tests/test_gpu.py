@@ -472,10 +472,12 @@ def test_cpp_shim_drop_in(P, oracle_mod, tmp_path):
 
 
 # ----------------------------------- (head x query-block range) sharding (§8e) --
-def test_qrange_pieces_reassemble_bitwise(P, oracle_mod):
+def test_qrange_pieces_reassemble(P, oracle_mod):
     """Eight simulated ranks over 3 heads (ragged L = 1000, N = 16): each runs
     pisa_b200_fwd_qrange on its (head, query-block range) pieces; the assembled
-    output, diagnostics and plan equal the full call's bit for bit."""
+    output equals the full call's to rounding (pieces may pair query blocks
+    differently, which moves the online softmax's lazy-rescale points), rows
+    outside a range are untouched."""
     import torch
 
     from paper_2602_01077_b200.sharding import fwd_pieces, unit_qblock_pieces
@@ -486,19 +488,54 @@ def test_qrange_pieces_reassemble_bitwise(P, oracle_mod):
     for r in range(8):
         fwd_pieces(q, k, v, out, unit_qblock_pieces(1, 3, 16, 8, r), **kw)
     torch.cuda.synchronize()
-    assert torch.equal(out, full)
+    assert not torch.isnan(out).any()
+    assert (out.float() - full.float()).abs().max().item() <= 4e-3
     # a single range: rows outside it are untouched, rows inside equal the full call
     part = torch.zeros_like(full)
     P.fwd(q, k, v, part, q_blocks=(5, 11), **kw)
     torch.cuda.synchronize()
-    assert torch.equal(part[:, :, 5 * 64:11 * 64], full[:, :, 5 * 64:11 * 64])
+    assert (part[:, :, 5 * 64:11 * 64].float() - full[:, :, 5 * 64:11 * 64].float()).abs().max().item() <= 4e-3
     assert not part[:, :, :5 * 64].any() and not part[:, :, 11 * 64:].any()
     # the ragged last block alone, and a lone first block
     for rng in ((15, 16), (0, 1)):
         part.zero_()
         P.fwd(q, k, v, part, q_blocks=rng, **kw)
         torch.cuda.synchronize()
-        assert torch.equal(part[:, :, rng[0] * 64:rng[1] * 64], full[:, :, rng[0] * 64:rng[1] * 64])
+        sl = slice(rng[0] * 64, rng[1] * 64)
+        assert (part[:, :, sl].float() - full[:, :, sl].float()).abs().max().item() <= 4e-3
     for bad in ((3, 3), (-1, 4), (0, 17), (12, 5)):
         with pytest.raises(P.InvalidDimension):
             P.fwd(q, k, v, part, q_blocks=bad, **kw)
+
+
+def test_pairing_modes_agree_and_fewer_tiles(P, oracle_mod):
+    """Overlap-aware query-block pairing only regroups work: the plan is bitwise
+    identical with it forced on or off, the outputs agree to rounding (a block's
+    key blocks are grouped into super-tiles differently, so the online softmax's
+    lazy-rescale points move), and on multi-cluster routing where alike blocks
+    are far apart it executes fewer union tiles."""
+    import torch
+    q, k, v = (dev_bf16(x) for x in oracle_mod.gen("clustered", 31, 2, 4096, 128))
+    # shuffle query blocks so that blocks routing alike are not neighbours
+    perm = torch.randperm(64, generator=torch.Generator().manual_seed(3))
+    q = q.view(1, 2, 64, 64, 128)[:, :, perm].reshape(1, 2, 4096, 128).contiguous()
+    ctx = P.Context.get(0)
+    outs, tiles = [], []
+    try:
+        for mode in (0, 2):
+            ctx.set_pairing(mode)
+            ctx.set_profiling(True)
+            ctx.fused_tiles()
+            o, ex = P.fwd(q, k, v, sparsity=0.875, return_plan=True)
+            torch.cuda.synchronize()
+            tiles.append(ctx.fused_tiles())
+            ctx.set_profiling(False)
+            outs.append((o, ex["selected"]))
+    finally:
+        ctx.set_pairing(1)
+        ctx.set_profiling(False)
+    assert torch.equal(outs[0][1], outs[1][1])
+    assert (outs[0][0].float() - outs[1][0].float()).abs().max().item() <= 4e-3
+    assert tiles[1] < tiles[0], tiles
+    with pytest.raises(P.InvalidDimension):
+        ctx.set_pairing(3)
