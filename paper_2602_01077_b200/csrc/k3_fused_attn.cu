@@ -253,13 +253,24 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_init(&bar.p_half[s], 8);  // (PISA_PSPLIT) first sub-tile of P
         }
         fence_mbar_init();
-        tma_prefetch(&tmQ);
         tma_prefetch(&tmK);
         tma_prefetch(&tmV);
+        // Q first: it needs nothing but its barrier, so its 16 TMA boxes go out
+        // before the CTA barrier (they used to sit on the prologue's critical
+        // path). Interleaved row order: the 16-row chunk (quadrant q4, block hh)
+        // of the tile lands at shared-memory / TMEM rows q4*32 + hh*16.
+        mbar_expect_tx(&bar.q_full, Cfg::kQ);
+#pragma unroll
+        for (int half = 0; half < D / 64; ++half)
+#pragma unroll
+            for (int c = 0; c < 8; ++c)
+                tma_load_4d(smem + Cfg::kOffQ + half * 16384 + c * 2048, &tmQ, &bar.q_full, half * 64,
+                            ((c & 1) && hasB ? iB : iA) * 64 + (c >> 1) * 16, h, b);
     }
     if (warp == 2) {
         tmem_alloc(&bar.tmem_base, 512);
         tmem_relinquish();
+        TRACE(12, 0);  // (trace builds) prologue: TMEM allocated
     }
     if (warp == 3) {
         // selection bitmasks of the two query blocks into shared memory, and the
@@ -268,14 +279,24 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t* mA = a.mask + (size_t(bh) * a.N + iA) * a.W;
         const uint32_t* mB = a.mask + (size_t(bh) * a.N + iB) * a.W;
         uint32_t nab = 0, na = 0, nb = 0;
-        for (int w = lane; w < a.W; w += 32) {
-            const uint32_t wa = mA[w];
-            const uint32_t wb = hasB ? mB[w] : 0u;
-            maskA[w] = wa;
-            maskB[w] = wb;
-            nab += __popc(wa & wb);
-            na += __popc(wa & ~wb);
-            nb += __popc(wb & ~wa);
+        // all loads in flight at once (one L2 round trip; W <= 128 for N <= 4096)
+        uint32_t ra[4], rb[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int w = lane + 32 * i;
+            ra[i] = w < a.W ? __ldcg(mA + w) : 0u;
+            rb[i] = (w < a.W && hasB) ? __ldcg(mB + w) : 0u;
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int w = lane + 32 * i;
+            if (w < a.W) {
+                maskA[w] = ra[i];
+                maskB[w] = rb[i];
+            }
+            nab += __popc(ra[i] & rb[i]);
+            na += __popc(ra[i] & ~rb[i]);
+            nb += __popc(rb[i] & ~ra[i]);
         }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
@@ -288,10 +309,12 @@ __global__ void __launch_bounds__(kThreads, 1)
             bar.n_a = na;
             bar.n_b = nb;
         }
+        TRACE(13, 0);  // masks copied, union sized
     }
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
+    if (warp == 0) TRACE(14, 0);  // CTA barrier passed
     const uint32_t tmem = bar.tmem_base;
     const int nAB = int(bar.n_ab), nAo = int(bar.n_a), nBo = int(bar.n_b);
     // Key tiles are processed in pairs ("super-tiles" of 128 keys): one K / V
@@ -409,18 +432,6 @@ __global__ void __launch_bounds__(kThreads, 1)
 
     if (warp == 0) {
         // ------------------------------------------------ producer: Q, K, H --
-        if (elect_one()) {
-            // Interleaved row order: the 16-row chunk (quadrant q4, block hh) of
-            // the tile lands at shared-memory / TMEM rows q4*32 + hh*16.
-            mbar_expect_tx(&bar.q_full, Cfg::kQ);
-#pragma unroll
-            for (int half = 0; half < D / 64; ++half)
-#pragma unroll
-                for (int c = 0; c < 8; ++c)
-                    tma_load_4d(smem + Cfg::kOffQ + half * 16384 + c * 2048, &tmQ, &bar.q_full, half * 64,
-                                ((c & 1) && hasB ? iB : iA) * 64 + (c >> 1) * 16, h, b);
-        }
-        __syncwarp();
         // K stage of S_g is free once S_{g-kSK} is done: s_full of that S
         // (no separate "empty" commit; S_{g-kSK+3} cannot complete before K_g is
         // loaded, so the parity is unambiguous)
@@ -546,6 +557,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         };
         if (a.tile_count && lane == 0) atomicAdd(a.tile_count, (unsigned long long)(2 * G));
         mma_wait(&bar.q_full, 0);
+        TRACE(15, 0);  // Q landed
         tc_fence_after();
         for (int g = 0; g < kSB && g < G; ++g) {
             mma_wait(&bar.k_full[sk], phk);
