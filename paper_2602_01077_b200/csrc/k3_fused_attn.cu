@@ -445,9 +445,12 @@ __global__ void __launch_bounds__(kThreads, 1)
             wait_s_done(g - kSK);
             const bool exact = g < G1;
             int r0, r1;
+            if (g == 0) TRACE(12, 1);
             tile_rows(cur, g, r0, r1);
+            if (g == 0) TRACE(13, 1);
             if (elect_one()) {
                 mbar_expect_tx(&bar.k_full[s], Cfg::kKV);
+                if (g == 0) TRACE(14, 1);
 #pragma unroll
                 for (int half = 0; half < D / 64; ++half) {
                     if (exact) {

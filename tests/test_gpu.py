@@ -275,6 +275,24 @@ def test_fused_matches_oracle(P, oracle_mod, variant, kind, H, L, d, r):
             np.testing.assert_allclose(et_gpu, et * np.exp(m), rtol=3e-2)
 
 
+@pytest.mark.parametrize("L,d,r", [(1, 128, 0.5), (17, 64, 0.5), (64, 128, 0.0), (65, 128, 0.5),
+                                   (127, 64, 0.5), (130, 128, 0.6), (200, 64, 0.99)])
+def test_tiny_and_ragged_lengths(P, oracle_mod, L, d, r):
+    """Degenerate shapes: one block (N = 1), a last block of 1 row (L = 65),
+    N = 2..4, k = 1 (r = 0.99), all variants' code paths through Hybrid."""
+    O = oracle_mod
+    q, k, v = O.gen("gaussian", 7, 2, L, d)
+    out, ex = run_fwd(P, q, k, v, sparsity=r)
+    scale = d ** -0.5
+    for h in range(2):
+        st = O.block_stats(k[h], v[h])
+        ref_sel = O.select_plain(O.query_means(q[h]), st[0], ex["selected"].shape[-1], scale)
+        assert np.array_equal(ex["selected"][h], ref_sel)
+        ref = O.pisa_attention(q[h], k[h], v[h], ex["selected"][h], st, scale, "hybrid")[0]
+        assert np.isfinite(out[h]).all()
+        assert float(np.abs(out[h] - ref).max()) <= ATOL
+
+
 @pytest.mark.parametrize("path", sorted(glob.glob(os.path.join(GOLDEN, "*_h*_l*.npz"))),
                          ids=lambda p: os.path.basename(p)[:-4])
 def test_fused_matches_reference_golden(P, path):

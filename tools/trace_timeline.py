@@ -37,7 +37,8 @@ def main():
     ds = [tr[2][t + 1] - tr[2][t] for t in range(20, n - 30)]
     print("median S-issue period (cycles):", sorted(ds)[len(ds) // 2] if ds else None)
     print(f"prologue (cycles from CTA start): TMEM alloc {tr[12][0]}, masks {tr[13][0]}, "
-          f"CTA barrier {tr[14][0]}, Q landed {tr[15][0]}, first K issued {tr[0][0]}, first S issued {tr[2][0]}")
+          f"CTA barrier {tr[14][0]}, Q landed {tr[15][0]}, first K issued {tr[0][0]}, first S issued {tr[2][0]}; "
+          f"K producer: loop entry {tr[12][1]}, rows {tr[13][1]}, expect_tx {tr[14][1]}")
     # per-warp P publish (roles 16..23: warpgroup A warps q4 = 0..3, then B) and
     # rescales (roles 24..31), relative to the warpgroup's q4 = 0 warp
     print("\nper-warp P publish - q4=0 warp (A: q4=1..3 | B: q4=1..3), rescale marks R")
