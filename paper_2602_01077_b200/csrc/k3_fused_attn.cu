@@ -613,6 +613,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                            hdesc0 + uint64_t((ks * 2048) >> 4), idQH, ks != 0);
             }
             mma_commit(&bar.qh_full);  // also: every PV done
+            TRACE(12, 2);  // (trace builds) tail: QH issued
         }
         __syncwarp();
     } else if (warp >= 4) {
@@ -808,6 +809,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         // ------------------------------------------------------- epilogue --
         mbar_wait(&bar.qh_full, 0);
         tc_fence_after();
+        if (warp == 4) TRACE(13, 2);  // tail: O and QH complete
         float mrow = m;
         float lfin = l + __shfl_xor_sync(0xffffffffu, l, 16);
         float ltot = lt + __shfl_xor_sync(0xffffffffu, lt, 16);
@@ -882,6 +884,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             if (bad && a.nonfinite) atomicExch(a.nonfinite, 1);
         }
+        if (warp == 4) TRACE(14, 2);  // tail: this warp's rows stored
     }
     tc_fence_before();
     __syncthreads();

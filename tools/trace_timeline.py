@@ -39,6 +39,9 @@ def main():
     print(f"prologue (cycles from CTA start): TMEM alloc {tr[12][0]}, masks {tr[13][0]}, "
           f"CTA barrier {tr[14][0]}, Q landed {tr[15][0]}, first K issued {tr[0][0]}, first S issued {tr[2][0]}; "
           f"K producer: loop entry {tr[12][1]}, rows {tr[13][1]}, expect_tx {tr[14][1]}")
+    last = max(t for t in range(1024) if tr[3][t])
+    print(f"tail: last PV issued {tr[3][last]} (t={last}), QH issued {tr[12][2]}, O+QH complete {tr[13][2]}, "
+          f"epilogue stored {tr[14][2]}")
     # per-warp P publish (roles 16..23: warpgroup A warps q4 = 0..3, then B) and
     # rescales (roles 24..31), relative to the warpgroup's q4 = 0 warp
     print("\nper-warp P publish - q4=0 warp (A: q4=1..3 | B: q4=1..3), rescale marks R")
