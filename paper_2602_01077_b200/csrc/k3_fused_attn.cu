@@ -624,7 +624,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int ch = lane >> 4;        // column half of a 64-key sub-tile
         const float sl2 = a.scale * 1.4426950408889634f;
         const uint32_t lbase = tmem + (uint32_t(q4 * 32 + hh * 16) << 16);
-        const int qblk = hh ? iB : iA;  // iB < 0: lone last block, its half is idle
+        // no partner (a lone last block, or iB outside a query-block range):
+        // warpgroup B is idle and writes nothing
+        const int qblk = hh ? (hasB ? iB : -1) : iA;
         const int grow = qblk * 64 + q4 * 16 + r16;
         const bool active = qblk >= 0 && grow < a.L;
         const bool wact = __all_sync(0xffffffffu, active);

@@ -521,6 +521,18 @@ def test_qrange_pieces_reassemble(P, oracle_mod):
         torch.cuda.synchronize()
         sl = slice(rng[0] * 64, rng[1] * 64)
         assert (part[:, :, sl].float() - full[:, :, sl].float()).abs().max().item() <= 4e-3
+    # odd-length ranges: the last block's would-be partner lies outside the
+    # range and must not be written (also with f32 output and diagnostics)
+    for rng in ((0, 1), (4, 7), (9, 12)):
+        part = torch.zeros_like(full)
+        P.fwd(q, k, v, part, q_blocks=rng, **kw)
+        part32 = torch.zeros(full.shape, dtype=torch.float32, device=full.device)
+        P.fwd(q, k, v, part32, q_blocks=rng, out_dtype=torch.float32, **kw)
+        torch.cuda.synchronize()
+        sl = slice(rng[0] * 64, rng[1] * 64)
+        for o in (part, part32):
+            assert (o[:, :, sl].float() - full[:, :, sl].float()).abs().max().item() <= 4e-3
+            assert not o[:, :, :rng[0] * 64].any() and not o[:, :, rng[1] * 64:].any(), rng
     for bad in ((3, 3), (-1, 4), (0, 17), (12, 5)):
         with pytest.raises(P.InvalidDimension):
             P.fwd(q, k, v, part, q_blocks=bad, **kw)
