@@ -53,8 +53,6 @@
 // units), and the two blocks' online softmaxes run in parallel. exp2 with
 // log2(e)*scale folded into one FFMA; lazy rescale of O (only when the running
 // max grows by > 2^8); P written back to TMEM as bf16 over its S columns.
-#include <algorithm>
-
 #include "kernels.h"
 #include "sm100.cuh"
 
@@ -98,8 +96,6 @@ constexpr uint32_t kPolyMask = PISA_POLY_MASK;
 #define PISA_SOFTMAX_NS 32
 #endif
 constexpr bool kSoftmaxSpin = PISA_SOFTMAX_SPIN != 0;
-constexpr int kRegsProducer = 80;   // setmaxnreg budgets (multiples of 8)
-constexpr int kRegsSoftmax = 208;
 __device__ __forceinline__ void softmax_wait(uint64_t* bar, uint32_t parity) {
 #if PISA_SOFTMAX_SPIN == 2
     mbar_wait_backoff<PISA_SOFTMAX_NS>(bar, parity);
@@ -159,7 +155,7 @@ struct FusedCfg {
 };
 
 struct Bars {
-    uint64_t q_full, h_full, qh_full, mask_ready, mask_free, o_free;
+    uint64_t q_full, h_full, qh_full;
     uint64_t k_full[kSK], v_full[kSV], v_empty[kSV];
     uint64_t s_full[kSB], p_full[kSB], p_half[kSB];
     uint32_t tmem_base;
@@ -169,11 +165,11 @@ static_assert(sizeof(Bars) <= 512, "barrier block");
 
 #if PISA_TRACE
 // Timeline of one CTA: trace[role][t] = clock64 delta from kernel start.
-__device__ __forceinline__ void trace_mark(const FusedArgs& a, int role, int t, long long t0, int it) {
-    if (a.trace && blockIdx.x == a.trace_tile && it == 0 && t < 1024)
+__device__ __forceinline__ void trace_mark(const FusedArgs& a, int role, int t, long long t0) {
+    if (a.trace && blockIdx.x == a.trace_tile && blockIdx.y == 0 && t < 1024)
         a.trace[role * 1024 + t] = (unsigned long long)(clock64() - t0);
 }
-#define TRACE(role, t) trace_mark(a, role, t, tstart, tr_it)
+#define TRACE(role, t) trace_mark(a, role, t, tstart)
 #else
 #define TRACE(role, t) ((void)0)
 #endif
@@ -225,61 +221,27 @@ __global__ void __launch_bounds__(kThreads, 1)
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
-    // Persistent over tiles: CTA c runs tiles c, c + gridDim.x, ... of the
-    // (batch*head, query-block pair) space (one tile per CTA when the grid
-    // covers them all). Rings, TMEM and barriers live across tiles; per-tile
-    // hand-offs: mask_ready / mask_free (selection masks + union sizes, loaded
-    // by warp 3 while the previous tile finishes), q_full / h_full / qh_full
-    // (parity = tile iteration & 1), o_free (the epilogue has read O and QH).
-    const int tpb = (a.qb1 - a.qb0 + 1) >> 1;  // tiles per (batch, head)
-    const int total = tpb * a.BH;
+    const int tile = blockIdx.x;
+    const int bh = blockIdx.y;
+    const int b = bh / a.H, h = bh % a.H;
+    // query blocks of this tile (within the range [qb0, qb1)): the pairing
+    // kernel's choice, or consecutive blocks
+    int iA = a.qb0 + 2 * tile, iB = iA + 1;
+    if (a.pairs) {
+        const int2 pr = a.pairs[size_t(bh) * ((a.N + 1) / 2) + tile];
+        iA = pr.x;
+        iB = pr.y;
+    }
+    const bool hasB = iB >= 0 && iB < a.qb1;
     const bool tail = a.variant != 0;                       // Zeroth, Hybrid, GlobalCentroid
     const bool first_order = a.variant == 3 || a.variant == 4;
     const int n_last = a.L - (a.N - 1) * 64;
-    int tr_it = 0;  // tile iteration (trace builds record the first)
-    (void)tr_it;
-    struct TileId {
-        int bh, b, h, iA, iB;
-        bool hasB;
-    };
-    // query blocks of tile t (within the range [qb0, qb1)): the pairing
-    // kernel's choice, or consecutive blocks
-    auto tile_id = [&](int t) -> TileId {
-        TileId x;
-        x.bh = t / tpb;
-        const int tile = t - x.bh * tpb;
-        x.b = x.bh / a.H;
-        x.h = x.bh % a.H;
-        x.iA = a.qb0 + 2 * tile;
-        x.iB = x.iA + 1;
-        if (a.pairs) {
-            const int2 pr = a.pairs[size_t(x.bh) * ((a.N + 1) / 2) + tile];
-            x.iA = pr.x;
-            x.iB = pr.y;
-        }
-        x.hasB = x.iB >= 0 && x.iB < a.qb1;
-        return x;
-    };
-    auto issue_q = [&](const TileId& T) {  // one thread: Q of tile T (16 TMA boxes)
-        // Interleaved row order: the 16-row chunk (quadrant q4, block hh) of
-        // the tile lands at shared-memory / TMEM rows q4*32 + hh*16.
-        mbar_expect_tx(&bar.q_full, Cfg::kQ);
-#pragma unroll
-        for (int half = 0; half < D / 64; ++half)
-#pragma unroll
-            for (int c = 0; c < 8; ++c)
-                tma_load_4d(smem + Cfg::kOffQ + half * 16384 + c * 2048, &tmQ, &bar.q_full, half * 64,
-                            ((c & 1) && T.hasB ? T.iB : T.iA) * 64 + (c >> 1) * 16, T.h, T.b);
-    };
 
     // ------------------------------------------------------------ setup --
     if (threadIdx.x == 0) {
         mbar_init(&bar.q_full, 1);
         mbar_init(&bar.h_full, 1);
         mbar_init(&bar.qh_full, 1);
-        mbar_init(&bar.mask_ready, 32);             // warp 3, every lane
-        mbar_init(&bar.mask_free, 1 + D / 64 + 8);  // K producer, V producers, softmax warps
-        mbar_init(&bar.o_free, 8);                  // softmax warps
         for (int s = 0; s < kSK; ++s) mbar_init(&bar.k_full[s], 1);
         for (int s = 0; s < kSV; ++s) {
             mbar_init(&bar.v_full[s], D / 64);  // one arrive per V producer (one per 64-col half)
@@ -293,20 +255,68 @@ __global__ void __launch_bounds__(kThreads, 1)
         fence_mbar_init();
         tma_prefetch(&tmK);
         tma_prefetch(&tmV);
-        // Q of the first tile before the CTA barrier: it needs nothing but its
-        // barrier (later tiles' Q is loaded by warp 0 once the previous QH is done)
-        if (int(blockIdx.x) < total) issue_q(tile_id(blockIdx.x));
+        // Q first: it needs nothing but its barrier, so its 16 TMA boxes go out
+        // before the CTA barrier (they used to sit on the prologue's critical
+        // path). Interleaved row order: the 16-row chunk (quadrant q4, block hh)
+        // of the tile lands at shared-memory / TMEM rows q4*32 + hh*16.
+        mbar_expect_tx(&bar.q_full, Cfg::kQ);
+#pragma unroll
+        for (int half = 0; half < D / 64; ++half)
+#pragma unroll
+            for (int c = 0; c < 8; ++c)
+                tma_load_4d(smem + Cfg::kOffQ + half * 16384 + c * 2048, &tmQ, &bar.q_full, half * 64,
+                            ((c & 1) && hasB ? iB : iA) * 64 + (c >> 1) * 16, h, b);
     }
     if (warp == 2) {
         tmem_alloc(&bar.tmem_base, 512);
         tmem_relinquish();
         TRACE(12, 0);  // (trace builds) prologue: TMEM allocated
     }
+    if (warp == 3) {
+        // selection bitmasks of the two query blocks into shared memory, and the
+        // sizes of the three parts of their union (A&B, A only, B only; every
+        // consumer walks them itself with a UnionCursor)
+        const uint32_t* mA = a.mask + (size_t(bh) * a.N + iA) * a.W;
+        const uint32_t* mB = a.mask + (size_t(bh) * a.N + iB) * a.W;
+        uint32_t nab = 0, na = 0, nb = 0;
+        // all loads in flight at once (one L2 round trip; W <= 128 for N <= 4096)
+        uint32_t ra[4], rb[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int w = lane + 32 * i;
+            ra[i] = w < a.W ? __ldcg(mA + w) : 0u;
+            rb[i] = (w < a.W && hasB) ? __ldcg(mB + w) : 0u;
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int w = lane + 32 * i;
+            if (w < a.W) {
+                maskA[w] = ra[i];
+                maskB[w] = rb[i];
+            }
+            nab += __popc(ra[i] & rb[i]);
+            na += __popc(ra[i] & ~rb[i]);
+            nb += __popc(rb[i] & ~ra[i]);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            nab += __shfl_xor_sync(0xffffffffu, nab, o);
+            na += __shfl_xor_sync(0xffffffffu, na, o);
+            nb += __shfl_xor_sync(0xffffffffu, nb, o);
+        }
+        if (lane == 0) {
+            bar.n_ab = nab;
+            bar.n_a = na;
+            bar.n_b = nb;
+        }
+        TRACE(13, 0);  // masks copied, union sized
+    }
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
     if (warp == 0) TRACE(14, 0);  // CTA barrier passed
     const uint32_t tmem = bar.tmem_base;
+    const int nAB = int(bar.n_ab), nAo = int(bar.n_a), nBo = int(bar.n_b);
     // Key tiles are processed in pairs ("super-tiles" of 128 keys): one K / V
     // stage, one S buffer, one barrier round trip and N=128 S MMAs per pair.
     // Phase 1 walks the union of the two selections in the order PISA_BALANCED
@@ -316,40 +326,19 @@ __global__ void __launch_bounds__(kThreads, 1)
     // with a copy of the previous entry whose use flags are zero (fully
     // masked: P = 0 and finite V rows).
     // Phase 2 pairs consecutive centroid chunks.
-    struct Counts {
-        int G1, G, gAB, nPair, kPairX, kPairR;
-        bool restA;
-    };
-    auto counts = [&]() -> Counts {  // of the current tile (after mask_ready)
-        const int nAB = int(bar.n_ab), nAo = int(bar.n_a), nBo = int(bar.n_b);
-        Counts c;
-        c.gAB = (nAB + 1) >> 1;
-        const int nX = min(nAo, nBo);
-        const int nR = max(nAo, nBo) - nX;
+    const int gAB = (nAB + 1) >> 1;
+    const int nX = min(nAo, nBo);
+    const int nR = max(nAo, nBo) - nX;
 #if PISA_BALANCED == 2
-        const int gA = (nAo + 1) >> 1, gB = (nBo + 1) >> 1;
-        c.G1 = c.gAB + gA + gB;
-        c.kPairX = nAo;
-        c.kPairR = nBo;
+    const int gA = (nAo + 1) >> 1, gB = (nBo + 1) >> 1;
+    const int G1 = gAB + gA + gB;
 #elif PISA_BALANCED
-        c.G1 = c.gAB + nX + ((nR + 1) >> 1);
-        c.kPairX = nX;
-        c.kPairR = nR;
+    const int G1 = gAB + nX + ((nR + 1) >> 1);
 #else
-        const int nU = nAB + nAo + nBo;
-        c.G1 = (nU + 1) >> 1;
-        c.kPairX = nX;
-        c.kPairR = nR;
+    const int nU = nAB + nAo + nBo;
+    const int G1 = (nU + 1) >> 1;
 #endif
-#if !PISA_BALANCED
-        c.nPair = nU;  // the union cursor's count (pair() reads it as nAB)
-#else
-        c.nPair = nAB;
-#endif
-        c.restA = nAo > nBo;
-        c.G = c.G1 + (tail ? (a.nchunk2 + 1) >> 1 : 0);
-        return c;
-    };
+    const int G = G1 + (tail ? (a.nchunk2 + 1) >> 1 : 0);
     // entry = block index | (selected by query block A) << 14 | (by B) << 15
     struct BitStream {
         const uint32_t* ma;
@@ -417,181 +406,104 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
         }
     };
-    auto tile_rows = [&](UnionCursor& cur, const Counts& C, int g, int& r0, int& r1) {
-        if (g < C.G1) {
+    const bool restA = nAo > nBo;
+#if PISA_BALANCED == 2
+    const int kPairX = nAo, kPairR = nBo;
+#else
+    const int kPairX = nX, kPairR = nR;
+#endif
+#if !PISA_BALANCED
+    const int nPair = nU;  // the union cursor's count (pair() reads it as nAB)
+#else
+    const int nPair = nAB;
+#endif
+    auto tile_rows = [&](UnionCursor& cur, int g, int& r0, int& r1) {
+        if (g < G1) {
             uint32_t e0, e1;
-            cur.pair(g, C.gAB, C.nPair, C.kPairX, C.kPairR, C.restA, e0, e1);
+            cur.pair(g, gAB, nPair, kPairX, kPairR, restA, e0, e1);
             r0 = int(e0 & 0x3FFFu) * 64;
             r1 = int(e1 & 0x3FFFu) * 64;
         } else {
-            const int c = 2 * (g - C.G1);
+            const int c = 2 * (g - G1);
             r0 = c * 64;
             r1 = (c + 1 < a.nchunk2 ? c + 1 : c) * 64;
         }
     };
 
-    // Register budget per warpgroup: the producer / MMA warpgroup (warps 0-3)
-    // needs few, the two softmax warpgroups (score tiles of 64 registers,
-    // online-softmax state, the union cursor) more than the 168 of an even
-    // split: 128 x 80 + 256 x 208 <= 64K.
-    // Each role branch starts with its warpgroup's setmaxnreg (ptxas applies
-    // the budget to the code the instruction dominates).
     if (warp == 0) {
-        asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(kRegsProducer));
         // ------------------------------------------------ producer: Q, K, H --
-        // K stage of S_j is free once S_{j-kSK} is done: s_full of that S (j:
-        // global S index; no separate "empty" commit, S_{j-kSK+3} cannot
-        // complete before K_j is loaded, so the parity is unambiguous)
+        // K stage of S_g is free once S_{g-kSK} is done: s_full of that S
+        // (no separate "empty" commit; S_{g-kSK+3} cannot complete before K_g is
+        // loaded, so the parity is unambiguous)
         auto wait_s_done = [&](int j) {
             if (j >= 0) mbar_wait(&bar.s_full[j % kSB], uint32_t((j / kSB) & 1));
         };
-        int s = 0;      // K ring position
-        int sbase = 0;  // global index of this tile's first S
-        int it = 0;
-        for (int t = blockIdx.x; t < total; t += gridDim.x, ++it) {
-            tr_it = it;
-            const TileId T = tile_id(t);
-            const int bh = T.bh, b = T.b, h = T.h, iA = T.iA, iB = T.iB;
-            const bool hasB = T.hasB;
-            (void)bh; (void)b; (void)h; (void)iA; (void)iB; (void)hasB;
-            if (it > 0) {
-                // Q of this tile once the previous tile's QH -- the last reader
-                // of Q, and of H_bar's K stage -- is done
-                mbar_wait(&bar.qh_full, uint32_t((it - 1) & 1));
-                if (elect_one()) issue_q(T);
-                __syncwarp();
-            }
-            mbar_wait(&bar.mask_ready, uint32_t(it & 1));
-            const Counts C = counts();
-            UnionCursor cur(maskA, maskB);
-            for (int g = 0; g < C.G; ++g) {
-                uint8_t* sK = smem + Cfg::kOffK + s * Cfg::kKV;
-                wait_s_done(sbase + g - kSK);
-                const bool exact = g < C.G1;
-                int r0, r1;
-                if (g == 0) TRACE(12, 1);
-                tile_rows(cur, C, g, r0, r1);
-                if (g == 0) TRACE(13, 1);
-                if (elect_one()) {
-                    mbar_expect_tx(&bar.k_full[s], Cfg::kKV);
-                    if (g == 0) TRACE(14, 1);
+        int s = 0;
+        UnionCursor cur(maskA, maskB);
+        for (int g = 0; g < G; ++g) {
+            uint8_t* sK = smem + Cfg::kOffK + s * Cfg::kKV;
+            wait_s_done(g - kSK);
+            const bool exact = g < G1;
+            int r0, r1;
+            if (g == 0) TRACE(12, 1);
+            tile_rows(cur, g, r0, r1);
+            if (g == 0) TRACE(13, 1);
+            if (elect_one()) {
+                mbar_expect_tx(&bar.k_full[s], Cfg::kKV);
+                if (g == 0) TRACE(14, 1);
 #pragma unroll
-                    for (int half = 0; half < D / 64; ++half) {
-                        if (exact) {
-                            tma_load_4d(sK + half * 16384, &tmK, &bar.k_full[s], half * 64, r0, h, b);
-                            tma_load_4d(sK + half * 16384 + 8192, &tmK, &bar.k_full[s], half * 64, r1, h, b);
-                        } else {
-                            tma_load_3d(sK + half * 16384, &tmKb, &bar.k_full[s], half * 64, r0, bh);
-                            tma_load_3d(sK + half * 16384 + 8192, &tmKb, &bar.k_full[s], half * 64, r1, bh);
-                        }
+                for (int half = 0; half < D / 64; ++half) {
+                    if (exact) {
+                        tma_load_4d(sK + half * 16384, &tmK, &bar.k_full[s], half * 64, r0, h, b);
+                        tma_load_4d(sK + half * 16384 + 8192, &tmK, &bar.k_full[s], half * 64, r1, h, b);
+                    } else {
+                        tma_load_3d(sK + half * 16384, &tmKb, &bar.k_full[s], half * 64, r0, bh);
+                        tma_load_3d(sK + half * 16384 + 8192, &tmKb, &bar.k_full[s], half * 64, r1, bh);
                     }
-                    TRACE(0, g);
                 }
-                __syncwarp();
-                if (++s == kSK) s = 0;
+                TRACE(0, g);
             }
             __syncwarp();
-            if (lane == 0) mbar_arrive(&bar.mask_free);
-            if (first_order) {
-                // H_bar (D x D = one stage) into K stage 0 once every S MMA of
-                // the tile is done (the next tile's K loads wait for its QH)
-                for (int j = C.G - kSK; j < C.G; ++j) wait_s_done(sbase + j);
-                if (elect_one()) {
-                    mbar_expect_tx(&bar.h_full, D * D * 2);
-#pragma unroll
-                    for (int half = 0; half < D / 64; ++half)
-                        tma_load_3d(smem + Cfg::kOffK + half * 16384, &tmH, &bar.h_full, half * 64, 0, bh);
-                }
-                __syncwarp();
-            }
-            sbase += C.G;
+            if (++s == kSK) s = 0;
         }
-    } else if (warp == 2 || warp == 3) {
-        asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(kRegsProducer));
-        // ------------------------- warp 3: selection masks; producers: V halves --
-        const bool vprod = warp == 2 || D == 128;
+        if (first_order) {
+            // H_bar (D x D = one stage) into K stage 0 once every S MMA is done
+            for (int j = G - kSK; j < G; ++j) wait_s_done(j);
+            if (elect_one()) {
+                mbar_expect_tx(&bar.h_full, D * D * 2);
+#pragma unroll
+                for (int half = 0; half < D / 64; ++half)
+                    tma_load_3d(smem + Cfg::kOffK + half * 16384, &tmH, &bar.h_full, half * 64, 0, bh);
+            }
+            __syncwarp();
+        }
+    } else if (warp == 2 || (warp == 3 && D == 128)) {
+        // -------------------------------------------- producers: V halves --
         const int vh = warp - 2;
         int s = 0;
         uint32_t ph = 0;
-        int it = 0;
-        for (int t = blockIdx.x; t < total; t += gridDim.x, ++it) {
-            tr_it = it;
-            const TileId T = tile_id(t);
-            const int bh = T.bh, b = T.b, h = T.h, iA = T.iA, iB = T.iB;
-            const bool hasB = T.hasB;
-            (void)bh; (void)b; (void)h; (void)iA; (void)iB; (void)hasB;
-            if (warp == 3) {
-                // selection bitmasks of the tile's two query blocks into shared
-                // memory and the sizes of the three parts of their union (A&B,
-                // A only, B only; every consumer walks them with a UnionCursor),
-                // once every consumer is done with the previous tile's
-                if (it > 0) mbar_wait(&bar.mask_free, uint32_t((it - 1) & 1));
-            const uint32_t* mA = a.mask + (size_t(bh) * a.N + iA) * a.W;
-            const uint32_t* mB = a.mask + (size_t(bh) * a.N + iB) * a.W;
-            uint32_t nab = 0, na = 0, nb = 0;
-            // all loads in flight at once (one L2 round trip; W <= 128 for N <= 4096)
-            uint32_t ra[4], rb[4];
-    #pragma unroll
-            for (int i = 0; i < 4; ++i) {
-                const int w = lane + 32 * i;
-                ra[i] = w < a.W ? __ldcg(mA + w) : 0u;
-                rb[i] = (w < a.W && hasB) ? __ldcg(mB + w) : 0u;
-            }
-    #pragma unroll
-            for (int i = 0; i < 4; ++i) {
-                const int w = lane + 32 * i;
-                if (w < a.W) {
-                    maskA[w] = ra[i];
-                    maskB[w] = rb[i];
+        UnionCursor cur(maskA, maskB);
+        for (int g = 0; g < G; ++g) {
+            uint8_t* sV = smem + Cfg::kOffV + s * Cfg::kKV + vh * 16384;
+            mbar_wait(&bar.v_empty[s], ph ^ 1);
+            const bool exact = g < G1;
+            int r0, r1;
+            tile_rows(cur, g, r0, r1);
+            if (elect_one()) {
+                mbar_expect_tx(&bar.v_full[s], 16384);
+                if (exact) {
+                    tma_load_4d(sV, &tmV, &bar.v_full[s], vh * 64, r0, h, b);
+                    tma_load_4d(sV + 8192, &tmV, &bar.v_full[s], vh * 64, r1, h, b);
+                } else {
+                    tma_load_3d(sV, &tmVh, &bar.v_full[s], vh * 64, r0, bh);
+                    tma_load_3d(sV + 8192, &tmVh, &bar.v_full[s], vh * 64, r1, bh);
                 }
-                nab += __popc(ra[i] & rb[i]);
-                na += __popc(ra[i] & ~rb[i]);
-                nb += __popc(rb[i] & ~ra[i]);
-            }
-    #pragma unroll
-            for (int o = 16; o > 0; o >>= 1) {
-                nab += __shfl_xor_sync(0xffffffffu, nab, o);
-                na += __shfl_xor_sync(0xffffffffu, na, o);
-                nb += __shfl_xor_sync(0xffffffffu, nb, o);
-            }
-            if (lane == 0) {
-                bar.n_ab = nab;
-                bar.n_a = na;
-                bar.n_b = nb;
-            }
-                TRACE(13, 0);  // masks copied, union sized
-                __syncwarp();
-                mbar_arrive(&bar.mask_ready);
-            }
-            if (!vprod) continue;
-            mbar_wait(&bar.mask_ready, uint32_t(it & 1));
-            const Counts C = counts();
-            UnionCursor cur(maskA, maskB);
-            for (int g = 0; g < C.G; ++g) {
-                uint8_t* sV = smem + Cfg::kOffV + s * Cfg::kKV + vh * 16384;
-                mbar_wait(&bar.v_empty[s], ph ^ 1);
-                const bool exact = g < C.G1;
-                int r0, r1;
-                tile_rows(cur, C, g, r0, r1);
-                if (elect_one()) {
-                    mbar_expect_tx(&bar.v_full[s], 16384);
-                    if (exact) {
-                        tma_load_4d(sV, &tmV, &bar.v_full[s], vh * 64, r0, h, b);
-                        tma_load_4d(sV + 8192, &tmV, &bar.v_full[s], vh * 64, r1, h, b);
-                    } else {
-                        tma_load_3d(sV, &tmVh, &bar.v_full[s], vh * 64, r0, bh);
-                        tma_load_3d(sV + 8192, &tmVh, &bar.v_full[s], vh * 64, r1, bh);
-                    }
-                    if (vh == 0) TRACE(1, g);
-                }
-                __syncwarp();
-                if (++s == kSV) { s = 0; ph ^= 1u; }
+                if (vh == 0) TRACE(1, g);
             }
             __syncwarp();
-            if (lane == 0) mbar_arrive(&bar.mask_free);
+            if (++s == kSV) { s = 0; ph ^= 1u; }
         }
     } else if (warp == 1) {
-        asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(kRegsProducer));
         // ------------------------------------------------------------- MMA --
         // Lean issue loop: shared-memory descriptors are built once and
         // advanced by adding (byte offset >> 4) to their address field; ring
@@ -646,74 +558,65 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (++sv == kSV) { sv = 0; phv ^= 1u; }
             if (++sbv == kSB) { sbv = 0; php ^= 1u; }
         };
-        int it = 0;
-        for (int t = blockIdx.x; t < total; t += gridDim.x, ++it) {
-            tr_it = it;
-            mma_wait(&bar.mask_ready, uint32_t(it & 1));
-            const Counts C = counts();
-            const int G = C.G;
-            if (a.tile_count && lane == 0) atomicAdd(a.tile_count, (unsigned long long)(2 * G));
-            if (it > 0) mma_wait(&bar.o_free, uint32_t((it - 1) & 1));  // O / QH of the last tile read
-            mma_wait(&bar.q_full, uint32_t(it & 1));
-            TRACE(15, 0);  // Q landed
+        if (a.tile_count && lane == 0) atomicAdd(a.tile_count, (unsigned long long)(2 * G));
+        mma_wait(&bar.q_full, 0);
+        TRACE(15, 0);  // Q landed
+        tc_fence_after();
+        for (int g = 0; g < kSB && g < G; ++g) {
+            mma_wait(&bar.k_full[sk], phk);
             tc_fence_after();
-            for (int g = 0; g < kSB && g < G; ++g) {
+            if (elect_one()) mma_s(g);
+            __syncwarp();
+            advance_s();
+        }
+        for (int g = 0; g < G; ++g) {
+            // PV_g as soon as P_g and V_g are in, then S_{g+3} once K_{g+3} is
+            // (in-order tensor pipe: S_{g+3} overwrites P_g after PV_g read it);
+            // a late K tile never holds back PV_g
+#if PISA_PSPLIT
+            mma_wait(&bar.p_half[sbv], php);
+            mma_wait(&bar.v_full[sv], phv);
+            tc_fence_after();
+            if (elect_one()) mma_pv(g, 0, 1);
+            __syncwarp();
+            mma_wait(&bar.p_full[sbv], php);
+            TRACE(9, g);
+            tc_fence_after();
+            if (elect_one()) mma_pv(g, 1, 2);
+            __syncwarp();
+#else
+            mma_wait(&bar.p_full[sbv], php);
+            TRACE(9, g);
+            mma_wait(&bar.v_full[sv], phv);
+            tc_fence_after();
+            if (elect_one()) mma_pv(g, 0, 2);
+            __syncwarp();
+#endif
+            advance_pv();
+            if (g + kSB < G) {
                 mma_wait(&bar.k_full[sk], phk);
                 tc_fence_after();
-                if (elect_one()) mma_s(g);
+                if (elect_one()) mma_s(g + kSB);
                 __syncwarp();
                 advance_s();
             }
-            for (int g = 0; g < G; ++g) {
-                // PV_g as soon as P_g and V_g are in, then S_{g+3} once K_{g+3} is
-                // (in-order tensor pipe: S_{g+3} overwrites P_g after PV_g read it);
-                // a late K tile never holds back PV_g
-    #if PISA_PSPLIT
-                mma_wait(&bar.p_half[sbv], php);
-                mma_wait(&bar.v_full[sv], phv);
-                tc_fence_after();
-                if (elect_one()) mma_pv(g, 0, 1);
-                __syncwarp();
-                mma_wait(&bar.p_full[sbv], php);
-                TRACE(9, g);
-                tc_fence_after();
-                if (elect_one()) mma_pv(g, 1, 2);
-                __syncwarp();
-    #else
-                mma_wait(&bar.p_full[sbv], php);
-                TRACE(9, g);
-                mma_wait(&bar.v_full[sv], phv);
-                tc_fence_after();
-                if (elect_one()) mma_pv(g, 0, 2);
-                __syncwarp();
-    #endif
-                advance_pv();
-                if (g + kSB < G) {
-                    mma_wait(&bar.k_full[sk], phk);
-                    tc_fence_after();
-                    if (elect_one()) mma_s(g + kSB);
-                    __syncwarp();
-                    advance_s();
-                }
-            }
-            if (first_order) {
-                mma_wait(&bar.h_full, uint32_t(it & 1));
-                tc_fence_after();
-            }
-            if (elect_one()) {
-                if (first_order) {
-    #pragma unroll
-                    for (int ks = 0; ks < D / 16; ++ks)
-                        mma_ss(tS, qdesc0 + uint64_t(((ks >> 2) * 16384 + (ks & 3) * 32) >> 4),
-                               hdesc0 + uint64_t((ks * 2048) >> 4), idQH, ks != 0);
-                }
-                mma_commit(&bar.qh_full);  // also: every PV done
-                TRACE(12, 2);  // (trace builds) tail: QH issued
-            }
-            __syncwarp();
         }
+        if (first_order) {
+            mma_wait(&bar.h_full, 0);
+            tc_fence_after();
+        }
+        if (elect_one()) {
+            if (first_order) {
+#pragma unroll
+                for (int ks = 0; ks < D / 16; ++ks)
+                    mma_ss(tS, qdesc0 + uint64_t(((ks >> 2) * 16384 + (ks & 3) * 32) >> 4),
+                           hdesc0 + uint64_t((ks * 2048) >> 4), idQH, ks != 0);
+            }
+            mma_commit(&bar.qh_full);  // also: every PV done
+            TRACE(12, 2);  // (trace builds) tail: QH issued
+        }
+        __syncwarp();
     } else if (warp >= 4) {
-        asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(kRegsSoftmax));
         // ------------------------------------------------ softmax warpgroups --
         const int hh = (warp - 4) >> 2;  // query block 2*tile + hh
         const int q4 = warp & 3;         // TMEM lane quadrant
@@ -721,8 +624,16 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int ch = lane >> 4;        // column half of a 64-key sub-tile
         const float sl2 = a.scale * 1.4426950408889634f;
         const uint32_t lbase = tmem + (uint32_t(q4 * 32 + hh * 16) << 16);
+        // no partner (a lone last block, or iB outside a query-block range):
+        // warpgroup B is idle and writes nothing
+        const int qblk = hh ? (hasB ? iB : -1) : iA;
+        const int grow = qblk * 64 + q4 * 16 + r16;
+        const bool active = qblk >= 0 && grow < a.L;
+        const bool wact = __all_sync(0xffffffffu, active);
+        const uint32_t* hmask = hh ? maskB : maskA;
+        const __nv_bfloat16* qrow = a.q + size_t(b) * a.qs_b + size_t(h) * a.qs_h + size_t(grow) * a.qs_l;
+
         float m = -INFINITY, l = 0.f, lt = 0.f;  // l, lt: this thread's partial sums
-        int vbase = 0;  // global index of this tile's first PV (rings persist across tiles)
 
         // Online-softmax step over one 128-key super-tile: bm_loc = max of this
         // thread's live scores (masked = -inf). Returns the shift to
@@ -735,7 +646,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (g > 0) {
                 // PV_{g-1-kSV} is known done (S_g was issued after PV_{g-3}), so
                 // the parity names PV_{g-1} unambiguously
-                const int j = vbase + g - 1;  // global PV index
+                const int j = g - 1;
                 mbar_wait<true>(&bar.v_empty[j % kSV], uint32_t((j / kSV) & 1));
                 tc_fence_after();
             }
@@ -783,234 +694,199 @@ __global__ void __launch_bounds__(kThreads, 1)
         };
         const uint32_t kZero16[16] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
 
-        int it = 0;
-        for (int t = blockIdx.x; t < total; t += gridDim.x, ++it) {
-            tr_it = it;
-            int qblk;  // this warpgroup's query block; -1: idle (a lone last block,
-                       // or iB outside a query-block range: writes nothing)
-            {
-                const TileId T = tile_id(t);
-                qblk = hh ? (T.hasB ? T.iB : -1) : T.iA;
-            }
-            mbar_wait(&bar.mask_ready, uint32_t(it & 1));
-            const Counts C = counts();
-            const int G1 = C.G1, G = C.G, gAB = C.gAB, nPair = C.nPair, kPairX = C.kPairX, kPairR = C.kPairR;
-            const bool restA = C.restA;
-            (void)gAB; (void)nPair; (void)kPairX; (void)kPairR; (void)restA; (void)G1;
-            const bool active = qblk >= 0 && qblk * 64 + q4 * 16 + r16 < a.L;
-            const bool wact = __all_sync(0xffffffffu, active);
-            const uint32_t* hmask = hh ? maskB : maskA;
-            m = -INFINITY;
-            l = 0.f;
-            lt = 0.f;
-            // ---- Phase 1: exact blocks of the union, two per super-tile
-            UnionCursor cur(maskA, maskB);
-            for (int g = 0; g < G1; ++g) {
-                uint32_t e0, e1;
-                cur.pair(g, gAB, nPair, kPairX, kPairR, restA, e0, e1);  // pad: use flags 0
-                const bool use0 = (e0 >> (14 + hh)) & 1u, use1 = (e1 >> (14 + hh)) & 1u;  // warp-uniform
-                const int nv0 = (int(e0 & 0x3FFFu) == a.N - 1) ? n_last : 64;
-                const int nv1 = (int(e1 & 0x3FFFu) == a.N - 1) ? n_last : 64;
-                const uint32_t sc = lbase + kColS + sb * 128;
-                softmax_wait(&bar.s_full[sb], phs);
-                tc_fence_after();
-                if (q4 == 0) TRACE(4 + hh, g);
-                if (use0 || use1) {
-                    // scores as raw bits, masked in place (only the ragged last key
-                    // block / rows past L need masks); loads only of the selected
-                    // sub-tiles
-                    uint32_t r0[32], r1[32];
-                    if (use0) tmem_ld16x2_32<32>(sc, r0);
-                    if (use1) tmem_ld16x2_32<32>(sc + 64, r1);
-                    tmem_ld_wait(r0);
-                    tmem_ld_wait(r1);
-                    if (!(wact && nv0 == 64 && nv1 == 64)) {
-    #pragma unroll
-                        for (int i = 0; i < 32; ++i) {
-                            const int col = ch * 32 + i;
-                            if (!(active && col < nv0)) r0[i] = 0xff800000u;  // -inf
-                            if (!(active && col < nv1)) r1[i] = 0xff800000u;
-                        }
-                    }
-                    float bm_loc = -INFINITY;
-                    if (use0) bm_loc = max32(reinterpret_cast<const float*>(r0));
-                    if (use1) bm_loc = fmaxf(bm_loc, max32(reinterpret_cast<const float*>(r1)));
-                    const float mm = update_max(bm_loc, g);
-                    // exponentials only for the selected sub-tiles (warp-uniform)
-                    auto expo_store = [&](const uint32_t (&r)[32], uint32_t addr) {
-                        uint32_t pk[16];
-                        float ps[4] = {0.f, 0.f, 0.f, 0.f};
-    #pragma unroll
-                        for (int i = 0; i < 32; i += 2) {
-                            const float p0 = ex2_mix(fmaf(__uint_as_float(r[i]), sl2, -mm), i);
-                            const float p1 = ex2_mix(fmaf(__uint_as_float(r[i + 1]), sl2, -mm), i + 1);
-                            ps[(i >> 1) & 3] += p0 + p1;
-                            pk[i >> 1] = pack_bf16(p0, p1);
-                        }
-                        l += (ps[0] + ps[1]) + (ps[2] + ps[3]);
-                        tmem_st16x2_16<16>(addr, pk);  // P (bf16 pairs)
-                    };
-                    if (use0) expo_store(r0, sc); else tmem_st16x2_16<16>(sc, kZero16);
-                    publish_half();
-                    if (use1) expo_store(r1, sc + 64); else tmem_st16x2_16<16>(sc + 64, kZero16);
-                } else {
-                    tmem_st16x2_16<16>(sc, kZero16);
-                    publish_half();
-                    tmem_st16x2_16<16>(sc + 64, kZero16);
-                }
-                publish_p(g);
-                advance();
-                if (q4 == 0) TRACE(6 + hh, g);
-            }
-            // ---- Phase 2: centroid chunks, two per super-tile; column mask = own
-            // selection, weight n_j (the ragged last block weighs n_last)
-            for (int g = G1; g < G; ++g) {
-                const int c0 = 2 * (g - G1);
-                const uint32_t sc = lbase + kColS + sb * 128;
-                // this thread's 32 columns of chunk c: blocks c*64 + ch*32 + i
-                auto colmask = [&](int c) -> uint32_t {
-                    const int w = 2 * c + ch;
-                    return (c < a.nchunk2 && w < a.W) ? hmask[w] : 0xffffffffu;
-                };
-                const uint32_t cm0 = colmask(c0), cm1 = colmask(c0 + 1);
-                const int nv0 = min(64, a.N - c0 * 64), nv1 = min(64, a.N - (c0 + 1) * 64);
-                softmax_wait(&bar.s_full[sb], phs);
-                tc_fence_after();
+        // ---- Phase 1: exact blocks of the union, two per super-tile
+        UnionCursor cur(maskA, maskB);
+        for (int g = 0; g < G1; ++g) {
+            uint32_t e0, e1;
+            cur.pair(g, gAB, nPair, kPairX, kPairR, restA, e0, e1);  // pad: use flags 0
+            const bool use0 = (e0 >> (14 + hh)) & 1u, use1 = (e1 >> (14 + hh)) & 1u;  // warp-uniform
+            const int nv0 = (int(e0 & 0x3FFFu) == a.N - 1) ? n_last : 64;
+            const int nv1 = (int(e1 & 0x3FFFu) == a.N - 1) ? n_last : 64;
+            const uint32_t sc = lbase + kColS + sb * 128;
+            softmax_wait(&bar.s_full[sb], phs);
+            tc_fence_after();
+            if (q4 == 0) TRACE(4 + hh, g);
+            if (use0 || use1) {
+                // scores as raw bits, masked in place (only the ragged last key
+                // block / rows past L need masks); loads only of the selected
+                // sub-tiles
                 uint32_t r0[32], r1[32];
-                tmem_ld16x2_32<32>(sc, r0);
-                tmem_ld16x2_32<32>(sc + 64, r1);
+                if (use0) tmem_ld16x2_32<32>(sc, r0);
+                if (use1) tmem_ld16x2_32<32>(sc + 64, r1);
                 tmem_ld_wait(r0);
                 tmem_ld_wait(r1);
-    #pragma unroll
-                for (int i = 0; i < 32; ++i) {
-                    const int col = ch * 32 + i;
-                    if (!(active && col < nv0 && !((cm0 >> i) & 1u))) r0[i] = 0xff800000u;
-                    if (!(active && col < nv1 && !((cm1 >> i) & 1u))) r1[i] = 0xff800000u;
+                if (!(wact && nv0 == 64 && nv1 == 64)) {
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) {
+                        const int col = ch * 32 + i;
+                        if (!(active && col < nv0)) r0[i] = 0xff800000u;  // -inf
+                        if (!(active && col < nv1)) r1[i] = 0xff800000u;
+                    }
                 }
-                const float mm = update_max(fmaxf(max32(reinterpret_cast<const float*>(r0)),
-                                                  max32(reinterpret_cast<const float*>(r1))), g);
-                // column (within this thread's 32) of the ragged last block, if here
-                const int lb = a.N - 1 - c0 * 64 - ch * 32;  // 0..31 -> sub-tile 0, 64..95 -> sub-tile 1
-                const bool ragged = n_last != 64;
-                float ps = 0.f, plast = 0.f;
-                auto expo_store = [&](const uint32_t (&r)[32], uint32_t addr, int lbo) {
+                float bm_loc = -INFINITY;
+                if (use0) bm_loc = max32(reinterpret_cast<const float*>(r0));
+                if (use1) bm_loc = fmaxf(bm_loc, max32(reinterpret_cast<const float*>(r1)));
+                const float mm = update_max(bm_loc, g);
+                // exponentials only for the selected sub-tiles (warp-uniform)
+                auto expo_store = [&](const uint32_t (&r)[32], uint32_t addr) {
                     uint32_t pk[16];
-                    float q0 = 0.f, q1 = 0.f;
-    #pragma unroll
+                    float ps[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
                     for (int i = 0; i < 32; i += 2) {
                         const float p0 = ex2_mix(fmaf(__uint_as_float(r[i]), sl2, -mm), i);
                         const float p1 = ex2_mix(fmaf(__uint_as_float(r[i + 1]), sl2, -mm), i + 1);
-                        q0 += p0;
-                        q1 += p1;
-                        if (ragged) plast += (lbo == i ? p0 : 0.f) + (lbo == i + 1 ? p1 : 0.f);
+                        ps[(i >> 1) & 3] += p0 + p1;
                         pk[i >> 1] = pack_bf16(p0, p1);
                     }
-                    ps += q0 + q1;
-                    tmem_st16x2_16<16>(addr, pk);
+                    l += (ps[0] + ps[1]) + (ps[2] + ps[3]);
+                    tmem_st16x2_16<16>(addr, pk);  // P (bf16 pairs)
                 };
-                expo_store(r0, sc, lb);
+                if (use0) expo_store(r0, sc); else tmem_st16x2_16<16>(sc, kZero16);
                 publish_half();
-                expo_store(r1, sc + 64, lb - 64);
-                l += 64.f * ps + (float(n_last) - 64.f) * plast;
-                lt += ps;
-                publish_p(g);
-                advance();
+                if (use1) expo_store(r1, sc + 64); else tmem_st16x2_16<16>(sc + 64, kZero16);
+            } else {
+                tmem_st16x2_16<16>(sc, kZero16);
+                publish_half();
+                tmem_st16x2_16<16>(sc + 64, kZero16);
             }
-
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&bar.mask_free);  // Phase 2 read the column masks last
-            {
-                // ---- tile quantities of the epilogue (recomputed: not live in the loops)
-                const TileId TE = tile_id(t);
-                const int bh = TE.bh, b = TE.b, h = TE.h;
-                const int grow = qblk * 64 + q4 * 16 + r16;
-                const __nv_bfloat16* qrow = a.q + size_t(b) * a.qs_b + size_t(h) * a.qs_h + size_t(grow) * a.qs_l;
-                // ------------------------------------------------------- epilogue --
-                mbar_wait(&bar.qh_full, uint32_t(it & 1));
-                tc_fence_after();
-                if (warp == 4) TRACE(13, 2);  // tail: O and QH complete
-                float mrow = m;
-                float lfin = l + __shfl_xor_sync(0xffffffffu, l, 16);
-                float ltot = lt + __shfl_xor_sync(0xffffffffu, lt, 16);
-                float cw = 0.f;
-                if (a.variant == 3) {
-                    cw = a.scale * ltot;
-                    if (a.literal_phase3) cw *= (1.0f / 64.0f);
-                }
-                float fo = 1.f;  // extra scale on O and l (GlobalCentroid shift)
-                if (a.variant == 4) {
-                    // slope = |U_i| exp(scale q.k_bar_global - m)   (engine.hpp:202-205)
-                    const float* kg = a.kbar_global + size_t(bh) * D;
-                    float dot = 0.f;
-                    if (active) {
-                        for (int c = ch * (D / 2); c < (ch + 1) * (D / 2); ++c)
-                            dot = fmaf(__bfloat162float(qrow[c]), kg[c], dot);
-                    }
-                    dot += __shfl_xor_sync(0xffffffffu, dot, 16);
-                    const float gx = dot * sl2;
-                    const int nU = a.N - a.k;
-                    if (active && nU > 0) {
-                        const float mm = fmaxf(mrow, gx);
-                        fo = ex2(mrow - mm);
-                        cw = a.scale * float(nU) * ex2(gx - mm);
-                        if (a.literal_phase3) cw *= (1.0f / 64.0f);
-                        mrow = mm;
-                        lfin *= fo;
-                        ltot *= fo;
-                    }
-                }
-                const float inv_l = 1.0f / lfin;
-                bool bad = false;
-                char* orow = reinterpret_cast<char*>(a.out) +
-                             (size_t(b) * a.os_b + size_t(h) * a.os_h + size_t(grow) * a.os_l) *
-                                 (a.out_f32 ? 4 : 2);
-        #pragma unroll 1
-                for (int cc = 0; cc < D / 2; cc += 32) {
-                    uint32_t ro[32], rq[32];
-                    tmem_ld16x2_32<D / 2>(lbase + kColO + cc, ro);
-                    if (first_order) tmem_ld16x2_32<D / 2>(lbase + kColS + cc, rq);
-                    tmem_ld_wait(ro);
-                    if (first_order) tmem_ld_wait(rq);
-                    float o[32];
-        #pragma unroll
-                    for (int i = 0; i < 32; ++i) {
-                        float acc = __uint_as_float(ro[i]) * fo;
-                        if (first_order) acc = fmaf(cw, __uint_as_float(rq[i]), acc);
-                        o[i] = acc * inv_l;
-                        bad |= active && !isfinite(o[i]);
-                    }
-                    const int col = ch * (D / 2) + cc;
-                    if (active) {
-                        if (a.out_f32) {
-                            float4* dst = reinterpret_cast<float4*>(orow) + col / 4;
-        #pragma unroll
-                            for (int i = 0; i < 32; i += 4) dst[i / 4] = make_float4(o[i], o[i + 1], o[i + 2], o[i + 3]);
-                        } else {
-                            uint4* dst = reinterpret_cast<uint4*>(orow + col * 2);
-        #pragma unroll
-                            for (int i = 0; i < 32; i += 8)
-                                dst[i / 8] = make_uint4(pack_bf16(o[i], o[i + 1]), pack_bf16(o[i + 2], o[i + 3]),
-                                                        pack_bf16(o[i + 4], o[i + 5]), pack_bf16(o[i + 6], o[i + 7]));
-                        }
-                    }
-                }
-                // O and QH are read out: the next tile's MMAs may overwrite them
-                tc_fence_before();
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&bar.o_free);
-                if (active) {
-                    const size_t di = size_t(bh) * a.L + grow;
-                    if (ch == 0) {
-                        if (a.diag_m) a.diag_m[di] = mrow * 0.6931471805599453f;  // log2 units -> natural log
-                        if (a.diag_l) a.diag_l[di] = lfin;
-                        if (a.diag_lt) a.diag_lt[di] = ltot;
-                    }
-                    if (bad && a.nonfinite) atomicExch(a.nonfinite, 1);
-                }
-                if (warp == 4) TRACE(14, 2);  // tail: this warp's rows stored
-}
-            vbase += G;
+            publish_p(g);
+            advance();
+            if (q4 == 0) TRACE(6 + hh, g);
         }
+        // ---- Phase 2: centroid chunks, two per super-tile; column mask = own
+        // selection, weight n_j (the ragged last block weighs n_last)
+        for (int g = G1; g < G; ++g) {
+            const int c0 = 2 * (g - G1);
+            const uint32_t sc = lbase + kColS + sb * 128;
+            // this thread's 32 columns of chunk c: blocks c*64 + ch*32 + i
+            auto colmask = [&](int c) -> uint32_t {
+                const int w = 2 * c + ch;
+                return (c < a.nchunk2 && w < a.W) ? hmask[w] : 0xffffffffu;
+            };
+            const uint32_t cm0 = colmask(c0), cm1 = colmask(c0 + 1);
+            const int nv0 = min(64, a.N - c0 * 64), nv1 = min(64, a.N - (c0 + 1) * 64);
+            softmax_wait(&bar.s_full[sb], phs);
+            tc_fence_after();
+            uint32_t r0[32], r1[32];
+            tmem_ld16x2_32<32>(sc, r0);
+            tmem_ld16x2_32<32>(sc + 64, r1);
+            tmem_ld_wait(r0);
+            tmem_ld_wait(r1);
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+                const int col = ch * 32 + i;
+                if (!(active && col < nv0 && !((cm0 >> i) & 1u))) r0[i] = 0xff800000u;
+                if (!(active && col < nv1 && !((cm1 >> i) & 1u))) r1[i] = 0xff800000u;
+            }
+            const float mm = update_max(fmaxf(max32(reinterpret_cast<const float*>(r0)),
+                                              max32(reinterpret_cast<const float*>(r1))), g);
+            // column (within this thread's 32) of the ragged last block, if here
+            const int lb = a.N - 1 - c0 * 64 - ch * 32;  // 0..31 -> sub-tile 0, 64..95 -> sub-tile 1
+            const bool ragged = n_last != 64;
+            float ps = 0.f, plast = 0.f;
+            auto expo_store = [&](const uint32_t (&r)[32], uint32_t addr, int lbo) {
+                uint32_t pk[16];
+                float q0 = 0.f, q1 = 0.f;
+#pragma unroll
+                for (int i = 0; i < 32; i += 2) {
+                    const float p0 = ex2_mix(fmaf(__uint_as_float(r[i]), sl2, -mm), i);
+                    const float p1 = ex2_mix(fmaf(__uint_as_float(r[i + 1]), sl2, -mm), i + 1);
+                    q0 += p0;
+                    q1 += p1;
+                    if (ragged) plast += (lbo == i ? p0 : 0.f) + (lbo == i + 1 ? p1 : 0.f);
+                    pk[i >> 1] = pack_bf16(p0, p1);
+                }
+                ps += q0 + q1;
+                tmem_st16x2_16<16>(addr, pk);
+            };
+            expo_store(r0, sc, lb);
+            publish_half();
+            expo_store(r1, sc + 64, lb - 64);
+            l += 64.f * ps + (float(n_last) - 64.f) * plast;
+            lt += ps;
+            publish_p(g);
+            advance();
+        }
+
+        // ------------------------------------------------------- epilogue --
+        mbar_wait(&bar.qh_full, 0);
+        tc_fence_after();
+        if (warp == 4) TRACE(13, 2);  // tail: O and QH complete
+        float mrow = m;
+        float lfin = l + __shfl_xor_sync(0xffffffffu, l, 16);
+        float ltot = lt + __shfl_xor_sync(0xffffffffu, lt, 16);
+        float cw = 0.f;
+        if (a.variant == 3) {
+            cw = a.scale * ltot;
+            if (a.literal_phase3) cw *= (1.0f / 64.0f);
+        }
+        float fo = 1.f;  // extra scale on O and l (GlobalCentroid shift)
+        if (a.variant == 4) {
+            // slope = |U_i| exp(scale q.k_bar_global - m)   (engine.hpp:202-205)
+            const float* kg = a.kbar_global + size_t(bh) * D;
+            float dot = 0.f;
+            if (active) {
+                for (int c = ch * (D / 2); c < (ch + 1) * (D / 2); ++c)
+                    dot = fmaf(__bfloat162float(qrow[c]), kg[c], dot);
+            }
+            dot += __shfl_xor_sync(0xffffffffu, dot, 16);
+            const float gx = dot * sl2;
+            const int nU = a.N - a.k;
+            if (active && nU > 0) {
+                const float mm = fmaxf(mrow, gx);
+                fo = ex2(mrow - mm);
+                cw = a.scale * float(nU) * ex2(gx - mm);
+                if (a.literal_phase3) cw *= (1.0f / 64.0f);
+                mrow = mm;
+                lfin *= fo;
+                ltot *= fo;
+            }
+        }
+        const float inv_l = 1.0f / lfin;
+        bool bad = false;
+        char* orow = reinterpret_cast<char*>(a.out) +
+                     (size_t(b) * a.os_b + size_t(h) * a.os_h + size_t(grow) * a.os_l) *
+                         (a.out_f32 ? 4 : 2);
+#pragma unroll 1
+        for (int cc = 0; cc < D / 2; cc += 32) {
+            uint32_t ro[32], rq[32];
+            tmem_ld16x2_32<D / 2>(lbase + kColO + cc, ro);
+            if (first_order) tmem_ld16x2_32<D / 2>(lbase + kColS + cc, rq);
+            tmem_ld_wait(ro);
+            if (first_order) tmem_ld_wait(rq);
+            float o[32];
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+                float acc = __uint_as_float(ro[i]) * fo;
+                if (first_order) acc = fmaf(cw, __uint_as_float(rq[i]), acc);
+                o[i] = acc * inv_l;
+                bad |= active && !isfinite(o[i]);
+            }
+            const int col = ch * (D / 2) + cc;
+            if (active) {
+                if (a.out_f32) {
+                    float4* dst = reinterpret_cast<float4*>(orow) + col / 4;
+#pragma unroll
+                    for (int i = 0; i < 32; i += 4) dst[i / 4] = make_float4(o[i], o[i + 1], o[i + 2], o[i + 3]);
+                } else {
+                    uint4* dst = reinterpret_cast<uint4*>(orow + col * 2);
+#pragma unroll
+                    for (int i = 0; i < 32; i += 8)
+                        dst[i / 8] = make_uint4(pack_bf16(o[i], o[i + 1]), pack_bf16(o[i + 2], o[i + 3]),
+                                                pack_bf16(o[i + 4], o[i + 5]), pack_bf16(o[i + 6], o[i + 7]));
+                }
+            }
+        }
+        if (active) {
+            const size_t di = size_t(bh) * a.L + grow;
+            if (ch == 0) {
+                if (a.diag_m) a.diag_m[di] = mrow * 0.6931471805599453f;  // log2 units -> natural log
+                if (a.diag_l) a.diag_l[di] = lfin;
+                if (a.diag_lt) a.diag_lt[di] = ltot;
+            }
+            if (bad && a.nonfinite) atomicExch(a.nonfinite, 1);
+        }
+        if (warp == 4) TRACE(14, 2);  // tail: this warp's rows stored
     }
     tc_fence_before();
     __syncthreads();
@@ -1029,8 +905,7 @@ cudaError_t launch_fused(int D, const CUtensorMap& tmQ, const CUtensorMap& tmK, 
                          const CUtensorMap& tmKb, const CUtensorMap& tmVh, const CUtensorMap& tmH,
                          const FusedArgs& a, int BH, cudaStream_t s) {
     const size_t smem = fused_smem_bytes(D, a.N, a.W);
-    const int total = (a.qb1 - a.qb0 + 1) / 2 * BH;
-    dim3 grid(a.ctas > 0 ? std::min(a.ctas, total) : total);
+    dim3 grid((a.qb1 - a.qb0 + 1) / 2, BH);
     if (D == 128) {
         auto k = fused_attn_kernel<128>;
         cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));

@@ -96,8 +96,6 @@ struct FusedArgs {
     int* nonfinite;  // device flag or null
     int L, N, H, W, nchunk2, variant, literal_phase3, out_f32, k;
     int qb0, qb1;  // query blocks [qb0, qb1) are computed (the rest of O is untouched)
-    int BH;        // batch * heads
-    int ctas;      // grid size: 0 = one CTA per tile, else persistent CTAs looping over tiles
     float scale;
     unsigned long long* trace;  // PISA_TRACE builds only: [8][1024] clock deltas
     unsigned long long* tile_count;  // instrumentation: += 64-key tiles processed (incl. padding), or null

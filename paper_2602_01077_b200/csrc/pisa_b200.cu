@@ -49,10 +49,7 @@ struct pisa_ctx {
     // for -50 us, Wan2.1-14B N=1182 +0.32 ms for -0.84 ms), 2 always.
     // env PISA_B200_PAIRING, API pisa_b200_set_pairing
     int pairing = 1;
-    int host_chunks = 16;
-    // persistent fused kernel (one CTA per SM looping over tiles) or one CTA
-    // per tile; env PISA_B200_PERSISTENT
-    bool persistent = true;  // head chunks of the host path's copy/compute pipeline (env PISA_B200_HOST_CHUNKS)
+    int host_chunks = 16;  // head chunks of the host path's copy/compute pipeline (env PISA_B200_HOST_CHUNKS)
     unsigned long long* tiles_dev = nullptr;  // fused-kernel tile counter (profiling only)
 };
 
@@ -405,8 +402,6 @@ pisa_status run_fused(pisa_ctx* ctx, const pisa_attn_desc& d, const Plan& p, con
     a.k = int(p.k);
     a.qb0 = qb0;
     a.qb1 = qb1;
-    a.BH = int(p.BH);
-    a.ctas = ctx->persistent ? ctx->sms : 0;
     a.scale = float(p.scale);
     a.trace = ctx->trace;
     a.tile_count = ctx->prof ? ctx->tiles_dev : nullptr;
@@ -468,7 +463,6 @@ pisa_status pisa_b200_create(pisa_ctx** out, int device) {
     cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, device);
     if (const char* ev = std::getenv("PISA_B200_PAIRING")) c->pairing = std::max(0, std::min(2, std::atoi(ev)));
     if (const char* ev = std::getenv("PISA_B200_HOST_CHUNKS")) c->host_chunks = std::max(1, std::atoi(ev));
-    if (const char* ev = std::getenv("PISA_B200_PERSISTENT")) c->persistent = std::atoi(ev) != 0;
     DeviceGuard g(device);
     if (cudaMallocHost(&c->flag_host, sizeof(int)) != cudaSuccess) {
         delete c;
