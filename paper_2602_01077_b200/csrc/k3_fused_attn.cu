@@ -96,6 +96,12 @@ constexpr uint32_t kPolyMask = PISA_POLY_MASK;
 #define PISA_SOFTMAX_NS 32
 #endif
 constexpr bool kSoftmaxSpin = PISA_SOFTMAX_SPIN != 0;
+#ifndef PISA_REGS_PRODUCER
+#define PISA_REGS_PRODUCER 0  // 0: no setmaxnreg
+#endif
+#ifndef PISA_REGS_SOFTMAX
+#define PISA_REGS_SOFTMAX 208
+#endif
 __device__ __forceinline__ void softmax_wait(uint64_t* bar, uint32_t parity) {
 #if PISA_SOFTMAX_SPIN == 2
     mbar_wait_backoff<PISA_SOFTMAX_NS>(bar, parity);
@@ -432,6 +438,9 @@ __global__ void __launch_bounds__(kThreads, 1)
 
     if (warp == 0) {
         // ------------------------------------------------ producer: Q, K, H --
+#if PISA_REGS_PRODUCER
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(PISA_REGS_PRODUCER));
+#endif
         // K stage of S_g is free once S_{g-kSK} is done: s_full of that S
         // (no separate "empty" commit; S_{g-kSK+3} cannot complete before K_g is
         // loaded, so the parity is unambiguous)
@@ -478,6 +487,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             __syncwarp();
         }
     } else if (warp == 2 || (warp == 3 && D == 128)) {
+#if PISA_REGS_PRODUCER
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(PISA_REGS_PRODUCER));
+#endif
         // -------------------------------------------- producers: V halves --
         const int vh = warp - 2;
         int s = 0;
@@ -503,7 +515,15 @@ __global__ void __launch_bounds__(kThreads, 1)
             __syncwarp();
             if (++s == kSV) { s = 0; ph ^= 1u; }
         }
+    } else if (warp == 3) {
+        // (D = 64: one V producer; warp 3 only joins its warpgroup's setmaxnreg)
+#if PISA_REGS_PRODUCER
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(PISA_REGS_PRODUCER));
+#endif
     } else if (warp == 1) {
+#if PISA_REGS_PRODUCER
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(PISA_REGS_PRODUCER));
+#endif
         // ------------------------------------------------------------- MMA --
         // Lean issue loop: shared-memory descriptors are built once and
         // advanced by adding (byte offset >> 4) to their address field; ring
@@ -617,6 +637,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         __syncwarp();
     } else if (warp >= 4) {
+#if PISA_REGS_PRODUCER
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(PISA_REGS_SOFTMAX));
+#endif
         // ------------------------------------------------ softmax warpgroups --
         const int hh = (warp - 4) >> 2;  // query block 2*tile + hh
         const int q4 = warp & 3;         // TMEM lane quadrant
