@@ -792,10 +792,26 @@ pisa_status pisa_b200_fwd_host(pisa_ctx* ctx, const pisa_attn_desc* d, const voi
         ctx->stage_bytes = 2 * set_bytes;
     }
     int64_t launches = 0;
-    const int64_t nchunks = (BH + chunk - 1) / chunk;
-    for (int64_t c = 0; c < nchunks; ++c) {
+    // chunk sizes: a remainder first, then `chunk`-sized ones, then a shrinking
+    // tail (2, 1) so that each chunk's compute hides behind the next chunk's
+    // H2D (compute is ~0.6x the H2D time per head) and the exposed tail --
+    // compute + D2H of the last chunk -- is one head
+    std::vector<int64_t> sizes;
+    {
+        const bool shrink = chunk >= 3 && BH >= chunk + 3;
+        const int64_t rest = shrink ? BH - 3 : BH;
+        if (rest % chunk) sizes.push_back(rest % chunk);
+        for (int64_t i = 0; i < rest / chunk; ++i) sizes.push_back(chunk);
+        if (shrink) {
+            sizes.push_back(2);
+            sizes.push_back(1);
+        }
+    }
+    const int64_t nchunks = int64_t(sizes.size());
+    int64_t h0 = 0;
+    for (int64_t c = 0; c < nchunks; h0 += sizes[size_t(c)], ++c) {
         const int sidx = int(c & 1);
-        const int64_t h0 = c * chunk, hc = std::min(chunk, BH - h0);
+        const int64_t hc = sizes[size_t(c)];
         char* set = static_cast<char*>(ctx->stage) + sidx * set_bytes;
         char* dq = set;
         char* dk = dq + chunk * in_bytes;

@@ -391,9 +391,12 @@ def test_attention_with_given_plan_and_validation(P, oracle_mod):
                          torch.tensor(bad.copy()).cuda()[None, None], stats)
 
 
-def test_host_path_equals_device_path(P):
+@pytest.mark.parametrize("B,H,L", [(1, 5, 2048), (2, 23, 512), (1, 40, 320)])
+def test_host_path_equals_device_path(P, B, H, L):
+    """pisa_b200_fwd_host (staged chunks: a remainder, full chunks, a 2 / 1
+    tail from 33 (b, h) units up) equals the device-resident forward."""
     import torch
-    B, H, L, d = 1, 5, 2048, 128
+    d = 128
     x = [torch.randn((B, H, L, d), device="cuda").bfloat16() for _ in range(3)]
     dev_out = P.fwd(*x, sparsity=0.875)
     hx = [t.cpu().pin_memory() for t in x]
