@@ -270,8 +270,8 @@ struct TcCfg {
     static constexpr int kOffV = 3 * kTile;               // hi | mid | lo | V
     static constexpr int kOffVec = 4 * kTile;             // Lanczos vector [128]
     static constexpr int kOffKb = kOffVec + 128 * 4;      // k_bar_j [128]
-    static constexpr int kOffRed = kOffKb + 128 * 4;      // [2][4] reduction scratch, alpha / beta
-    static constexpr int kOffBar = (kOffRed + (8 + 2 * kLanczos) * 4 + 7) & ~7;
+    static constexpr int kOffRed = kOffKb + 128 * 4;      // [2][4][2] reduction scratch, alpha / beta
+    static constexpr int kOffBar = (kOffRed + (16 + 2 * kLanczos) * 4 + 7) & ~7;
     static constexpr int kSmem = 1024 + kOffBar + 48;
 };
 
@@ -319,7 +319,7 @@ __global__ void __launch_bounds__(kTcThreads, 3)
     float* vs = reinterpret_cast<float*>(smem + Cfg::kOffVec);
     float* kb = reinterpret_cast<float*>(smem + Cfg::kOffKb);
     float* red = reinterpret_cast<float*>(smem + Cfg::kOffRed);
-    float* ab = red + 8;
+    float* ab = red + 16;
     // [0] tiles landed, [1] H_j MMAs done, [2] / [3] G passes done
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem + Cfg::kOffBar);
     uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 4);
@@ -448,27 +448,41 @@ __global__ void __launch_bounds__(kTcThreads, 3)
         mbar_wait(&bar[2 + pass], 0);  // the tiles are rewritten by the next pass
         tc_fence_after();
     }
-    // ---- 6. row a of G into registers; Lanczos on G
+    // ---- 6. row a of G into registers; Lanczos on G with delayed
+    // normalisation: the matvec runs on the unnormalised w_m = beta_{m-1} v_m,
+    // and ONE reduction of (|w_m|^2, w_m . G w_m) gives beta_{m-1} and alpha_m
+    // exactly (no cancellation formula) -- one reduction and two barriers per
+    // step instead of two and three; the steps are latency-bound
     tmem_row128(trow, x);
-    float vcur = rsqrtf(float(D)), vprev = 0.f, beta_prev = 0.f;
-    vs[tid] = vcur;
+    float wown = rsqrtf(float(D)), vprev = 0.f, alpha_prev = 0.f;  // w_0 = v_0, |v_0| = 1
+    vs[tid] = wown;
     tc_fence_before();
     __syncthreads();
     if (warp == 0) tmem_dealloc(tmem, 128);
 
     int par = 0;
-    auto block_sum = [&](float v) -> float {
+    auto block_sum2 = [&](float p, float q) -> float2 {
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-        if (lane == 0) red[par * 4 + warp] = v;
+        for (int o = 16; o > 0; o >>= 1) {
+            p += __shfl_xor_sync(0xffffffffu, p, o);
+            q += __shfl_xor_sync(0xffffffffu, q, o);
+        }
+        if (lane == 0) {
+            red[par * 8 + warp * 2] = p;
+            red[par * 8 + warp * 2 + 1] = q;
+        }
         __syncthreads();
-        const float s = (red[par * 4] + red[par * 4 + 1]) + (red[par * 4 + 2] + red[par * 4 + 3]);
+        const float* r = red + par * 8;
         par ^= 1;
-        return s;
+        return make_float2((r[0] + r[2]) + (r[4] + r[6]), (r[1] + r[3]) + (r[5] + r[7]));
     };
     int m = 0;
     for (; m < kLanczos; ++m) {
-        // y_a = G[a] . v (v broadcast from shared memory)
+        if (m > 0) {
+            vs[tid] = wown;  // every read of vs in step m-1 preceded its reduction barrier
+            __syncthreads();
+        }
+        // y_a = G[a] . w (w broadcast from shared memory)
         float2 y0 = make_float2(0.f, 0.f), y1 = y0, y2 = y0, y3 = y0;
 #pragma unroll
         for (int c = 0; c < D; c += 8) {
@@ -479,23 +493,20 @@ __global__ void __launch_bounds__(kTcThreads, 3)
             y2 = ffma2(make_float2(x[c + 4], x[c + 5]), make_float2(w4.x, w4.y), y2);
             y3 = ffma2(make_float2(x[c + 6], x[c + 7]), make_float2(w4.z, w4.w), y3);
         }
-        float y = ((y0.x + y0.y) + (y1.x + y1.y)) + ((y2.x + y2.y) + (y3.x + y3.y));
-        const float alpha = block_sum(vcur * y);
-        y -= alpha * vcur + beta_prev * vprev;
-        const float beta = sqrtf(block_sum(y * y));
-        if (tid == 0) {
-            ab[m] = alpha;
-            ab[kLanczos + m] = beta;
+        const float y = ((y0.x + y0.y) + (y1.x + y1.y)) + ((y2.x + y2.y) + (y3.x + y3.y));
+        const float2 r = block_sum2(wown * wown, wown * y);
+        const float b = m == 0 ? 1.f : sqrtf(r.x);  // beta_{m-1} = |w_m|
+        if (m > 0) {
+            if (tid == 0) ab[kLanczos + m - 1] = b;
+            if (!(b > 1e-30f * fmaxf(1.f, fabsf(alpha_prev)))) break;  // invariant subspace (or D == 0)
         }
-        if (!(beta > 1e-30f * fmaxf(1.f, fabsf(alpha)))) {  // invariant subspace (or D == 0)
-            ++m;
-            break;
-        }
-        vprev = vcur;
-        vcur = y / beta;
-        vs[tid] = vcur;  // every read of v for this step preceded the first barrier above
-        beta_prev = beta;
-        __syncthreads();
+        const float inv = 1.f / b;
+        const float vm = wown * inv;             // v_m
+        const float alpha = r.y * inv * inv;     // v_m . G v_m
+        if (tid == 0) ab[m] = alpha;
+        wown = y * inv - alpha * vm - b * vprev;  // w_{m+1} = G v_m - alpha_m v_m - beta_{m-1} v_{m-1}
+        vprev = vm;
+        alpha_prev = alpha;
     }
     __syncthreads();
     if (warp == 0) ritz_max_and_store(ab, m, lane, a, size_t(bh) * a.N + j);
