@@ -13,7 +13,7 @@ from .pisa import (  # noqa: F401
     pisa_multihead, pisa_reference, pisa_streaming, resolve, select_topk_plain, selftest_mma,
     block_norms, select_topk_covariance, BadMagic, IoError, IoFailure, MalformedFile,
     NonFiniteValue, UnsupportedDtype, UnsupportedVersion,
-    sparsity_to_k, variant_name,
+    sparsity_to_k, variant_name, dense_online,
 )
 
 from . import dit  # noqa: F401,E402  (DiT integration surface: warmup policy, joint attention)

@@ -573,6 +573,21 @@ def pisa_reference(q, k, v, plan, stats, variant: PisaVariant,
     return pisa_attention(q, k, v, sel, stats, cfg, variant, **kw)
 
 
+def dense_online(q, k, v, cfg: AttentionConfig = AttentionConfig()):
+    """dense_online (attention.hpp:186-193): the dense softmax-attention baseline
+    the reference's CLI times PISA against (pisa_cli.cpp:719-723). ``q``/``k``/``v``
+    [L][d] or [..., L, d] CUDA tensors; scale from ``cfg`` (0 -> 1/sqrt(d),
+    attention.hpp:34-37). Runs cuDNN / flash SDPA on the device: a baseline,
+    not the PISA path."""
+    import torch.nn.functional as F
+    scale = cfg.resolved_scale(q.shape[-1])
+    squeeze = q.dim() == 2
+    if squeeze:
+        q, k, v = (t.unsqueeze(0) for t in (q, k, v))
+    o = F.scaled_dot_product_attention(q, k, v, scale=scale)
+    return o.squeeze(0) if squeeze else o
+
+
 def pisa_multihead(bundle: TensorBundle, r: float, router: RouterOptions = RouterOptions(),
                    variant: PisaVariant = PisaVariant.Hybrid,
                    cfg: AttentionConfig = AttentionConfig(), use_streaming: bool = False,

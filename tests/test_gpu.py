@@ -572,3 +572,15 @@ def test_pairing_modes_agree_and_fewer_tiles(P, oracle_mod):
     assert tiles[1] < tiles[0], tiles
     with pytest.raises(P.InvalidDimension):
         ctx.set_pairing(3)
+
+
+@pytest.mark.parametrize("L,d", [(1024, 128), (1000, 64)])
+def test_dense_online_matches_reference(P, oracle_mod, L, d):
+    """dense_online (attention.hpp:186-193), the baseline PISA is timed against,
+    vs the reference's own dense_online through the oracle library."""
+    import torch
+    q, k, v = oracle_mod.gen("gaussian", 9, 1, L, d)
+    o = P.dense_online(*(torch.from_numpy(x[0]).to(torch.bfloat16).cuda() for x in (q, k, v)))
+    ref = oracle_mod.dense(*(torch.from_numpy(x[0]).to(torch.bfloat16).float().numpy() for x in (q, k, v)),
+                           d ** -0.5)
+    check_close(o.float().cpu().numpy(), ref)
