@@ -35,6 +35,7 @@ WORKLOADS = {
     "wan14b": (1, 40, 75600, 128, 0.125, "Wan2.1-14B 720p 81-frame video attention"),
     "wan13b": (1, 12, 32760, 128, 0.125, "Wan2.1-1.3B 480p 81-frame video attention"),
     "flux": (1, 24, 4608, 128, 0.125, "FLUX.1 1024px image DiT attention"),
+    "sd35": (1, 24, 4429, 64, 0.125, "SD3.5-Medium 1024px joint attention (4096 image + 333 text tokens, d=64)"),
     "hunyuan": (1, 24, 118800, 128, 0.125, "HunyuanVideo 720p 129-frame attention"),
     "smoke": (1, 2, 4096, 64, 0.25, "CPU-oracle smoke"),
 }
