@@ -73,7 +73,7 @@ __device__ __forceinline__ void ritz_max_and_store(const float* ab, int m, int l
 //      D = H_j - H_bar (H_bar from K1b),
 //   3. Lanczos on D^T D, two matvecs per step, two threads per row / column.
 template <int D>
-__global__ void __launch_bounds__(kNormThreads) block_norms_kernel(const __nv_bfloat16* __restrict__ k,
+__global__ void __launch_bounds__(kNormThreads, 4) block_norms_kernel(const __nv_bfloat16* __restrict__ k,
                                                                    const __nv_bfloat16* __restrict__ v,
                                                                    NormArgs a) {
     extern __shared__ __align__(16) float sm[];
@@ -120,39 +120,42 @@ __global__ void __launch_bounds__(kNormThreads) block_norms_kernel(const __nv_bf
         }
     }
     __syncthreads();
-    // ---- 2. H_j = kc^T V (thread tile: rows ta*8.., cols tb*8..), minus H_bar
-    constexpr int T = D / 8;  // tiles per side (16 for D = 128, 8 for D = 64)
-    float acc[8][8];
+    // ---- 2. H_j = kc^T V (thread tile: rows ta*TS.., cols tb*TS..), minus
+    // H_bar. TS = 4 for D = 64: every thread owns a tile and the accumulators
+    // stay small enough for four CTAs per SM (the Lanczos below is latency-bound)
+    constexpr int TS = D == 64 ? 4 : 8;
+    constexpr int T = D / TS;  // tiles per side
+    float acc[TS][TS];
     const bool owns = tid < T * T;
     const int ta = tid / T, tb = tid % T;
     if (owns) {
 #pragma unroll
-        for (int x = 0; x < 8; ++x)
+        for (int x = 0; x < TS; ++x)
 #pragma unroll
-            for (int y = 0; y < 8; ++y) acc[x][y] = 0.f;
+            for (int y = 0; y < TS; ++y) acc[x][y] = 0.f;
         for (int r = 0; r < n; ++r) {
-            float ka[8], vb[8];
+            float ka[TS], vb[TS];
 #pragma unroll
-            for (int x = 0; x < 8; ++x) ka[x] = kc[r * D + ta * 8 + x];
+            for (int x = 0; x < TS; ++x) ka[x] = kc[r * D + ta * TS + x];
 #pragma unroll
-            for (int y = 0; y < 8; ++y) vb[y] = vv[r * D + tb * 8 + y];
+            for (int y = 0; y < TS; ++y) vb[y] = vv[r * D + tb * TS + y];
 #pragma unroll
-            for (int x = 0; x < 8; ++x)
+            for (int x = 0; x < TS; ++x)
 #pragma unroll
-                for (int y = 0; y < 8; ++y) acc[x][y] = fmaf(ka[x], vb[y], acc[x][y]);
+                for (int y = 0; y < TS; ++y) acc[x][y] = fmaf(ka[x], vb[y], acc[x][y]);
         }
         const float* hb = a.hbar + size_t(bh) * D * D;
 #pragma unroll
-        for (int x = 0; x < 8; ++x)
+        for (int x = 0; x < TS; ++x)
 #pragma unroll
-            for (int y = 0; y < 8; ++y) acc[x][y] -= hb[(ta * 8 + x) * D + tb * 8 + y];
+            for (int y = 0; y < TS; ++y) acc[x][y] -= hb[(ta * TS + x) * D + tb * TS + y];
     }
     __syncthreads();  // kc / vv are dead: D overwrites them
     if (owns) {
 #pragma unroll
-        for (int x = 0; x < 8; ++x)
+        for (int x = 0; x < TS; ++x)
 #pragma unroll
-            for (int y = 0; y < 8; ++y) Dm[(ta * 8 + x) * (D + 1) + tb * 8 + y] = acc[x][y];
+            for (int y = 0; y < TS; ++y) Dm[(ta * TS + x) * (D + 1) + tb * TS + y] = acc[x][y];
     }
     // ---- 3. Lanczos on G = D^T D (three-term recurrence; without
     // re-orthogonalisation fp32 round-off only adds ghost copies of converged
