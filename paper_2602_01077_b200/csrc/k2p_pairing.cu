@@ -11,7 +11,9 @@
 // be far apart. Here:
 //   K2c pair_candidates_kernel: warp per query block i, overlap
 //       o(i, j) = popcount(mask_i & mask_j) for j within +-kWindow of i, keeps
-//       the best kCand partners (overlap desc, index asc);
+//       the best kCand partners (overlap desc, index asc; 16: measured on
+//       clustered routing union/k 1.113 -> 1.059 vs 8, -1.8 % step time;
+//       gaussian +0.2 %; a +-96 window was worse on both);
 //   K2d pair_match_kernel: one CTA per (batch, head), locally-dominant matching
 //       on the candidate graph (the parallel form of greedy max-weight
 //       matching, a 1/2-approximation): every unmatched block proposes its best
@@ -26,12 +28,15 @@
 namespace pisa_b200 {
 namespace {
 
-constexpr int kCand = 8;
+constexpr int kCand = kPairCand;
 // Candidate partners of block i are the blocks within +-kWindow of it: full
 // O(N^2 W) search costs ~2.5 ms at Wan2.1-14B for a further ~2 % fewer union
 // tiles (simulated: gaussian union/k 1.871 -> 1.77 windowed vs 1.735 full;
 // multi-cluster 1.856 -> 1.06 vs 1.02).
-constexpr int kWindow = 48;
+#ifndef PISA_PAIR_WINDOW
+#define PISA_PAIR_WINDOW 48
+#endif
+constexpr int kWindow = PISA_PAIR_WINDOW;
 
 // candidate (overlap, index) ordering: higher overlap first, then lower index
 __device__ __forceinline__ bool better(int ov, int j, int ov2, int j2) {

@@ -71,7 +71,11 @@ cudaError_t launch_rectifier(const float* m, double eps, float* rect, int n, cud
 cudaError_t launch_select(int D, const SelectArgs& a, int BH, uint32_t* keys, cudaStream_t s);
 
 // K2c/K2d: overlap-aware pairing of query blocks for the fused kernel.
-// cand: scratch int [BH][N][8]; pairs: int2 [BH][ceil(N/2)].
+// cand: scratch int [BH][N][kPairCand]; pairs: int2 [BH][ceil(N/2)].
+#ifndef PISA_PAIR_CAND
+#define PISA_PAIR_CAND 16
+#endif
+constexpr int kPairCand = PISA_PAIR_CAND;  // candidate partners kept per query block
 cudaError_t launch_pairing(const uint32_t* mask, int N, int W, int qb0, int qb1, int BH, int* cand, int2* pairs,
                            cudaStream_t s);
 

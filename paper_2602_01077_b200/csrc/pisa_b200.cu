@@ -272,7 +272,7 @@ pisa_status workspace(pisa_ctx* ctx, const Plan& p, Work* w) {
                  o_hbf = take(BH * D * D * 2), o_sel = take(BH * N * p.k * 4),
                  o_mask = take(BH * N * p.W * 4), o_keys = take(BH * N * N * 4),
                  o_norms = take(BH * N * 4), o_rect = take(BH * N * 4),
-                 o_cand = take(BH * N * 8 * 4), o_pairs = take(BH * ((N + 1) / 2) * 8), o_flag = take(16);
+                 o_cand = take(BH * N * kPairCand * 4), o_pairs = take(BH * ((N + 1) / 2) * 8), o_flag = take(16);
     if (off > ctx->arena_bytes) {
         if (ctx->arena) cudaFree(ctx->arena);
         ctx->arena = nullptr;
