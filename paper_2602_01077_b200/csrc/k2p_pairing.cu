@@ -45,16 +45,21 @@ __device__ __forceinline__ bool better(int ov, int j, int ov2, int j2) {
 
 __global__ void __launch_bounds__(256) pair_candidates_kernel(const uint32_t* __restrict__ mask, int N,
                                                              int W, int qb0, int qb1, int* __restrict__ cand) {
-    extern __shared__ uint32_t mrow[];  // [8 warps][W]
+    // The CTA's 8 query blocks share one window: its rows [wb, we) are staged
+    // in shared memory with coalesced loads (a W-word row stride with W odd is
+    // conflict-free across lanes reading 32 consecutive rows; even W costs a
+    // 2-way conflict at most for the W <= 128 this path sees).
+    extern __shared__ uint32_t mrow[];  // [we - wb][W]
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int bh = blockIdx.y;
-    const int i = qb0 + blockIdx.x * 8 + warp;
-    uint32_t* mi = mrow + warp * W;
+    const int ib = qb0 + blockIdx.x * 8;
+    const int i = ib + warp;
+    const int wb = max(qb0, ib - kWindow), we = min(qb1, ib + 8 + kWindow);
     const uint32_t* M = mask + size_t(bh) * N * W;
-    if (i < qb1)
-        for (int w = lane; w < W; w += 32) mi[w] = M[size_t(i) * W + w];
-    __syncwarp();
+    for (int e = threadIdx.x; e < (we - wb) * W; e += blockDim.x) mrow[e] = __ldg(M + size_t(wb) * W + e);
+    __syncthreads();
     if (i >= qb1) return;
+    const uint32_t* mi = mrow + (i - wb) * W;
     int bo[kCand], bj[kCand];
 #pragma unroll
     for (int c = 0; c < kCand; ++c) {
@@ -64,7 +69,7 @@ __global__ void __launch_bounds__(256) pair_candidates_kernel(const uint32_t* __
     const int j0 = max(qb0, i - kWindow), j1 = min(qb1, i + kWindow + 1);
     for (int j = j0 + lane; j < j1; j += 32) {
         if (j == i) continue;
-        const uint32_t* mj = M + size_t(j) * W;
+        const uint32_t* mj = mrow + (j - wb) * W;
         int ov = 0;
         for (int w = 0; w < W; ++w) ov += __popc(mi[w] & mj[w]);
         if (better(ov, j, bo[kCand - 1], bj[kCand - 1])) {  // insert into the sorted list
@@ -157,7 +162,7 @@ __global__ void __launch_bounds__(1024) pair_match_kernel(const int* __restrict_
 
 cudaError_t launch_pairing(const uint32_t* mask, int N, int W, int qb0, int qb1, int BH, int* cand,
                            int2* pairs, cudaStream_t s) {
-    const size_t sm1 = size_t(8) * W * 4;
+    const size_t sm1 = size_t(8 + 2 * kWindow) * W * 4;
     cudaFuncSetAttribute(pair_candidates_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm1));
     pair_candidates_kernel<<<dim3((qb1 - qb0 + 7) / 8, BH), 256, sm1, s>>>(mask, N, W, qb0, qb1, cand);
     cudaError_t e = cudaGetLastError();
