@@ -584,3 +584,50 @@ def test_dense_online_matches_reference(P, oracle_mod, L, d):
     ref = oracle_mod.dense(*(torch.from_numpy(x[0]).to(torch.bfloat16).float().numpy() for x in (q, k, v)),
                            d ** -0.5)
     check_close(o.float().cpu().numpy(), ref)
+
+
+def _random_configs(n, seed=2602):
+    rng = np.random.default_rng(seed)
+    out = []
+    for _ in range(n):
+        out.append(dict(kind=str(rng.choice(["gaussian", "clustered"])), H=int(rng.integers(1, 4)),
+                        L=int(rng.integers(65, 5000)), d=int(rng.choice([64, 128])),
+                        r=float(rng.choice([0.5, 0.75, 0.875, 0.95])),
+                        variant=str(rng.choice(["hybrid", "zeroth", "sparse_only", "global_centroid"])),
+                        router=str(rng.choice(["plain", "covariance"])), pairing=int(rng.choice([0, 2])),
+                        layout=str(rng.choice(["bhld", "blhd"])), seed=int(rng.integers(0, 1 << 16))))
+    return out
+
+
+@pytest.mark.parametrize("cfg", _random_configs(32), ids=lambda c: "-".join(str(v) for v in c.values()))
+def test_randomized_shapes_match_oracle(P, oracle_mod, cfg):
+    """Seeded random shapes (ragged L, d 64 / 128), variants, routers, layouts
+    and pairing modes: the fused output equals the oracle's attention on the
+    GPU's own plan (max abs <= 2e-2, cosine >= 0.999)."""
+    import torch
+    O = oracle_mod
+    V = {"hybrid": P.PisaVariant.Hybrid, "zeroth": P.PisaVariant.Zeroth,
+         "sparse_only": P.PisaVariant.SparseOnly, "global_centroid": P.PisaVariant.GlobalCentroid}
+    q, k, v = O.gen(cfg["kind"], cfg["seed"], cfg["H"], cfg["L"], cfg["d"])
+    to = lambda x: torch.from_numpy(np.ascontiguousarray(x)).to(torch.bfloat16).cuda().unsqueeze(0)
+    qd, kd, vd = to(q), to(k), to(v)
+    if cfg["layout"] == "blhd":
+        qd, kd, vd = (t.transpose(1, 2).contiguous() for t in (qd, kd, vd))
+    router = P.RouterStrategy.CovarianceAware if cfg["router"] == "covariance" else P.RouterStrategy.Plain
+    ctx = P.Context.get(0)
+    ctx.set_pairing(cfg["pairing"])
+    try:
+        out, ex = P.fwd(qd, kd, vd, layout=cfg["layout"], out_dtype=torch.float32, return_plan=True,
+                        sparsity=cfg["r"], variant=V[cfg["variant"]], router=router)
+        torch.cuda.synchronize()
+    finally:
+        ctx.set_pairing(1)
+    if cfg["layout"] == "blhd":
+        out = out.transpose(1, 2)
+    out = out[0].cpu().numpy()
+    sel = ex["selected"][0].cpu().numpy()
+    scale = cfg["d"] ** -0.5
+    for h in range(cfg["H"]):
+        st = O.block_stats(k[h], v[h])
+        ref = O.pisa_attention(q[h], k[h], v[h], sel[h], st, scale, cfg["variant"])[0]
+        check_close(out[h], ref)
