@@ -25,7 +25,10 @@ using namespace pisa_sm100;
 namespace {
 
 constexpr int kNormThreads = 256;
-constexpr int kLanczos = 24;  // fp32-converged (<5e-8 rel.) on gaussian / clustered blocks
+#ifndef PISA_LANCZOS_STEPS
+#define PISA_LANCZOS_STEPS 24
+#endif
+constexpr int kLanczos = PISA_LANCZOS_STEPS;  // fp32-converged (<5e-8 rel.) on gaussian / clustered blocks
 
 // Largest eigenvalue of the m x m Lanczos tridiagonal (alpha = ab[0..m),
 // beta = ab[kLanczos..]) by a 32-way multisection on its Sturm count (the
@@ -470,6 +473,10 @@ __global__ void __launch_bounds__(kTcThreads, 3)
             p += __shfl_xor_sync(0xffffffffu, p, o);
             q += __shfl_xor_sync(0xffffffffu, q, o);
         }
+#if PISA_K1C_DIAG_WARPSUM  // diagnostic only (wrong numerics): warp-local sums, no CTA barrier
+        par ^= 1;
+        return make_float2(4.f * p, 4.f * q);
+#endif
         if (lane == 0) {
             red[par * 8 + warp * 2] = p;
             red[par * 8 + warp * 2 + 1] = q;
