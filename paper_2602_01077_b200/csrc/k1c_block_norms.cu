@@ -338,6 +338,14 @@ __global__ void __launch_bounds__(kTcThreads, 3)
 #pragma unroll
         for (int i = 0; i < 4; ++i) mbar_init(&bar[i], 1);
         fence_mbar_init();
+        // K_j / V_j first: their latency overlaps the TMEM allocation and the
+        // CTA barrier below
+        mbar_expect_tx(&bar[0], 2 * Cfg::kTile);
+#pragma unroll
+        for (int half = 0; half < 2; ++half) {
+            tma_load_4d(smem + half * 8192, &tmK, &bar[0], half * 64, j * 64, h, b);
+            tma_load_4d(smem + Cfg::kOffV + half * 8192, &tmV, &bar[0], half * 64, j * 64, h, b);
+        }
     }
     if (warp == 0) {
         tmem_alloc(tslot, 128);
@@ -349,17 +357,6 @@ __global__ void __launch_bounds__(kTcThreads, 3)
     tc_fence_after();
     const uint32_t tmem = *tslot;
     const uint32_t trow = tmem + (uint32_t(warp * 32) << 16);  // this thread's TMEM lane = tid
-    if (warp == 0) {
-        if (elect_one()) {
-            mbar_expect_tx(&bar[0], 2 * Cfg::kTile);
-#pragma unroll
-            for (int half = 0; half < 2; ++half) {
-                tma_load_4d(smem + half * 8192, &tmK, &bar[0], half * 64, j * 64, h, b);
-                tma_load_4d(smem + Cfg::kOffV + half * 8192, &tmV, &bar[0], half * 64, j * 64, h, b);
-            }
-        }
-        __syncwarp();
-    }
     mbar_wait(&bar[0], 0);
 
     // ---- 2. centre and split, one 16-byte chunk (8 keys of one row) at a time
