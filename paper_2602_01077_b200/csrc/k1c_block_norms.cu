@@ -357,6 +357,26 @@ __global__ void __launch_bounds__(kTcThreads, 3)
     tc_fence_after();
     const uint32_t tmem = *tslot;
     const uint32_t trow = tmem + (uint32_t(warp * 32) << 16);  // this thread's TMEM lane = tid
+    // -H_bar into this thread's TMEM row, the accumulator the H_j MMAs add to
+    // (so they produce D = H_j - H_bar directly): the H_bar load latency
+    // overlaps the K / V TMA and the split instead of following the MMAs
+    {
+        const float4* hb = reinterpret_cast<const float4*>(a.hbar + (size_t(bh) * D + tid) * D);
+#pragma unroll
+        for (int cc = 0; cc < D / 32; ++cc) {
+            uint32_t r[32];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const float4 hv = __ldg(hb + cc * 8 + i);
+                r[4 * i] = __float_as_uint(-hv.x);
+                r[4 * i + 1] = __float_as_uint(-hv.y);
+                r[4 * i + 2] = __float_as_uint(-hv.z);
+                r[4 * i + 3] = __float_as_uint(-hv.w);
+            }
+            tmem_st32(trow + cc * 32, r);
+        }
+        tmem_st_wait();
+    }
     mbar_wait(&bar[0], 0);
 
     // ---- 2. centre and split, one 16-byte chunk (8 keys of one row) at a time
@@ -380,6 +400,7 @@ __global__ void __launch_bounds__(kTcThreads, 3)
         *reinterpret_cast<uint4*>(smem + 2 * Cfg::kTile + ci * 16) = lw;
     }
     fence_proxy_async();  // generic-proxy tile writes -> tcgen05 operand reads
+    tc_fence_before();    // the -H_bar TMEM stores precede the MMAs
     __syncthreads();
 
     constexpr uint32_t idesc = idesc_bf16(128, 128, 1, 1);
@@ -392,7 +413,7 @@ __global__ void __launch_bounds__(kTcThreads, 3)
 #pragma unroll
             for (int part = 2; part >= 0; --part)
 #pragma unroll
-                for (int ks = 0; ks < 4; ++ks) mma_ss(tmem, desc(part, ks), desc(3, ks), idesc, part != 2 || ks != 0);
+                for (int ks = 0; ks < 4; ++ks) mma_ss(tmem, desc(part, ks), desc(3, ks), idesc, 1u);
             mma_commit(&bar[1]);
         }
         __syncwarp();
@@ -400,20 +421,9 @@ __global__ void __launch_bounds__(kTcThreads, 3)
     mbar_wait(&bar[1], 0);
     tc_fence_after();
 
-    // ---- 4. row a = tid of D = H_j - H_bar
+    // ---- 4. row a = tid of D = H_j - H_bar (the accumulator started at -H_bar)
     float x[D];
     tmem_row128(trow, x);
-    {
-        const float4* hb = reinterpret_cast<const float4*>(a.hbar + (size_t(bh) * D + tid) * D);
-#pragma unroll
-        for (int i = 0; i < D / 4; ++i) {
-            const float4 hv = __ldg(hb + i);
-            x[4 * i] -= hv.x;
-            x[4 * i + 1] -= hv.y;
-            x[4 * i + 2] -= hv.z;
-            x[4 * i + 3] -= hv.w;
-        }
-    }
     // ---- 5. G = D^T D, rows of D 64 at a time through the split tiles
 #pragma unroll
     for (int pass = 0; pass < 2; ++pass) {
