@@ -16,6 +16,8 @@
 //     G = D^T D on the tensor cores, Lanczos on G from registers;
 //   * block_norms_kernel<64>: CUDA-core H_j and Lanczos on D^T D as two
 //     matvecs per step (D = 64 is 8x less work per block).
+#include <type_traits>
+
 #include "kernels.h"
 #include "sm100.cuh"
 
@@ -25,6 +27,10 @@ using namespace pisa_sm100;
 namespace {
 
 constexpr int kNormThreads = 256;
+#ifndef PISA_K1C_PAIR_D64
+#define PISA_K1C_PAIR_D64 1  // d = 64: the paired tensor-core kernel (0: CUDA-core kernel)
+#endif
+constexpr bool kK1cPairD64 = PISA_K1C_PAIR_D64 != 0;
 #ifndef PISA_LANCZOS_STEPS
 #define PISA_LANCZOS_STEPS 24
 #endif
@@ -277,7 +283,7 @@ struct TcCfg {
     static constexpr int kOffVec = 4 * kTile;             // Lanczos vector [128]
     static constexpr int kOffKb = kOffVec + 128 * 4;      // k_bar_j [128]
     static constexpr int kOffRed = kOffKb + 128 * 4;      // [2][4][2] reduction scratch, alpha / beta
-    static constexpr int kOffBar = (kOffRed + (16 + 2 * kLanczos) * 4 + 7) & ~7;
+    static constexpr int kOffBar = (kOffRed + (16 + 4 * kLanczos) * 4 + 7) & ~7;  // alpha / beta x 2 halves
     static constexpr int kSmem = 1024 + kOffBar + 48;
 };
 
@@ -315,11 +321,20 @@ __device__ __forceinline__ void tmem_row128(uint32_t taddr, float (&x)[128]) {
     }
 }
 
+// kPair (head dim 64): two key blocks per CTA in the same 128-wide shapes.
+// Block j0 fills TMA half 0 (d columns 0-63 of the MN-major operands), block
+// j1 = j0 + 1 half 1, so one M = N = 128 MMA yields H_j0 and H_j1 on its
+// diagonal quadrants (the cross quadrants pair one block's keys with the
+// other's values and are dropped). D is then block-diagonal, so G = D^T D is
+// blockdiag(G_j0, G_j1), and threads 0-63 / 64-127 run two independent
+// Lanczos processes on their quadrants.
+template <bool kPair>
 __global__ void __launch_bounds__(kTcThreads, 3)
     block_norms_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
                           NormArgs a) {
     using Cfg = TcCfg;
-    constexpr int D = 128;
+    constexpr int D = 128;   // MMA / register width
+    constexpr int DR = kPair ? 64 : 128;  // head dim
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     float* vs = reinterpret_cast<float*>(smem + Cfg::kOffVec);
@@ -329,10 +344,12 @@ __global__ void __launch_bounds__(kTcThreads, 3)
     // [0] tiles landed, [1] H_j MMAs done, [2] / [3] G passes done
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem + Cfg::kOffBar);
     uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 4);
-    const int j = blockIdx.x, bh = blockIdx.y;
+    const int j = kPair ? 2 * blockIdx.x : blockIdx.x, bh = blockIdx.y;
     const int b = bh / a.H, h = bh % a.H;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int hq = tid >> 6;  // kPair: this thread's block (quadrant)
     const int n = min(64, a.L - j * 64);
+    const int n1 = kPair ? min(64, a.L - (j + 1) * 64) : n;  // rows of block j + 1 (<= 0: absent)
 
     if (tid == 0) {
 #pragma unroll
@@ -343,15 +360,20 @@ __global__ void __launch_bounds__(kTcThreads, 3)
         mbar_expect_tx(&bar[0], 2 * Cfg::kTile);
 #pragma unroll
         for (int half = 0; half < 2; ++half) {
-            tma_load_4d(smem + half * 8192, &tmK, &bar[0], half * 64, j * 64, h, b);
-            tma_load_4d(smem + Cfg::kOffV + half * 8192, &tmV, &bar[0], half * 64, j * 64, h, b);
+            // kPair: half = block j + half, all 64 columns; else: column half of block j
+            const int c0 = kPair ? 0 : half * 64, r0 = (kPair ? j + half : j) * 64;
+            tma_load_4d(smem + half * 8192, &tmK, &bar[0], c0, r0, h, b);
+            tma_load_4d(smem + Cfg::kOffV + half * 8192, &tmV, &bar[0], c0, r0, h, b);
         }
     }
     if (warp == 0) {
         tmem_alloc(tslot, 128);
         tmem_relinquish();
     }
-    kb[tid] = a.kbar[(size_t(bh) * a.N + j) * D + tid];
+    if constexpr (kPair)
+        kb[tid] = (j + hq < a.N) ? a.kbar[(size_t(bh) * a.N + j + hq) * DR + (tid & 63)] : 0.f;
+    else
+        kb[tid] = a.kbar[(size_t(bh) * a.N + j) * D + tid];
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
@@ -361,13 +383,15 @@ __global__ void __launch_bounds__(kTcThreads, 3)
     // (so they produce D = H_j - H_bar directly): the H_bar load latency
     // overlaps the K / V TMA and the split instead of following the MMAs
     {
-        const float4* hb = reinterpret_cast<const float4*>(a.hbar + (size_t(bh) * D + tid) * D);
+        // kPair: row a of block hq gets -H_bar[a % 64] in its own quadrant, 0 in the other
+        const float4* hb = reinterpret_cast<const float4*>(a.hbar + (size_t(bh) * DR + (kPair ? (tid & 63) : tid)) * DR);
 #pragma unroll
         for (int cc = 0; cc < D / 32; ++cc) {
             uint32_t r[32];
+            const bool own = !kPair || (cc >> 1) == hq;
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
-                const float4 hv = __ldg(hb + cc * 8 + i);
+                const float4 hv = own ? __ldg(hb + (kPair ? (cc & 1) : cc) * 8 + i) : make_float4(0.f, 0.f, 0.f, 0.f);
                 r[4 * i] = __float_as_uint(-hv.x);
                 r[4 * i + 1] = __float_as_uint(-hv.y);
                 r[4 * i + 2] = __float_as_uint(-hv.z);
@@ -391,8 +415,9 @@ __global__ void __launch_bounds__(kTcThreads, 3)
 #pragma unroll
         for (int t = 0; t < 4; ++t) {
             const float2 kf = __bfloat1622float2(k2[t]);
-            const float x0 = r < n ? kf.x - kb[d0 + 2 * t] : 0.f;
-            const float x1 = r < n ? kf.y - kb[d0 + 2 * t + 1] : 0.f;
+            const int nr = (kPair && (ci >> 9)) ? n1 : n;  // rows of this half's block
+            const float x0 = r < nr ? kf.x - kb[d0 + 2 * t] : 0.f;
+            const float x1 = r < nr ? kf.y - kb[d0 + 2 * t + 1] : 0.f;
             split3(x0, x1, (&hw.x)[t], (&mw.x)[t], (&lw.x)[t]);
         }
         *reinterpret_cast<uint4*>(smem + ci * 16) = hw;
@@ -424,6 +449,11 @@ __global__ void __launch_bounds__(kTcThreads, 3)
     // ---- 4. row a = tid of D = H_j - H_bar (the accumulator started at -H_bar)
     float x[D];
     tmem_row128(trow, x);
+    if constexpr (kPair) {  // drop the cross quadrant: D = blockdiag(D_j0, D_j1)
+#pragma unroll
+        for (int c = 0; c < D; ++c)
+            if ((c >> 6) != hq) x[c] = 0.f;
+    }
     // ---- 5. G = D^T D, rows of D 64 at a time through the split tiles
 #pragma unroll
     for (int pass = 0; pass < 2; ++pass) {
@@ -467,7 +497,7 @@ __global__ void __launch_bounds__(kTcThreads, 3)
     // exactly (no cancellation formula) -- one reduction and two barriers per
     // step instead of two and three; the steps are latency-bound
     tmem_row128(trow, x);
-    float wown = rsqrtf(float(D)), vprev = 0.f, alpha_prev = 0.f;  // w_0 = v_0, |v_0| = 1
+    float wown = rsqrtf(float(DR)), vprev = 0.f, alpha_prev = 0.f;  // w_0 = v_0, |v_0| = 1
     vs[tid] = wown;
     tc_fence_before();
     __syncthreads();
@@ -491,42 +521,61 @@ __global__ void __launch_bounds__(kTcThreads, 3)
         __syncthreads();
         const float* r = red + par * 8;
         par ^= 1;
+        if constexpr (kPair)  // the two warps of this thread's block
+            return make_float2(r[4 * hq] + r[4 * hq + 2], r[4 * hq + 1] + r[4 * hq + 3]);
         return make_float2((r[0] + r[2]) + (r[4] + r[6]), (r[1] + r[3]) + (r[5] + r[7]));
     };
-    int m = 0;
-    for (; m < kLanczos; ++m) {
+    float* abq = ab + (kPair ? hq * 2 * kLanczos : 0);  // this block's alpha / beta
+    const bool lead = (tid & (kPair ? 63 : 127)) == 0;
+    bool done = false;  // kPair: a block's Lanczos may stop earlier than the other's
+    int mq = kLanczos;
+    for (int m = 0; m < kLanczos; ++m) {
         if (m > 0) {
             vs[tid] = wown;  // every read of vs in step m-1 preceded its reduction barrier
             __syncthreads();
         }
-        // y_a = G[a] . w (w broadcast from shared memory)
+        // y_a = G[a] . w (w broadcast from shared memory; kPair: own quadrant)
         float2 y0 = make_float2(0.f, 0.f), y1 = y0, y2 = y0, y3 = y0;
+        auto matvec = [&](auto c_begin) {
+            constexpr int cb = decltype(c_begin)::value;
 #pragma unroll
-        for (int c = 0; c < D; c += 8) {
-            const float4 v4 = *reinterpret_cast<const float4*>(vs + c);
-            const float4 w4 = *reinterpret_cast<const float4*>(vs + c + 4);
-            y0 = ffma2(make_float2(x[c], x[c + 1]), make_float2(v4.x, v4.y), y0);
-            y1 = ffma2(make_float2(x[c + 2], x[c + 3]), make_float2(v4.z, v4.w), y1);
-            y2 = ffma2(make_float2(x[c + 4], x[c + 5]), make_float2(w4.x, w4.y), y2);
-            y3 = ffma2(make_float2(x[c + 6], x[c + 7]), make_float2(w4.z, w4.w), y3);
-        }
+            for (int c = cb; c < cb + (kPair ? 64 : D); c += 8) {
+                const float4 v4 = *reinterpret_cast<const float4*>(vs + c);
+                const float4 w4 = *reinterpret_cast<const float4*>(vs + c + 4);
+                y0 = ffma2(make_float2(x[c], x[c + 1]), make_float2(v4.x, v4.y), y0);
+                y1 = ffma2(make_float2(x[c + 2], x[c + 3]), make_float2(v4.z, v4.w), y1);
+                y2 = ffma2(make_float2(x[c + 4], x[c + 5]), make_float2(w4.x, w4.y), y2);
+                y3 = ffma2(make_float2(x[c + 6], x[c + 7]), make_float2(w4.z, w4.w), y3);
+            }
+        };
+        if (!kPair || hq == 0)
+            matvec(std::integral_constant<int, 0>{});
+        else
+            matvec(std::integral_constant<int, 64>{});
         const float y = ((y0.x + y0.y) + (y1.x + y1.y)) + ((y2.x + y2.y) + (y3.x + y3.y));
         const float2 r = block_sum2(wown * wown, wown * y);
+        if (done) continue;  // (kPair) keep joining the barriers
         const float b = m == 0 ? 1.f : sqrtf(r.x);  // beta_{m-1} = |w_m|
         if (m > 0) {
-            if (tid == 0) ab[kLanczos + m - 1] = b;
-            if (!(b > 1e-30f * fmaxf(1.f, fabsf(alpha_prev)))) break;  // invariant subspace (or D == 0)
+            if (lead) abq[kLanczos + m - 1] = b;
+            if (!(b > 1e-30f * fmaxf(1.f, fabsf(alpha_prev)))) {  // invariant subspace (or D == 0)
+                done = true;
+                mq = m;
+                if constexpr (!kPair) break;
+                continue;
+            }
         }
         const float inv = 1.f / b;
         const float vm = wown * inv;             // v_m
         const float alpha = r.y * inv * inv;     // v_m . G v_m
-        if (tid == 0) ab[m] = alpha;
+        if (lead) abq[m] = alpha;
         wown = y * inv - alpha * vm - b * vprev;  // w_{m+1} = G v_m - alpha_m v_m - beta_{m-1} v_{m-1}
         vprev = vm;
         alpha_prev = alpha;
     }
     __syncthreads();
-    if (warp == 0) ritz_max_and_store(ab, m, lane, a, size_t(bh) * a.N + j);
+    if (warp == 0) ritz_max_and_store(abq, mq, lane, a, size_t(bh) * a.N + j);
+    if (kPair && warp == 2 && j + 1 < a.N) ritz_max_and_store(abq, mq, lane, a, size_t(bh) * a.N + j + 1);
 }
 
 }  // namespace
@@ -545,8 +594,12 @@ cudaError_t launch_block_norms(int D, const CUtensorMap& tmK, const CUtensorMap&
     const size_t smem = block_norms_smem_bytes(D);
     dim3 grid(a.N, BH);
     if (D == 128) {
-        cudaFuncSetAttribute(block_norms_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-        block_norms_tc_kernel<<<grid, kTcThreads, smem, s>>>(tmK, tmV, a);
+        cudaFuncSetAttribute(block_norms_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        block_norms_tc_kernel<false><<<grid, kTcThreads, smem, s>>>(tmK, tmV, a);
+    } else if (kK1cPairD64) {  // two key blocks per CTA on the tensor cores
+        const size_t smem2 = TcCfg::kSmem;
+        cudaFuncSetAttribute(block_norms_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem2));
+        block_norms_tc_kernel<true><<<dim3((a.N + 1) / 2, BH), kTcThreads, smem2, s>>>(tmK, tmV, a);
     } else {
         auto kern = block_norms_kernel<64>;
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
