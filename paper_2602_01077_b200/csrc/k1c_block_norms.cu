@@ -34,6 +34,9 @@ constexpr bool kK1cPairD64 = PISA_K1C_PAIR_D64 != 0;
 #ifndef PISA_LANCZOS_STEPS
 #define PISA_LANCZOS_STEPS 24
 #endif
+#ifndef PISA_K1C_CLOCKS
+#define PISA_K1C_CLOCKS 0  // diagnostic: 1..5 store a phase's cycles in place of M_j
+#endif
 constexpr int kLanczos = PISA_LANCZOS_STEPS;  // fp32-converged (<5e-8 rel.) on gaussian / clustered blocks
 
 // Largest eigenvalue of the m x m Lanczos tridiagonal (alpha = ab[0..m),
@@ -72,6 +75,21 @@ __device__ __forceinline__ void ritz_max_and_store(const float* ab, int m, int l
         a.m[o] = float(sigma);
         if (a.rect) a.rect[o] = float(log(sigma + a.eps));
     }
+}
+
+// The extreme Ritz value off the K1c CTA: the tensor-core kernel stores each
+// block's tridiagonal (alpha, beta, step count) and exits, and this kernel runs
+// the multisection with one warp per key block at full occupancy, where the
+// dependent Sturm chains of many blocks overlap. Inside K1c the single-warp
+// multisection held the CTA's 64 KB of registers and 67 KB of shared memory for
+// ~22K cycles, 28% of the CTA's lifetime (PISA_K1C_CLOCKS=2).
+constexpr int kRitzWarps = 8;
+static_assert(2 * kLanczos <= kTriStride, "tridiagonal row does not fit");
+__global__ void __launch_bounds__(32 * kRitzWarps) ritz_kernel(NormArgs a, int nblk) {
+    const int w = blockIdx.x * kRitzWarps + int(threadIdx.x >> 5);
+    if (w >= nblk) return;
+    const float* ab = a.tri + size_t(w) * kTriStride;
+    ritz_max_and_store(ab, __float_as_int(ab[2 * kLanczos - 1]), threadIdx.x & 31, a, size_t(w));
 }
 
 // ---------------------------------------------------------------------------
@@ -350,6 +368,10 @@ __global__ void __launch_bounds__(kTcThreads, 3)
     const int hq = tid >> 6;  // kPair: this thread's block (quadrant)
     const int n = min(64, a.L - j * 64);
     const int n1 = kPair ? min(64, a.L - (j + 1) * 64) : n;  // rows of block j + 1 (<= 0: absent)
+#if PISA_K1C_CLOCKS  // diagnostic build: M_j is replaced by a phase's cycle count
+    const long long t0 = clock64();
+    long long t1 = 0, t4 = 0, t5 = 0;
+#endif
 
     if (tid == 0) {
 #pragma unroll
@@ -402,6 +424,9 @@ __global__ void __launch_bounds__(kTcThreads, 3)
         tmem_st_wait();
     }
     mbar_wait(&bar[0], 0);
+#if PISA_K1C_CLOCKS
+    t1 = clock64();
+#endif
 
     // ---- 2. centre and split, one 16-byte chunk (8 keys of one row) at a time
 #pragma unroll 2
@@ -497,6 +522,9 @@ __global__ void __launch_bounds__(kTcThreads, 3)
     // exactly (no cancellation formula) -- one reduction and two barriers per
     // step instead of two and three; the steps are latency-bound
     tmem_row128(trow, x);
+#if PISA_K1C_CLOCKS
+    t4 = clock64();
+#endif
     float wown = rsqrtf(float(DR)), vprev = 0.f, alpha_prev = 0.f;  // w_0 = v_0, |v_0| = 1
     vs[tid] = wown;
     tc_fence_before();
@@ -574,11 +602,27 @@ __global__ void __launch_bounds__(kTcThreads, 3)
         alpha_prev = alpha;
     }
     __syncthreads();
-    if (warp == 0) ritz_max_and_store(abq, mq, lane, a, size_t(bh) * a.N + j);
-    if (kPair && warp == 2 && j + 1 < a.N) ritz_max_and_store(abq, mq, lane, a, size_t(bh) * a.N + j + 1);
+#if PISA_K1C_CLOCKS
+    t5 = clock64();
+#endif
+    {  // this block's tridiagonal (kPair: each half its own block) -> ritz_kernel
+        const int t = kPair ? (tid & 63) : tid;
+        const int jb = j + (kPair ? hq : 0);
+        if (t < 2 * kLanczos && jb < a.N)
+            a.tri[(size_t(bh) * a.N + jb) * kTriStride + t] = t == 2 * kLanczos - 1 ? __int_as_float(mq) : abq[t];
+    }
+#if PISA_K1C_CLOCKS  // (the ritz kernel overwrites M_j: read the clocks with it disabled)
+    if (tid == 0) {
+        const long long t6 = clock64();
+        const long long c[5] = {t5 - t4, t6 - t5, t4 - t0, t6 - t0, t1 - t0};
+        a.m[size_t(bh) * a.N + j] = float(c[PISA_K1C_CLOCKS - 1]);
+    }
+#endif
 }
 
 }  // namespace
+
+int block_norms_launches(int D) { return (D == 128 || kK1cPairD64) ? 2 : 1; }
 
 size_t block_norms_smem_bytes(int D) {
     if (D == 128) return TcCfg::kSmem;
@@ -593,13 +637,19 @@ cudaError_t launch_block_norms(int D, const CUtensorMap& tmK, const CUtensorMap&
                                const __nv_bfloat16* v, const NormArgs& a, int BH, cudaStream_t s) {
     const size_t smem = block_norms_smem_bytes(D);
     dim3 grid(a.N, BH);
-    if (D == 128) {
-        cudaFuncSetAttribute(block_norms_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-        block_norms_tc_kernel<false><<<grid, kTcThreads, smem, s>>>(tmK, tmV, a);
-    } else if (kK1cPairD64) {  // two key blocks per CTA on the tensor cores
-        const size_t smem2 = TcCfg::kSmem;
-        cudaFuncSetAttribute(block_norms_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem2));
-        block_norms_tc_kernel<true><<<dim3((a.N + 1) / 2, BH), kTcThreads, smem2, s>>>(tmK, tmV, a);
+    const int nblk = a.N * BH;
+    if (D == 128 || kK1cPairD64) {
+        if (D == 128) {
+            cudaFuncSetAttribute(block_norms_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+            block_norms_tc_kernel<false><<<grid, kTcThreads, smem, s>>>(tmK, tmV, a);
+        } else {  // two key blocks per CTA on the tensor cores
+            const size_t smem2 = TcCfg::kSmem;
+            cudaFuncSetAttribute(block_norms_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem2));
+            block_norms_tc_kernel<true><<<dim3((a.N + 1) / 2, BH), kTcThreads, smem2, s>>>(tmK, tmV, a);
+        }
+#if !PISA_K1C_CLOCKS
+        ritz_kernel<<<(nblk + kRitzWarps - 1) / kRitzWarps, 32 * kRitzWarps, 0, s>>>(a, nblk);
+#endif
     } else {
         auto kern = block_norms_kernel<64>;
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));

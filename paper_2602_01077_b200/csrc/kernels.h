@@ -49,11 +49,14 @@ struct NormArgs {
     double eps;
     int L, N, H;
     int64_t ks_b, ks_h, ks_l, vs_b, vs_h, vs_l;  // element strides of k / v
+    float* tri;  // [BH][N][kTriStride] Lanczos tridiagonal per block (tensor-core kernel -> ritz kernel)
 };
+constexpr int kTriStride = 64;  // alpha [kLanczos] | beta [kLanczos - 1] | step count
 // D = 128 reads K / V through the tensor maps (64-row boxes), D = 64 through k / v
 cudaError_t launch_block_norms(int D, const CUtensorMap& tmK, const CUtensorMap& tmV, const __nv_bfloat16* k,
                                const __nv_bfloat16* v, const NormArgs& a, int BH, cudaStream_t s);
 size_t block_norms_smem_bytes(int D);
+int block_norms_launches(int D);  // kernels launch_block_norms launches (tensor-core path: K1c + ritz)
 
 // K2: fp32 block scoring + top-k (score desc, index asc) per query block.
 struct SelectArgs {

@@ -245,7 +245,7 @@ pisa_status resolve(pisa_ctx* ctx, const pisa_attn_desc* d, Plan* p) {
 
 // ------------------------------------------------------------ workspace --
 struct Work {
-    float *kbar, *vhat, *qbar, *hpart, *hbar, *kglob, *norms, *rect;
+    float *kbar, *vhat, *qbar, *hpart, *hbar, *kglob, *norms, *rect, *tri;
     int* cand;
     int2* pairs;
     __nv_bfloat16 *kbar_bf, *vhat_bf, *hbar_bf;
@@ -271,7 +271,7 @@ pisa_status workspace(pisa_ctx* ctx, const Plan& p, Work* w) {
                  o_kbf = take(BH * p.Npad * D * 2), o_vbf = take(BH * p.Npad * D * 2),
                  o_hbf = take(BH * D * D * 2), o_sel = take(BH * N * p.k * 4),
                  o_mask = take(BH * N * p.W * 4), o_keys = take(BH * N * N * 4),
-                 o_norms = take(BH * N * 4), o_rect = take(BH * N * 4),
+                 o_norms = take(BH * N * 4), o_rect = take(BH * N * 4), o_tri = take(BH * N * kTriStride * 4),
                  o_cand = take(BH * N * kPairCand * 4), o_pairs = take(BH * ((N + 1) / 2) * 8), o_flag = take(16);
     if (off > ctx->arena_bytes) {
         if (ctx->arena) cudaFree(ctx->arena);
@@ -290,6 +290,7 @@ pisa_status workspace(pisa_ctx* ctx, const Plan& p, Work* w) {
     w->kglob = reinterpret_cast<float*>(b + o_kglob);
     w->norms = reinterpret_cast<float*>(b + o_norms);
     w->rect = reinterpret_cast<float*>(b + o_rect);
+    w->tri = reinterpret_cast<float*>(b + o_tri);
     w->cand = reinterpret_cast<int*>(b + o_cand);
     w->pairs = reinterpret_cast<int2*>(b + o_pairs);
     w->kbar_bf = reinterpret_cast<__nv_bfloat16*>(b + o_kbf);
@@ -330,7 +331,7 @@ pisa_status run_norms(pisa_ctx* ctx, const pisa_attn_desc& d, const Plan& p, con
                       const void* k, const void* v, cudaStream_t s) {
     NormArgs a{w.kbar,      w.hbar,        w.norms,       w.rect,        d.epsilon,
                int(p.L),    int(p.N),      int(d.heads),  d.k_strides[0], d.k_strides[1],
-               d.k_strides[2], d.v_strides[0], d.v_strides[1], d.v_strides[2]};
+               d.k_strides[2], d.v_strides[0], d.v_strides[1], d.v_strides[2], w.tri};
     CUtensorMap tk, tv;
     if (!make_qkv_map(&tk, k, d, d.k_strides, 64) || !make_qkv_map(&tv, v, d, d.v_strides, 64))
         return fail(ctx, PISA_ERR_INVALID_DIMENSION, "TMA descriptor rejected the k/v layout");
@@ -338,7 +339,7 @@ pisa_status run_norms(pisa_ctx* ctx, const pisa_attn_desc& d, const Plan& p, con
     const cudaError_t e = launch_block_norms(int(p.D), tk, tv, static_cast<const __nv_bfloat16*>(k),
                                              static_cast<const __nv_bfloat16*>(v), a, int(p.BH), s);
     if (e != cudaSuccess) return cuda_fail(ctx, e, "block_norms launch");
-    ctx->launches += 1;
+    ctx->launches += block_norms_launches(int(p.D));
     return PISA_OK;
 }
 
