@@ -34,6 +34,9 @@ constexpr bool kK1cPairD64 = PISA_K1C_PAIR_D64 != 0;
 #ifndef PISA_LANCZOS_STEPS
 #define PISA_LANCZOS_STEPS 24
 #endif
+#ifndef PISA_K1C_HBAR_STAGE
+#define PISA_K1C_HBAR_STAGE 1  // H_bar pre-load through shared memory (0: per-thread row loads)
+#endif
 #ifndef PISA_K1C_CLOCKS
 #define PISA_K1C_CLOCKS 0  // diagnostic: 1..5 store a phase's cycles in place of M_j
 #endif
@@ -370,7 +373,7 @@ __global__ void __launch_bounds__(kTcThreads, 3)
     const int n1 = kPair ? min(64, a.L - (j + 1) * 64) : n;  // rows of block j + 1 (<= 0: absent)
 #if PISA_K1C_CLOCKS  // diagnostic build: M_j is replaced by a phase's cycle count
     const long long t0 = clock64();
-    long long t1 = 0, t4 = 0, t5 = 0;
+    long long t1 = 0, t4 = 0, t5 = 0, ta = 0, tb = 0;
 #endif
 
     if (tid == 0) {
@@ -399,11 +402,61 @@ __global__ void __launch_bounds__(kTcThreads, 3)
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
+#if PISA_K1C_CLOCKS
+    ta = clock64();
+#endif
     const uint32_t tmem = *tslot;
     const uint32_t trow = tmem + (uint32_t(warp * 32) << 16);  // this thread's TMEM lane = tid
     // -H_bar into this thread's TMEM row, the accumulator the H_j MMAs add to
     // (so they produce D = H_j - H_bar directly): the H_bar load latency
     // overlaps the K / V TMA and the split instead of following the MMAs
+#if PISA_K1C_HBAR_STAGE
+    // Coalesced: rows of H_bar read 256 B per 16 threads into the mid / lo tiles
+    // (free until the split), 16-byte chunks XOR-swizzled by row, then each
+    // thread reads its own row back. Loading row tid straight from global made
+    // every warp load touch 32 lines (one 16-byte chunk each): ~4K L1 wavefronts
+    // and ~5K cycles per CTA (PISA_K1C_CLOCKS=7), a tenth of its lifetime.
+    {
+        float4* stage = reinterpret_cast<float4*>(smem + Cfg::kTile);  // [rows][16 chunks of 4 floats]
+        constexpr int kRows = kPair ? 64 : 128;  // kPair: one 64 x 64 H_bar for both blocks
+        constexpr int kHalves = kPair ? 1 : 2;   // 64-column halves of H_bar
+        const float4* hb = reinterpret_cast<const float4*>(a.hbar + size_t(bh) * DR * DR);
+#pragma unroll
+        for (int half = 0; half < kHalves; ++half) {
+#pragma unroll
+            for (int i = 0; i < kRows * 16 / kTcThreads; ++i) {
+                const int ci = tid + kTcThreads * i, r = ci >> 4, c = ci & 15;
+                stage[r * 16 + (c ^ (r & 15))] = __ldg(hb + r * (DR / 4) + half * 16 + c);
+            }
+            __syncthreads();
+            const int row = kPair ? (tid & 63) : tid;
+#pragma unroll
+            for (int cc = 0; cc < 2; ++cc) {  // 32 TMEM columns per store
+                uint32_t r[32];
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    const int c = cc * 8 + i;
+                    const float4 h4 = stage[row * 16 + (c ^ (row & 15))];
+                    r[4 * i] = __float_as_uint(-h4.x);
+                    r[4 * i + 1] = __float_as_uint(-h4.y);
+                    r[4 * i + 2] = __float_as_uint(-h4.z);
+                    r[4 * i + 3] = __float_as_uint(-h4.w);
+                }
+                // kPair: block hq's row goes to its own 64-column quadrant
+                tmem_st32(trow + ((kPair ? hq : half) * 2 + cc) * 32, r);
+            }
+            __syncthreads();  // every row is read before the next half (or the split) overwrites the stage
+        }
+        if constexpr (kPair) {  // the cross quadrant starts at 0
+            uint32_t z[32];
+#pragma unroll
+            for (int i = 0; i < 32; ++i) z[i] = 0u;
+            tmem_st32(trow + ((1 - hq) * 2) * 32, z);
+            tmem_st32(trow + ((1 - hq) * 2 + 1) * 32, z);
+        }
+        tmem_st_wait();
+    }
+#else
     {
         // kPair: row a of block hq gets -H_bar[a % 64] in its own quadrant, 0 in the other
         const float4* hb = reinterpret_cast<const float4*>(a.hbar + (size_t(bh) * DR + (kPair ? (tid & 63) : tid)) * DR);
@@ -413,16 +466,20 @@ __global__ void __launch_bounds__(kTcThreads, 3)
             const bool own = !kPair || (cc >> 1) == hq;
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
-                const float4 hv = own ? __ldg(hb + (kPair ? (cc & 1) : cc) * 8 + i) : make_float4(0.f, 0.f, 0.f, 0.f);
-                r[4 * i] = __float_as_uint(-hv.x);
-                r[4 * i + 1] = __float_as_uint(-hv.y);
-                r[4 * i + 2] = __float_as_uint(-hv.z);
-                r[4 * i + 3] = __float_as_uint(-hv.w);
+                const float4 h4 = own ? __ldg(hb + (kPair ? (cc & 1) : cc) * 8 + i) : make_float4(0.f, 0.f, 0.f, 0.f);
+                r[4 * i] = __float_as_uint(-h4.x);
+                r[4 * i + 1] = __float_as_uint(-h4.y);
+                r[4 * i + 2] = __float_as_uint(-h4.z);
+                r[4 * i + 3] = __float_as_uint(-h4.w);
             }
             tmem_st32(trow + cc * 32, r);
         }
         tmem_st_wait();
     }
+#endif
+#if PISA_K1C_CLOCKS
+    tb = clock64();
+#endif
     mbar_wait(&bar[0], 0);
 #if PISA_K1C_CLOCKS
     t1 = clock64();
@@ -614,7 +671,7 @@ __global__ void __launch_bounds__(kTcThreads, 3)
 #if PISA_K1C_CLOCKS  // (the ritz kernel overwrites M_j: read the clocks with it disabled)
     if (tid == 0) {
         const long long t6 = clock64();
-        const long long c[5] = {t5 - t4, t6 - t5, t4 - t0, t6 - t0, t1 - t0};
+        const long long c[7] = {t5 - t4, t6 - t5, t4 - t0, t6 - t0, t1 - t0, ta - t0, tb - t0};
         a.m[size_t(bh) * a.N + j] = float(c[PISA_K1C_CLOCKS - 1]);
     }
 #endif
