@@ -631,3 +631,32 @@ def test_randomized_shapes_match_oracle(P, oracle_mod, cfg):
         st = O.block_stats(k[h], v[h])
         ref = O.pisa_attention(q[h], k[h], v[h], sel[h], st, scale, cfg["variant"])[0]
         check_close(out[h], ref)
+
+
+@pytest.mark.parametrize("router", ["plain", "covariance"])
+def test_fwd_cuda_graph_capture_replays_bit_identical(P, router):
+    """P.fwd is stream-ordered with no host syncs (profiling and check_finite
+    off), so a CUDA graph captures the whole forward; the replay recomputes
+    from the current inputs and matches the eager call bit for bit."""
+    import torch
+    g = torch.Generator(device="cuda").manual_seed(77)
+    q, k, v = (torch.randn((1, 3, 2000, 128), generator=g, device="cuda", dtype=torch.bfloat16) for _ in range(3))
+    out = torch.empty_like(q)
+    kw = dict(sparsity=0.75, router=P.RouterStrategy.CovarianceAware if router == "covariance"
+              else P.RouterStrategy.Plain)
+    P.fwd(q, k, v, out, **kw)
+    torch.cuda.synchronize()
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(side):
+        P.fwd(q, k, v, out, **kw)
+    torch.cuda.current_stream().wait_stream(side)
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph):
+        P.fwd(q, k, v, out, **kw)
+    q.copy_(torch.randn(q.shape, generator=g, device="cuda", dtype=torch.bfloat16))  # new inputs, same buffers
+    ref = P.fwd(q, k, v, **kw)
+    out.zero_()
+    graph.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(out, ref)
