@@ -38,7 +38,10 @@ constexpr bool kK1cPairD64 = PISA_K1C_PAIR_D64 != 0;
 #define PISA_K1C_HBAR_STAGE 1  // H_bar pre-load through shared memory (0: per-thread row loads)
 #endif
 #ifndef PISA_K1C_CLOCKS
-#define PISA_K1C_CLOCKS 0  // diagnostic: 1..5 store a phase's cycles in place of M_j
+#define PISA_K1C_CLOCKS 0  // diagnostic: n = 1..7 stores a phase's cycles in place of M_j
+// (1 Lanczos loop, 2 tridiagonal store, 3 start -> G in registers, 4 whole CTA,
+// 5 start -> K/V landed, 6 start -> CTA barrier, 7 start -> -H_bar in TMEM);
+// the ritz kernel is not launched in these builds
 #endif
 constexpr int kLanczos = PISA_LANCZOS_STEPS;  // fp32-converged (<5e-8 rel.) on gaussian / clustered blocks
 
@@ -85,7 +88,7 @@ __device__ __forceinline__ void ritz_max_and_store(const float* ab, int m, int l
 // the multisection with one warp per key block at full occupancy, where the
 // dependent Sturm chains of many blocks overlap. Inside K1c the single-warp
 // multisection held the CTA's 64 KB of registers and 67 KB of shared memory for
-// ~22K cycles, 28% of the CTA's lifetime (PISA_K1C_CLOCKS=2).
+// ~22K cycles, 28% of the CTA's lifetime (PISA_K1C_CLOCKS=2 before the split).
 constexpr int kRitzWarps = 8;
 static_assert(2 * kLanczos <= kTriStride, "tridiagonal row does not fit");
 __global__ void __launch_bounds__(32 * kRitzWarps) ritz_kernel(NormArgs a, int nblk) {
