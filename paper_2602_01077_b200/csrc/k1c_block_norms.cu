@@ -43,7 +43,7 @@ constexpr bool kK1cPairD64 = PISA_K1C_PAIR_D64 != 0;
 // 5 start -> K/V landed, 6 start -> CTA barrier, 7 start -> -H_bar in TMEM);
 // the ritz kernel is not launched in these builds
 #endif
-constexpr int kLanczos = PISA_LANCZOS_STEPS;  // fp32-converged (<5e-8 rel.) on gaussian / clustered blocks
+constexpr int kLanczos = PISA_LANCZOS_STEPS;  // fp32-converged on every Wan2.1-14B block (20 steps: 0.8% off)
 
 // Largest eigenvalue of the m x m Lanczos tridiagonal (alpha = ab[0..m),
 // beta = ab[kLanczos..]) by a 32-way multisection on its Sturm count (the
