@@ -27,7 +27,7 @@
 extern "C" {
 #endif
 
-#define PISA_B200_ABI_VERSION 2
+#define PISA_B200_ABI_VERSION 3
 
 /* Status codes. Reference class in brackets (errors.hpp line). */
 typedef enum pisa_status {
@@ -57,7 +57,11 @@ typedef enum pisa_router { PISA_ROUTER_PLAIN = 0, PISA_ROUTER_COVARIANCE = 1 } p
 
 /* Element type of Q/K/V/O. The reference's T in {float, double} (bundle.hpp:15)
  * becomes bf16 on the GPU; O may also be written as fp32 (parity mode). */
-typedef enum pisa_dtype { PISA_DTYPE_BF16 = 0, PISA_DTYPE_F32 = 1 } pisa_dtype;
+typedef enum pisa_dtype {
+    PISA_DTYPE_BF16 = 0,
+    PISA_DTYPE_F32 = 1,
+    PISA_DTYPE_F64 = 2 /* the generators' output only (TensorBundle<double>) */
+} pisa_dtype;
 
 /* Problem descriptor: the reference's TensorBundle shape (bundle.hpp:28-51) plus
  * AttentionConfig (attention.hpp:19-49) plus RouterOptions (engine.hpp:385-390)
@@ -81,10 +85,17 @@ typedef struct pisa_attn_desc {
     int32_t variant;        /* pisa_variant */
     int32_t router;         /* pisa_router (RouterOptions::strategy, engine.hpp:386) */
     int32_t force_diagonal; /* RouterOptions::force_diagonal (router.hpp:146-148) */
-    int32_t literal_phase3; /* AttentionConfig::literal_phase3 (engine.hpp:346) */
+    int32_t literal_phase3; /* AttentionConfig::literal_phase3 (engine.hpp:345-346): Phase-3
+                               weight / B. Honoured for HYBRID only (the streaming path's
+                               diagnostic; pisa_reference ignores it, so callers mirroring
+                               pisa_reference / use_streaming=false clear it) */
     int32_t ragged;         /* 1: allow L % 64 != 0 (documented extension); 0: BLOCK_DIVISIBILITY */
     int32_t out_dtype;      /* pisa_dtype of O */
-    int32_t check_finite;   /* 1: synchronize and report NUMERICAL_OVERFLOW (engine.hpp:83-93) */
+    int32_t check_finite;   /* 1: report NUMERICAL_OVERFLOW on a non-finite output
+                               (check_output_finite, engine.hpp:83-93): pisa_b200_fwd /
+                               _qrange / _attention synchronize the stream to read the
+                               device flag; pisa_b200_fwd_host reads it after its final
+                               synchronisation (no extra sync) */
     int32_t row_level;      /* RouterOptions::row_level (engine.hpp:389): not on the GPU path
                                (UNSUPPORTED); must be 0 */
     double epsilon;         /* RouterOptions::epsilon (engine.hpp:387), default 1e-6; the
@@ -103,6 +114,12 @@ typedef struct pisa_diag {
     int32_t* selected;
 } pisa_diag;
 
+/* A context owns the device workspace. It may be used from several streams
+ * (each stream gets its own workspace, so forwards enqueued on different streams
+ * never share scratch), but not from several host threads concurrently.
+ * Workspaces grow with the problem size and are only freed by
+ * pisa_b200_destroy, so a CUDA graph captured from a call stays valid for the
+ * lifetime of the context. */
 typedef struct pisa_ctx pisa_ctx;
 
 /* ---- lifetime ------------------------------------------------------------ */
@@ -191,6 +208,45 @@ pisa_status pisa_b200_attention(pisa_ctx* ctx, const pisa_attn_desc* desc, const
                                 const float* k_bar, const float* v_hat, const float* h_bar,
                                 void* o, const pisa_diag* diag, void* stream);
 
+/* ---- the steps with HOST buffers (synchronous) ---------------------------- */
+/* Same as the device entries above, for callers that keep tensors in host memory
+ * like the reference (the C++ shim's compute_block_stats, query_block_means,
+ * compute_global_stats(.., compute_norms), select_topk_plain / _covariance,
+ * pisa_streaming, pisa_reference). Inputs bf16, dense [batch][heads][seq_len][d]
+ * (desc strides are ignored); statistics fp32 as in the device entries. The ctx
+ * stages through temporary device buffers and returns when the outputs are in
+ * host memory. */
+/* q may be NULL (then q_bar must be NULL): k_bar / v_hat / h_bar only. */
+pisa_status pisa_b200_block_stats_host(pisa_ctx* ctx, const pisa_attn_desc* desc, const void* q,
+                                       const void* k, const void* v, float* k_bar, float* v_hat,
+                                       float* q_bar, float* h_bar);
+pisa_status pisa_b200_block_norms_host(pisa_ctx* ctx, const pisa_attn_desc* desc, const void* k,
+                                       const void* v, float* m);
+/* m == NULL: select_topk_plain; else select_topk_covariance with desc->epsilon. */
+pisa_status pisa_b200_select_host(pisa_ctx* ctx, const pisa_attn_desc* desc, const float* q_bar,
+                                  const float* k_bar, const float* m, int32_t* selected);
+/* diag: HOST pointers (row_max / ell / ell_tail; `selected` is ignored). */
+pisa_status pisa_b200_attention_host(pisa_ctx* ctx, const pisa_attn_desc* desc, const void* q,
+                                     const void* k, const void* v, const int32_t* selected,
+                                     const float* k_bar, const float* v_hat, const float* h_bar,
+                                     void* o, const pisa_diag* diag);
+
+/* ---- synthetic inputs: the reference's generators, bit-identical ---------- */
+/* gen_gaussian (generate.hpp:29-49) and gen_clustered (generate.hpp:57-116) on
+ * the reference RNG (xoshiro256++ seeded by splitmix64, Box-Muller pairs,
+ * rng.hpp:10-72): q, k, v HOST arrays [heads][L][d] of dtype PISA_DTYPE_F32
+ * (the reference's T = float), PISA_DTYPE_F64 (T = double) or PISA_DTYPE_BF16
+ * (RNE rounding of the T = float value).
+ * The single reference stream is split over `threads` host threads (<= 0: all)
+ * by exact GF(2) jumps of the generator state, so the values do not depend on
+ * the thread count. Errors: INVALID_DIMENSION / DEGENERATE_SCALE as the
+ * reference throws them. */
+pisa_status pisa_b200_gen_gaussian(uint64_t seed, int64_t heads, int64_t L, int64_t d, double std_dev,
+                                   int32_t dtype, void* q, void* k, void* v, int threads);
+pisa_status pisa_b200_gen_clustered(uint64_t seed, int64_t heads, int64_t L, int64_t d,
+                                    int64_t n_clusters, double concentration, double noise_std,
+                                    int32_t dtype, void* q, void* k, void* v, int threads);
+
 /* ---- instrumentation ----------------------------------------------------- */
 /* Number of kernel launches the last pisa_b200_fwd / _attention / _block_stats /
  * _select call issued (bench.py's gpu_launches). */
@@ -211,9 +267,11 @@ pisa_status pisa_b200_read_profile(pisa_ctx* ctx, double* ms, int64_t* launches)
  * synchronises and resets the counter. bench.py derives executed MMA FLOPs from it. */
 pisa_status pisa_b200_fused_tiles(pisa_ctx* ctx, int64_t* tiles);
 
-/* Standalone tensor-core self test: runs the three tcgen05 operand modes the fused
- * kernel uses (K-major SS, MN-major SS, TMEM-A TS) on small tiles and writes the
- * fp32 results for host comparison. a,b bf16 [128][128]; out fp32 [3][128][128]. */
+/* Standalone tensor-core self test: runs the tcgen05 operand modes the fused
+ * kernel and K1 use (K-major SS, MN-major SS, TMEM-A TS, K-major A with MN-major
+ * B) on small
+ * tiles and writes the fp32 results for host comparison. a,b bf16 [128][128];
+ * out fp32 [4][128][128]. */
 pisa_status pisa_b200_selftest_mma(pisa_ctx* ctx, const void* a, const void* b, float* out,
                                    void* stream);
 

@@ -20,5 +20,6 @@ from . import dit  # noqa: F401,E402  (DiT integration surface: warmup policy, j
 from .dit import PRESETS, PisaAttention, WarmupPolicy  # noqa: F401,E402
 from . import pqkv  # noqa: F401,E402  (PQKV tensor files, io.hpp)
 from . import analysis  # noqa: F401,E402  (theory checks on GPU outputs, analysis.hpp)
+from .generate import gen_clustered, gen_gaussian  # noqa: F401,E402  (generate.hpp fixtures)
 
 __all__ = [n for n in dir() if not n.startswith("_")]

@@ -40,7 +40,9 @@ EXPORTED = [
     "pisa_b200_select_cov", "pisa_b200_attention",
     "pisa_b200_last_launch_count", "pisa_b200_kernel_name", "pisa_b200_selftest_mma",
     "pisa_b200_set_profiling", "pisa_b200_read_profile", "pisa_b200_fused_tiles",
-    "pisa_b200_debug_trace",
+    "pisa_b200_debug_trace", "pisa_b200_block_stats_host", "pisa_b200_block_norms_host",
+    "pisa_b200_select_host", "pisa_b200_attention_host", "pisa_b200_gen_gaussian",
+    "pisa_b200_gen_clustered",
 ]
 
 _lib = None
@@ -93,7 +95,18 @@ def load(build_if_missing: bool = False):
     L.pisa_b200_read_profile.argtypes = [vp, C.POINTER(C.c_double), C.POINTER(i64)]
     L.pisa_b200_fused_tiles.argtypes = [vp, C.POINTER(i64)]
     L.pisa_b200_fused_tiles.restype = C.c_int
-    for name in ("pisa_b200_set_profiling", "pisa_b200_read_profile", "pisa_b200_create", "pisa_b200_sparsity_to_k", "pisa_b200_resolve",
+    L.pisa_b200_block_stats_host.argtypes = [vp, C.POINTER(AttnDesc), vp, vp, vp, vp, vp, vp, vp]
+    L.pisa_b200_block_norms_host.argtypes = [vp, C.POINTER(AttnDesc), vp, vp, vp]
+    L.pisa_b200_select_host.argtypes = [vp, C.POINTER(AttnDesc), vp, vp, vp, vp]
+    L.pisa_b200_attention_host.argtypes = [vp, C.POINTER(AttnDesc), vp, vp, vp, vp, vp, vp, vp, vp,
+                                           C.POINTER(Diag)]
+    L.pisa_b200_gen_gaussian.argtypes = [C.c_uint64, i64, i64, i64, C.c_double, C.c_int32, vp, vp, vp,
+                                         C.c_int]
+    L.pisa_b200_gen_clustered.argtypes = [C.c_uint64, i64, i64, i64, i64, C.c_double, C.c_double,
+                                          C.c_int32, vp, vp, vp, C.c_int]
+    for name in ("pisa_b200_block_stats_host", "pisa_b200_block_norms_host", "pisa_b200_select_host",
+                 "pisa_b200_attention_host", "pisa_b200_gen_gaussian", "pisa_b200_gen_clustered",
+                 "pisa_b200_set_profiling", "pisa_b200_read_profile", "pisa_b200_create", "pisa_b200_sparsity_to_k", "pisa_b200_resolve",
                  "pisa_b200_fwd", "pisa_b200_fwd_host", "pisa_b200_fwd_qrange", "pisa_b200_set_pairing",
                  "pisa_b200_block_stats", "pisa_b200_select", "pisa_b200_block_norms", "pisa_b200_select_cov",
                  "pisa_b200_attention", "pisa_b200_selftest_mma"):

@@ -858,8 +858,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (active && nU > 0) {
                 const float mm = fmaxf(mrow, gx);
                 fo = ex2(mrow - mm);
-                cw = a.scale * float(nU) * ex2(gx - mm);
-                if (a.literal_phase3) cw *= (1.0f / 64.0f);
+                cw = a.scale * float(nU) * ex2(gx - mm);  // pisa_reference: no literal_phase3
                 mrow = mm;
                 lfin *= fo;
                 ltot *= fo;

@@ -23,10 +23,19 @@ struct pisa_ctx {
     int device = 0;
     int sms = 148;  // multiprocessor count (K1 chunk sizing)
     std::string last_error;
-    // grow-only device arena
-    void* arena = nullptr;
-    size_t arena_bytes = 0;
-    int* flag_host = nullptr;  // pinned mirror of the non-finite flag
+    // Device workspace, one grow-only arena per stream that has called into
+    // this ctx, so forwards enqueued on different streams never share scratch.
+    // A superseded arena is retired, not freed, until pisa_b200_destroy: a CUDA
+    // graph captured from an earlier call keeps pointing at it.
+    struct Arena {
+        cudaStream_t stream = nullptr;
+        void* base = nullptr;
+        size_t bytes = 0;
+        int* flags = nullptr;  // [0] non-finite output, [1] invalid plan (never reallocated)
+    };
+    std::vector<Arena> arenas;
+    std::vector<void*> retired;
+    int* flag_host = nullptr;  // pinned mirror of a device flag
     int64_t launches = 0;
     // host-staged path
     cudaStream_t st_h2d = nullptr, st_comp = nullptr, st_d2h = nullptr;
@@ -221,11 +230,15 @@ pisa_status resolve(pisa_ctx* ctx, const pisa_attn_desc* d, Plan* p) {
                     "k must lie in [1, N], got " + std::to_string(k) + " for N = " + std::to_string(N));
     }
     const int64_t D = d->head_dim;
-    auto st_ok = [&](const int64_t* s) {
-        return s[2] % 8 == 0 && s[1] % 8 == 0 && s[0] % 8 == 0 && s[2] >= D;
+    // strides of extents > 1 must keep 16-byte rows: TMA (q/k/v) and the fused
+    // epilogue's 16-byte stores (o: 8 bf16 or 4 fp32 elements)
+    auto st_ok = [&](const int64_t* s, int64_t m) {
+        return s[2] >= D && s[2] % m == 0 && (d->heads == 1 || (s[1] >= 0 && s[1] % m == 0)) &&
+               (d->batch == 1 || (s[0] >= 0 && s[0] % m == 0));
     };
-    if (!st_ok(d->q_strides) || !st_ok(d->k_strides) || !st_ok(d->v_strides))
+    if (!st_ok(d->q_strides, 8) || !st_ok(d->k_strides, 8) || !st_ok(d->v_strides, 8))
         return fail(ctx, PISA_ERR_INVALID_DIMENSION, "q/k/v strides must be multiples of 8 elements");
+
     p->BH = d->batch * d->heads;
     p->L = d->seq_len;
     p->D = D;
@@ -257,7 +270,30 @@ struct Work {
 
 size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
 
-pisa_status workspace(pisa_ctx* ctx, const Plan& p, Work* w) {
+// cudaMalloc is a "potentially unsafe" call while a stream of this thread is
+// being captured in global mode (torch.cuda.graph's default); allocating a
+// workspace for a new stream / shape inside a capture is still correct (the
+// memory outlives the graph), so allocate in relaxed mode, as torch's own
+// caching allocator does.
+struct RelaxedCapture {
+    cudaStreamCaptureMode prev = cudaStreamCaptureModeRelaxed;
+    RelaxedCapture() { cudaThreadExchangeStreamCaptureMode(&prev); }
+    ~RelaxedCapture() { cudaThreadExchangeStreamCaptureMode(&prev); }
+};
+
+pisa_ctx::Arena* arena_of(pisa_ctx* ctx, cudaStream_t s) {
+    for (auto& a : ctx->arenas)
+        if (a.stream == s) return &a;
+    pisa_ctx::Arena a;
+    a.stream = s;
+    // flags are reset with cudaMemsetAsync on the stream before every use
+    RelaxedCapture rc;
+    if (cudaMalloc(&a.flags, 16 * sizeof(int)) != cudaSuccess) return nullptr;
+    ctx->arenas.push_back(a);
+    return &ctx->arenas.back();
+}
+
+pisa_status workspace(pisa_ctx* ctx, const Plan& p, Work* w, cudaStream_t s) {
     const size_t BH = size_t(p.BH), N = size_t(p.N), D = size_t(p.D);
     size_t off = 0;
     auto take = [&](size_t bytes) {
@@ -272,16 +308,21 @@ pisa_status workspace(pisa_ctx* ctx, const Plan& p, Work* w) {
                  o_hbf = take(BH * D * D * 2), o_sel = take(BH * N * p.k * 4),
                  o_mask = take(BH * N * p.W * 4), o_keys = take(BH * N * N * 4),
                  o_norms = take(BH * N * 4), o_rect = take(BH * N * 4), o_tri = take(BH * N * kTriStride * 4),
-                 o_cand = take(BH * N * kPairCand * 4), o_pairs = take(BH * ((N + 1) / 2) * 8), o_flag = take(16);
-    if (off > ctx->arena_bytes) {
-        if (ctx->arena) cudaFree(ctx->arena);
-        ctx->arena = nullptr;
-        ctx->arena_bytes = 0;
-        const cudaError_t e = cudaMalloc(&ctx->arena, off);
+                 o_cand = take(BH * N * kPairCand * 4), o_pairs = take(BH * ((N + 1) / 2) * 8);
+    pisa_ctx::Arena* ar = arena_of(ctx, s);
+    if (!ar) return fail(ctx, PISA_ERR_CUDA, "workspace flag allocation failed");
+    if (off > ar->bytes) {
+        // grow geometrically (few retired arenas under slowly growing shapes)
+        const size_t want = std::max(off, ar->bytes + ar->bytes / 2);
+        void* nb = nullptr;
+        RelaxedCapture rc;
+        const cudaError_t e = cudaMalloc(&nb, want);
         if (e != cudaSuccess) return cuda_fail(ctx, e, "workspace cudaMalloc");
-        ctx->arena_bytes = off;
+        if (ar->base) ctx->retired.push_back(ar->base);
+        ar->base = nb;
+        ar->bytes = want;
     }
-    char* b = static_cast<char*>(ctx->arena);
+    char* b = static_cast<char*>(ar->base);
     w->kbar = reinterpret_cast<float*>(b + o_kbar);
     w->vhat = reinterpret_cast<float*>(b + o_vhat);
     w->qbar = reinterpret_cast<float*>(b + o_qbar);
@@ -299,7 +340,7 @@ pisa_status workspace(pisa_ctx* ctx, const Plan& p, Work* w) {
     w->selected = reinterpret_cast<int32_t*>(b + o_sel);
     w->mask = reinterpret_cast<uint32_t*>(b + o_mask);
     w->keys = reinterpret_cast<uint32_t*>(b + o_keys);
-    w->flag = reinterpret_cast<int*>(b + o_flag);
+    w->flag = ar->flags;
     return PISA_OK;
 }
 
@@ -355,9 +396,17 @@ pisa_status run_select(pisa_ctx* ctx, const pisa_attn_desc& d, const Plan& p, co
     return PISA_OK;
 }
 
+// Non-finite output check (check_output_finite, engine.hpp:83-93):
+//   kFiniteOff   no check;
+//   kFiniteArm   the fused kernel ORs into the stream's device flag, nobody
+//                resets or reads it (the host path resets it once and reads it
+//                after its final synchronisation);
+//   kFiniteSync  reset, arm, synchronise and report NUMERICAL_OVERFLOW.
+enum FiniteMode { kFiniteOff = 0, kFiniteArm = 1, kFiniteSync = 2 };
+
 pisa_status run_fused(pisa_ctx* ctx, const pisa_attn_desc& d, const Plan& p, const Work& w,
                       const void* q, const void* k, const void* v, void* o, const pisa_diag* diag,
-                      cudaStream_t s) {
+                      cudaStream_t s, FiniteMode fm) {
     CUtensorMap tq, tk, tv, tkb, tvh, th;
     if (!make_qkv_map(&tq, q, d, d.q_strides, 16) || !make_qkv_map(&tk, k, d, d.k_strides, 64) ||
         !make_qkv_map(&tv, v, d, d.v_strides, 64))
@@ -391,7 +440,7 @@ pisa_status run_fused(pisa_ctx* ctx, const pisa_attn_desc& d, const Plan& p, con
     a.diag_m = diag ? diag->row_max : nullptr;
     a.diag_l = diag ? diag->ell : nullptr;
     a.diag_lt = diag ? diag->ell_tail : nullptr;
-    a.nonfinite = d.check_finite ? w.flag : nullptr;
+    a.nonfinite = fm != kFiniteOff ? w.flag : nullptr;
     a.L = int(p.L);
     a.N = int(p.N);
     a.H = int(d.heads);
@@ -407,7 +456,7 @@ pisa_status run_fused(pisa_ctx* ctx, const pisa_attn_desc& d, const Plan& p, con
     a.trace = ctx->trace;
     a.tile_count = ctx->prof ? ctx->tiles_dev : nullptr;
     a.trace_tile = ctx->trace_tile;
-    if (d.check_finite) {
+    if (fm == kFiniteSync) {
         const cudaError_t e = cudaMemsetAsync(w.flag, 0, sizeof(int), s);
         if (e != cudaSuccess) return cuda_fail(ctx, e, "flag reset");
     }
@@ -418,7 +467,7 @@ pisa_status run_fused(pisa_ctx* ctx, const pisa_attn_desc& d, const Plan& p, con
     }
     if (e != cudaSuccess) return cuda_fail(ctx, e, "fused launch");
     ctx->launches += 1;
-    if (d.check_finite) {
+    if (fm == kFiniteSync) {
         cudaError_t e2 = cudaMemcpyAsync(ctx->flag_host, w.flag, sizeof(int), cudaMemcpyDeviceToHost, s);
         if (e2 == cudaSuccess) e2 = cudaStreamSynchronize(s);
         if (e2 != cudaSuccess) return cuda_fail(ctx, e2, "non-finite check");
@@ -428,8 +477,68 @@ pisa_status run_fused(pisa_ctx* ctx, const pisa_attn_desc& d, const Plan& p, con
     return PISA_OK;
 }
 
-bool out_dtype_ok(const pisa_attn_desc* d) {
-    return d->out_dtype == PISA_DTYPE_BF16 || d->out_dtype == PISA_DTYPE_F32;
+// The streams (and events) of the host-buffer entries, created on first use.
+pisa_status host_streams(pisa_ctx* ctx) {
+    if (ctx->st_h2d) return PISA_OK;
+    cudaError_t e = cudaStreamCreateWithFlags(&ctx->st_h2d, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->st_comp, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->st_d2h, cudaStreamNonBlocking);
+    for (int i = 0; i < 2 && e == cudaSuccess; ++i) {
+        e = cudaEventCreateWithFlags(&ctx->ev_h2d[i], cudaEventDisableTiming);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->ev_comp[i], cudaEventDisableTiming);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->ev_d2h[i], cudaEventDisableTiming);
+    }
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "stream setup");
+    return PISA_OK;
+}
+
+// Device copies of host arrays for the synchronous host-buffer step entries
+// (not a hot path: plain cudaMalloc / cudaMemcpy, freed on scope exit).
+struct DevBufs {
+    std::vector<void*> ptrs;
+    cudaError_t err = cudaSuccess;
+    void* alloc(size_t bytes) {
+        void* p = nullptr;
+        if (err == cudaSuccess) err = cudaMalloc(&p, std::max<size_t>(bytes, 16));
+        if (err == cudaSuccess) ptrs.push_back(p);
+        return err == cudaSuccess ? p : nullptr;
+    }
+    void* upload(const void* h, size_t bytes) {
+        void* p = h ? alloc(bytes) : nullptr;
+        if (p && err == cudaSuccess) err = cudaMemcpy(p, h, bytes, cudaMemcpyHostToDevice);
+        return p;
+    }
+    ~DevBufs() {
+        for (void* p : ptrs) cudaFree(p);
+    }
+};
+
+// dense [B][H][L][d] strides (the host entries' layout)
+void dense_strides(pisa_attn_desc& d) {
+    const int64_t ld = d.seq_len * d.head_dim;
+    for (int64_t* s : {d.q_strides, d.k_strides, d.v_strides, d.o_strides}) {
+        s[0] = d.heads * ld;
+        s[1] = ld;
+        s[2] = d.head_dim;
+    }
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+// Output checks of the calls that write O: dtype, and strides of extents > 1
+// keeping 16-byte rows for the fused epilogue's 16-byte stores.
+pisa_status check_out(pisa_ctx* ctx, const pisa_attn_desc* d, const void* o) {
+    if (d->out_dtype != PISA_DTYPE_BF16 && d->out_dtype != PISA_DTYPE_F32)
+        return fail(ctx, PISA_ERR_UNSUPPORTED, "output dtype must be bf16 or fp32");
+    const int64_t m = d->out_dtype == PISA_DTYPE_F32 ? 4 : 8;
+    const int64_t* s = d->o_strides;
+    const bool ok = s[2] >= d->head_dim && s[2] % m == 0 && (d->heads == 1 || (s[1] >= 0 && s[1] % m == 0)) &&
+                    (d->batch == 1 || (s[0] >= 0 && s[0] % m == 0));
+    if (!ok)
+        return fail(ctx, PISA_ERR_INVALID_DIMENSION,
+                    "o strides must be >= head_dim and multiples of 16 bytes (8 bf16 / 4 fp32 elements)");
+    if (o && !aligned16(o)) return fail(ctx, PISA_ERR_INVALID_DIMENSION, "o must be 16-byte aligned");
+    return PISA_OK;
 }
 
 struct DeviceGuard {
@@ -478,7 +587,11 @@ void pisa_b200_destroy(pisa_ctx* c) {
     if (!c) return;
     DeviceGuard g(c->device);
     cudaDeviceSynchronize();
-    if (c->arena) cudaFree(c->arena);
+    for (auto& a : c->arenas) {
+        if (a.base) cudaFree(a.base);
+        if (a.flags) cudaFree(a.flags);
+    }
+    for (void* r : c->retired) cudaFree(r);
     if (c->stage) cudaFree(c->stage);
     if (c->flag_host) cudaFreeHost(c->flag_host);
     for (auto& r : c->recs) {
@@ -583,7 +696,8 @@ pisa_status pisa_b200_resolve(const pisa_attn_desc* d, int64_t* num_blocks, int6
 
 namespace {
 pisa_status fwd_range(pisa_ctx* ctx, const pisa_attn_desc* d, const void* q, const void* k, const void* v,
-                      void* o, int64_t qb_begin, int64_t qb_end, const pisa_diag* diag, void* stream) {
+                      void* o, int64_t qb_begin, int64_t qb_end, const pisa_diag* diag, void* stream,
+                      FiniteMode fm) {
     if (!ctx) return PISA_ERR_INVALID_DIMENSION;
     ctx->launches = 0;
     Plan p;
@@ -597,11 +711,13 @@ pisa_status fwd_range(pisa_ctx* ctx, const pisa_attn_desc* d, const void* q, con
     p.qb0 = qb_begin;
     p.qb1 = qb_end;
     if (!q || !k || !v || !o) return fail(ctx, PISA_ERR_INVALID_DIMENSION, "null tensor pointer");
-    if (!out_dtype_ok(d)) return fail(ctx, PISA_ERR_UNSUPPORTED, "output dtype");
+    if (!aligned16(q) || !aligned16(k) || !aligned16(v) || !aligned16(o))
+        return fail(ctx, PISA_ERR_INVALID_DIMENSION, "q/k/v/o must be 16-byte aligned");
+    if ((st = check_out(ctx, d, o)) != PISA_OK) return st;
     DeviceGuard g(ctx->device);
     const cudaStream_t s = static_cast<cudaStream_t>(stream);
     Work w;
-    if ((st = workspace(ctx, p, &w)) != PISA_OK) return st;
+    if ((st = workspace(ctx, p, &w, s)) != PISA_OK) return st;
     if ((st = run_stats(ctx, *d, p, w, q, k, v, s)) != PISA_OK) return st;
     const bool cov = d->router == PISA_ROUTER_COVARIANCE;
     if (cov && (st = run_norms(ctx, *d, p, w, k, v, s)) != PISA_OK) return st;
@@ -609,7 +725,7 @@ pisa_status fwd_range(pisa_ctx* ctx, const pisa_attn_desc* d, const void* q, con
     if ((st = run_select(ctx, *d, p, w.qbar, w.kbar, cov ? w.rect : nullptr, sel, w.mask, w.keys, s)) !=
         PISA_OK)
         return st;
-    return run_fused(ctx, *d, p, w, q, k, v, o, diag, s);
+    return run_fused(ctx, *d, p, w, q, k, v, o, diag, s, fm);
 }
 }  // namespace
 
@@ -622,13 +738,16 @@ pisa_status pisa_b200_set_pairing(pisa_ctx* ctx, int mode) {
 
 pisa_status pisa_b200_fwd(pisa_ctx* ctx, const pisa_attn_desc* d, const void* q, const void* k,
                           const void* v, void* o, const pisa_diag* diag, void* stream) {
-    return fwd_range(ctx, d, q, k, v, o, 0, -1, diag, stream);
+    if (!d) return fail(ctx, PISA_ERR_INVALID_DIMENSION, "null descriptor");
+    return fwd_range(ctx, d, q, k, v, o, 0, -1, diag, stream, d->check_finite ? kFiniteSync : kFiniteOff);
 }
 
 pisa_status pisa_b200_fwd_qrange(pisa_ctx* ctx, const pisa_attn_desc* d, const void* q, const void* k,
                                  const void* v, void* o, int64_t qb_begin, int64_t qb_end,
                                  const pisa_diag* diag, void* stream) {
-    return fwd_range(ctx, d, q, k, v, o, qb_begin, qb_end, diag, stream);
+    if (!d) return fail(ctx, PISA_ERR_INVALID_DIMENSION, "null descriptor");
+    return fwd_range(ctx, d, q, k, v, o, qb_begin, qb_end, diag, stream,
+                     d->check_finite ? kFiniteSync : kFiniteOff);
 }
 
 pisa_status pisa_b200_block_stats(pisa_ctx* ctx, const pisa_attn_desc* d, const void* q,
@@ -640,10 +759,12 @@ pisa_status pisa_b200_block_stats(pisa_ctx* ctx, const pisa_attn_desc* d, const 
     pisa_status st = resolve(ctx, d, &p);
     if (st != PISA_OK) return st;
     if (!q || !k || !v) return fail(ctx, PISA_ERR_INVALID_DIMENSION, "null tensor pointer");
+    if (!aligned16(q) || !aligned16(k) || !aligned16(v))
+        return fail(ctx, PISA_ERR_INVALID_DIMENSION, "q/k/v must be 16-byte aligned");
     DeviceGuard g(ctx->device);
     const cudaStream_t s = static_cast<cudaStream_t>(stream);
     Work w;
-    if ((st = workspace(ctx, p, &w)) != PISA_OK) return st;
+    if ((st = workspace(ctx, p, &w, s)) != PISA_OK) return st;
     if ((st = run_stats(ctx, *d, p, w, q, k, v, s)) != PISA_OK) return st;
     const size_t nd = size_t(p.BH) * p.N * p.D * 4, dd = size_t(p.BH) * p.D * p.D * 4;
     cudaError_t e = cudaSuccess;
@@ -667,7 +788,7 @@ pisa_status pisa_b200_select(pisa_ctx* ctx, const pisa_attn_desc* d, const float
     DeviceGuard g(ctx->device);
     const cudaStream_t s = static_cast<cudaStream_t>(stream);
     Work w;
-    if ((st = workspace(ctx, p, &w)) != PISA_OK) return st;
+    if ((st = workspace(ctx, p, &w, s)) != PISA_OK) return st;
     if (d->router != PISA_ROUTER_PLAIN)
         return fail(ctx, PISA_ERR_INVALID_DIMENSION, "covariance routing: use pisa_b200_select_cov");
     return run_select(ctx, *d, p, q_bar, k_bar, nullptr, selected, mask ? mask : w.mask, w.keys, s);
@@ -684,7 +805,7 @@ pisa_status pisa_b200_block_norms(pisa_ctx* ctx, const pisa_attn_desc* d, const 
     DeviceGuard g(ctx->device);
     const cudaStream_t s = static_cast<cudaStream_t>(stream);
     Work w;
-    if ((st = workspace(ctx, p, &w)) != PISA_OK) return st;
+    if ((st = workspace(ctx, p, &w, s)) != PISA_OK) return st;
     if ((st = run_stats(ctx, *d, p, w, q, k, v, s)) != PISA_OK) return st;
     pisa_attn_desc dd = *d;
     if (!(dd.epsilon > 0.0)) dd.epsilon = 1e-6;  // M_j itself does not depend on eps
@@ -710,7 +831,7 @@ pisa_status pisa_b200_select_cov(pisa_ctx* ctx, const pisa_attn_desc* d, const f
     DeviceGuard g(ctx->device);
     const cudaStream_t s = static_cast<cudaStream_t>(stream);
     Work w;
-    if ((st = workspace(ctx, p, &w)) != PISA_OK) return st;
+    if ((st = workspace(ctx, p, &w, s)) != PISA_OK) return st;
     cudaError_t e = launch_rectifier(m, d->epsilon, w.rect, int(p.BH) * int(p.N), s);
     if (e != cudaSuccess) return cuda_fail(ctx, e, "rectifier launch");
     ctx->launches += 1;
@@ -728,11 +849,13 @@ pisa_status pisa_b200_attention(pisa_ctx* ctx, const pisa_attn_desc* d, const vo
     if (st != PISA_OK) return st;
     if (!q || !k || !v || !o || !selected || !k_bar || !v_hat || !h_bar)
         return fail(ctx, PISA_ERR_INVALID_DIMENSION, "null pointer");
-    if (!out_dtype_ok(d)) return fail(ctx, PISA_ERR_UNSUPPORTED, "output dtype");
+    if (!aligned16(q) || !aligned16(k) || !aligned16(v) || !aligned16(o))
+        return fail(ctx, PISA_ERR_INVALID_DIMENSION, "q/k/v/o must be 16-byte aligned");
+    if ((st = check_out(ctx, d, o)) != PISA_OK) return st;
     DeviceGuard g(ctx->device);
     const cudaStream_t s = static_cast<cudaStream_t>(stream);
     Work w;
-    if ((st = workspace(ctx, p, &w)) != PISA_OK) return st;
+    if ((st = workspace(ctx, p, &w, s)) != PISA_OK) return st;
     // plan -> mask, with SelectionPlan::validate (router.hpp:50-70)
     cudaError_t e = cudaMemsetAsync(w.flag + 1, 0, sizeof(int), s);
     if (e == cudaSuccess) {
@@ -752,7 +875,7 @@ pisa_status pisa_b200_attention(pisa_ctx* ctx, const pisa_attn_desc* d, const vo
     ctx->launches += 2;
     if (*ctx->flag_host)
         return fail(ctx, PISA_ERR_INVALID_SPARSITY, "plan has out-of-range or non-ascending indices");
-    return run_fused(ctx, *d, p, w, q, k, v, o, diag, s);
+    return run_fused(ctx, *d, p, w, q, k, v, o, diag, s, d->check_finite ? kFiniteSync : kFiniteOff);
 }
 
 pisa_status pisa_b200_fwd_host(pisa_ctx* ctx, const pisa_attn_desc* d, const void* q,
@@ -762,7 +885,8 @@ pisa_status pisa_b200_fwd_host(pisa_ctx* ctx, const pisa_attn_desc* d, const voi
     pisa_status st = resolve(ctx, d, &p);
     if (st != PISA_OK) return st;
     if (!q || !k || !v || !o) return fail(ctx, PISA_ERR_INVALID_DIMENSION, "null tensor pointer");
-    if (!out_dtype_ok(d)) return fail(ctx, PISA_ERR_UNSUPPORTED, "output dtype");
+    if (d->out_dtype != PISA_DTYPE_BF16 && d->out_dtype != PISA_DTYPE_F32)
+        return fail(ctx, PISA_ERR_UNSUPPORTED, "output dtype must be bf16 or fp32");
     DeviceGuard g(ctx->device);
     // host layout: dense [B][H][L][d]; stage a few (b,h) slices at a time
     const int64_t BH = p.BH, L = p.L, D = p.D;
@@ -773,17 +897,7 @@ pisa_status pisa_b200_fwd_host(pisa_ctx* ctx, const pisa_attn_desc* d, const voi
     const size_t diag_bytes = want_diag ? size_t(L) * 4 * 3 + size_t(p.N) * p.k * 4 : 0;
     const size_t set_bytes = size_t(chunk) * (3 * in_bytes + out_bytes + diag_bytes);
     cudaError_t e = cudaSuccess;
-    if (!ctx->st_h2d) {
-        e = cudaStreamCreateWithFlags(&ctx->st_h2d, cudaStreamNonBlocking);
-        if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->st_comp, cudaStreamNonBlocking);
-        if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->st_d2h, cudaStreamNonBlocking);
-        for (int i = 0; i < 2 && e == cudaSuccess; ++i) {
-            e = cudaEventCreateWithFlags(&ctx->ev_h2d[i], cudaEventDisableTiming);
-            if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->ev_comp[i], cudaEventDisableTiming);
-            if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->ev_d2h[i], cudaEventDisableTiming);
-        }
-        if (e != cudaSuccess) return cuda_fail(ctx, e, "stream setup");
-    }
+    if ((st = host_streams(ctx)) != PISA_OK) return st;
     if (2 * set_bytes > ctx->stage_bytes) {
         if (ctx->stage) cudaFree(ctx->stage);
         ctx->stage = nullptr;
@@ -793,6 +907,16 @@ pisa_status pisa_b200_fwd_host(pisa_ctx* ctx, const pisa_attn_desc* d, const voi
         ctx->stage_bytes = 2 * set_bytes;
     }
     int64_t launches = 0;
+    // non-finite check over all chunks: reset the compute stream's flag once,
+    // every chunk's fused kernel ORs into it, read after the final sync
+    int* flag = nullptr;
+    if (d->check_finite) {
+        pisa_ctx::Arena* ar = arena_of(ctx, ctx->st_comp);
+        if (!ar) return fail(ctx, PISA_ERR_CUDA, "workspace flag allocation failed");
+        flag = ar->flags;
+        e = cudaMemsetAsync(flag, 0, sizeof(int), ctx->st_comp);
+        if (e != cudaSuccess) return cuda_fail(ctx, e, "flag reset");
+    }
     // chunk sizes: a remainder first, then `chunk`-sized ones, then a shrinking
     // tail (2, 1) so that each chunk's compute hides behind the next chunk's
     // H2D (compute is ~0.6x the H2D time per head) and the exposed tail --
@@ -847,8 +971,8 @@ pisa_status pisa_b200_fwd_host(pisa_ctx* ctx, const pisa_attn_desc* d, const voi
         dc.o_strides[0] = hc * ld;
         dc.o_strides[1] = ld;
         dc.o_strides[2] = D;
-        dc.check_finite = 0;
-        st = pisa_b200_fwd(ctx, &dc, dq, dk, dv, dout, want_diag ? &dd : nullptr, ctx->st_comp);
+        st = fwd_range(ctx, &dc, dq, dk, dv, dout, 0, -1, want_diag ? &dd : nullptr, ctx->st_comp,
+                       flag ? kFiniteArm : kFiniteOff);
         if (st != PISA_OK) return st;
         launches += ctx->launches;
         cudaEventRecord(ctx->ev_comp[sidx], ctx->st_comp);
@@ -873,7 +997,159 @@ pisa_status pisa_b200_fwd_host(pisa_ctx* ctx, const pisa_attn_desc* d, const voi
     if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->st_comp);
     if (e != cudaSuccess) return cuda_fail(ctx, e, "host-path sync");
     ctx->launches = launches;
+    if (flag) {
+        e = cudaMemcpy(ctx->flag_host, flag, sizeof(int), cudaMemcpyDeviceToHost);
+        if (e != cudaSuccess) return cuda_fail(ctx, e, "non-finite check");
+        if (*ctx->flag_host)  // engine.hpp:83-93, :368
+            return fail(ctx, PISA_ERR_NUMERICAL_OVERFLOW, "non-finite output");
+    }
     return PISA_OK;
+}
+
+// ---- the step entries with HOST buffers (synchronous; the C++ shim's
+// compute_block_stats / query_block_means / select_topk_* / pisa_streaming /
+// pisa_reference). Inputs bf16 dense [B][H][L][d]; desc strides are ignored.
+namespace {
+struct HostCall {
+    pisa_ctx* ctx;
+    pisa_attn_desc d;
+    Plan p;
+    size_t in_bytes = 0, nd = 0, dd = 0;
+    pisa_status st = PISA_OK;
+    HostCall(pisa_ctx* c, const pisa_attn_desc* desc) : ctx(c) {
+        if (!c) {
+            st = PISA_ERR_INVALID_DIMENSION;
+            return;
+        }
+        if (!desc) {
+            st = fail(c, PISA_ERR_INVALID_DIMENSION, "null descriptor");
+            return;
+        }
+        d = *desc;
+        dense_strides(d);
+        if ((st = resolve(c, &d, &p)) != PISA_OK) return;
+        st = host_streams(c);
+        in_bytes = size_t(p.BH) * p.L * p.D * 2;
+        nd = size_t(p.BH) * p.N * p.D * 4;
+        dd = size_t(p.BH) * p.D * p.D * 4;
+    }
+    pisa_status finish(DevBufs& b, const char* where) {
+        if (b.err != cudaSuccess) return cuda_fail(ctx, b.err, where);
+        const cudaError_t e = cudaStreamSynchronize(ctx->st_comp);
+        return e == cudaSuccess ? PISA_OK : cuda_fail(ctx, e, where);
+    }
+};
+
+cudaError_t download(void* h, const void* dptr, size_t bytes, cudaError_t e) {
+    if (e == cudaSuccess && h && dptr) e = cudaMemcpy(h, dptr, bytes, cudaMemcpyDeviceToHost);
+    return e;
+}
+}  // namespace
+
+pisa_status pisa_b200_block_stats_host(pisa_ctx* ctx, const pisa_attn_desc* desc, const void* q,
+                                       const void* k, const void* v, float* k_bar, float* v_hat,
+                                       float* q_bar, float* h_bar) {
+    HostCall c(ctx, desc);
+    if (c.st != PISA_OK) return c.st;
+    if (!k || !v || (!q && q_bar)) return fail(ctx, PISA_ERR_INVALID_DIMENSION, "null tensor pointer");
+    DeviceGuard g(ctx->device);
+    DevBufs b;
+    void* dk = b.upload(k, c.in_bytes);
+    void* dv = b.upload(v, c.in_bytes);
+    void* dq = q ? b.upload(q, c.in_bytes) : dk;
+    float* o[4] = {nullptr, nullptr, nullptr, nullptr};
+    float* h[4] = {k_bar, v_hat, q_bar, h_bar};
+    const size_t sz[4] = {c.nd, c.nd, c.nd, c.dd};
+    for (int i = 0; i < 4; ++i)
+        if (h[i]) o[i] = static_cast<float*>(b.alloc(sz[i]));
+    if (b.err != cudaSuccess) return cuda_fail(ctx, b.err, "block_stats_host staging");
+    pisa_status st = pisa_b200_block_stats(ctx, &c.d, dq, dk, dv, o[0], o[1], o[2], o[3], ctx->st_comp);
+    if (st != PISA_OK) return st;
+    if ((st = c.finish(b, "block_stats_host")) != PISA_OK) return st;
+    cudaError_t e = cudaSuccess;
+    for (int i = 0; i < 4; ++i) e = download(h[i], o[i], sz[i], e);
+    return e == cudaSuccess ? PISA_OK : cuda_fail(ctx, e, "block_stats_host copy-out");
+}
+
+pisa_status pisa_b200_block_norms_host(pisa_ctx* ctx, const pisa_attn_desc* desc, const void* k,
+                                       const void* v, float* m) {
+    HostCall c(ctx, desc);
+    if (c.st != PISA_OK) return c.st;
+    if (!k || !v || !m) return fail(ctx, PISA_ERR_INVALID_DIMENSION, "null pointer");
+    DeviceGuard g(ctx->device);
+    DevBufs b;
+    void* dk = b.upload(k, c.in_bytes);
+    void* dv = b.upload(v, c.in_bytes);
+    float* dm = static_cast<float*>(b.alloc(size_t(c.p.BH) * c.p.N * 4));
+    if (b.err != cudaSuccess) return cuda_fail(ctx, b.err, "block_norms_host staging");
+    pisa_status st = pisa_b200_block_norms(ctx, &c.d, dk, dk, dv, dm, ctx->st_comp);
+    if (st != PISA_OK) return st;
+    if ((st = c.finish(b, "block_norms_host")) != PISA_OK) return st;
+    const cudaError_t e = download(m, dm, size_t(c.p.BH) * c.p.N * 4, cudaSuccess);
+    return e == cudaSuccess ? PISA_OK : cuda_fail(ctx, e, "block_norms_host copy-out");
+}
+
+pisa_status pisa_b200_select_host(pisa_ctx* ctx, const pisa_attn_desc* desc, const float* q_bar,
+                                  const float* k_bar, const float* m, int32_t* selected) {
+    HostCall c(ctx, desc);
+    if (c.st != PISA_OK) return c.st;
+    if (!q_bar || !k_bar || !selected) return fail(ctx, PISA_ERR_INVALID_DIMENSION, "null pointer");
+    DeviceGuard g(ctx->device);
+    DevBufs b;
+    const float* dq = static_cast<const float*>(b.upload(q_bar, c.nd));
+    const float* dk = static_cast<const float*>(b.upload(k_bar, c.nd));
+    const float* dm = m ? static_cast<const float*>(b.upload(m, size_t(c.p.BH) * c.p.N * 4)) : nullptr;
+    const size_t sb = size_t(c.p.BH) * c.p.N * c.p.k * 4;
+    int32_t* ds = static_cast<int32_t*>(b.alloc(sb));
+    if (b.err != cudaSuccess) return cuda_fail(ctx, b.err, "select_host staging");
+    pisa_status st = m ? pisa_b200_select_cov(ctx, &c.d, dq, dk, dm, ds, nullptr, ctx->st_comp)
+                       : pisa_b200_select(ctx, &c.d, dq, dk, ds, nullptr, ctx->st_comp);
+    if (st != PISA_OK) return st;
+    if ((st = c.finish(b, "select_host")) != PISA_OK) return st;
+    const cudaError_t e = download(selected, ds, sb, cudaSuccess);
+    return e == cudaSuccess ? PISA_OK : cuda_fail(ctx, e, "select_host copy-out");
+}
+
+pisa_status pisa_b200_attention_host(pisa_ctx* ctx, const pisa_attn_desc* desc, const void* q,
+                                     const void* k, const void* v, const int32_t* selected,
+                                     const float* k_bar, const float* v_hat, const float* h_bar,
+                                     void* o, const pisa_diag* hdiag) {
+    HostCall c(ctx, desc);
+    if (c.st != PISA_OK) return c.st;
+    if (!q || !k || !v || !o || !selected || !k_bar || !v_hat || !h_bar)
+        return fail(ctx, PISA_ERR_INVALID_DIMENSION, "null pointer");
+    DeviceGuard g(ctx->device);
+    DevBufs b;
+    const Plan& p = c.p;
+    void* dq = b.upload(q, c.in_bytes);
+    void* dk = b.upload(k, c.in_bytes);
+    void* dv = b.upload(v, c.in_bytes);
+    const size_t sb = size_t(p.BH) * p.N * p.k * 4;
+    const int32_t* ds = static_cast<const int32_t*>(b.upload(selected, sb));
+    const float* dkb = static_cast<const float*>(b.upload(k_bar, c.nd));
+    const float* dvh = static_cast<const float*>(b.upload(v_hat, c.nd));
+    const float* dhb = static_cast<const float*>(b.upload(h_bar, c.dd));
+    const size_t ob = size_t(p.BH) * p.L * p.D * (c.d.out_dtype == PISA_DTYPE_F32 ? 4 : 2);
+    void* dout = b.alloc(ob);
+    pisa_diag dd{};
+    const size_t rb = size_t(p.BH) * p.L * 4;
+    if (hdiag) {
+        if (hdiag->row_max) dd.row_max = static_cast<float*>(b.alloc(rb));
+        if (hdiag->ell) dd.ell = static_cast<float*>(b.alloc(rb));
+        if (hdiag->ell_tail) dd.ell_tail = static_cast<float*>(b.alloc(rb));
+    }
+    if (b.err != cudaSuccess) return cuda_fail(ctx, b.err, "attention_host staging");
+    pisa_status st = pisa_b200_attention(ctx, &c.d, dq, dk, dv, ds, dkb, dvh, dhb, dout, hdiag ? &dd : nullptr,
+                                         ctx->st_comp);
+    if (st != PISA_OK) return st;
+    if ((st = c.finish(b, "attention_host")) != PISA_OK) return st;
+    cudaError_t e = download(o, dout, ob, cudaSuccess);
+    if (hdiag) {
+        e = download(hdiag->row_max, dd.row_max, rb, e);
+        e = download(hdiag->ell, dd.ell, rb, e);
+        e = download(hdiag->ell_tail, dd.ell_tail, rb, e);
+    }
+    return e == cudaSuccess ? PISA_OK : cuda_fail(ctx, e, "attention_host copy-out");
 }
 
 pisa_status pisa_b200_selftest_mma(pisa_ctx* ctx, const void* a, const void* b, float* out,

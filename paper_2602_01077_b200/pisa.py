@@ -371,6 +371,16 @@ def _check_inputs(*ts):
             raise Unsupported("Unsupported: q/k/v must be bfloat16")
 
 
+def _check_out(q, out):
+    if tuple(out.shape) != tuple(q.shape):
+        raise InvalidDimension(f"InvalidDimension: output shape {tuple(out.shape)} != query shape "
+                               f"{tuple(q.shape)}")
+    if out.device != q.device:
+        raise InvalidDimension("InvalidDimension: output must live on the inputs' device")
+    if out.dtype not in (torch.bfloat16, torch.float32):
+        raise Unsupported(f"Unsupported: output dtype {out.dtype} (bfloat16 or float32)")
+
+
 def resolve(desc: _abi.AttnDesc):
     n = _abi.i64()
     k = _abi.i64()
@@ -393,6 +403,7 @@ def fwd(q, k, v, out=None, *, layout="bhld", out_dtype=torch.bfloat16, diagnosti
     ctx = ctx or Context.get(q.device.index)
     if out is None:
         out = torch.empty(q.shape, dtype=out_dtype, device=q.device)
+    _check_out(q, out)
     desc = make_desc(q, k, v, out, layout=layout, **kw)
     N, kk, _ = resolve(desc)
     B, H, L = desc.batch, desc.heads, desc.seq_len
@@ -530,11 +541,38 @@ def select_topk_covariance(q_bar: torch.Tensor, k_bar: torch.Tensor, m: torch.Te
     return sel
 
 
+def _check_engine_inputs(desc, selected, stats: BlockStatistics, cfg: AttentionConfig):
+    """detail::check_engine_inputs (engine.hpp:61-80): the plan and the block
+    statistics must describe these inputs, else InvalidDimension (the plan's
+    ordering / range is validated on the device, SelectionPlan::validate)."""
+    B, H, L, d = desc.batch, desc.heads, desc.seq_len, desc.head_dim
+    N = -(-L // cfg.block_size)
+    lead = [(B, H), (H,)] if B == 1 else [(B, H)]  # [B][H][..] or, for B = 1, [H][..]
+
+    def fits(t, tail):
+        return tuple(t.shape[-len(tail):]) == tail and tuple(t.shape[:-len(tail)]) in lead
+
+    if stats.block_size != cfg.block_size or stats.num_blocks != N or stats.dim != d:
+        raise InvalidDimension("InvalidDimension: block statistics do not match inputs")
+    for t, tail in ((stats.k_bar, (N, d)), (stats.v_hat, (N, d)), (stats.h_bar, (d, d))):
+        if not fits(t, tail) or t.device != selected.device:
+            raise InvalidDimension("InvalidDimension: block statistics do not match inputs")
+    if selected.dim() < 3 or not fits(selected, (N, selected.shape[-1])):
+        raise InvalidDimension("InvalidDimension: selection plan does not match inputs")
+    if selected.shape[-1] < 1:
+        raise EmptySelection("EmptySelection: query blocks select no key block")
+
+
 def pisa_attention(q, k, v, selected: torch.Tensor, stats: BlockStatistics,
                    cfg: AttentionConfig = AttentionConfig(), variant=PisaVariant.Hybrid,
-                   out_dtype=torch.bfloat16, diagnostics=True, ragged=True):
+                   out_dtype=torch.bfloat16, diagnostics=True, ragged=True,
+                   literal_phase3: Optional[bool] = None):
     """pisa_streaming / pisa_reference (engine.hpp:103-383) for a given plan and
-    prepare products. q/k/v [H][L][d] or [B][H][L][d]; selected [..][N][k]."""
+    prepare products. q/k/v [H][L][d] or [B][H][L][d]; selected [..][N][k].
+    ``literal_phase3`` defaults to ``cfg.literal_phase3`` for Hybrid (the
+    streaming path's diagnostic, engine.hpp:345-346) and is off otherwise."""
+    if literal_phase3 is None:
+        literal_phase3 = cfg.literal_phase3 and int(variant) == int(PisaVariant.Hybrid)
     q4, k4, v4 = _bundle4(q), _bundle4(k), _bundle4(v)
     _check_inputs(q4, k4, v4)
     ctx = Context.get(q4.device.index)
@@ -542,8 +580,9 @@ def pisa_attention(q, k, v, selected: torch.Tensor, stats: BlockStatistics,
     kk = selected.shape[-1]
     desc = make_desc(q4, k4, v4, out, block_size=cfg.block_size, group_size=cfg.group_size,
                      scale=cfg.scale, topk=kk, variant=variant,
-                     literal_phase3=cfg.literal_phase3, ragged=ragged, check_finite=True)
+                     literal_phase3=literal_phase3, ragged=ragged, check_finite=True)
     B, H, L = desc.batch, desc.heads, desc.seq_len
+    _check_engine_inputs(desc, selected, stats, cfg)
     diag = _abi.Diag()
     ex = {}
     if diagnostics:
@@ -570,6 +609,7 @@ def pisa_reference(q, k, v, plan, stats, variant: PisaVariant,
                    cfg: AttentionConfig = AttentionConfig(), **kw):
     """engine.hpp:103-223 (SparseOnly / Zeroth / Hybrid / GlobalCentroid)."""
     sel = plan.selected if isinstance(plan, SelectionPlan) else plan
+    kw.setdefault("literal_phase3", False)  # pisa_reference has no literal Phase 3
     return pisa_attention(q, k, v, sel, stats, cfg, variant, **kw)
 
 
@@ -598,7 +638,8 @@ def pisa_multihead(bundle: TensorBundle, r: float, router: RouterOptions = Route
     On the GPU all heads run in one stream-ordered K1 -> K2 -> K3 sequence; the
     streaming and reference formulations are the same kernel (they agree to
     1e-10 in the reference, test_engine.cpp:137-150), so ``use_streaming`` only
-    selects which variant set is legal, as in the reference (:460)."""
+    decides whether ``cfg.literal_phase3`` applies (streaming Hybrid only, :460).
+    A non-finite output raises NumericalOverflow (engine.hpp:368)."""
     if router.row_level:
         raise Unsupported("Unsupported: row-level routing is not on the GPU path")
     cfg.check(bundle.seq_len, ragged=ragged)
@@ -607,11 +648,15 @@ def pisa_multihead(bundle: TensorBundle, r: float, router: RouterOptions = Route
     res_k = sparsity_to_k(r, n)
     q4, k4, v4 = _bundle4(bundle.q), _bundle4(bundle.k), _bundle4(bundle.v)
     t0 = time.perf_counter()
+    # the streaming path (use_streaming and Hybrid, engine.hpp:460) is the only
+    # one that honours literal_phase3; every head's output is checked for
+    # non-finite values (check_output_finite, engine.hpp:221,368)
+    literal = cfg.literal_phase3 and use_streaming and int(variant) == int(PisaVariant.Hybrid)
     out, ex = fwd(q4, k4, v4, out_dtype=out_dtype, diagnostics=diagnostics, return_plan=True,
                   block_size=cfg.block_size, group_size=cfg.group_size, scale=cfg.scale,
                   sparsity=r, variant=variant, force_diagonal=router.force_diagonal,
-                  literal_phase3=cfg.literal_phase3, ragged=ragged, router=router.strategy,
-                  epsilon=router.epsilon)
+                  literal_phase3=literal, ragged=ragged, router=router.strategy,
+                  epsilon=router.epsilon, check_finite=True)
     torch.cuda.current_stream().synchronize()
     ms = (time.perf_counter() - t0) * 1e3
     res = MultiheadResult(k=res_k.k, num_blocks=n, sparsity_requested=r,

@@ -33,7 +33,7 @@ def test_exports_every_declared_symbol(lib):
 
 
 def test_abi_version(lib):
-    assert lib.pisa_b200_abi_version() == 2  # v2: RouterOptions epsilon / row_level in the descriptor
+    assert lib.pisa_b200_abi_version() == 3  # v3: host-buffer step entries + reference generators
 
 
 def test_kernel_names(lib):

@@ -368,6 +368,113 @@ def test_numerical_overflow_reported(P):
         P.fwd(q, k, v, topk=1, check_finite=True, out_dtype=torch.float32)
 
 
+def test_numerical_overflow_through_multihead_and_host_path(P):
+    """check_output_finite (engine.hpp:83-93, :368) on the reference-facing
+    entries: pisa_multihead raises NumericalOverflow; the host-buffer forward
+    ORs the device flag over all staged chunks and reports it after its final
+    synchronisation; with the check off the call returns the non-finite output."""
+    import torch
+    H, L, d = 3, 320, 64
+    q, k = (torch.randn((1, H, L, d), device="cuda").bfloat16() for _ in range(2))
+    v = torch.randn((1, H, L, d), device="cuda").bfloat16()
+    v[0, 1] = 3.0e38  # one head of three overflows
+    with pytest.raises(P.NumericalOverflow):
+        P.pisa_multihead(P.TensorBundle(q[0], k[0], v[0]), 0.75, P.RouterOptions(), P.PisaVariant.Hybrid,
+                         P.AttentionConfig(), True)
+    hq, hk, hv = (t.cpu().pin_memory() for t in (q, k, v))
+    ho = torch.empty((1, H, L, d), dtype=torch.bfloat16).pin_memory()
+    with pytest.raises(P.NumericalOverflow):
+        P.fwd_host(hq, hk, hv, ho, sparsity=0.75, check_finite=True)
+    P.fwd_host(hq, hk, hv, ho, sparsity=0.75)  # unchecked: returns
+    assert not torch.isfinite(ho[0, 1].float()).all() and torch.isfinite(ho[0, 0].float()).all()
+    v[0, 1] = 1.0
+    hv = v.cpu().pin_memory()
+    P.fwd_host(hq, hk, hv, ho, sparsity=0.75, check_finite=True)  # the flag was reset
+    assert torch.isfinite(ho.float()).all()
+
+
+def test_output_and_engine_input_validation(P, oracle_mod):
+    """fwd() checks O (shape, device, dtype, 16-byte rows) and pisa_streaming /
+    pisa_reference check the plan and statistics against the inputs
+    (check_engine_inputs, engine.hpp:61-80) instead of reading past buffers."""
+    import torch
+    O = oracle_mod
+    q, k, v = (dev_bf16(x) for x in O.gen("gaussian", 1, 1, 512, 128))
+    with pytest.raises(P.InvalidDimension):
+        P.fwd(q, k, v, torch.empty((1, 1, 448, 128), dtype=torch.bfloat16, device="cuda"))
+    with pytest.raises(P.Unsupported):
+        P.fwd(q, k, v, torch.empty_like(q, dtype=torch.float16))
+    wide = torch.zeros((1, 1, 512, 132), dtype=torch.bfloat16, device="cuda")
+    with pytest.raises(P.InvalidDimension):  # row stride 132 bf16 = 264 B: not 16-byte rows
+        P.fwd(q, k, v, wide[..., :128])
+    wide = torch.zeros((1, 1, 512, 136), dtype=torch.bfloat16, device="cuda")
+    P.fwd(q, k, v, wide[..., :128], sparsity=0.75)  # 272 B rows: fine, padding untouched
+    torch.cuda.synchronize()
+    assert not wide[..., 128:].any() and torch.equal(wide[..., :128], P.fwd(q, k, v, sparsity=0.75))
+    st = P.compute_prepare(q[0], k[0], v[0])
+    sel = P.select_topk_plain(st.q_bar, st.k_bar, 2, 128 ** -0.5)
+    out, _ = P.pisa_streaming(q[0], k[0], v[0], sel, st)
+    with pytest.raises(P.InvalidDimension):  # plan for fewer query blocks
+        P.pisa_streaming(q[0], k[0], v[0], sel[:, :, :7], st)
+    with pytest.raises(P.InvalidDimension):  # statistics of another length
+        P.pisa_streaming(q[0], k[0], v[0], sel,
+                         P.BlockStatistics(7, 64, 128, st.k_bar[:, :, :7], st.v_hat[:, :, :7], st.h_bar))
+    with pytest.raises(P.InvalidDimension):  # block size mismatch
+        P.pisa_reference(q[0], k[0], v[0], sel, P.BlockStatistics(8, 32, 128, st.k_bar, st.v_hat, st.h_bar),
+                         P.PisaVariant.Zeroth)
+
+
+def test_literal_phase3_only_on_the_streaming_path(P, oracle_mod):
+    """literal_phase3 divides the Phase-3 weight by B on the streaming path only
+    (engine.hpp:345-346); pisa_reference and GlobalCentroid ignore it
+    (engine.hpp:194-209), and pisa_multihead(use_streaming=False) with it."""
+    import torch
+    O = oracle_mod
+    q, k, v = (dev_bf16(x, False) for x in O.gen("clustered", 4, 1, 1024, 128))
+    st = P.compute_prepare(q, k, v)
+    sel = P.select_topk_plain(st.q_bar, st.k_bar, 4, 128 ** -0.5)
+    lit_cfg = P.AttentionConfig(literal_phase3=True)
+    a, _ = P.pisa_reference(q, k, v, sel, st, P.PisaVariant.Hybrid, lit_cfg)
+    b, _ = P.pisa_reference(q, k, v, sel, st, P.PisaVariant.Hybrid)
+    c, _ = P.pisa_streaming(q, k, v, sel, st, lit_cfg)
+    assert torch.equal(a, b) and not torch.equal(b, c)
+    g0, _ = P.pisa_reference(q, k, v, sel, st, P.PisaVariant.GlobalCentroid, lit_cfg)
+    g3, _ = P.pisa_reference(q, k, v, sel, st, P.PisaVariant.GlobalCentroid)
+    g1 = P.fwd(q[None], k[None], v[None], topk=4, variant=P.PisaVariant.GlobalCentroid, literal_phase3=True)
+    g2 = P.fwd(q[None], k[None], v[None], topk=4, variant=P.PisaVariant.GlobalCentroid)
+    assert torch.equal(g1, g2) and torch.equal(g0, g3)
+    bundle = P.TensorBundle(q, k, v)
+    r_ref = P.pisa_multihead(bundle, 0.75, P.RouterOptions(), P.PisaVariant.Hybrid, lit_cfg, False)
+    r_dflt = P.pisa_multihead(bundle, 0.75, P.RouterOptions(), P.PisaVariant.Hybrid, P.AttentionConfig(), True)
+    r_lit = P.pisa_multihead(bundle, 0.75, P.RouterOptions(), P.PisaVariant.Hybrid, lit_cfg, True)
+    assert torch.equal(r_ref.heads[0].output, r_dflt.heads[0].output)
+    assert not torch.equal(r_lit.heads[0].output, r_dflt.heads[0].output)
+
+
+def test_concurrent_streams_do_not_share_workspace(P):
+    """Forwards of different shapes enqueued back to back on two streams of one
+    context (no synchronisation in between) equal the same forwards run alone:
+    each stream has its own workspace."""
+    import torch
+    g = torch.Generator(device="cuda").manual_seed(5)
+    xa = [torch.randn((1, 4, 4096, 128), generator=g, device="cuda", dtype=torch.bfloat16) for _ in range(3)]
+    xb = [torch.randn((1, 2, 2000, 64), generator=g, device="cuda", dtype=torch.bfloat16) for _ in range(3)]
+    ref_a = P.fwd(*xa, sparsity=0.875)
+    ref_b = P.fwd(*xb, sparsity=0.5)
+    torch.cuda.synchronize()
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    outs = []
+    for _ in range(3):
+        with torch.cuda.stream(s1):
+            oa = P.fwd(*xa, sparsity=0.875)
+        with torch.cuda.stream(s2):
+            ob = P.fwd(*xb, sparsity=0.5)
+        outs.append((oa, ob))
+    torch.cuda.synchronize()
+    for oa, ob in outs:
+        assert torch.equal(oa, ref_a) and torch.equal(ob, ref_b)
+
+
 def test_attention_with_given_plan_and_validation(P, oracle_mod):
     """pisa_streaming / pisa_reference with the REFERENCE plan and fp32 stats,
     and SelectionPlan::validate semantics for a bad plan (router.hpp:50-70)."""
@@ -461,12 +568,17 @@ def test_full_size_head_parity(P, oracle_mod, name, L, r):
 
 def test_cpp_shim_drop_in(P, oracle_mod, tmp_path):
     """A reference-style C++ caller (tests/cpp/shim_demo.cpp) compiled against
-    include/pisa_b200.hpp and linked to the C ABI library."""
+    include/pisa_b200.hpp and linked to the C ABI library: pisa_multihead on one
+    and on two "devices", the step functions (compute_block_stats ->
+    compute_global_stats -> query_block_means -> select_topk_plain ->
+    pisa_streaming / pisa_reference), NumericalOverflow, the error classes and
+    the reference generators -- all checked here against the oracle / the
+    reference's own values."""
     import subprocess
     O = oracle_mod
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     exe = tmp_path / "shim_demo"
-    subprocess.run(["g++", "-std=c++17", "-O2", "-I", os.path.join(root, "include"),
+    subprocess.run(["g++", "-std=c++17", "-O2", "-pthread", "-I", os.path.join(root, "include"),
                     os.path.join(root, "tests", "cpp", "shim_demo.cpp"),
                     "-L", os.path.join(root, "paper_2602_01077_b200", "lib"), "-lpisa_b200",
                     "-Wl,-rpath," + os.path.join(root, "paper_2602_01077_b200", "lib"),
@@ -477,19 +589,42 @@ def test_cpp_shim_drop_in(P, oracle_mod, tmp_path):
     with open(inp, "wb") as f:
         for x in (q, k, v):
             f.write(np.ascontiguousarray(x, np.float32).tobytes())
-    out_p, plan_p = tmp_path / "out.bin", tmp_path / "plan.bin"
-    res = subprocess.run([str(exe), str(inp), str(out_p), str(plan_p), str(H), str(L), str(d), str(r)],
-                         capture_output=True, text=True, timeout=300)
-    assert res.returncode == 0, res.stderr
-    assert "BlockDivisibility ok" in res.stdout
-    out = np.fromfile(out_p, np.float32).reshape(H, L, d)
+    res = subprocess.run([str(exe), str(inp), str(tmp_path), str(H), str(L), str(d), str(r)],
+                         capture_output=True, text=True, timeout=600)
+    assert res.returncode == 0, res.stdout + res.stderr
+    for check in ("multidevice ok", "BlockDivisibility ok", "steps ok", "covariance ok",
+                  "InvalidDimension ok", "NumericalOverflow ok", "gen ok"):
+        assert check in res.stdout, (check, res.stdout)
+    out = np.fromfile(tmp_path / "multihead_out.bin", np.float32).reshape(H, L, d)
     N = 16
     kk = int(res.stdout.split()[0])
-    plan = np.fromfile(plan_p, np.int32).reshape(H, N, kk)
+    plan = np.fromfile(tmp_path / "multihead_plan.bin", np.int32).reshape(H, N, kk)
     ref = O.multihead(q, k, v, r=r)
     assert np.array_equal(plan, ref["selected"])
     for h in range(H):
         check_close(out[h], ref["out"][h])
+    # step functions on head 0 floored to 960 rows vs the oracle's steps
+    Lf, Nf = 960, 15
+    kf = O.sparsity_to_k(r, Nf)[0]
+    kb, vh, hb, kg = O.block_stats(k[0, :Lf], v[0, :Lf])
+    qb = O.query_means(q[0, :Lf])
+    stats = np.fromfile(tmp_path / "steps_stats.bin", np.float64)
+    g_kb, g_vh, g_qb = (stats[i * Nf * d:(i + 1) * Nf * d].reshape(Nf, d) for i in range(3))
+    g_hb = stats[3 * Nf * d:].reshape(d, d)
+    np.testing.assert_allclose(g_kb, kb, rtol=0, atol=1e-6)
+    np.testing.assert_allclose(g_vh, vh, rtol=0, atol=1e-5)
+    np.testing.assert_allclose(g_qb, qb, rtol=0, atol=1e-6)
+    assert np.abs(g_hb - hb).max() <= 1e-4 * max(1.0, np.abs(hb).max())
+    splan = np.fromfile(tmp_path / "steps_plan.bin", np.int32).reshape(Nf, kf)
+    assert np.array_equal(splan, O.select_plain(qb, kb, kf, d ** -0.5))
+    sout = np.fromfile(tmp_path / "steps_out.bin", np.float32).reshape(Lf, d)
+    ref_s = O.pisa_attention(q[0, :Lf], k[0, :Lf], v[0, :Lf], splan, (kb, vh, hb, kg), d ** -0.5,
+                             "hybrid")[0]
+    check_close(sout, ref_s)
+    # the reference's generator values (gen_gaussian<float>(42, 2, 64, 8, 1.0))
+    gen = np.fromfile(tmp_path / "gen.bin", np.float32).reshape(3, 2, 64, 8)
+    gq, gk, gv = O.gen("gaussian", 42, 2, 64, 8, bf16=False)
+    assert np.array_equal(gen[0], gq) and np.array_equal(gen[1], gk) and np.array_equal(gen[2], gv)
 
 
 # ----------------------------------- (head x query-block range) sharding (§8e) --
