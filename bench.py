@@ -118,17 +118,18 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------ CPU legs --
-def cpu_reference_sample(wl, steps, warmup, log):
+def cpu_reference_sample(wl, steps, warmup, log, data="gaussian", density=None):
     """Times the unmodified reference (oracle/_ref, compiled from /root/reference)
     on the host cores: prepare over a full head + route + pisa_streaming for a
-    bounded range of query blocks (pisa_cli.cpp:728-729 semantics, accum F32)."""
-    import ctypes as C
-
-    import numpy as np
+    bounded range of query blocks (pisa_cli.cpp:728-729 semantics, accum F32).
+    Inputs: head 0 of the GPU arm's bundle (gen_gaussian / gen_clustered seed 0,
+    bf16-rounded), floored to whole blocks."""
+    import numpy as np  # noqa: F401
 
     import oracle as O
 
-    B, H, L, d, density, _ = WORKLOADS[wl]
+    B, H, L, d, dens0, _ = WORKLOADS[wl]
+    density = dens0 if density is None else density
     Lf = (L // 64) * 64  # the reference rejects L % 64 != 0 (attention.hpp:43-47)
     N = Lf // 64
     threads = os.cpu_count() or 1
@@ -136,8 +137,10 @@ def cpu_reference_sample(wl, steps, warmup, log):
     if not O.ref_available():
         O.build()
     R = O.ref()
-    q, k, v = O.ref_gen("gaussian", 0, 1, Lf, d)
-    q, k, v = (O.round_bf16(x[0]) for x in (q, k, v))
+    if data == "gaussian":  # head 0 of gen_gaussian(0, B*H, L, d) without the other heads
+        q, k, v = O.gen_gaussian_head(0, B * H, L, d, 0, rows=Lf)
+    else:  # gen_clustered draws head 0 first: a one-head bundle has the same head 0
+        q, k, v = (x[0, :Lf].copy() for x in O.gen("clustered", 0, 1, L, d))
     # Bounded sample: prepare over the full head, routing + streaming attention for a
     # range of query blocks sized to ~2 s of CPU work. The full-head time is
     # extrapolated linearly in query blocks (heads are serial, engine.hpp:432, and
@@ -146,7 +149,7 @@ def cpu_reference_sample(wl, steps, warmup, log):
     ms = np.zeros(3)
 
     def run(nqb):
-        st = R.ref_bench_sample(q, k, v, Lf, d, 1.0 - density, 0, nqb, threads, out, ms)
+        st = R.ref_bench_sample(q, k, v, Lf, d, 1.0 - density, 0, nqb, threads, out, ms)  # noqa: B023
         if st != 0:
             raise RuntimeError(f"ref_bench_sample status {st}")
         return ms.copy()
@@ -161,14 +164,53 @@ def cpu_reference_sample(wl, steps, warmup, log):
             heads.append(m[0] + (m[1] + m[2]) * N / qb1)
     tm = statistics.median(heads)
     value = 4.0 * Lf * Lf * d / (tm * 1e-3) / 1e12  # dense-equivalent TFLOPS of one head
-    sample = (f"1 head of {wl} at L={Lf} (floored to a multiple of 64): prepare over the full "
-              f"head + routing and Hybrid streaming (accum f32) for query blocks [0,{qb1}) of "
-              f"{N}, extrapolated to the head (t_prep + t_blocks*N/{qb1}); gen_gaussian seed 0 "
-              f"bf16-rounded; median of {len(heads)} after {warmup} warmup; "
-              f"PISA_THREADS={threads}")
+    sample = (f"head 0 of {wl} (the GPU arm's gen_{data} seed-0 bundle, bf16-rounded) floored to "
+              f"L={Lf}: prepare over the full head + routing and Hybrid streaming (accum f32) for "
+              f"query blocks [0,{qb1}) of {N}, extrapolated to the head (t_prep + t_blocks*N/{qb1}); "
+              f"median of {len(heads)} after {warmup} warmup; PISA_THREADS={threads}")
     return {"value": value, "unit": "TFLOPS (dense-equivalent)", "cores": threads,
             "kind": "reference", "sample": sample, "ms_per_sample": tm,
             "lib": os.path.basename(R._path), "ms_per_head": tm}
+
+
+def gen_inputs(P, kind, heads, L, d):
+    """Host bf16 [heads][L][d] q, k, v: the reference's gen_gaussian / gen_clustered
+    values (seed 0; generate.hpp:29-116) through pisa_b200_gen_* (bit-identical,
+    tests/test_generate.py)."""
+    import torch
+    if kind == "gaussian":
+        return P.gen_gaussian(0, heads, L, d, 1.0, dtype=torch.bfloat16)
+    return P.gen_clustered(0, heads, L, d, 16, 2.0, 0.15, dtype=torch.bfloat16)
+
+
+def plan_parity(P, q, k, v, plan, density, d):
+    """The GPU's routing plan of every head against the CPU restatement of the
+    reference's prepare + select_topk_plain at the workload's own (ragged) length
+    (oracle, pinned to oracle/_ref in tests/test_oracle.py): rows that differ,
+    and how many of them are near-ties (fp64 gap to the k-th score <= 1e-6 |s_k|)."""
+    import concurrent.futures as cf
+
+    import oracle as O
+    from oracle import parity
+
+    H, N, k = plan.shape
+    scale = d ** -0.5
+
+    def head(h):
+        qf, kf, vf = (x[0, h].float().numpy() for x in (q, k, v))
+        st = O.block_stats(kf, vf)
+        qb = O.query_means(qf)
+        return parity.classify_rows(plan[h], O.select_plain(qb, st[0], k, scale), qb, st[0], k, scale)
+
+    t0 = time.perf_counter()
+    with cf.ThreadPoolExecutor(min(H, os.cpu_count() or 1)) as ex:
+        res = list(ex.map(head, range(H)))
+    return {"plan_rows": H * N, "rows_differing": sum(r[0] for r in res),
+            "near_tie_rows": sum(r[1] for r in res), "near_tie_swaps": sum(r[2] for r in res),
+            "non_tie_rows": sum(len(r[3]) for r in res),
+            "against": "oracle restatement of compute_block_stats + select_topk_plain at this L "
+                       "(PARITY_r02.json: the unmodified reference at the floored length)",
+            "seconds": round(time.perf_counter() - t0, 1)}
 
 
 # ---------------------------------------------------------- GPU arm ----
@@ -210,12 +252,12 @@ def main():
     if args.impl == "reference":
         if rank != 0:
             return
-        res = cpu_reference_sample(args.workload, args.steps, warmup, None)
+        res = cpu_reference_sample(args.workload, args.steps, warmup, None, args.data, density)
         line = {"impl": "reference", "metric": METRIC, "value": res["value"], "unit": res["unit"],
                 "n_gpus": args.gpus, "steps": args.steps, "warmup": warmup,
                 "ms_per_step": res["ms_per_sample"] * H, "higher_is_better": True,
                 "scaling": "strong", "vs_baseline": None, "dtype": "f32",
-                "data": "synthetic gen_gaussian(seed 0) rounded to bf16",
+                "data": f"synthetic gen_{args.data}(seed 0) rounded to bf16 (head 0 of the GPU arm's bundle)",
                 "config": {"workload": f"{cfg_name} (bounded CPU sample)", "B": B, "H": H,
                            "L": L, "d": d, "density": density, "block": 64,
                            "variant": "hybrid", "router": "plain"},
@@ -255,23 +297,18 @@ def main():
         h0, h1 = min(p.h0 for p in pieces), max(p.h1 for p in pieces)
     Hr = h1 - h0  # heads whose Q/K/V this rank holds
 
-    g = torch.Generator(device=dev)
-    g.manual_seed(1234 + rank)
+    # The reference's own synthetic bundle (gen_gaussian(seed 0, std 1) or
+    # gen_clustered(seed 0, 16 clusters, concentration 2, noise 0.15), the CLI
+    # defaults, pisa_cli.cpp:27-39), bf16-rounded, from the library's
+    # bit-identical generator on the host cores; this rank's heads are uploaded.
+    # The reference arm times the same values (head 0, floored to whole blocks).
     shape = (B, Hr, L, d)
-    if args.data == "gaussian":
-        q, kk, v = (torch.randn(shape, generator=g, device=dev, dtype=torch.bfloat16)
-                    for _ in range(3))
-    else:  # gen_clustered-like structure (generate.hpp:132-190) drawn on the GPU
-        nc = 16
-        run = -(-L // nc)
-        ctr = torch.randn((B, Hr, nc, d), generator=g, device=dev)
-        zi = torch.clamp(torch.arange(L, device=dev) // run, max=nc - 1)
-        kk = (ctr[:, :, zi] + 0.15 * torch.randn(shape, generator=g, device=dev)).bfloat16()
-        sub = torch.randint(0, nc, (B, Hr, max(1, nc // 4)), generator=g, device=dev)
-        pick = torch.gather(sub, 2, torch.randint(0, sub.shape[-1], (B, Hr, L), generator=g, device=dev))
-        q = (2.0 * torch.gather(ctr, 2, pick.unsqueeze(-1).expand(B, Hr, L, d))
-             + torch.randn(shape, generator=g, device=dev)).bfloat16()
-        v = torch.randn(shape, generator=g, device=dev, dtype=torch.bfloat16)
+    t_gen = time.perf_counter()
+    host = gen_inputs(P, args.data, B * H, L, d)
+    hq, hk, hv = (x[h0:h1].unsqueeze(0).pin_memory() for x in host)
+    del host
+    q, kk, v = (x.to(dev) for x in (hq, hk, hv))
+    t_gen = time.perf_counter() - t_gen
     out = torch.empty(shape, device=dev, dtype=torch.bfloat16)
     ctx = P.Context.get(local_rank)
     kw = dict(sparsity=1.0 - density, variant=P.PisaVariant.Hybrid)
@@ -377,33 +414,49 @@ def main():
 
     total_dense = H * B * flops_dense(L, d)
     value = total_dense / (t_ms * 1e-3) / 1e12
-    # roofline of the dominant kernel (fused) on this rank
+    # roofline of the dominant kernel (fused) on this rank: against the measured
+    # BURST dense bf16 peak (MEASURED_PEAKS.json bf16_tflops); the sustained
+    # figure (cuBLAS back to back under the power cap) is reported beside it
     peak_burst, peak_sus, hbm, peak_src = load_peaks()
-    # The burst figure applies to a kernel timed alone, the sustained one
-    # (MEASURED_PEAKS.json: cuBLAS back to back, power-capped) to a kernel timed
-    # inside a long step. The fused kernel runs 25 ms per launch, so it is
-    # sustained whenever the clocks sampled over the timed region show the power
-    # cap engaged.
     capped = "sw_power_cap" in (clocks.get("reasons") or [])
-    peak = peak_sus if capped else peak_burst
-    peak_src = f"{peak_src} {'sustained (power cap engaged during the timed region)' if capped else 'burst'}"
+    peak = peak_burst
+    peak_src = f"{peak_src} burst (bf16_tflops); sustained in peak_sustained / frac_sustained"
     fused_ms, fused_n = prof.get("fused_attn_kernel", (0.0, 0))
     fused_avg = fused_ms / max(1, fused_n)
     fused_step = fused_ms / args.steps  # one launch per piece, pieces per step
     alg = B * flops_fused(L, d, N, k) * sum((p.h1 - p.h0) * (p.qb1 - p.qb0) for p in pieces) / N
     achieved = alg / (fused_step * 1e-3) / 1e12 if fused_step > 0 else None
     executed = exec_flops / (fused_step * 1e-3) / 1e12 if fused_step > 0 else None
-    traffic = None
+    # DRAM bytes per launch from the committed ncu --set full capture of this
+    # workload (profiles/traffic.json names the capture); not measured live
+    traffic, traffic_src = None, None
     tp = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tp):
         try:
             with open(tp) as f:
-                traffic = json.load(f).get(args.workload, {}).get("fused_attn_kernel_bytes")
+                tj = json.load(f)
+            traffic = tj.get(args.workload, {}).get("fused_attn_kernel_bytes")
+            traffic_src = tj.get(args.workload, {}).get("source")
         except Exception:
             traffic = None
     kernels = {n: {"ms_per_launch": ms / max(1, c), "launches": c,
                    "share": ms / max(1e-9, sum(x[0] for x in prof.values()))}
                for n, (ms, c) in prof.items()}
+    # HBM rooflines of the prepare (K1) and select (K2) kernels, SURVEY §8(d):
+    # K1 reads Q, K, V (3 L d 2 B) and writes k_bar / v_hat / q_bar fp32 and the
+    # bf16 k_bar / v_hat copies (3 N d 4 + 2 N d 2 B) per head; K2 reads q_bar /
+    # k_bar (2 N d 4 B) and writes the plan (N k 4 B) per head
+    units = B * sum((p.h1 - p.h0) for p in pieces)
+    k1_bytes = units * (3 * L * d * 2 + 3 * N * d * 4 + 2 * N * d * 2)
+    k2_bytes = units * (2 * N * d * 4 + N * k * 4)
+    hbm_rooflines = {}
+    for name, nbytes, extra in (("block_stats_kernel", k1_bytes, {}),
+                                ("select_kernels", k2_bytes, {"fp32_flops_per_launch": units * 2.0 * N * N * d})):
+        ms, c = prof.get(name, (0.0, 0))
+        if c:
+            gbs = nbytes / (ms / c * 1e-3) / 1e9
+            hbm_rooflines[name] = {"bound": "hbm", "achieved": gbs, "peak": hbm, "unit": "GB/s", "frac": gbs / hbm,
+                                   "algorithmic_bytes_per_launch": nbytes, "ms_per_launch": ms / c, **extra}
 
     # dense attention baseline on the same B200 (cuDNN/flash SDPA via torch), this rank's heads
     dense = None
@@ -428,7 +481,6 @@ def main():
     # end to end through the C-ABI host path: pinned host buffers, H2D + D2H timed
     e2e = None
     if not args.no_e2e:
-        hq, hk, hv = (x.cpu().pin_memory() for x in (q, kk, v))
         ho = torch.empty(shape, dtype=torch.bfloat16).pin_memory()
         for _ in range(2):
             P.fwd_host(hq, hk, hv, ho, device=local_rank, **kw)
@@ -451,10 +503,21 @@ def main():
                "path": "pisa_b200_fwd_host (pinned host Q/K/V/O; H2D, compute, D2H overlapped per head chunk)"
                        + ("" if even else "; whole heads of each rank's span (partial heads computed in full)")}
 
+    # routing plan of the timed inputs vs the CPU restatement of the reference
+    # (every head; near-tie swaps counted), rank 0 at N = 1
+    parity_res = None
+    if rank == 0 and world == 1 and not args.no_cpu and args.router == "plain":
+        try:
+            _, exq = P.fwd(q, kk, v, return_plan=True, **kw)
+            parity_res = plan_parity(P, hq, hk, hv, exq["selected"][0].cpu().numpy(), density, d)
+            del exq
+        except Exception as e:  # noqa: BLE001
+            parity_res = {"error": str(e)[:200]}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         try:
-            cpu = cpu_reference_sample(args.workload, 3, 1, None)
+            cpu = cpu_reference_sample(args.workload, 3, 1, None, args.data, density)
             cpu.pop("ms_per_sample", None)
             cpu.pop("lib", None)
         except Exception as e:  # noqa: BLE001
@@ -465,7 +528,8 @@ def main():
             "metric": METRIC, "value": value, "unit": "TFLOPS (dense-equivalent)",
             "n_gpus": world, "steps": args.steps, "warmup": warmup, "ms_per_step": t_ms,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
-            "data": f"synthetic {args.data} (torch RNG on device), bf16",
+            "data": f"synthetic gen_{args.data}(seed 0) values of the reference's generator, bf16-rounded",
+            "input_generation_s": t_gen,
             "config": {"workload": cfg_name, "B": B, "H": H, "L": L, "d": d, "N": N, "k": k,
                        "density": density, "block": 64, "variant": "hybrid", "router": args.router,
                        "parallelism": (f"head-sharded x{world}" if even
@@ -474,10 +538,14 @@ def main():
                        "l2": l2_note},
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                          "frac": (achieved / peak) if achieved else None, "traffic": traffic,
+                         "traffic_source": traffic_src,
                          "kernel": "fused_attn_kernel", "kernel_ms": fused_avg,
                          "algorithmic_flops_per_launch": alg, "executed_flops_per_launch": exec_flops,
                          "executed_tflops": executed,
                          "executed_frac": (executed / peak) if executed else None,
+                         "frac_sustained": (achieved / peak_sus) if achieved else None,
+                         "executed_frac_sustained": (executed / peak_sus) if executed else None,
+                         "power_capped": capped,
                          "union_over_k": union_ratio, "peak_source": peak_src, "peak_burst": peak_burst,
                          "peak_sustained": peak_sus,
                          "kernel_timing": ("library events around each launch inside the timed region"
@@ -485,6 +553,8 @@ def main():
                                            f"library events around each launch in a pass of the same "
                                            f"{args.steps} steps after the timed region (step < 5 ms)")},
             "kernels": kernels,
+            "hbm_rooflines": hbm_rooflines,
+            "plan_parity": parity_res,
             "graph": (None if graph_ms is None else
                       {"ms_per_step": graph_ms, "value": total_dense / (graph_ms * 1e-3) / 1e12,
                        "note": "the same step replayed from a CUDA graph (rank 0); not the headline value"}),

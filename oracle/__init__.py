@@ -50,6 +50,8 @@ def lib():
         L.oracle_rng_u64.argtypes = [C.c_uint64, _u64p, i64]
         L.oracle_rng_gaussian.argtypes = [C.c_uint64, _f64p, i64]
         L.oracle_gen_gaussian.argtypes = [C.c_uint64, i64, i64, i64, C.c_double, _f32p, _f32p, _f32p]
+        L.oracle_gen_gaussian_head.argtypes = [C.c_uint64, i64, i64, i64, C.c_double, i64, i64, _f32p,
+                                               _f32p, _f32p]
         L.oracle_gen_clustered.argtypes = [C.c_uint64, i64, i64, i64, i64, C.c_double, C.c_double,
                                            _f32p, _f32p, _f32p]
         L.oracle_round_bf16.argtypes = [_f32p, i64]
@@ -113,6 +115,9 @@ def ref():
         R.ref_bench_sample.argtypes = [_f32p, _f32p, _f32p, i64, i64, C.c_double, i64, i64,
                                        C.c_uint, _f32p, _f64p]
         R.ref_dense_online.argtypes = [_f32p, _f32p, _f32p, i64, i64, C.c_int, C.c_uint, _f32p]
+        R.ref_head_parity.argtypes = [_f32p, _f32p, _f32p, i64, i64, C.c_double, C.c_int, i64,
+                                      C.c_void_p, C.c_void_p, C.c_int, C.c_uint, _i32p, C.c_void_p,
+                                      C.c_void_p, C.c_void_p]
         R._path = path
         _ref = R
     return _ref
@@ -153,6 +158,16 @@ def gen(kind: str, seed: int, heads: int, L: int, d: int, std: float = 1.0, clus
     if bf16:
         out = [round_bf16(a) for a in out]
     return out
+
+
+def gen_gaussian_head(seed: int, heads: int, L: int, d: int, head: int, rows: int | None = None,
+                      std: float = 1.0, bf16: bool = True):
+    """Rows [0, rows) of head `head` of gen_gaussian(seed, heads, L, d, std), without
+    generating the other heads ([rows][d] float32 q, k, v; bf16-rounded by default)."""
+    rows = L if rows is None else rows
+    out = [np.empty((rows, d), np.float32) for _ in range(3)]
+    _check(lib().oracle_gen_gaussian_head(seed, heads, L, d, std, head, rows, *out), "gen_gaussian_head")
+    return [round_bf16(x) for x in out] if bf16 else out
 
 
 def sparsity_to_k(r: float, n: int):
@@ -390,6 +405,28 @@ def ref_theorem1(q, k, v, ksel: int, B: int = 64):
     return dict(plan=plan, actual_err=rows[0], bound=rows[1], rho=rows[2], alpha_sum=rows[3],
                 jensen_rhs=rows[4], c_q=scal[0], m_max=scal[1], violations=int(scal[2]),
                 jensen_violations=int(scal[3]), max_slack_ratio=scal[4], jensen_check=int(scal[5]))
+
+
+def ref_head_parity(q, k, v, r: float, blocks=(), force_diagonal=False, accum_f64=True, threads=0,
+                    B: int = 64, sub_plan=None):
+    """One head through the reference's own pipeline (engine.hpp:437-461): the full
+    plan [N][k], the fp64 q_bar / k_bar [N][d], and pisa_streaming's output rows
+    of the query blocks `blocks` ([len(blocks)*B][d] float32; None without
+    blocks). `sub_plan` ([len(blocks)][k]) replaces the reference's plan rows of
+    those blocks in the streaming step (e.g. the GPU's plan). L % 64 == 0."""
+    L, d = q.shape
+    N = L // B
+    kk, _ = sparsity_to_k(r, N)
+    sel = np.empty((N, kk), np.int32)
+    qb = np.empty((N, d)); kb = np.empty((N, d))
+    blk = np.ascontiguousarray(np.asarray(blocks, np.int64))
+    sp = None if sub_plan is None else np.ascontiguousarray(sub_plan, np.int32)
+    out = np.empty((max(1, len(blk)) * B, d), np.float32)
+    _check(ref().ref_head_parity(np.ascontiguousarray(q, np.float32), np.ascontiguousarray(k, np.float32),
+                                 np.ascontiguousarray(v, np.float32), L, d, r, int(force_diagonal), len(blk),
+                                 blk.ctypes.data, None if sp is None else sp.ctypes.data, int(accum_f64),
+                                 threads, sel, qb.ctypes.data, kb.ctypes.data, out.ctypes.data), "ref_head_parity")
+    return sel, qb, kb, (out[:len(blk) * B] if len(blk) else None)
 
 
 def ref_multihead(q, k, v, r=0.875, variant="hybrid", force_diagonal=False, B=64, group=8,

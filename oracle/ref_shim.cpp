@@ -369,6 +369,62 @@ int ref_bench_sample(const float* q, const float* k, const float* v, int64_t L, 
     });
 }
 
+// Parity of one head against the reference's own pipeline (engine.hpp:437-461):
+// compute_block_stats + compute_global_stats(norms off) + query_block_means +
+// select_topk_plain over the whole head -> the full plan (selected [N][k]) and
+// the fp64 prepare products (q_bar / k_bar [N][d], for near-tie scoring); then
+// pisa_streaming (accum F32 or F64) over `nsample` query blocks `blocks`
+// (gathered into one query view with the matching sub-plan: query blocks are
+// independent, engine.hpp:272) -> out [nsample*B][d] float.
+// sub_plan (optional, [nsample][k]) replaces the reference's own plan rows of
+// the sampled blocks, e.g. with the GPU's plan, so that the attention step is
+// compared on identical selections (isolates attention error from
+// near-tie selection swaps); SelectionPlan::validate still runs on it.
+int ref_head_parity(const float* q, const float* k, const float* v, int64_t L, int64_t d, double r,
+                    int force_diagonal, int64_t nsample, const int64_t* blocks, const int32_t* sub_plan,
+                    int accum_f64, unsigned threads, int32_t* selected, double* qbar, double* kbar,
+                    float* out) {
+    return guarded([&] {
+        const std::size_t B = 64;
+        const auto cfg = make_cfg(int64_t(B), 8, 0.0, accum_f64, 0, threads);
+        pisa::ConstView<float> qv(q, std::size_t(L), std::size_t(d));
+        pisa::ConstView<float> kv(k, std::size_t(L), std::size_t(d));
+        pisa::ConstView<float> vv(v, std::size_t(L), std::size_t(d));
+        cfg.check(std::size_t(L));
+        auto st = pisa::compute_block_stats(kv, vv, B);
+        pisa::compute_global_stats(st, pisa::SpectralMethod::Exact, false);
+        const auto qb = pisa::query_block_means(qv, B);
+        const auto res = pisa::sparsity_to_k(r, st.num_blocks);
+        const auto plan = pisa::select_topk_plain(qb, st.k_bar, res.k, cfg.resolved_scale(std::size_t(d)),
+                                                  force_diagonal != 0);
+        const std::size_t n = st.num_blocks, kk = res.k;
+        for (std::size_t i = 0; i < n; ++i)
+            for (std::size_t p = 0; p < kk; ++p) selected[i * kk + p] = int32_t(plan.selected[i][p]);
+        if (qbar) std::memcpy(qbar, qb.data.data(), qb.data.size() * sizeof(double));
+        if (kbar) std::memcpy(kbar, st.k_bar.data.data(), st.k_bar.data.size() * sizeof(double));
+        if (nsample <= 0) return;
+        std::vector<float> qs(std::size_t(nsample) * B * std::size_t(d));
+        pisa::SelectionPlan sub;
+        sub.num_key_blocks = n;
+        sub.k = kk;
+        for (int64_t s = 0; s < nsample; ++s) {
+            const std::size_t i = std::size_t(blocks[s]);
+            std::memcpy(qs.data() + std::size_t(s) * B * std::size_t(d), q + i * B * std::size_t(d),
+                        B * std::size_t(d) * sizeof(float));
+            if (sub_plan) {
+                std::vector<std::size_t> row(kk);
+                for (std::size_t p = 0; p < kk; ++p) row[p] = std::size_t(sub_plan[std::size_t(s) * kk + p]);
+                sub.selected.push_back(std::move(row));
+            } else {
+                sub.selected.push_back(plan.selected[i]);
+            }
+        }
+        pisa::ConstView<float> qsv(qs.data(), std::size_t(nsample) * B, std::size_t(d));
+        const auto o = pisa::pisa_streaming(qsv, kv, vv, sub, st, cfg);
+        std::memcpy(out, o.output.data.data(), o.output.data.size() * sizeof(float));
+    });
+}
+
 int ref_dense_online(const float* q, const float* k, const float* v, int64_t L, int64_t d,
                      int accum_f64, unsigned threads, float* out) {
     return guarded([&] {

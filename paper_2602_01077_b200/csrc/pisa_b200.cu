@@ -246,10 +246,12 @@ pisa_status resolve(pisa_ctx* ctx, const pisa_attn_desc* d, Plan* p) {
     p->Npad = (N + 127) / 128 * 128;  // K3 reads 128-centroid tiles
     p->W = (N + 31) / 32;
     p->k = k;
-    // K1: up to kStatsG key blocks per CTA, fewer when that would leave SMs idle
-    // (small shapes: FLUX's N = 72 x 24 heads would be 72 CTAs at 32 per CTA)
-    const int64_t sms = ctx ? ctx->sms : 148;
-    p->statsG = std::max<int64_t>(4, std::min<int64_t>(kStatsG, (N * p->BH + 2 * sms - 1) / (2 * sms)));
+    // K1: up to kStatsG key blocks per CTA, fewer for short heads (FLUX's N = 72
+    // at 32 per CTA would be 3 CTAs per head). A function of N only: a head's
+    // H_bar partial sums -- and with them its output bits -- do not depend on
+    // how many other heads share the launch, so head-sharded ranks reproduce
+    // the single-GPU result exactly.
+    p->statsG = std::max<int64_t>(4, std::min<int64_t>(kStatsG, (N + 23) / 24));
     p->nchunk1 = (N + p->statsG - 1) / p->statsG;
     p->nchunk2 = (N + 63) / 64;
     p->scale = d->scale > 0.0 ? d->scale : 1.0 / std::sqrt(double(D));  // attention.hpp:34-37

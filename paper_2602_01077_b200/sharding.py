@@ -80,14 +80,59 @@ def unit_qblock_pieces(B: int, H: int, N: int, world: int, rank: int) -> List[Pi
     return pieces
 
 
-def fwd_pieces(q, k, v, out, pieces: List[Piece], **kw):
+def fwd_pieces(q, k, v, out, pieces: List[Piece], fwd=None, **kw):
     """Runs this rank's pieces on [B][H][L][d] device tensors (views per piece,
-    no copies); rows of `out` outside the pieces are not written."""
-    from . import pisa as P
+    no copies); rows of `out` outside the pieces are not written. ``fwd`` is
+    the forward with P.fwd's signature (default P.fwd)."""
+    if fwd is None:
+        from . import pisa as P
+        fwd = P.fwd
 
     for pc in pieces:
         sl = (slice(pc.b, pc.b + 1), slice(pc.h0, pc.h1))
         N = -(-q.shape[2] // 64)
         rng = None if (pc.qb0, pc.qb1) == (0, N) else (pc.qb0, pc.qb1)
-        P.fwd(q[sl], k[sl], v[sl], out[sl], q_blocks=rng, **kw)
+        fwd(q[sl], k[sl], v[sl], out[sl], q_blocks=rng, **kw)
     return out
+
+
+def _piece_rows(pc: Piece, L: int):
+    return pc.qb0 * 64, min(L, pc.qb1 * 64)
+
+
+def gather_pieces(out: torch.Tensor, B: int, H: int, N: int, world: int, rank: int, group=None) -> torch.Tensor:
+    """The optional final gather for (unit x query-block) sharding: every rank
+    holds a full-size [B][H][L][d] ``out`` in which only its pieces are written;
+    the rows of all ranks' pieces are exchanged with one all_gather (packed
+    per rank in piece order, padded to the largest share) and the assembled
+    output is returned on every rank. The piece lists are recomputed locally
+    (unit_qblock_pieces is deterministic), so no metadata travels."""
+    import torch.distributed as dist
+
+    if world == 1:
+        return out
+    L, d = out.shape[2], out.shape[3]
+
+    def pack_len(r):
+        return sum((pc.h1 - pc.h0) * (lambda a: a[1] - a[0])(_piece_rows(pc, L))
+                   for pc in unit_qblock_pieces(B, H, N, world, r))
+
+    mx = max(pack_len(r) for r in range(world))
+    buf = torch.zeros((mx, d), dtype=out.dtype, device=out.device)
+    o = 0
+    for pc in unit_qblock_pieces(B, H, N, world, rank):
+        r0, r1 = _piece_rows(pc, L)
+        rows = out[pc.b, pc.h0:pc.h1, r0:r1].reshape(-1, d)
+        buf[o:o + rows.shape[0]] = rows
+        o += rows.shape[0]
+    bufs = [torch.empty_like(buf) for _ in range(world)]
+    dist.all_gather(bufs, buf, group=group)
+    full = torch.empty_like(out)
+    for r in range(world):
+        o = 0
+        for pc in unit_qblock_pieces(B, H, N, world, r):
+            r0, r1 = _piece_rows(pc, L)
+            n = (pc.h1 - pc.h0) * (r1 - r0)
+            full[pc.b, pc.h0:pc.h1, r0:r1] = bufs[r][o:o + n].reshape(pc.h1 - pc.h0, r1 - r0, d)
+            o += n
+    return full

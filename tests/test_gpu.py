@@ -434,19 +434,22 @@ def test_literal_phase3_only_on_the_streaming_path(P, oracle_mod):
     st = P.compute_prepare(q, k, v)
     sel = P.select_topk_plain(st.q_bar, st.k_bar, 4, 128 ** -0.5)
     lit_cfg = P.AttentionConfig(literal_phase3=True)
-    a, _ = P.pisa_reference(q, k, v, sel, st, P.PisaVariant.Hybrid, lit_cfg)
-    b, _ = P.pisa_reference(q, k, v, sel, st, P.PisaVariant.Hybrid)
-    c, _ = P.pisa_streaming(q, k, v, sel, st, lit_cfg)
+    f32 = dict(out_dtype=torch.float32)
+    a, _ = P.pisa_reference(q, k, v, sel, st, P.PisaVariant.Hybrid, lit_cfg, **f32)
+    b, _ = P.pisa_reference(q, k, v, sel, st, P.PisaVariant.Hybrid, **f32)
+    c, _ = P.pisa_streaming(q, k, v, sel, st, lit_cfg, **f32)
     assert torch.equal(a, b) and not torch.equal(b, c)
-    g0, _ = P.pisa_reference(q, k, v, sel, st, P.PisaVariant.GlobalCentroid, lit_cfg)
-    g3, _ = P.pisa_reference(q, k, v, sel, st, P.PisaVariant.GlobalCentroid)
-    g1 = P.fwd(q[None], k[None], v[None], topk=4, variant=P.PisaVariant.GlobalCentroid, literal_phase3=True)
-    g2 = P.fwd(q[None], k[None], v[None], topk=4, variant=P.PisaVariant.GlobalCentroid)
+    g0, _ = P.pisa_reference(q, k, v, sel, st, P.PisaVariant.GlobalCentroid, lit_cfg, **f32)
+    g3, _ = P.pisa_reference(q, k, v, sel, st, P.PisaVariant.GlobalCentroid, **f32)
+    g1 = P.fwd(q[None], k[None], v[None], topk=4, variant=P.PisaVariant.GlobalCentroid, literal_phase3=True,
+               **f32)
+    g2 = P.fwd(q[None], k[None], v[None], topk=4, variant=P.PisaVariant.GlobalCentroid, **f32)
     assert torch.equal(g1, g2) and torch.equal(g0, g3)
     bundle = P.TensorBundle(q, k, v)
-    r_ref = P.pisa_multihead(bundle, 0.75, P.RouterOptions(), P.PisaVariant.Hybrid, lit_cfg, False)
-    r_dflt = P.pisa_multihead(bundle, 0.75, P.RouterOptions(), P.PisaVariant.Hybrid, P.AttentionConfig(), True)
-    r_lit = P.pisa_multihead(bundle, 0.75, P.RouterOptions(), P.PisaVariant.Hybrid, lit_cfg, True)
+    r_ref = P.pisa_multihead(bundle, 0.75, P.RouterOptions(), P.PisaVariant.Hybrid, lit_cfg, False, **f32)
+    r_dflt = P.pisa_multihead(bundle, 0.75, P.RouterOptions(), P.PisaVariant.Hybrid, P.AttentionConfig(), True,
+                              **f32)
+    r_lit = P.pisa_multihead(bundle, 0.75, P.RouterOptions(), P.PisaVariant.Hybrid, lit_cfg, True, **f32)
     assert torch.equal(r_ref.heads[0].output, r_dflt.heads[0].output)
     assert not torch.equal(r_lit.heads[0].output, r_dflt.heads[0].output)
 
@@ -674,6 +677,30 @@ def test_qrange_pieces_reassemble(P, oracle_mod):
     for bad in ((3, 3), (-1, 4), (0, 17), (12, 5)):
         with pytest.raises(P.InvalidDimension):
             P.fwd(q, k, v, part, q_blocks=bad, **kw)
+
+
+def test_torchrun_world2_same_gpu(tmp_path):
+    """The multi-rank path end to end under torchrun (world 2, both ranks on
+    GPU 0, gloo): head sharding + all_gather reproduces the single-rank output
+    bit for bit (a head's result does not depend on the other heads in the
+    launch); (head x query-block) pieces + the pieces gather agree to rounding."""
+    import json
+    import socket
+    import subprocess
+    import sys
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = tmp_path / "dist.json"
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nproc-per-node", "2",
+                        "--master-addr", "127.0.0.1", "--master-port", str(port),
+                        os.path.join(root, "tests", "dist_fwd_worker.py"), str(out)],
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-4000:]
+    res = json.loads(out.read_text())
+    assert res["world"] == 2 and res["heads_bit_equal"], res
+    assert res["pieces_max_abs_diff"] <= 4e-3, res
 
 
 def test_pairing_modes_agree_and_fewer_tiles(P, oracle_mod):

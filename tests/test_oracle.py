@@ -275,3 +275,36 @@ def test_oracle_rejects_block_first(oracle_mod):
     with pytest.raises(O.OracleError) as e:
         O.pisa_attention(q[0], k[0], v[0], np.array([[0], [1]], np.int32), st, 0.5, "block_first")
     assert e.value.status == 8
+
+
+# ------------------------------------------- parity harness (oracle/parity.py) --
+def test_ref_head_parity_is_the_reference_pipeline(oracle_mod, ref_available):
+    """ref_head_parity = the reference's own per-head pipeline: its plan equals
+    pisa_multihead's, and pisa_streaming on gathered query blocks equals the
+    same rows of the full-head output (query blocks are independent)."""
+    if not ref_available:
+        pytest.skip("oracle/_ref not built (reference sources absent)")
+    from oracle import parity
+    O = oracle_mod
+    q, k, v = O.gen("clustered", 3, 1, 1024, 64)
+    blocks = parity.sample_blocks(16, 8, run=2)
+    sel, qb, kb, out = O.ref_head_parity(q[0], k[0], v[0], 0.75, blocks=blocks)
+    # the same with the plan rows given explicitly: identical
+    out2 = O.ref_head_parity(q[0], k[0], v[0], 0.75, blocks=blocks, sub_plan=sel[blocks])[3]
+    assert np.array_equal(out, out2)
+    full = O.ref_multihead(q, k, v, r=0.75, accum_f64=True, streaming=True)
+    assert np.array_equal(sel, full["selected"][0])
+    rows = np.concatenate([np.arange(i * 64, (i + 1) * 64) for i in blocks])
+    assert np.abs(out - full["out"][0][rows]).max() <= 1e-6
+    np.testing.assert_allclose(kb, O.ref_block_stats(q[0], k[0], v[0])[0], rtol=0, atol=0)
+    # the classifier: identical plans -> nothing; a swap across the k-th score -> non-tie
+    assert parity.classify_rows(sel, sel, qb, kb, 4, 0.125) == (0, 0, 0, [])
+    bad = sel.copy()
+    N = sel.shape[0]
+    s = 0.125 * (kb @ qb[3])
+    worst = np.argsort(-s)[N - 1]  # the lowest-scoring block replaces a selected one
+    bad[3, 0] = worst
+    nb, near, pairs, non = parity.classify_rows(bad, sel, qb, kb, 4, 0.125)
+    assert nb == 1 and near == 0 and non == [3]
+    assert list(parity.runs_of(np.array([0, 1, 2, 7, 8, 15]))) == [(0, 3), (7, 9), (15, 16)]
+    assert parity.sample_blocks(1182, 64)[-1] == 1181 and len(parity.sample_blocks(1182, 64)) == 64
