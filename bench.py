@@ -193,14 +193,14 @@ def plan_parity(P, q, k, v, plan, density, d):
     import oracle as O
     from oracle import parity
 
-    H, N, k = plan.shape
+    H, N, ksel = plan.shape
     scale = d ** -0.5
 
     def head(h):
         qf, kf, vf = (x[0, h].float().numpy() for x in (q, k, v))
         st = O.block_stats(kf, vf)
         qb = O.query_means(qf)
-        return parity.classify_rows(plan[h], O.select_plain(qb, st[0], k, scale), qb, st[0], k, scale)
+        return parity.classify_rows(plan[h], O.select_plain(qb, st[0], ksel, scale), qb, st[0], ksel, scale)
 
     t0 = time.perf_counter()
     with cf.ThreadPoolExecutor(min(H, os.cpu_count() or 1)) as ex:

@@ -13,6 +13,8 @@
 // so the tensor core sees exact bf16 inputs and accumulates in fp32; only the
 // rank-one correction runs on CUDA cores. HBM-bound: every input byte is read
 // once. Ragged last block: TMA zero-fills rows >= L, means divide by n_j.
+#include <algorithm>
+
 #include "kernels.h"
 #include "sm100.cuh"
 
@@ -22,6 +24,7 @@ using namespace pisa_sm100;
 namespace {
 
 constexpr int kStages = 3;
+constexpr int kCtasPerSm = 1;
 constexpr int kThreads = 192;
 
 template <int D>
@@ -35,7 +38,7 @@ struct StatsCfg {
 };
 
 template <int D>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kThreads, kCtasPerSm)
     block_stats_kernel(const __grid_constant__ CUtensorMap tmQ,
                        const __grid_constant__ CUtensorMap tmK,
                        const __grid_constant__ CUtensorMap tmV, StatsArgs a) {
@@ -245,6 +248,279 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (warp == 1) tmem_dealloc(tmem, 128);
 }
 
+// Persistent form of the same computation (the default): one CTA per SM walks
+// the flattened (b*h, chunk) list with stride gridDim.x, so the TMA ring never
+// drains between chunks. The TMEM accumulator and the chunk's k_bar / v_hat
+// are double-buffered, and a dedicated epilogue warpgroup turns chunk i into
+// its H partial while the producer, the MMA warp and the column warps already
+// stream chunk i + 1. Every chunk is computed exactly as in the one-chunk-per-
+// CTA kernel above (same block order, same reductions), so the outputs are
+// bit-identical; only which CTA computes a chunk changes.
+constexpr int kPThreads = 320;  // warp 0 TMA, 1 MMA, 2-5 columns, 6-9 epilogue
+
+template <int D>
+struct PStatsCfg {
+    static constexpr int kTile = 64 * D * 2;
+    static constexpr int kStage = 3 * kTile;
+    static constexpr int kRing = 3 * kStage;        // 3 stages
+    static constexpr int kKbS = kStatsG * D * 4;    // one chunk's k_bar (fp32)
+    static constexpr int kRed = 2 * 4 * 3 * D * 4;
+    static constexpr int kSmem = 1024 + kRing + 4 * kKbS + kRed + 512;
+};
+
+template <int D>
+__global__ void __launch_bounds__(kPThreads, 1)
+    block_stats_persistent_kernel(const __grid_constant__ CUtensorMap tmQ,
+                                  const __grid_constant__ CUtensorMap tmK,
+                                  const __grid_constant__ CUtensorMap tmV, StatsArgs a, int BH) {
+    using Cfg = PStatsCfg<D>;
+    constexpr int kS = 3;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                               ~uintptr_t(1023));
+    uint8_t* ring = smem;
+    float* kb_s = reinterpret_cast<float*>(smem + Cfg::kRing);  // [2][G][D]
+    float* vh_s = kb_s + 2 * kStatsG * D;                        // [2][G][D]
+    float* red = vh_s + 2 * kStatsG * D;                         // [2][4][3][D]
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Cfg::kRing + 4 * Cfg::kKbS + Cfg::kRed);
+    uint64_t* full = bars;             // [3] stage loaded
+    uint64_t* empty = bars + 3;        // [3] stage consumed (MMA + 4 column warps)
+    uint64_t* acc_full = bars + 6;     // [2] chunk's K^T V complete (MMA commit)
+    uint64_t* stats_full = bars + 8;   // [2] chunk's k_bar / v_hat in smem (4 column warps)
+    uint64_t* acc_empty = bars + 10;   // [2] epilogue done with the buffer (4 epilogue warps)
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 12);
+
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    const int total = BH * a.nchunk;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kS; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1 + 4);
+        }
+        for (int s = 0; s < 2; ++s) {
+            mbar_init(&acc_full[s], 1);
+            mbar_init(&stats_full[s], 4);
+            mbar_init(&acc_empty[s], 4);
+        }
+        fence_mbar_init();
+        tma_prefetch(&tmQ);
+        tma_prefetch(&tmK);
+        tma_prefetch(&tmV);
+    }
+    if (warp == 1) {
+        tmem_alloc(tmem_slot, 256);
+        tmem_relinquish();
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    // blocks of chunk t: (bh, j0, nb)
+    auto chunk_of = [&](int t, int& bh, int& chunk, int& j0, int& nb) {
+        bh = t / a.nchunk;
+        chunk = t % a.nchunk;
+        j0 = chunk * a.G;
+        nb = min(a.G, a.N - j0);
+    };
+
+    if (warp == 0) {
+        int it = 0;  // ring position over all blocks of all chunks
+        for (int t = blockIdx.x; t < total; t += gridDim.x) {
+            int bh, chunk, j0, nb;
+            chunk_of(t, bh, chunk, j0, nb);
+            const int b = bh / a.H, h = bh % a.H;
+            for (int jl = 0; jl < nb; ++jl, ++it) {
+                const int s = it % kS;
+                mbar_wait(&empty[s], ((it / kS) & 1) ^ 1);
+                uint8_t* st = ring + s * Cfg::kStage;
+                const int row = (j0 + jl) * 64;
+                if (elect_one()) {
+                    mbar_expect_tx(&full[s], Cfg::kStage);
+#pragma unroll
+                    for (int half = 0; half < D / 64; ++half) {
+                        tma_load_4d(st + half * 8192, &tmK, &full[s], half * 64, row, h, b);
+                        tma_load_4d(st + Cfg::kTile + half * 8192, &tmV, &full[s], half * 64, row, h, b);
+                        tma_load_4d(st + 2 * Cfg::kTile + half * 8192, &tmQ, &full[s], half * 64, row, h, b);
+                    }
+                }
+                __syncwarp();
+            }
+        }
+    } else if (warp == 1) {
+        constexpr uint32_t idesc = idesc_bf16(128, D, 1, 1);
+        int it = 0, ci = 0;
+        for (int t = blockIdx.x; t < total; t += gridDim.x, ++ci) {
+            int bh, chunk, j0, nb;
+            chunk_of(t, bh, chunk, j0, nb);
+            const int buf = ci & 1;
+            if (ci >= 2) mbar_wait(&acc_empty[buf], ((ci >> 1) - 1) & 1);
+            tc_fence_after();
+            const uint32_t acc = tmem + uint32_t(buf) * 128;
+            for (int jl = 0; jl < nb; ++jl, ++it) {
+                const int s = it % kS;
+                mbar_wait(&full[s], (it / kS) & 1);
+                tc_fence_after();
+                const uint32_t kbase = smem_u32(ring + s * Cfg::kStage);
+                const uint32_t vbase = kbase + Cfg::kTile;
+                if (elect_one()) {
+#pragma unroll
+                    for (int ks = 0; ks < 4; ++ks) {
+                        const uint64_t ad = sdesc_sw128(kbase + ks * 2048, 8192, 1024);
+                        const uint64_t bd = sdesc_sw128(vbase + ks * 2048, 8192, 1024);
+                        mma_ss(acc, ad, bd, idesc, (jl | ks) != 0);
+                    }
+                    mma_commit(&empty[s]);
+                    if (jl == nb - 1) mma_commit(&acc_full[buf]);
+                }
+                __syncwarp();
+            }
+        }
+    } else if (warp < 6) {
+        // Column warps (as in block_stats_kernel): per-block column sums ->
+        // k_bar / v_hat / q_bar, and the chunk's k_bar / v_hat into kb_s[buf]
+        const int q = warp & 3;
+        const int c = q * 32 + lane;
+        const bool has_col = c < D;
+        const int tt = threadIdx.x - 64;
+        constexpr int kCh = D / 8;
+        constexpr int kRows = 64 * kCh / 128;
+        const int cg = tt % kCh, rg = tt / kCh;
+        int it = 0, ci = 0;
+        for (int t = blockIdx.x; t < total; t += gridDim.x, ++ci) {
+            int bh, chunk, j0, nb;
+            chunk_of(t, bh, chunk, j0, nb);
+            const int buf = ci & 1;
+            float* kbs = kb_s + buf * kStatsG * D;
+            float* vhs = vh_s + buf * kStatsG * D;
+            // kb_s[buf] is free once the epilogue of chunk ci - 2 is done
+            if (ci >= 2) mbar_wait(&acc_empty[buf], ((ci >> 1) - 1) & 1);
+            for (int jl = 0; jl < nb; ++jl, ++it) {
+                const int s = it % kS;
+                mbar_wait(&full[s], (it / kS) & 1);
+                const int j = j0 + jl;
+                const int nrow = min(64, a.L - j * 64);
+                const uint8_t* st = ring + s * Cfg::kStage;
+                float acc[3][8];
+#pragma unroll
+                for (int m = 0; m < 3; ++m)
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) acc[m][e] = 0.f;
+#pragma unroll
+                for (int rr = 0; rr < kRows; ++rr) {
+                    const int r = rg * kRows + rr;
+                    const uint32_t off = uint32_t((cg >> 3) * 8192 + r * 128 + (((cg & 7) ^ (r & 7)) << 4));
+#pragma unroll
+                    for (int m = 0; m < 3; ++m) {
+                        const uint4 w = *reinterpret_cast<const uint4*>(st + m * Cfg::kTile + off);
+                        const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&w);
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) {
+                            const float2 f = __bfloat1622float2(b2[e]);
+                            acc[m][2 * e] += f.x;
+                            acc[m][2 * e + 1] += f.y;
+                        }
+                    }
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&empty[s]);
+#pragma unroll
+                for (int o = kCh; o < 32; o <<= 1)
+#pragma unroll
+                    for (int m = 0; m < 3; ++m)
+#pragma unroll
+                        for (int e = 0; e < 8; ++e) acc[m][e] += __shfl_xor_sync(0xffffffffu, acc[m][e], o);
+                float* rb = red + (it & 1) * (4 * 3 * D) + q * (3 * D);
+                if (lane < kCh) {
+#pragma unroll
+                    for (int m = 0; m < 3; ++m) {
+                        *reinterpret_cast<float4*>(rb + m * D + cg * 8) =
+                            make_float4(acc[m][0], acc[m][1], acc[m][2], acc[m][3]);
+                        *reinterpret_cast<float4*>(rb + m * D + cg * 8 + 4) =
+                            make_float4(acc[m][4], acc[m][5], acc[m][6], acc[m][7]);
+                    }
+                }
+                asm volatile("bar.sync 2, 128;" ::: "memory");
+                if (has_col) {
+                    const float* rb0 = red + (it & 1) * (4 * 3 * D);
+                    float sk = 0.f, sv = 0.f, sq = 0.f;
+#pragma unroll
+                    for (int w = 0; w < 4; ++w) {
+                        sk += rb0[w * 3 * D + c];
+                        sv += rb0[w * 3 * D + D + c];
+                        sq += rb0[w * 3 * D + 2 * D + c];
+                    }
+                    const float inv = 1.0f / float(nrow);
+                    const float kbv = sk * inv;
+                    const size_t o = (size_t(bh) * a.N + j) * D + c;
+                    a.kbar[o] = kbv;
+                    a.vhat[o] = sv;
+                    a.qbar[o] = sq * inv;
+                    const size_t ob = (size_t(bh) * a.Npad + j) * D + c;
+                    a.kbar_bf[ob] = __float2bfloat16_rn(kbv);
+                    a.vhat_bf[ob] = __float2bfloat16_rn(sv);
+                    kbs[jl * D + c] = kbv;
+                    vhs[jl * D + c] = sv;
+                }
+            }
+            if (has_col && j0 + nb == a.N) {
+                for (int j = a.N; j < a.Npad; ++j) {
+                    const size_t ob = (size_t(bh) * a.Npad + j) * D + c;
+                    a.kbar_bf[ob] = __float2bfloat16_rn(0.f);
+                    a.vhat_bf[ob] = __float2bfloat16_rn(0.f);
+                }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&stats_full[buf]);  // (release: mbarrier arrive orders the smem stores)
+        }
+    } else {
+        // Epilogue warps 6..9: H partial of chunk ci from TMEM buffer ci & 1,
+        // lanes (warp % 4) * 32 .. +31 (= rows a of the D x D partial)
+        const int q = warp & 3;  // TMEM lane quadrant this warp may access
+        const int arow = q * 32 + lane;
+        int ci = 0;
+        for (int t = blockIdx.x; t < total; t += gridDim.x, ++ci) {
+            int bh, chunk, j0, nb;
+            chunk_of(t, bh, chunk, j0, nb);
+            const int buf = ci & 1;
+            mbar_wait(&acc_full[buf], (ci >> 1) & 1);
+            mbar_wait(&stats_full[buf], (ci >> 1) & 1);
+            tc_fence_after();
+            const float* kbs = kb_s + buf * kStatsG * D;
+            const float* vhs = vh_s + buf * kStatsG * D;
+            if (q < D / 32) {
+                float* dst = a.hpart + ((size_t(bh) * a.nchunk + chunk) * D + arow) * D;
+#pragma unroll 1
+                for (int cc = 0; cc < D; cc += 32) {
+                    uint32_t r[32];
+                    tmem_ld32(tmem + uint32_t(buf) * 128 + (uint32_t(q * 32) << 16) + cc, r);
+                    tmem_ld_wait(r);
+                    float acc[32];
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) acc[i] = __uint_as_float(r[i]);
+                    for (int jl = 0; jl < nb; ++jl) {
+                        const float ka = kbs[jl * D + arow];
+#pragma unroll
+                        for (int i = 0; i < 32; ++i) acc[i] = fmaf(-ka, vhs[jl * D + cc + i], acc[i]);
+                    }
+#pragma unroll
+                    for (int i = 0; i < 32; i += 4)
+                        *reinterpret_cast<float4*>(dst + cc + i) =
+                            make_float4(acc[i], acc[i + 1], acc[i + 2], acc[i + 3]);
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&acc_empty[buf]);
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) tmem_dealloc(tmem, 256);
+}
+
 template <int D>
 __global__ void hbar_reduce_kernel(const float* __restrict__ hpart, int nchunk, int N,
                                    const float* __restrict__ kbar, float* __restrict__ hbar,
@@ -297,9 +573,29 @@ __global__ void stats_to_bf16_kernel(const float* __restrict__ kbar,
 
 }  // namespace
 
+#ifndef PISA_K1_PERSISTENT
+#define PISA_K1_PERSISTENT 1
+#endif
+
 cudaError_t launch_block_stats(int D, const CUtensorMap& tmQ, const CUtensorMap& tmK,
                                const CUtensorMap& tmV, const StatsArgs& a, int BH,
                                cudaStream_t s) {
+    if (PISA_K1_PERSISTENT) {
+        int dev = 0, sms = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        const int grid = std::min(sms, BH * a.nchunk);
+        if (D == 128) {
+            auto k = block_stats_persistent_kernel<128>;
+            cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, PStatsCfg<128>::kSmem);
+            k<<<grid, kPThreads, PStatsCfg<128>::kSmem, s>>>(tmQ, tmK, tmV, a, BH);
+        } else {
+            auto k = block_stats_persistent_kernel<64>;
+            cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, PStatsCfg<64>::kSmem);
+            k<<<grid, kPThreads, PStatsCfg<64>::kSmem, s>>>(tmQ, tmK, tmV, a, BH);
+        }
+        return cudaGetLastError();
+    }
     dim3 grid(a.nchunk, BH);
     if (D == 128) {
         auto k = block_stats_kernel<128>;

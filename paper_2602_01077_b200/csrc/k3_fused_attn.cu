@@ -85,6 +85,17 @@ constexpr uint32_t kColO = 0, kColS = 128;  // O | three S/P buffers (P_g over t
 #define PISA_POLY_MASK 0x00
 #endif
 constexpr uint32_t kPolyMask = PISA_POLY_MASK;
+// Sub-tiles that BOTH query blocks of the tile selected (every Phase-1 entry
+// on clustered routing, every Phase-2 centroid chunk) are exponentiated by
+// both warpgroups, which share the four MUFU units: the softmax is then
+// MUFU-bound (2 x 8192 ex2 per 128-key super-tile = 1024 MUFU cycles = the
+// tensor time). There, elements whose index bit is set in kPolyBoth go to
+// the FMA pipe (ex2_poly). Single-use sub-tiles (gaussian routing) stay
+// all-MUFU (kPolyMask): their softmax is issue-bound, not MUFU-bound.
+#ifndef PISA_POLY_BOTH
+#define PISA_POLY_BOTH 0x11
+#endif
+constexpr uint32_t kPolyBoth = PISA_POLY_BOTH;
 // The softmax warps' wait for S: spin (poll) or suspend in hardware between
 // polls. Polling steals issue slots from the other warpgroup's warps on the
 // same sub-partitions while one warpgroup runs ahead.
@@ -142,8 +153,9 @@ __device__ __forceinline__ void mma_wait(uint64_t* bar, uint32_t parity) {
 #ifndef PISA_BALANCED
 #define PISA_BALANCED 0
 #endif
+template <uint32_t Mask>
 __device__ __forceinline__ float ex2_mix(float x, int i) {
-    return ((kPolyMask >> (i & 7)) & 1u) ? ex2_poly(x) : ex2(x);
+    return ((Mask >> (i & 7)) & 1u) ? ex2_poly(x) : ex2(x);
 }
 
 template <int D>
@@ -750,23 +762,35 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (use0) bm_loc = max32(reinterpret_cast<const float*>(r0));
                 if (use1) bm_loc = fmaxf(bm_loc, max32(reinterpret_cast<const float*>(r1)));
                 const float mm = update_max(bm_loc, g);
-                // exponentials only for the selected sub-tiles (warp-uniform)
-                auto expo_store = [&](const uint32_t (&r)[32], uint32_t addr) {
+                // exponentials only for the selected sub-tiles (warp-uniform);
+                // sub-tiles both blocks selected split exp2 across MUFU and FMA
+                auto expo_store = [&](const uint32_t (&r)[32], uint32_t addr, bool both) {
                     uint32_t pk[16];
                     float ps[4] = {0.f, 0.f, 0.f, 0.f};
+                    if (both) {
 #pragma unroll
-                    for (int i = 0; i < 32; i += 2) {
-                        const float p0 = ex2_mix(fmaf(__uint_as_float(r[i]), sl2, -mm), i);
-                        const float p1 = ex2_mix(fmaf(__uint_as_float(r[i + 1]), sl2, -mm), i + 1);
-                        ps[(i >> 1) & 3] += p0 + p1;
-                        pk[i >> 1] = pack_bf16(p0, p1);
+                        for (int i = 0; i < 32; i += 2) {
+                            const float p0 = ex2_mix<kPolyBoth>(fmaf(__uint_as_float(r[i]), sl2, -mm), i);
+                            const float p1 = ex2_mix<kPolyBoth>(fmaf(__uint_as_float(r[i + 1]), sl2, -mm), i + 1);
+                            ps[(i >> 1) & 3] += p0 + p1;
+                            pk[i >> 1] = pack_bf16(p0, p1);
+                        }
+                    } else {
+#pragma unroll
+                        for (int i = 0; i < 32; i += 2) {
+                            const float p0 = ex2_mix<kPolyMask>(fmaf(__uint_as_float(r[i]), sl2, -mm), i);
+                            const float p1 = ex2_mix<kPolyMask>(fmaf(__uint_as_float(r[i + 1]), sl2, -mm), i + 1);
+                            ps[(i >> 1) & 3] += p0 + p1;
+                            pk[i >> 1] = pack_bf16(p0, p1);
+                        }
                     }
                     l += (ps[0] + ps[1]) + (ps[2] + ps[3]);
                     tmem_st16x2_16<16>(addr, pk);  // P (bf16 pairs)
                 };
-                if (use0) expo_store(r0, sc); else tmem_st16x2_16<16>(sc, kZero16);
+                const bool both0 = ((e0 >> 14) & 3u) == 3u, both1 = ((e1 >> 14) & 3u) == 3u;
+                if (use0) expo_store(r0, sc, both0); else tmem_st16x2_16<16>(sc, kZero16);
                 publish_half();
-                if (use1) expo_store(r1, sc + 64); else tmem_st16x2_16<16>(sc + 64, kZero16);
+                if (use1) expo_store(r1, sc + 64, both1); else tmem_st16x2_16<16>(sc + 64, kZero16);
             } else {
                 tmem_st16x2_16<16>(sc, kZero16);
                 publish_half();
@@ -812,8 +836,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                 float q0 = 0.f, q1 = 0.f;
 #pragma unroll
                 for (int i = 0; i < 32; i += 2) {
-                    const float p0 = ex2_mix(fmaf(__uint_as_float(r[i]), sl2, -mm), i);
-                    const float p1 = ex2_mix(fmaf(__uint_as_float(r[i + 1]), sl2, -mm), i + 1);
+                    const float p0 = ex2_mix<kPolyBoth>(fmaf(__uint_as_float(r[i]), sl2, -mm), i);
+                    const float p1 = ex2_mix<kPolyBoth>(fmaf(__uint_as_float(r[i + 1]), sl2, -mm), i + 1);
                     q0 += p0;
                     q1 += p1;
                     if (ragged) plast += (lbo == i ? p0 : 0.f) + (lbo == i + 1 ? p1 : 0.f);

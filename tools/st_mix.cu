@@ -1,0 +1,146 @@
+// Microbenchmark for the "transposed" Phase-1 tile the r01 verdict asked to
+// evaluate (S^T = K_pair Q_i^T with M = 128 keys of two key blocks of ONE
+// query block, N = 64 queries; O^T += V^T P^T), against the current union tile
+// (S = Q_pair [K_a;K_b]^T, N = 128, SS; O += P V, TS with P from TMEM).
+//
+// Per loop iteration, all operands resident in shared memory / TMEM:
+//   mode 0  current tile : 8 x SS M128 N128 (S) + 8 x TS M128 N128 (PV)   = 4 (q-block, k-block) slots
+//   mode 1  transposed   : 8 x SS M128 N64  (S^T) + 8 x SS M128 N64 (PV^T, A = V^T MN-major,
+//                          B = P^T MN-major)                               = 2 slots, all useful
+//   mode 2  transposed + the 16 KB of P^T stores per iteration (8 warps of st.shared.v4,
+//                          the softmax's output) on the same shared-memory port
+//   mode 3  transposed + P^T stores + a 32 KB-per-iteration TMA-like copy stream
+//                          (cp.async.bulk global->shared, the K/V tiles)
+// Prints cycles per iteration and per USEFUL (query block, key block) pair at
+// gaussian routing (union/k = 1.78 -> 4 slots hold 2.25 useful pairs).
+//
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -I../paper_2602_01077_b200/csrc st_mix.cu -o st_mix -lcuda
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdio>
+
+#include "sm100.cuh"
+
+using namespace pisa_sm100;
+
+__global__ void __launch_bounds__(384, 1) st_mix(int mode, int iters, unsigned long long* out, const uint8_t* gsrc) {
+    extern __shared__ uint8_t raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(raw) + 1023) & ~uintptr_t(1023));
+    // [0,64K): operand A/B tiles, [64K,80K): P^T, [96K, 224K): copy ring (4 x 32 KB)
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + 229376 - 4096);
+    uint32_t* slot = reinterpret_cast<uint32_t*>(bar + 16);
+    volatile uint32_t* stop = reinterpret_cast<volatile uint32_t*>(bar + 17);
+    const int warp = threadIdx.x >> 5;
+    for (int i = threadIdx.x; i < 98304 / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(smem)[i] = 0x3c003c00u;
+    if (threadIdx.x == 0) {
+        *stop = 0;
+        for (int i = 0; i < 8; ++i) mbar_init(bar + i, 1);
+        fence_mbar_init();
+    }
+    if (warp == 1) {
+        tmem_alloc(slot, 512);
+        tmem_relinquish();
+    }
+    fence_proxy_async();
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *slot;
+    if (warp >= 4 && mode >= 2) {
+        // P^T producer traffic: each of 8 warps stores 2 KB (16 B per lane x 4) per round
+        uint4* pt = reinterpret_cast<uint4*>(smem + 65536) + (warp - 4) * 128;
+        uint4 v = make_uint4(threadIdx.x, 1, 2, 3);
+        while (*stop == 0) {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) pt[j * 32 + lane_id()] = v;
+            v.x += 1;
+            __syncwarp();
+        }
+    }
+    if (warp == 2 && mode >= 3) {
+        // 32 KB per round through cp.async.bulk (the K / V tile stream)
+        uint8_t* ring = smem + 98304;
+        int i = 0;
+        for (; *stop == 0; ++i) {
+            const int s = i & 3;
+            if (i >= 4) mbar_wait(bar + 4 + s, ((i >> 2) - 1) & 1);
+            if (elect_one()) {
+                mbar_expect_tx(bar + 4 + s, 32768);
+                asm volatile(
+                    "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                        smem_u32(ring + s * 32768)),
+                    "l"(gsrc + size_t((i * 7919) & 4095) * 32768), "r"(32768), "r"(smem_u32(bar + 4 + s))
+                    : "memory");
+            }
+            __syncwarp();
+        }
+        for (int j = i - 4; j < i; ++j)
+            if (j >= 0) mbar_wait(bar + 4 + (j & 3), (j >> 2) & 1);
+    }
+    if (warp == 0) {
+        const uint32_t a = smem_u32(smem), b = smem_u32(smem + 32768), p = smem_u32(smem + 65536);
+        const uint32_t dS = tmem + 256, dO = tmem;
+        const long long t0 = clock64();
+        for (int it = 0; it < iters; ++it) {
+            if (elect_one()) {
+                if (mode == 0) {
+#pragma unroll
+                    for (int ks = 0; ks < 8; ++ks)
+                        mma_ss(dS, sdesc_sw128(a + (ks & 3) * 32, 16, 1024), sdesc_sw128(b + (ks & 3) * 32, 16, 1024),
+                               idesc_bf16(128, 128, 0, 0), 1);
+#pragma unroll
+                    for (int ks = 0; ks < 8; ++ks)
+                        mma_ts(dO, dS + ks * 8, sdesc_sw128(b + (ks & 3) * 2048, 8192, 1024), idesc_bf16(128, 128, 0, 1),
+                               1);
+                } else {
+#pragma unroll
+                    for (int ks = 0; ks < 8; ++ks)  // S^T: A = K (K-major), B = Q (K-major)
+                        mma_ss(dS, sdesc_sw128(a + (ks & 3) * 32, 16, 1024), sdesc_sw128(b + (ks & 3) * 32, 16, 1024),
+                               idesc_bf16(128, 64, 0, 0), 1);
+#pragma unroll
+                    for (int ks = 0; ks < 8; ++ks)  // PV^T: A = V^T (MN-major), B = P^T (MN-major)
+                        mma_ss(dO, sdesc_sw128(a + (ks & 3) * 2048, 8192, 1024),
+                               sdesc_sw128(p + (ks & 3) * 2048, 8192, 1024), idesc_bf16(128, 64, 1, 1), 1);
+                }
+            }
+            __syncwarp();
+        }
+        if (elect_one()) mma_commit(bar);
+        __syncwarp();
+        mbar_wait(bar, 0);
+        const long long t1 = clock64();
+        if (lane_id() == 0) {
+            atomicAdd(out, (unsigned long long)(t1 - t0));
+            *stop = 1;
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) tmem_dealloc(tmem, 512);
+}
+
+int main() {
+    unsigned long long* d;
+    cudaMalloc(&d, 8);
+    uint8_t* g;
+    cudaMalloc(&g, size_t(4096) * 32768);
+    cudaMemset(g, 0, size_t(4096) * 32768);
+    const int smem = 229376 - 1024;
+    cudaFuncSetAttribute(st_mix, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    const char* names[] = {"current union tile (8 SS N128 + 8 TS N128)", "transposed (8 SS N64 S^T + 8 SS N64 PV^T)",
+                           "transposed + 16 KB P^T st.shared / iter", "transposed + P^T stores + 32 KB bulk copies"};
+    const double useful[] = {2.25, 2.0, 2.0, 2.0};  // useful (q-block, k-block) pairs per iteration (gaussian)
+    for (int mode = 0; mode < 4; ++mode) {
+        st_mix<<<148, 384, smem>>>(mode, 16, d, g);
+        cudaMemset(d, 0, 8);
+        const int iters = 4096;
+        st_mix<<<148, 384, smem>>>(mode, iters, d, g);
+        unsigned long long h = 0;
+        cudaMemcpy(&h, d, 8, cudaMemcpyDeviceToHost);
+        const double cyc = double(h) / 148 / iters;
+        printf("%-48s %7.1f cyc/iter  %6.1f cyc per useful pair  (%s)\n", names[mode], cyc, cyc / useful[mode],
+               cudaGetErrorString(cudaGetLastError()));
+    }
+    return 0;
+}
