@@ -23,6 +23,19 @@ using namespace pisa_sm100;
 
 namespace {
 
+// k_bar = hi + mid + lo, each bf16, exact to 2^-27 relative (the fused K2's
+// operand split, identical to split3 in k2_select.cu)
+__device__ __forceinline__ void store_split3(const StatsArgs& a, int bh, int j, int c, int D, float x) {
+    const __nv_bfloat16 h = __float2bfloat16_rn(x);
+    const float y = x - __bfloat162float(h);
+    const __nv_bfloat16 m = __float2bfloat16_rn(y);
+    const __nv_bfloat16 l = __float2bfloat16_rn(y - __bfloat162float(m));
+    const size_t part = size_t(a.BH) * a.N * D, o = (size_t(bh) * a.N + j) * D + c;
+    a.kbar_split[o] = h;
+    a.kbar_split[part + o] = m;
+    a.kbar_split[2 * part + o] = l;
+}
+
 constexpr int kStages = 3;
 constexpr int kCtasPerSm = 1;
 constexpr int kThreads = 192;
@@ -204,6 +217,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
                 const size_t ob = (size_t(bh) * a.Npad + j) * D + c;
                 a.kbar_bf[ob] = __float2bfloat16_rn(kbv);
                 a.vhat_bf[ob] = __float2bfloat16_rn(sv);
+                if (a.kbar_split) store_split3(a, bh, j, c, D, kbv);
                 kb_s[jl * D + c] = kbv;
                 vh_s[jl * D + c] = sv;
             }
@@ -461,6 +475,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
                     const size_t ob = (size_t(bh) * a.Npad + j) * D + c;
                     a.kbar_bf[ob] = __float2bfloat16_rn(kbv);
                     a.vhat_bf[ob] = __float2bfloat16_rn(sv);
+                    if (a.kbar_split) store_split3(a, bh, j, c, D, kbv);
                     kbs[jl * D + c] = kbv;
                     vhs[jl * D + c] = sv;
                 }

@@ -181,22 +181,17 @@ __global__ void __launch_bounds__(kScoreThreads, 1) score_kernel(const float* __
 // it plus the lowest-index ties: topk_ascending semantics (router.hpp:96-108).
 constexpr int kRowsPerCta = 4;
 
-__global__ void __launch_bounds__(kRowsPerCta * 32) topk_kernel(const uint32_t* __restrict__ keys,
-                                                                SelectArgs a) {
-    extern __shared__ uint32_t smk[];
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int bh = blockIdx.y;
-    const int i = blockIdx.x * kRowsPerCta + warp;
-    const int N = a.N;
-    uint32_t* kr = smk + warp * (N + 256);
-    uint32_t* hw = kr + N;
-    if (i >= N) return;
-    const uint32_t* src = keys + (size_t(bh) * N + i) * N;
-    for (int j = lane; j < N; j += 32) kr[j] = src[j];
-    __syncwarp();
-
+// One query block's top-k from its N order keys in shared memory (kr), one
+// warp: radix-select the k-th largest key (8-bit digits from the top, hw = 256
+// shared counters), then a ballot compaction in ascending index order takes
+// every key above it plus the lowest-index ties (topk_ascending,
+// router.hpp:96-108), with optional diagonal forcing (force_block, :111-121)
+// for query block i. Writes the ascending list (sel, may be null) and the
+// bitmask row (mrow).
+__device__ __forceinline__ void select_row(const uint32_t* kr, uint32_t* hw, int N, int kk, int i,
+                                           bool force_diagonal, int32_t* sel, uint32_t* mrow, int lane) {
     uint32_t prefix = 0, pmask = 0;
-    int rem = a.k;  // rank (1-based) of the wanted element among prefix matches
+    int rem = kk;  // rank (1-based) of the wanted element among prefix matches
     for (int shift = 24; shift >= 0; shift -= 8) {
         for (int b = lane; b < 256; b += 32) hw[b] = 0;
         __syncwarp();
@@ -245,7 +240,7 @@ __global__ void __launch_bounds__(kRowsPerCta * 32) topk_kernel(const uint32_t* 
     const uint32_t lt_mask = (1u << lane) - 1u;
     int swap_out = -1;  // force_diagonal: the kept tie to drop (worst kept, highest index)
     bool swap_in = false;
-    if (a.force_diagonal && i < N) {
+    if (force_diagonal && i < N) {
         int ties = 0, last_tie = -1;
         bool diag_sel = false;
         for (int j0 = 0; j0 < N; j0 += 32) {
@@ -267,8 +262,6 @@ __global__ void __launch_bounds__(kRowsPerCta * 32) topk_kernel(const uint32_t* 
         }
     }
     int ties = 0, out = 0;
-    int32_t* sel = a.selected ? a.selected + (size_t(bh) * N + i) * a.k : nullptr;
-    uint32_t* mrow = a.mask + (size_t(bh) * N + i) * a.W;
     for (int j0 = 0; j0 < N; j0 += 32) {
         const int j = j0 + lane;
         const uint32_t key = j < N ? kr[j] : 0u;
@@ -286,6 +279,221 @@ __global__ void __launch_bounds__(kRowsPerCta * 32) topk_kernel(const uint32_t* 
         out += __popc(tb);
         ties += __popc(eqb);
     }
+}
+
+__global__ void __launch_bounds__(kRowsPerCta * 32) topk_kernel(const uint32_t* __restrict__ keys,
+                                                                SelectArgs a) {
+    extern __shared__ uint32_t smk[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int bh = blockIdx.y;
+    const int i = blockIdx.x * kRowsPerCta + warp;
+    const int N = a.N;
+    uint32_t* kr = smk + warp * (N + 256);
+    uint32_t* hw = kr + N;
+    if (i >= N) return;
+    const uint32_t* src = keys + (size_t(bh) * N + i) * N;
+    for (int j = lane; j < N; j += 32) kr[j] = src[j];
+    __syncwarp();
+    select_row(kr, hw, N, a.k, i, a.force_diagonal != 0,
+               a.selected ? a.selected + (size_t(bh) * N + i) * a.k : nullptr,
+               a.mask + (size_t(bh) * N + i) * a.W, lane);
+}
+
+// ------------------------------------------------------------------ K2 fused --
+// One CTA per (128 query blocks i0.., b*h), 256 threads, one CTA per SM:
+//   all warps  : q_bar rows -> exact bf16 hi / mid / lo split -> TMEM (the A
+//                operand of every score MMA, 3 x D/2 columns)
+//   warp 0     : TMA of the k_bar split tiles (128 key blocks x D, 3 parts),
+//                double-buffered
+//   warp 1     : 6 cross products x D/16 TS MMAs per key tile into one of two
+//                TMEM accumulators (the same products, in the same order, as
+//                score_kernel: fp32-accurate, deterministic)
+//   warps 4-7  : order keys of the tile (scale * s [+ rect]) -> this SM's
+//                scratch, column-major ([key][row]: 128-byte warp stores)
+// then all 8 warps select the top-k of the CTA's rows, RB rows at a time
+// staged through the (now free) tile buffers. The scratch is indexed by the
+// SM, so successive CTAs on an SM overwrite the same lines: the keys live in
+// L2 and never make the HBM round trip of the two-kernel path.
+constexpr int kFThreads = 256;
+
+template <int D>
+struct FusedSelCfg {
+    static constexpr int kPart = 128 * D * 2;    // one split part of a 128-key tile
+    static constexpr int kStage = 3 * kPart;     // hi | mid | lo
+    static constexpr int kSmem = 1024 + 2 * kStage + 256;
+    static constexpr int kAcol = D / 2;          // TMEM columns per A part
+};
+
+__device__ __forceinline__ uint32_t smid() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(r));
+    return r;
+}
+
+template <int D>
+__global__ void __launch_bounds__(kFThreads, 1)
+    select_fused_kernel(const __grid_constant__ CUtensorMap tmKs, SelectArgs a, uint32_t* __restrict__ scratch,
+                        int BH) {
+    using Cfg = FusedSelCfg<D>;
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 2 * Cfg::kStage);
+    uint64_t* bfull = bars;       // [2]
+    uint64_t* bempty = bars + 2;  // [2]
+    uint64_t* afull = bars + 4;   // [2]
+    uint64_t* aempty = bars + 6;  // [2]
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 8);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int N = a.N;
+    const int i0 = blockIdx.x * 128;
+    const int bh = blockIdx.y;
+    const int nt = (N + 127) / 128;
+    const uint32_t sm = smid();
+    if (sm >= uint32_t(kScratchSlots)) __trap();  // the scratch has one slot per SM id
+    uint32_t* ks = scratch + size_t(sm) * 128 * N;  // [key][row], this SM's slot
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < 2; ++s) {
+            mbar_init(&bfull[s], 1);
+            mbar_init(&bempty[s], 1);
+            mbar_init(&afull[s], 1);
+            mbar_init(&aempty[s], 4);
+        }
+        fence_mbar_init();
+        tma_prefetch(&tmKs);
+    }
+    if (warp == 1) {
+        tmem_alloc(tslot, 512);
+        tmem_relinquish();
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tslot;
+    // A operand: row i0 + r of q_bar, split exactly into three bf16 parts,
+    // packed pairs in TMEM columns [part * D/2, +D/2) of lane r. Warps w and
+    // w + 4 share lane quadrant w % 4 and take the two column halves.
+    {
+        const int q4 = warp & 3, r = q4 * 32 + lane, i = i0 + r;
+        const int c0 = (warp >> 2) * (D / 2);
+        const float* src = a.qbar + (size_t(bh) * N + i) * D + c0;
+        constexpr int kP = D / 4;  // packed pairs per warp half: 32 (D = 128) or 16 (D = 64)
+        uint32_t h[kP], m[kP], l[kP];
+#pragma unroll
+        for (int e = 0; e < kP; ++e) {
+            const float2 x = i < N ? *reinterpret_cast<const float2*>(src + 2 * e) : make_float2(0.f, 0.f);
+            split3(x.x, x.y, h[e], m[e], l[e]);
+        }
+        const uint32_t lb = tmem + (uint32_t(q4 * 32) << 16) + uint32_t(c0 / 2);
+        if constexpr (D == 128) {
+            tmem_st32(lb, h);
+            tmem_st32(lb + Cfg::kAcol, m);
+            tmem_st32(lb + 2 * Cfg::kAcol, l);
+        } else {
+            tmem_st16(lb, h);
+            tmem_st16(lb + Cfg::kAcol, m);
+            tmem_st16(lb + 2 * Cfg::kAcol, l);
+        }
+        tmem_st_wait();
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    constexpr uint32_t kAcc = 256;  // two accumulators of 128 columns at 256 / 384
+    if (warp == 0) {
+        for (int t = 0; t < nt; ++t) {
+            const int s = t & 1;
+            if (t >= 2) mbar_wait(&bempty[s], ((t >> 1) - 1) & 1);
+            if (elect_one()) {
+                mbar_expect_tx(&bfull[s], Cfg::kStage);
+                uint8_t* st = smem + s * Cfg::kStage;
+#pragma unroll
+                for (int p = 0; p < 3; ++p)
+#pragma unroll
+                    for (int half = 0; half < D / 64; ++half)
+                        tma_load_3d(st + p * Cfg::kPart + half * 16384, &tmKs, &bfull[s], half * 64, t * 128,
+                                    p * BH + bh);
+            }
+            __syncwarp();
+        }
+    } else if (warp == 1) {
+        constexpr uint32_t idesc = idesc_bf16(128, 128, 0, 0);
+        // (lo,hi) (hi,lo) (mid,mid) (mid,hi) (hi,mid) (hi,hi): small terms first
+        constexpr int kA[6] = {2, 0, 1, 1, 0, 0}, kB[6] = {0, 2, 1, 0, 1, 0};
+        for (int t = 0; t < nt; ++t) {
+            const int s = t & 1;
+            mbar_wait(&bfull[s], (t >> 1) & 1);
+            if (t >= 2) mbar_wait(&aempty[s], ((t >> 1) - 1) & 1);
+            tc_fence_after();
+            const uint32_t b = smem_u32(smem + s * Cfg::kStage);
+            const uint32_t acc = tmem + kAcc + uint32_t(s) * 128;
+            if (elect_one()) {
+#pragma unroll
+                for (int p = 0; p < 6; ++p)
+#pragma unroll
+                    for (int kq = 0; kq < D / 16; ++kq)
+                        mma_ts(acc, tmem + uint32_t(kA[p] * Cfg::kAcol + kq * 8),
+                               sdesc_sw128(b + kB[p] * Cfg::kPart + (kq >> 2) * 16384 + (kq & 3) * 32, 16, 1024),
+                               idesc, (p | kq) != 0);
+                mma_commit(&bempty[s]);
+                mma_commit(&afull[s]);
+            }
+            __syncwarp();
+        }
+    } else if (warp >= 4) {
+        const int q4 = warp & 3, r = q4 * 32 + lane;
+        const float* rc = a.rect ? a.rect + size_t(bh) * N : nullptr;
+        for (int t = 0; t < nt; ++t) {
+            const int s = t & 1;
+            mbar_wait(&afull[s], (t >> 1) & 1);
+            tc_fence_after();
+            const uint32_t acc = tmem + kAcc + uint32_t(s) * 128 + (uint32_t(q4 * 32) << 16);
+#pragma unroll 1
+            for (int cc = 0; cc < 128; cc += 32) {
+                uint32_t v[32];
+                tmem_ld32(acc + cc, v);
+                tmem_ld_wait(v);
+                const int j0 = t * 128 + cc;
+#pragma unroll
+                for (int e = 0; e < 32; ++e) {
+                    const int j = j0 + e;
+                    if (j < N) {
+                        float x = a.scale * __uint_as_float(v[e]);
+                        if (rc) x += rc[j];
+                        ks[size_t(j) * 128 + r] = order_key(x);
+                    }
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&aempty[s]);
+        }
+    }
+    tc_fence_before();
+    __syncthreads();  // every key of the CTA's rows is in the scratch (block-scope ordering)
+    tc_fence_after();
+    // top-k of rows [i0, i0 + nrows): RB rows per round, transposed into smem
+    // (coalesced 128-byte reads of the [key][row] scratch), one warp per row
+    const int nrows = min(128, N - i0);
+    const int RB = max(1, min(32, (2 * Cfg::kStage - 8 * 256 * 4) / ((N + 1) * 4)));
+    uint32_t* kr_all = reinterpret_cast<uint32_t*>(smem);
+    uint32_t* hist = kr_all + RB * (N + 1);
+    for (int r0 = 0; r0 < nrows; r0 += RB) {
+        const int nr = min(RB, nrows - r0);
+        for (int idx = threadIdx.x; idx < RB * N; idx += kFThreads) {
+            const int j = idx / RB, rr = idx % RB;
+            if (rr < nr) kr_all[rr * (N + 1) + j] = ks[size_t(j) * 128 + r0 + rr];
+        }
+        __syncthreads();
+        for (int rr = warp; rr < nr; rr += kFThreads / 32) {
+            const int i = i0 + r0 + rr;
+            select_row(kr_all + rr * (N + 1), hist + warp * 256, N, a.k, i, a.force_diagonal != 0,
+                       a.selected ? a.selected + (size_t(bh) * N + i) * a.k : nullptr,
+                       a.mask + (size_t(bh) * N + i) * a.W, lane);
+        }
+        __syncthreads();
+    }
+    if (warp == 1) tmem_dealloc(tmem, 512);
 }
 
 __global__ void plan_to_mask_kernel(const int32_t* __restrict__ selected, int N, int k, int W,
@@ -323,6 +531,21 @@ cudaError_t launch_select(int D, const SelectArgs& a, int BH, uint32_t* keys, cu
     const size_t smem = sizeof(uint32_t) * size_t(kRowsPerCta) * (a.N + 256);
     cudaFuncSetAttribute(topk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     topk_kernel<<<dim3((a.N + kRowsPerCta - 1) / kRowsPerCta, BH), kRowsPerCta * 32, smem, s>>>(keys, a);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_select_fused(int D, const CUtensorMap& tmKs, const SelectArgs& a, int BH, uint32_t* keys,
+                                cudaStream_t s) {
+    dim3 grid((a.N + 127) / 128, BH);
+    if (D == 128) {
+        auto k = select_fused_kernel<128>;
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, FusedSelCfg<128>::kSmem);
+        k<<<grid, kFThreads, FusedSelCfg<128>::kSmem, s>>>(tmKs, a, keys, BH);
+    } else {
+        auto k = select_fused_kernel<64>;
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, FusedSelCfg<64>::kSmem);
+        k<<<grid, kFThreads, FusedSelCfg<64>::kSmem, s>>>(tmKs, a, keys, BH);
+    }
     return cudaGetLastError();
 }
 

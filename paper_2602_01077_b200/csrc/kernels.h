@@ -20,6 +20,9 @@ struct StatsArgs {
     __nv_bfloat16* kbar_bf;
     __nv_bfloat16* vhat_bf;
     float* hpart;
+    __nv_bfloat16* kbar_split;  // [3][BH][N][D] exact bf16 hi / mid / lo split of k_bar (fused K2's
+                                // B operand), or null
+    int BH;
     int L, N, Npad, H, nchunk;
     int G;  // key blocks per CTA (<= kStatsG)
 };
@@ -72,6 +75,17 @@ struct SelectArgs {
 cudaError_t launch_rectifier(const float* m, double eps, float* rect, int n, cudaStream_t s);
 // keys: scratch uint32 [BH][N][N]
 cudaError_t launch_select(int D, const SelectArgs& a, int BH, uint32_t* keys, cudaStream_t s);
+
+// K2 fused (N >= kSelectFusedMinN): one CTA per (128 query blocks, b*h) scores
+// its rows against every key tile on tcgen05 (q_bar split into TMEM, k_bar
+// splits from K1 by TMA), writes the order keys of its rows to an L2-resident
+// scratch and selects each row's top-k right away. keys: scratch uint32
+// [BH][N][N] (rows of the CTA only are touched); tmKs: 3-D map over
+// kbar_split (D, N, 3*BH), 64 x 128 boxes, SW128.
+constexpr int kSelectFusedMinN = 512;
+constexpr int kScratchSlots = 256;  // scratch rows: kScratchSlots x 128 x N uint32 (one slot per SM id)
+cudaError_t launch_select_fused(int D, const CUtensorMap& tmKs, const SelectArgs& a, int BH, uint32_t* keys,
+                                cudaStream_t s);
 
 // K2c/K2d: overlap-aware pairing of query blocks for the fused kernel.
 // cand: scratch int [BH][N][kPairCand]; pairs: int2 [BH][ceil(N/2)].

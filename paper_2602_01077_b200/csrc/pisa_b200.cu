@@ -179,6 +179,15 @@ bool make_3d_map(CUtensorMap* m, const void* base, uint64_t D, uint64_t rows, ui
     return make_map(m, base, 3, dims, strides, box);
 }
 
+// env PISA_B200_FUSED_SELECT=0 keeps the two-kernel select (A/B and fallback)
+bool fused_select_off() {
+    static const bool off = [] {
+        const char* e = std::getenv("PISA_B200_FUSED_SELECT");
+        return e && e[0] == '0';
+    }();
+    return off;
+}
+
 // ------------------------------------------------------------ resolve --
 struct Plan {
     int64_t BH, L, D, N, Npad, W, k, nchunk1, nchunk2;
@@ -264,6 +273,7 @@ struct Work {
     int* cand;
     int2* pairs;
     __nv_bfloat16 *kbar_bf, *vhat_bf, *hbar_bf;
+    __nv_bfloat16* ksplit;  // k_bar hi / mid / lo [3][BH][N][D] (fused K2 only, else null)
     int32_t* selected;
     uint32_t* mask;
     uint32_t* keys;
@@ -308,7 +318,9 @@ pisa_status workspace(pisa_ctx* ctx, const Plan& p, Work* w, cudaStream_t s) {
                  o_hbar = take(BH * D * D * 4), o_kglob = take(BH * D * 4),
                  o_kbf = take(BH * p.Npad * D * 2), o_vbf = take(BH * p.Npad * D * 2),
                  o_hbf = take(BH * D * D * 2), o_sel = take(BH * N * p.k * 4),
-                 o_mask = take(BH * N * p.W * 4), o_keys = take(BH * N * N * 4),
+                 o_mask = take(BH * N * p.W * 4),
+                 o_keys = take(std::max(BH * N * N, p.N >= kSelectFusedMinN ? size_t(kScratchSlots) * 128 * N : 0) * 4),
+                 o_ksplit = take(p.N >= kSelectFusedMinN ? 3 * BH * N * D * 2 : 0),
                  o_norms = take(BH * N * 4), o_rect = take(BH * N * 4), o_tri = take(BH * N * kTriStride * 4),
                  o_cand = take(BH * N * kPairCand * 4), o_pairs = take(BH * ((N + 1) / 2) * 8);
     pisa_ctx::Arena* ar = arena_of(ctx, s);
@@ -342,6 +354,7 @@ pisa_status workspace(pisa_ctx* ctx, const Plan& p, Work* w, cudaStream_t s) {
     w->selected = reinterpret_cast<int32_t*>(b + o_sel);
     w->mask = reinterpret_cast<uint32_t*>(b + o_mask);
     w->keys = reinterpret_cast<uint32_t*>(b + o_keys);
+    w->ksplit = p.N >= kSelectFusedMinN ? reinterpret_cast<__nv_bfloat16*>(b + o_ksplit) : nullptr;
     w->flag = ar->flags;
     return PISA_OK;
 }
@@ -352,8 +365,9 @@ pisa_status run_stats(pisa_ctx* ctx, const pisa_attn_desc& d, const Plan& p, con
     if (!make_qkv_map(&tq, q, d, d.q_strides, 64) || !make_qkv_map(&tk, k, d, d.k_strides, 64) ||
         !make_qkv_map(&tv, v, d, d.v_strides, 64))
         return fail(ctx, PISA_ERR_INVALID_DIMENSION, "TMA descriptor rejected the q/k/v layout");
-    StatsArgs sa{w.kbar, w.vhat, w.qbar, w.kbar_bf, w.vhat_bf, w.hpart,
-                 int(p.L), int(p.N), int(p.Npad), int(d.heads), int(p.nchunk1), int(p.statsG)};
+    StatsArgs sa{w.kbar,  w.vhat,      w.qbar,       w.kbar_bf,        w.vhat_bf,
+                 w.hpart, w.ksplit,    int(p.BH),    int(p.L),         int(p.N),
+                 int(p.Npad), int(d.heads), int(p.nchunk1), int(p.statsG)};
     cudaError_t e;
     {
         ProfScope ps(ctx, kK1, s);
@@ -386,11 +400,24 @@ pisa_status run_norms(pisa_ctx* ctx, const pisa_attn_desc& d, const Plan& p, con
     return PISA_OK;
 }
 
+// ksplit: K1's hi / mid / lo split of k_bar (the forward's own statistics):
+// the fused one-launch select; null (caller-supplied statistics, short
+// heads): score_kernel + topk_kernel
 pisa_status run_select(pisa_ctx* ctx, const pisa_attn_desc& d, const Plan& p, const float* qbar,
                        const float* kbar, const float* rect, int32_t* selected, uint32_t* mask,
-                       uint32_t* keys, cudaStream_t s) {
+                       uint32_t* keys, cudaStream_t s, const __nv_bfloat16* ksplit = nullptr) {
     SelectArgs a{qbar, kbar, rect, selected, mask, int(p.N), int(p.W), int(p.k), d.force_diagonal,
                  float(p.scale)};
+    if (ksplit && !fused_select_off()) {
+        CUtensorMap tks;
+        if (!make_3d_map(&tks, ksplit, p.D, p.N, 3 * p.BH, 128))
+            return fail(ctx, PISA_ERR_CUDA, "TMA descriptor creation failed (k_bar split)");
+        ProfScope ps(ctx, kK2, s);
+        const cudaError_t e = launch_select_fused(int(p.D), tks, a, int(p.BH), keys, s);
+        if (e != cudaSuccess) return cuda_fail(ctx, e, "select launch");
+        ctx->launches += 1;
+        return PISA_OK;
+    }
     ProfScope ps(ctx, kK2, s);
     const cudaError_t e = launch_select(int(p.D), a, int(p.BH), keys, s);
     if (e != cudaSuccess) return cuda_fail(ctx, e, "select launch");
@@ -724,7 +751,7 @@ pisa_status fwd_range(pisa_ctx* ctx, const pisa_attn_desc* d, const void* q, con
     const bool cov = d->router == PISA_ROUTER_COVARIANCE;
     if (cov && (st = run_norms(ctx, *d, p, w, k, v, s)) != PISA_OK) return st;
     int32_t* sel = (diag && diag->selected) ? diag->selected : nullptr;
-    if ((st = run_select(ctx, *d, p, w.qbar, w.kbar, cov ? w.rect : nullptr, sel, w.mask, w.keys, s)) !=
+    if ((st = run_select(ctx, *d, p, w.qbar, w.kbar, cov ? w.rect : nullptr, sel, w.mask, w.keys, s, w.ksplit)) !=
         PISA_OK)
         return st;
     return run_fused(ctx, *d, p, w, q, k, v, o, diag, s, fm);

@@ -117,6 +117,35 @@ def test_select_index_sets_exact(P, oracle_mod, kind, L, d, r, fd):
     assert nbad <= max(1, N // 1000), f"{nbad} near-tie rows"
 
 
+@pytest.mark.parametrize("kind,H,L,d,r,fd", [("gaussian", 2, 40000, 128, 0.875, False),
+                                              ("clustered", 3, 33000, 64, 0.75, True),
+                                              ("clustered", 1, 118800, 128, 0.9, False),
+                                              ("gaussian", 1, 262144, 64, 0.99, True)])
+def test_fused_select_equals_two_kernel_select(P, kind, H, L, d, r, fd):
+    """From N = 512 key blocks the forward routes with the fused select kernel
+    (q_bar split in TMEM, K1's k_bar splits by TMA, keys in an L2 scratch,
+    top-k in the same CTA); its plans equal the two-kernel select
+    (score_kernel + topk_kernel) on the same statistics bit for bit, for the
+    plain and the covariance router, d = 64 / 128, up to N = 4096."""
+    import torch
+    gen = P.gen_gaussian if kind == "gaussian" else P.gen_clustered
+    q, k, v = (x.reshape(1, H, L, d).cuda() for x in gen(7, H, L, d))
+    N = -(-L // 64)
+    kk = P.sparsity_to_k(r, N).k
+    st = P.compute_prepare(q[0], k[0], v[0])
+    for router in (P.RouterStrategy.Plain, P.RouterStrategy.CovarianceAware):
+        _, ex = P.fwd(q, k, v, return_plan=True, sparsity=r, force_diagonal=fd, router=router, epsilon=1e-6)
+        if router == P.RouterStrategy.Plain:
+            ref = P.select_topk_plain(st.q_bar, st.k_bar, kk, d ** -0.5, force_diagonal=fd)
+        else:
+            m = P.block_norms(q[0], k[0], v[0])
+            ref = P.select_topk_covariance(st.q_bar, st.k_bar, m, 1e-6, kk, d ** -0.5, force_diagonal=fd)
+        torch.cuda.synchronize()
+        assert torch.equal(ex["selected"], ref), router
+    del q, k, v
+    torch.cuda.empty_cache()
+
+
 # ------------------------------------------- covariance-aware router (§8f #1) --
 @pytest.mark.parametrize("kind,H,L,d", [("gaussian", 1, 1024, 64), ("clustered", 2, 1000, 128),
                                         ("gaussian", 1, 4096, 128)])
