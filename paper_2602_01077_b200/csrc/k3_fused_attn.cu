@@ -87,13 +87,15 @@ constexpr uint32_t kColO = 0, kColS = 128;  // O | three S/P buffers (P_g over t
 constexpr uint32_t kPolyMask = PISA_POLY_MASK;
 // Sub-tiles that BOTH query blocks of the tile selected (every Phase-1 entry
 // on clustered routing, every Phase-2 centroid chunk) are exponentiated by
-// both warpgroups, which share the four MUFU units: the softmax is then
-// MUFU-bound (2 x 8192 ex2 per 128-key super-tile = 1024 MUFU cycles = the
-// tensor time). There, elements whose index bit is set in kPolyBoth go to
-// the FMA pipe (ex2_poly). Single-use sub-tiles (gaussian routing) stay
-// all-MUFU (kPolyMask): their softmax is issue-bound, not MUFU-bound.
+// both warpgroups, which share the four MUFU units (2 x 8192 ex2 per 128-key
+// super-tile = 1024 MUFU cycles = the tensor time). Elements whose index bit
+// is set in kPolyBoth go to the FMA pipe (ex2_poly) on those sub-tiles only.
+// Measured (Wan2.1-14B, same box, 2 x interleaved, profiles/r02_ab_poly.log):
+// 0x00 19.02-19.13 ms clustered / 25.31-25.39 gaussian, 0x11 19.18-19.30 /
+// 25.47-25.58, 0x55 20.18-20.22 / 25.89-26.02: the softmax is not MUFU-bound
+// even when both blocks use every sub-tile, so the default is off.
 #ifndef PISA_POLY_BOTH
-#define PISA_POLY_BOTH 0x11
+#define PISA_POLY_BOTH 0x00
 #endif
 constexpr uint32_t kPolyBoth = PISA_POLY_BOTH;
 // The softmax warps' wait for S: spin (poll) or suspend in hardware between

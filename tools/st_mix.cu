@@ -9,8 +9,13 @@
 //                          B = P^T MN-major)                               = 2 slots, all useful
 //   mode 2  transposed + the 16 KB of P^T stores per iteration (8 warps of st.shared.v4,
 //                          the softmax's output) on the same shared-memory port
-//   mode 3  transposed + P^T stores + a 32 KB-per-iteration TMA-like copy stream
-//                          (cp.async.bulk global->shared, the K/V tiles)
+//   mode 3  transposed + P^T stores + a free-running cp.async.bulk copy stream
+//                          (global->shared, like the K/V tiles)
+//   mode 4  current tile + exactly 64 KB of bulk copies per iteration (the K
+//                          and V tiles of one super-tile): is the fused kernel's
+//                          tile bound by the shared-memory port?
+//   mode 5  current tile with Q in TMEM (S as TS, A from TMEM) + 64 KB copies
+//                          per iteration: the shared-memory traffic of S halves
 // Prints cycles per iteration and per USEFUL (query block, key block) pair at
 // gaussian routing (union/k = 1.78 -> 4 slots hold 2.25 useful pairs).
 //
@@ -27,14 +32,16 @@ using namespace pisa_sm100;
 __global__ void __launch_bounds__(384, 1) st_mix(int mode, int iters, unsigned long long* out, const uint8_t* gsrc) {
     extern __shared__ uint8_t raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(raw) + 1023) & ~uintptr_t(1023));
-    // [0,64K): operand A/B tiles, [64K,80K): P^T, [96K, 224K): copy ring (4 x 32 KB)
-    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + 229376 - 4096);
+    // [0,64K): operand A/B tiles, [64K,80K): P^T, [96K, 192K): copy ring (3 x 32 KB), 200K: barriers
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + 204800);
     uint32_t* slot = reinterpret_cast<uint32_t*>(bar + 16);
     volatile uint32_t* stop = reinterpret_cast<volatile uint32_t*>(bar + 17);
     const int warp = threadIdx.x >> 5;
     for (int i = threadIdx.x; i < 98304 / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(smem)[i] = 0x3c003c00u;
+    volatile uint32_t* ctr = reinterpret_cast<volatile uint32_t*>(bar + 18);  // MMA iterations issued
     if (threadIdx.x == 0) {
         *stop = 0;
+        *ctr = 0;
         for (int i = 0; i < 8; ++i) mbar_init(bar + i, 1);
         fence_mbar_init();
     }
@@ -59,12 +66,16 @@ __global__ void __launch_bounds__(384, 1) st_mix(int mode, int iters, unsigned l
         }
     }
     if (warp == 2 && mode >= 3) {
-        // 32 KB per round through cp.async.bulk (the K / V tile stream)
+        // 32 KB per round through cp.async.bulk (the K / V tile stream); modes
+        // 4 / 5 pace it at two rounds (64 KB) per MMA iteration
         uint8_t* ring = smem + 98304;
         int i = 0;
         for (; *stop == 0; ++i) {
-            const int s = i & 3;
-            if (i >= 4) mbar_wait(bar + 4 + s, ((i >> 2) - 1) & 1);
+            if (mode >= 4)
+                while (*stop == 0 && uint32_t(i) >= 2u * (*ctr) + 3u) {
+                }
+            const int s = i % 3;
+            if (i >= 3) mbar_wait(bar + 4 + s, ((i / 3) - 1) & 1);
             if (elect_one()) {
                 mbar_expect_tx(bar + 4 + s, 32768);
                 asm volatile(
@@ -75,8 +86,8 @@ __global__ void __launch_bounds__(384, 1) st_mix(int mode, int iters, unsigned l
             }
             __syncwarp();
         }
-        for (int j = i - 4; j < i; ++j)
-            if (j >= 0) mbar_wait(bar + 4 + (j & 3), (j >> 2) & 1);
+        for (int j = i - 3; j < i; ++j)
+            if (j >= 0) mbar_wait(bar + 4 + (j % 3), (j / 3) & 1);
     }
     if (warp == 0) {
         const uint32_t a = smem_u32(smem), b = smem_u32(smem + 32768), p = smem_u32(smem + 65536);
@@ -84,11 +95,18 @@ __global__ void __launch_bounds__(384, 1) st_mix(int mode, int iters, unsigned l
         const long long t0 = clock64();
         for (int it = 0; it < iters; ++it) {
             if (elect_one()) {
-                if (mode == 0) {
+                if (mode == 0 || mode == 4 || mode == 5) {
+                    if (mode == 5) {
 #pragma unroll
-                    for (int ks = 0; ks < 8; ++ks)
-                        mma_ss(dS, sdesc_sw128(a + (ks & 3) * 32, 16, 1024), sdesc_sw128(b + (ks & 3) * 32, 16, 1024),
-                               idesc_bf16(128, 128, 0, 0), 1);
+                        for (int ks = 0; ks < 8; ++ks)  // S = Q K^T with Q in TMEM (columns 448..511)
+                            mma_ts(dS, tmem + 448 + ks * 8, sdesc_sw128(b + (ks & 3) * 32, 16, 1024),
+                                   idesc_bf16(128, 128, 0, 0), 1);
+                    } else {
+#pragma unroll
+                        for (int ks = 0; ks < 8; ++ks)
+                            mma_ss(dS, sdesc_sw128(a + (ks & 3) * 32, 16, 1024),
+                                   sdesc_sw128(b + (ks & 3) * 32, 16, 1024), idesc_bf16(128, 128, 0, 0), 1);
+                    }
 #pragma unroll
                     for (int ks = 0; ks < 8; ++ks)
                         mma_ts(dO, dS + ks * 8, sdesc_sw128(b + (ks & 3) * 2048, 8192, 1024), idesc_bf16(128, 128, 0, 1),
@@ -105,6 +123,7 @@ __global__ void __launch_bounds__(384, 1) st_mix(int mode, int iters, unsigned l
                 }
             }
             __syncwarp();
+            if (lane_id() == 0) *ctr = uint32_t(it + 1);
         }
         if (elect_one()) mma_commit(bar);
         __syncwarp();
@@ -129,9 +148,10 @@ int main() {
     const int smem = 229376 - 1024;
     cudaFuncSetAttribute(st_mix, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     const char* names[] = {"current union tile (8 SS N128 + 8 TS N128)", "transposed (8 SS N64 S^T + 8 SS N64 PV^T)",
-                           "transposed + 16 KB P^T st.shared / iter", "transposed + P^T stores + 32 KB bulk copies"};
-    const double useful[] = {2.25, 2.0, 2.0, 2.0};  // useful (q-block, k-block) pairs per iteration (gaussian)
-    for (int mode = 0; mode < 4; ++mode) {
+                           "transposed + 16 KB P^T st.shared / iter", "transposed + P^T stores + bulk copies",
+                           "current tile + 64 KB bulk copies / iter", "current, Q in TMEM + 64 KB copies / iter"};
+    const double useful[] = {2.25, 2.0, 2.0, 2.0, 2.25, 2.25};  // useful (q-block, k-block) pairs / iter (gaussian)
+    for (int mode = 0; mode < 6; ++mode) {
         st_mix<<<148, 384, smem>>>(mode, 16, d, g);
         cudaMemset(d, 0, 8);
         const int iters = 4096;
