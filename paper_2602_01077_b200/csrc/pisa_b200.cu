@@ -179,13 +179,15 @@ bool make_3d_map(CUtensorMap* m, const void* base, uint64_t D, uint64_t rows, ui
     return make_map(m, base, 3, dims, strides, box);
 }
 
-// env PISA_B200_FUSED_SELECT=0 keeps the two-kernel select (A/B and fallback)
+// The one-launch select is opt-in (env PISA_B200_FUSED_SELECT=1): measured
+// 1.32 ms against 0.56 ms for score_kernel + topk_kernel at Wan2.1-14B
+// (profiles/r02c_ab_select.log): its 400 CTAs leave 2.7 waves on 148 SMs and
+// each selects 128 rows with 8 warps, where topk_kernel spreads one row per
+// warp over the whole chip.
+// (read per call, so a test can switch it)
 bool fused_select_off() {
-    static const bool off = [] {
-        const char* e = std::getenv("PISA_B200_FUSED_SELECT");
-        return e && e[0] == '0';
-    }();
-    return off;
+    const char* e = std::getenv("PISA_B200_FUSED_SELECT");
+    return !(e && e[0] == '1');
 }
 
 // ------------------------------------------------------------ resolve --

@@ -16,6 +16,9 @@
 //                          tile bound by the shared-memory port?
 //   mode 5  current tile with Q in TMEM (S as TS, A from TMEM) + 64 KB copies
 //                          per iteration: the shared-memory traffic of S halves
+//   mode 6  transposed + 16 KB P^T stores + 64 KB bulk copies per iteration,
+//                          both paced (the full shared-memory load of a
+//                          transposed tile: K and V of 128 keys, P^T)
 // Prints cycles per iteration and per USEFUL (query block, key block) pair at
 // gaussian routing (union/k = 1.78 -> 4 slots hold 2.25 useful pairs).
 //
@@ -24,6 +27,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdio>
+#include <cstdlib>
 
 #include "sm100.cuh"
 
@@ -54,11 +58,15 @@ __global__ void __launch_bounds__(384, 1) st_mix(int mode, int iters, unsigned l
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *slot;
-    if (warp >= 4 && mode >= 2) {
+    const bool ptx = mode == 2 || mode == 3 || mode == 6;  // transposed modes with P^T stores
+    if (warp >= 4 && ptx) {
         // P^T producer traffic: each of 8 warps stores 2 KB (16 B per lane x 4) per round
         uint4* pt = reinterpret_cast<uint4*>(smem + 65536) + (warp - 4) * 128;
         uint4 v = make_uint4(threadIdx.x, 1, 2, 3);
-        while (*stop == 0) {
+        for (uint32_t r = 0; __shfl_sync(0xffffffffu, *stop, 0) == 0; ++r) {
+            if (mode == 6)  // paced: one 16 KB P^T per MMA iteration
+                while (__shfl_sync(0xffffffffu, (*stop == 0 && r >= (*ctr) + 2u) ? 1u : 0u, 0)) {
+                }
 #pragma unroll
             for (int j = 0; j < 4; ++j) pt[j * 32 + lane_id()] = v;
             v.x += 1;
@@ -70,9 +78,9 @@ __global__ void __launch_bounds__(384, 1) st_mix(int mode, int iters, unsigned l
         // 4 / 5 pace it at two rounds (64 KB) per MMA iteration
         uint8_t* ring = smem + 98304;
         int i = 0;
-        for (; *stop == 0; ++i) {
+        for (; __shfl_sync(0xffffffffu, *stop, 0) == 0; ++i) {
             if (mode >= 4)
-                while (*stop == 0 && uint32_t(i) >= 2u * (*ctr) + 3u) {
+                while (__shfl_sync(0xffffffffu, (*stop == 0 && uint32_t(i) >= 2u * (*ctr) + 3u) ? 1u : 0u, 0)) {
                 }
             const int s = i % 3;
             if (i >= 3) mbar_wait(bar + 4 + s, ((i / 3) - 1) & 1);
@@ -139,7 +147,8 @@ __global__ void __launch_bounds__(384, 1) st_mix(int mode, int iters, unsigned l
     if (warp == 1) tmem_dealloc(tmem, 512);
 }
 
-int main() {
+int main(int argc, char** argv) {
+    const int only = argc > 1 ? atoi(argv[1]) : -1;
     unsigned long long* d;
     cudaMalloc(&d, 8);
     uint8_t* g;
@@ -149,9 +158,11 @@ int main() {
     cudaFuncSetAttribute(st_mix, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     const char* names[] = {"current union tile (8 SS N128 + 8 TS N128)", "transposed (8 SS N64 S^T + 8 SS N64 PV^T)",
                            "transposed + 16 KB P^T st.shared / iter", "transposed + P^T stores + bulk copies",
-                           "current tile + 64 KB bulk copies / iter", "current, Q in TMEM + 64 KB copies / iter"};
-    const double useful[] = {2.25, 2.0, 2.0, 2.0, 2.25, 2.25};  // useful (q-block, k-block) pairs / iter (gaussian)
-    for (int mode = 0; mode < 6; ++mode) {
+                           "current tile + 64 KB bulk copies / iter", "current, Q in TMEM + 64 KB copies / iter",
+                           "transposed + P^T + 64 KB copies / iter (paced)"};
+    const double useful[] = {2.25, 2.0, 2.0, 2.0, 2.25, 2.25, 2.0};  // useful (q-block, k-block) pairs / iter (gaussian)
+    for (int mode = 0; mode < 7; ++mode) {
+        if (only >= 0 && mode != only) continue;
         st_mix<<<148, 384, smem>>>(mode, 16, d, g);
         cudaMemset(d, 0, 8);
         const int iters = 4096;
