@@ -1,0 +1,6 @@
+# round-2 batch f: per-CTA pipeline timelines (trace builds), previous and new K3, both routings
+L=$PWD/paper_2602_01077_b200/lib
+for d in clustered gaussian; do
+  PISA_B200_LIB=$L/libpisa_b200_k3oldtr.so timeout 300 python tools/trace_timeline.py 40 $d > gpurun_out/trace_old_$d.txt 2>&1
+  PISA_B200_LIB=$L/libpisa_b200_trace.so timeout 300 python tools/trace_timeline.py 40 $d > gpurun_out/trace_new_$d.txt 2>&1
+done

@@ -1,5 +1,7 @@
 """Pipeline timeline of one fused-kernel CTA (needs the PISA_TRACE build:
-PISA_B200_LIB=.../libpisa_b200_trace.so). Prints per-role timestamps (cycles)."""
+PISA_B200_LIB=.../libpisa_b200_trace.so). Prints per-role timestamps (cycles).
+
+    python tools/trace_timeline.py [H] [gaussian|clustered]"""
 import os
 import sys
 
@@ -20,7 +22,11 @@ def main():
     H, L, d = int(sys.argv[1]) if len(sys.argv) > 1 else 40, 75600, 128
     tile = 100
     dev = torch.device("cuda", 0)
-    q, k, v = (torch.randn((1, H, L, d), device=dev, dtype=torch.bfloat16) for _ in range(3))
+    kind = sys.argv[2] if len(sys.argv) > 2 else "gaussian"
+    if kind == "clustered":
+        q, k, v = (x.reshape(1, H, L, d).to(dev) for x in P.gen_clustered(0, H, L, d))
+    else:
+        q, k, v = (torch.randn((1, H, L, d), device=dev, dtype=torch.bfloat16) for _ in range(3))
     ctx = P.Context.get(0)
     buf = torch.zeros(32 * 1024, dtype=torch.int64, device=dev)
     for _ in range(2):
