@@ -190,6 +190,22 @@ bool fused_select_off() {
     return !(e && e[0] == '1');
 }
 
+// heads per two-kernel select chunk (env PISA_B200_SELECT_CHUNK_MB: key
+// matrices of at most that many MB, so they stay L2-resident between the two
+// kernels). Default 0 = all heads in one pair of launches: at Wan2.1-14B the
+// chunked form measured 0.60 / 0.66 / 0.83 ms for 80 / 40 / 20 MB chunks
+// against 0.56 ms (profiles/r02p_ab_select_chunks.log) -- smaller launches
+// cost more than the HBM round trip of the keys saves.
+int64_t select_chunk_heads(int64_t N, int64_t BH) {
+    static const int64_t mb = [] {
+        const char* e = std::getenv("PISA_B200_SELECT_CHUNK_MB");
+        return e ? int64_t(std::atoll(e)) : int64_t(0);
+    }();
+    if (mb <= 0) return BH;
+    const int64_t per_head = N * N * 4;
+    return std::max<int64_t>(1, std::min<int64_t>(BH, (mb << 20) / per_head));
+}
+
 // ------------------------------------------------------------ resolve --
 struct Plan {
     int64_t BH, L, D, N, Npad, W, k, nchunk1, nchunk2;
@@ -321,7 +337,8 @@ pisa_status workspace(pisa_ctx* ctx, const Plan& p, Work* w, cudaStream_t s) {
                  o_kbf = take(BH * p.Npad * D * 2), o_vbf = take(BH * p.Npad * D * 2),
                  o_hbf = take(BH * D * D * 2), o_sel = take(BH * N * p.k * 4),
                  o_mask = take(BH * N * p.W * 4),
-                 o_keys = take(std::max(BH * N * N, p.N >= kSelectFusedMinN ? size_t(kScratchSlots) * 128 * N : 0) * 4),
+                 o_keys = take(std::max(size_t(select_chunk_heads(p.N, p.BH)) * N * N,
+                                        p.N >= kSelectFusedMinN ? size_t(kScratchSlots) * 128 * N : 0) * 4),
                  o_ksplit = take(p.N >= kSelectFusedMinN ? 3 * BH * N * D * 2 : 0),
                  o_norms = take(BH * N * 4), o_rect = take(BH * N * 4), o_tri = take(BH * N * kTriStride * 4),
                  o_cand = take(BH * N * kPairCand * 4), o_pairs = take(BH * ((N + 1) / 2) * 8);
@@ -420,10 +437,23 @@ pisa_status run_select(pisa_ctx* ctx, const pisa_attn_desc& d, const Plan& p, co
         ctx->launches += 1;
         return PISA_OK;
     }
+    // (optionally) heads in chunks whose N x N key matrix (u32) stays
+    // L2-resident between score_kernel and topk_kernel: the scratch is reused
+    // chunk after chunk (select_chunk_heads)
+    const int64_t hc = select_chunk_heads(p.N, p.BH);
     ProfScope ps(ctx, kK2, s);
-    const cudaError_t e = launch_select(int(p.D), a, int(p.BH), keys, s);
-    if (e != cudaSuccess) return cuda_fail(ctx, e, "select launch");
-    ctx->launches += 2;
+    for (int64_t h0 = 0; h0 < p.BH; h0 += hc) {
+        const int64_t nh = std::min(hc, p.BH - h0);
+        SelectArgs c = a;
+        c.qbar = qbar + h0 * p.N * p.D;
+        c.kbar = kbar + h0 * p.N * p.D;
+        c.rect = rect ? rect + h0 * p.N : nullptr;
+        c.selected = selected ? selected + h0 * p.N * p.k : nullptr;
+        c.mask = mask + h0 * p.N * p.W;
+        const cudaError_t e = launch_select(int(p.D), c, int(nh), keys, s);
+        if (e != cudaSuccess) return cuda_fail(ctx, e, "select launch");
+        ctx->launches += 2;
+    }
     return PISA_OK;
 }
 
