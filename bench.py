@@ -61,18 +61,66 @@ def load_peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """SM clock + throttle reasons sampled during the timed region: NVML polled
+    every 0.5 ms from a thread (so a few-millisecond region of image-size steps
+    still gets samples), nvidia-smi at 100 ms when NVML is unavailable. The NVML
+    device is found by the CUDA device's PCI bus id (NVML ignores
+    CUDA_VISIBLE_DEVICES)."""
 
     Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
          "clocks_event_reasons.sw_power_cap")
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
-    def __init__(self, gpu_index: int):
+    def __init__(self, gpu_index: int, pci_bus_id: str | None = None):
         self.gpu = gpu_index
+        self.pci = pci_bus_id
         self.proc = None
         self.lines = []
+        self.samples = []  # (sm MHz, reasons bitmask) from NVML
+        self.nv = None
+        self.stop = threading.Event()
+
+    def _nvml_handle(self):
+        try:
+            import pynvml as nv
+            nv.nvmlInit()
+            h = None
+            if self.pci:
+                try:
+                    h = nv.nvmlDeviceGetHandleByPciBusId_v2(self.pci.encode())
+                except Exception:
+                    h = None
+            if h is None:
+                h = nv.nvmlDeviceGetHandleByIndex(self.gpu)
+            self.max_mhz = float(nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM))
+            self.bits = {"hw_slowdown": nv.nvmlClocksEventReasonHwSlowdown,
+                         "hw_thermal_slowdown": nv.nvmlClocksEventReasonHwThermalSlowdown,
+                         "sw_thermal_slowdown": nv.nvmlClocksEventReasonSwThermalSlowdown,
+                         "sw_power_cap": nv.nvmlClocksEventReasonSwPowerCap}
+            self.nv = nv
+            return h
+        except Exception:
+            return None
+
+    def _poll(self, h):
+        nv = self.nv
+        while True:
+            try:
+                self.samples.append((float(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)),
+                                     int(nv.nvmlDeviceGetCurrentClocksEventReasons(h))))
+            except Exception:
+                pass
+            if self.stop.wait(0.0005):
+                break
 
     def __enter__(self):
+        h = self._nvml_handle()
+        if h is not None:
+            self.t = threading.Thread(target=self._poll, args=(h,), daemon=True)
+            self.t.start()
+            time.sleep(0.005)  # a first sample before the timed work starts
+            return self
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
@@ -89,6 +137,10 @@ class ClockSampler:
             self.lines.append(line.strip())
 
     def __exit__(self, *a):
+        if self.nv is not None:
+            self.stop.set()
+            self.t.join(timeout=1)
+            return
         if self.proc:
             self.proc.terminate()
             try:
@@ -98,7 +150,13 @@ class ClockSampler:
 
     def summary(self):
         sm, mx, reasons = [], None, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        if self.nv is not None:
+            for mhz, bits in self.samples:
+                sm.append(mhz)
+                for n in self.NAMES:
+                    if bits & self.bits[n]:
+                        reasons.add(n)
+            mx = self.max_mhz
         for ln in self.lines:
             parts = [p.strip() for p in ln.split(",")]
             if len(parts) < 6:
@@ -108,13 +166,13 @@ class ClockSampler:
                 mx = float(parts[1])
             except ValueError:
                 continue
-            for n, v in zip(names, parts[2:6]):
+            for n, v in zip(self.NAMES, parts[2:6]):
                 if v.lower() == "active":
                     reasons.add(n)
         if not sm:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
         return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
-                "samples": len(sm)}
+                "samples": len(sm), "source": "nvml 0.5 ms" if self.nv is not None else "nvidia-smi 100 ms"}
 
 
 # ------------------------------------------------------------ CPU legs --
@@ -369,7 +427,11 @@ def main():
     ctx.set_profiling(inline_prof)
     ctx.read_profile()
     launches = 0
-    with ClockSampler(local_rank) as clk:
+    props = torch.cuda.get_device_properties(dev)
+    pci = None
+    if hasattr(props, "pci_bus_id"):
+        pci = f"{getattr(props, 'pci_domain_id', 0):08X}:{props.pci_bus_id:02X}:{getattr(props, 'pci_device_id', 0):02X}.0"
+    with ClockSampler(local_rank, pci) as clk:
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
@@ -435,10 +497,21 @@ def main():
         try:
             with open(tp) as f:
                 tj = json.load(f)
-            traffic = tj.get(args.workload, {}).get("fused_attn_kernel_bytes")
-            traffic_src = tj.get(args.workload, {}).get("source")
+            ent = tj.get(args.workload, {})
+            traffic = ent.get("fused_attn_kernel_bytes")
+            if traffic is not None:
+                traffic_src = ent.get("source") or (
+                    f"not measured in this run: dram__bytes_read.sum + dram__bytes_write.sum of "
+                    f"fused_attn_kernel from the {ent.get('round', '?')} ncu --set full capture "
+                    f"(profiles/{ent.get('round', '?')}_ncu_summary.md), default gaussian workload")
         except Exception:
             traffic = None
+    # The stream that bounds the fused kernel (profiles/r02_k3_variants.log,
+    # tools/k3_variants/README.md): K and V tiles from L2 into shared memory,
+    # 2 x 64 rows x d x 2 B per 64-key tile (the tile counter is live)
+    kv_step = tiles * 2 * 64 * d * 2
+    kv_bytes = kv_step / max(1, len(pieces))
+    kv_tbps = kv_step / (fused_step * 1e-3) / 1e12 if fused_step > 0 else None
     kernels = {n: {"ms_per_launch": ms / max(1, c), "launches": c,
                    "share": ms / max(1e-9, sum(x[0] for x in prof.values()))}
                for n, (ms, c) in prof.items()}
@@ -547,6 +620,10 @@ def main():
                          "executed_frac_sustained": (executed / peak_sus) if executed else None,
                          "power_capped": capped,
                          "union_over_k": union_ratio, "peak_source": peak_src, "peak_burst": peak_burst,
+                         "l2_to_smem_kv": {"bytes_per_launch": kv_bytes, "achieved_TBps": kv_tbps,
+                                           "note": "K/V tiles streamed L2 -> shared memory by TMA (live tile "
+                                                   "count); on gaussian routing this stream, not the tensor "
+                                                   "pipe, sets the kernel's time (tools/k3_variants/README.md)"},
                          "peak_sustained": peak_sus,
                          "kernel_timing": ("library events around each launch inside the timed region"
                                            if inline_prof else
