@@ -66,8 +66,10 @@ using namespace pisa_sm100;
 namespace {
 
 constexpr int kThreads = 384;
+// K stages: 2 measured as fast as 3 with the previous softmax and 1-1.5 %
+// faster with the single-pass one (profiles/r02_k3_variants.log, batches l, s)
 #ifndef PISA_KSTAGES
-#define PISA_KSTAGES 3
+#define PISA_KSTAGES 2
 #endif
 #ifndef PISA_VSTAGES
 #define PISA_VSTAGES 3
@@ -152,6 +154,10 @@ __device__ __forceinline__ void mma_wait(uint64_t* bar, uint32_t parity) {
 // balanced 26.5 / 19.7 ms, grouped 25.4 / 20.0 ms -- the per-super-tile fixed
 // softmax cost penalises balancing, and scrambling the order costs the L2
 // reuse between neighbouring CTAs walking similar selections in step.
+// PISA_SPEC_MAX 1: single-pass softmax (see Phase 1)
+#ifndef PISA_SPEC_MAX
+#define PISA_SPEC_MAX 1
+#endif
 #ifndef PISA_BALANCED
 #define PISA_BALANCED 0
 #endif
@@ -760,13 +766,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                         if (!(active && col < nv1)) r1[i] = 0xff800000u;
                     }
                 }
-                float bm_loc = -INFINITY;
-                if (use0) bm_loc = max32(reinterpret_cast<const float*>(r0));
-                if (use1) bm_loc = fmaxf(bm_loc, max32(reinterpret_cast<const float*>(r1)));
-                const float mm = update_max(bm_loc, g);
                 // exponentials only for the selected sub-tiles (warp-uniform);
                 // sub-tiles both blocks selected split exp2 across MUFU and FMA
-                auto expo_store = [&](const uint32_t (&r)[32], uint32_t addr, bool both) {
+                float lsum = 0.f;
+                auto expo_store = [&](const uint32_t (&r)[32], uint32_t addr, bool both, float mm) {
                     uint32_t pk[16];
                     float ps[4] = {0.f, 0.f, 0.f, 0.f};
                     if (both) {
@@ -786,13 +789,43 @@ __global__ void __launch_bounds__(kThreads, 1)
                             pk[i >> 1] = pack_bf16(p0, p1);
                         }
                     }
-                    l += (ps[0] + ps[1]) + (ps[2] + ps[3]);
+                    lsum += (ps[0] + ps[1]) + (ps[2] + ps[3]);
                     tmem_st16x2_16<16>(addr, pk);  // P (bf16 pairs)
                 };
                 const bool both0 = ((e0 >> 14) & 3u) == 3u, both1 = ((e1 >> 14) & 3u) == 3u;
-                if (use0) expo_store(r0, sc, both0); else tmem_st16x2_16<16>(sc, kZero16);
+                auto exact_max = [&]() -> float {  // lazy update of m from the super-tile's row max
+                    float bm_loc = -INFINITY;
+                    if (use0) bm_loc = max32(reinterpret_cast<const float*>(r0));
+                    if (use1) bm_loc = fmaxf(bm_loc, max32(reinterpret_cast<const float*>(r1)));
+                    return update_max(bm_loc, g);
+                };
+#if PISA_SPEC_MAX
+                // single pass: exponentiate against the running max without this
+                // super-tile's max; it is only needed (the exact lazy update, then
+                // P again) when the row has no max yet or the p sum exceeds 2^16,
+                // which keeps p bounded as the 2^8 rescale threshold did
+                // (warp-uniform: the P stores are warp-collective tcgen05.st)
+                const bool fresh = __any_sync(0xffffffffu, m == -INFINITY && active);
+                if (!fresh) {
+                    const float mm = m == -INFINITY ? 0.f : m;
+                    if (use0) expo_store(r0, sc, both0, mm);
+                    if (use1) expo_store(r1, sc + 64, both1, mm);
+                }
+                if (__any_sync(0xffffffffu, fresh || !(lsum <= 65536.f))) {
+                    const float mm = exact_max();
+                    lsum = 0.f;
+                    if (use0) expo_store(r0, sc, both0, mm);
+                    if (use1) expo_store(r1, sc + 64, both1, mm);
+                }
+                if (!use0) tmem_st16x2_16<16>(sc, kZero16);
+                if (!use1) tmem_st16x2_16<16>(sc + 64, kZero16);
+#else
+                const float mm = exact_max();
+                if (use0) expo_store(r0, sc, both0, mm); else tmem_st16x2_16<16>(sc, kZero16);
                 publish_half();
-                if (use1) expo_store(r1, sc + 64, both1); else tmem_st16x2_16<16>(sc + 64, kZero16);
+                if (use1) expo_store(r1, sc + 64, both1, mm); else tmem_st16x2_16<16>(sc + 64, kZero16);
+#endif
+                l += lsum;
             } else {
                 tmem_st16x2_16<16>(sc, kZero16);
                 publish_half();
@@ -827,13 +860,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (!(active && col < nv0 && !((cm0 >> i) & 1u))) r0[i] = 0xff800000u;
                 if (!(active && col < nv1 && !((cm1 >> i) & 1u))) r1[i] = 0xff800000u;
             }
-            const float mm = update_max(fmaxf(max32(reinterpret_cast<const float*>(r0)),
-                                              max32(reinterpret_cast<const float*>(r1))), g);
             // column (within this thread's 32) of the ragged last block, if here
             const int lb = a.N - 1 - c0 * 64 - ch * 32;  // 0..31 -> sub-tile 0, 64..95 -> sub-tile 1
             const bool ragged = n_last != 64;
             float ps = 0.f, plast = 0.f;
-            auto expo_store = [&](const uint32_t (&r)[32], uint32_t addr, int lbo) {
+            auto expo_store = [&](const uint32_t (&r)[32], uint32_t addr, int lbo, float mm) {
                 uint32_t pk[16];
                 float q0 = 0.f, q1 = 0.f;
 #pragma unroll
@@ -848,9 +879,22 @@ __global__ void __launch_bounds__(kThreads, 1)
                 ps += q0 + q1;
                 tmem_st16x2_16<16>(addr, pk);
             };
-            expo_store(r0, sc, lb);
-            publish_half();
-            expo_store(r1, sc + 64, lb - 64);
+            auto run = [&](float mm) {
+                ps = plast = 0.f;
+                expo_store(r0, sc, lb, mm);
+                expo_store(r1, sc + 64, lb - 64, mm);
+            };
+            auto exact_max = [&]() -> float {
+                return update_max(fmaxf(max32(reinterpret_cast<const float*>(r0)),
+                                        max32(reinterpret_cast<const float*>(r1))), g);
+            };
+#if PISA_SPEC_MAX
+            const bool fresh = __any_sync(0xffffffffu, m == -INFINITY && active);
+            if (!fresh) run(m == -INFINITY ? 0.f : m);
+            if (__any_sync(0xffffffffu, fresh || !(ps <= 65536.f))) run(exact_max());
+#else
+            run(exact_max());
+#endif
             l += 64.f * ps + (float(n_last) - 64.f) * plast;
             lt += ps;
             publish_p(g);
