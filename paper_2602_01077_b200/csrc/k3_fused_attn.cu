@@ -146,21 +146,11 @@ __device__ __forceinline__ void mma_wait(uint64_t* bar, uint32_t parity) {
 #endif
 }
 
-// Phase-1 block order. 0: the ascending union (default). 1: balanced (A&B
-// pairs, then (A-only, B-only) pairs: equal softmax work per warpgroup in every
-// super-tile). 2: grouped (A&B pairs, then alternating (A, A) / (B, B) pairs:
-// each warpgroup active in the fewest super-tiles). Measured on one B200
-// (Wan2.1-14B, gaussian / clustered): ascending 24.7-25.1 / 19.2-19.3 ms,
-// balanced 26.5 / 19.7 ms, grouped 25.4 / 20.0 ms -- the per-super-tile fixed
-// softmax cost penalises balancing, and scrambling the order costs the L2
-// reuse between neighbouring CTAs walking similar selections in step.
-// PISA_SPEC_MAX 1: single-pass softmax (see Phase 1)
-#ifndef PISA_SPEC_MAX
-#define PISA_SPEC_MAX 1
-#endif
-#ifndef PISA_BALANCED
-#define PISA_BALANCED 0
-#endif
+// Phase-1 block order: the ascending union. (A balanced order -- A&B pairs,
+// then (A-only, B-only) pairs -- and a grouped one measured slower: 26.5 / 25.4
+// vs 24.7-25.1 ms gaussian, round 1; the per-super-tile fixed softmax cost
+// penalises balancing, and scrambling the order costs the L2 reuse between
+// neighbouring CTAs walking similar selections in step.)
 template <uint32_t Mask>
 __device__ __forceinline__ float ex2_mix(float x, int i) {
     return ((Mask >> (i & 7)) & 1u) ? ex2_poly(x) : ex2(x);
@@ -185,7 +175,7 @@ struct Bars {
     uint64_t k_full[kSK], v_full[kSV], v_empty[kSV];
     uint64_t s_full[kSB], p_full[kSB], p_half[kSB];
     uint32_t tmem_base;
-    uint32_t n_ab, n_a, n_b;
+    uint32_t n_u;  // |A u B|
 };
 static_assert(sizeof(Bars) <= 512, "barrier block");
 
@@ -241,6 +231,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     Bars& bar = *reinterpret_cast<Bars*>(smem + Cfg::kOffBar);
     uint32_t* maskA = reinterpret_cast<uint32_t*>(smem + Cfg::kOffMask);
     uint32_t* maskB = maskA + a.W;
+    uint16_t* ulist = reinterpret_cast<uint16_t*>(maskB + a.W);  // [2 * ceil(|A u B| / 2)]
 #if PISA_TRACE
     const long long tstart = clock64();
 #endif
@@ -300,11 +291,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     if (warp == 3) {
         // selection bitmasks of the two query blocks into shared memory, and the
-        // sizes of the three parts of their union (A&B, A only, B only; every
-        // consumer walks them itself with a UnionCursor)
+        // ascending union as a list of 16-bit entries: block index | (selected by
+        // A) << 14 | (by B) << 15, padded to an even length with a copy of the
+        // last entry whose use flags are 0 (fully masked: P = 0, finite V rows).
+        // Every role reads super-tile g's two entries with one shared load.
         const uint32_t* mA = a.mask + (size_t(bh) * a.N + iA) * a.W;
         const uint32_t* mB = a.mask + (size_t(bh) * a.N + iB) * a.W;
-        uint32_t nab = 0, na = 0, nb = 0;
         // all loads in flight at once (one L2 round trip; W <= 128 for N <= 4096)
         uint32_t ra[4], rb[4];
 #pragma unroll
@@ -313,6 +305,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             ra[i] = w < a.W ? __ldcg(mA + w) : 0u;
             rb[i] = (w < a.W && hasB) ? __ldcg(mB + w) : 0u;
         }
+        uint32_t base = 0;  // entries before this lane's word of chunk i
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
             const int w = lane + 32 * i;
@@ -320,133 +313,47 @@ __global__ void __launch_bounds__(kThreads, 1)
                 maskA[w] = ra[i];
                 maskB[w] = rb[i];
             }
-            nab += __popc(ra[i] & rb[i]);
-            na += __popc(ra[i] & ~rb[i]);
-            nb += __popc(rb[i] & ~ra[i]);
-        }
+            const uint32_t u = ra[i] | rb[i];
+            const uint32_t c = __popc(u);
+            uint32_t x = c;  // inclusive prefix over the lanes of chunk i
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            nab += __shfl_xor_sync(0xffffffffu, nab, o);
-            na += __shfl_xor_sync(0xffffffffu, na, o);
-            nb += __shfl_xor_sync(0xffffffffu, nb, o);
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+                if (lane >= o) x += y;
+            }
+            uint32_t pos = base + x - c;
+            for (uint32_t bits = u; bits; bits &= bits - 1) {
+                const int bt = __ffs(bits) - 1;
+                ulist[pos++] = uint16_t((w * 32 + bt) | (((ra[i] >> bt) & 1u) << 14) | (((rb[i] >> bt) & 1u) << 15));
+            }
+            base += __shfl_sync(0xffffffffu, x, 31);
         }
         if (lane == 0) {
-            bar.n_ab = nab;
-            bar.n_a = na;
-            bar.n_b = nb;
+            bar.n_u = base;
+            if (base & 1u) ulist[base] = uint16_t(ulist[base - 1] & 0x3FFFu);
         }
-        TRACE(13, 0);  // masks copied, union sized
+        TRACE(13, 0);  // masks copied, union listed
     }
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
     if (warp == 0) TRACE(14, 0);  // CTA barrier passed
     const uint32_t tmem = bar.tmem_base;
-    const int nAB = int(bar.n_ab), nAo = int(bar.n_a), nBo = int(bar.n_b);
+    const int nU = int(bar.n_u);
     // Key tiles are processed in pairs ("super-tiles" of 128 keys): one K / V
     // stage, one S buffer, one barrier round trip and N=128 S MMAs per pair.
-    // Phase 1 walks the union of the two selections in the order PISA_BALANCED
-    // picks (the online softmax is order-independent up to rounding; default:
-    // ascending). The balanced / grouped orders use the split A&B, A-only,
-    // B-only (|A-only| == |B-only| since both select k). An odd tail is padded
-    // with a copy of the previous entry whose use flags are zero (fully
-    // masked: P = 0 and finite V rows).
-    // Phase 2 pairs consecutive centroid chunks.
-    const int gAB = (nAB + 1) >> 1;
-    const int nX = min(nAo, nBo);
-    const int nR = max(nAo, nBo) - nX;
-#if PISA_BALANCED == 2
-    const int gA = (nAo + 1) >> 1, gB = (nBo + 1) >> 1;
-    const int G1 = gAB + gA + gB;
-#elif PISA_BALANCED
-    const int G1 = gAB + nX + ((nR + 1) >> 1);
-#else
-    const int nU = nAB + nAo + nBo;
+    // Phase 1 walks the union list; Phase 2 pairs consecutive centroid chunks.
     const int G1 = (nU + 1) >> 1;
-#endif
     const int G = G1 + (tail ? (a.nchunk2 + 1) >> 1 : 0);
-    // entry = block index | (selected by query block A) << 14 | (by B) << 15
-    struct BitStream {
-        const uint32_t* ma;
-        const uint32_t* mb;
-        int kind;  // 0: A&B, 1: A only, 2: B only, 3: A|B (with use flags)
-        int w;
-        uint32_t bits;
-        __device__ __forceinline__ uint32_t next() {
-            while (bits == 0) {
-                ++w;
-                const uint32_t x = ma[w], y = mb[w];
-                bits = kind == 0 ? (x & y) : kind == 1 ? (x & ~y) : kind == 2 ? (y & ~x) : (x | y);
-            }
-            const int b = __ffs(bits) - 1;
-            bits &= bits - 1;
-            const uint32_t f = kind == 3 ? ((((ma[w] >> b) & 1u) << 14) | (((mb[w] >> b) & 1u) << 15)) : 0u;
-            return uint32_t(w * 32 + b) | f;
-        }
+    auto pair_of = [&](int g, uint32_t& e0, uint32_t& e1) {
+        const uint32_t v = reinterpret_cast<const uint32_t*>(ulist)[g];
+        e0 = v & 0xFFFFu;
+        e1 = v >> 16;
     };
-    struct UnionCursor {
-        BitStream ab, ao, bo;
-        __device__ __forceinline__ UnionCursor(const uint32_t* ma, const uint32_t* mb)
-            : ab{ma, mb, PISA_BALANCED ? 0 : 3, -1, 0u}, ao{ma, mb, 1, -1, 0u}, bo{ma, mb, 2, -1, 0u} {}
-        // the two entries of super-tile g (called for g = 0, 1, ... in order)
-        __device__ __forceinline__ void pair(int g, int gAB, int nAB, int nX, int nR, bool restA, uint32_t& e0,
-                                             uint32_t& e1) {
-#if !PISA_BALANCED
-            // ascending union order (kept as a build variant for A/B timing)
-            if (true) {
-                BitStream& u = ab;  // constructed with kind 3 in this build
-                e0 = u.next();
-                e1 = (2 * g + 1 < nAB) ? u.next() : (e0 & 0x3FFFu);
-                return;
-            }
-#endif
-#if PISA_BALANCED == 2
-            // grouped: (A&B, A&B), then alternating (A, A) / (B, B) pairs so
-            // each warpgroup has a used sub-tile in as few super-tiles as
-            // possible (the other skips ahead on zero P)
-            if (g >= gAB) {
-                const int j = g - gAB;
-                const int gA = (nX + 1) >> 1, gB = (nR + 1) >> 1;  // here nX = |A only|, nR = |B only|
-                const int m2 = 2 * min(gA, gB);
-                const bool useA = j < m2 ? !(j & 1) : gA > gB;
-                const int i = j < m2 ? (j >> 1) : (min(gA, gB) + j - m2);
-                BitStream& r = useA ? ao : bo;
-                const uint32_t f = useA ? (1u << 14) : (2u << 14);
-                e0 = r.next() | f;
-                e1 = (2 * i + 1 < (useA ? nX : nR)) ? (r.next() | f) : (e0 & 0x3FFFu);
-                return;
-            }
-#endif
-            if (g < gAB) {
-                e0 = ab.next() | (3u << 14);
-                e1 = (2 * g + 1 < nAB) ? (ab.next() | (3u << 14)) : (e0 & 0x3FFFu);
-            } else if (g < gAB + nX) {
-                e0 = ao.next() | (1u << 14);
-                e1 = bo.next() | (2u << 14);
-            } else {
-                const int j = g - gAB - nX;
-                BitStream& r = restA ? ao : bo;
-                const uint32_t f = restA ? (1u << 14) : (2u << 14);
-                e0 = r.next() | f;
-                e1 = (2 * j + 1 < nR) ? (r.next() | f) : (e0 & 0x3FFFu);
-            }
-        }
-    };
-    const bool restA = nAo > nBo;
-#if PISA_BALANCED == 2
-    const int kPairX = nAo, kPairR = nBo;
-#else
-    const int kPairX = nX, kPairR = nR;
-#endif
-#if !PISA_BALANCED
-    const int nPair = nU;  // the union cursor's count (pair() reads it as nAB)
-#else
-    const int nPair = nAB;
-#endif
-    auto tile_rows = [&](UnionCursor& cur, int g, int& r0, int& r1) {
+    auto tile_rows = [&](int g, int& r0, int& r1) {
         if (g < G1) {
             uint32_t e0, e1;
-            cur.pair(g, gAB, nPair, kPairX, kPairR, restA, e0, e1);
+            pair_of(g, e0, e1);
             r0 = int(e0 & 0x3FFFu) * 64;
             r1 = int(e1 & 0x3FFFu) * 64;
         } else {
@@ -468,14 +375,13 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (j >= 0) mbar_wait(&bar.s_full[j % kSB], uint32_t((j / kSB) & 1));
         };
         int s = 0;
-        UnionCursor cur(maskA, maskB);
         for (int g = 0; g < G; ++g) {
             uint8_t* sK = smem + Cfg::kOffK + s * Cfg::kKV;
             wait_s_done(g - kSK);
             const bool exact = g < G1;
             int r0, r1;
             if (g == 0) TRACE(12, 1);
-            tile_rows(cur, g, r0, r1);
+            tile_rows(g, r0, r1);
             if (g == 0) TRACE(13, 1);
             if (elect_one()) {
                 mbar_expect_tx(&bar.k_full[s], Cfg::kKV);
@@ -514,13 +420,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int vh = warp - 2;
         int s = 0;
         uint32_t ph = 0;
-        UnionCursor cur(maskA, maskB);
         for (int g = 0; g < G; ++g) {
             uint8_t* sV = smem + Cfg::kOffV + s * Cfg::kKV + vh * 16384;
             mbar_wait(&bar.v_empty[s], ph ^ 1);
             const bool exact = g < G1;
             int r0, r1;
-            tile_rows(cur, g, r0, r1);
+            tile_rows(g, r0, r1);
             if (elect_one()) {
                 mbar_expect_tx(&bar.v_full[s], 16384);
                 if (exact) {
@@ -611,8 +516,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         for (int g = 0; g < G; ++g) {
             // PV_g as soon as P_g and V_g are in, then S_{g+3} once K_{g+3} is
-            // (in-order tensor pipe: S_{g+3} overwrites P_g after PV_g read it);
-            // a late K tile never holds back PV_g
+            // (in-order tensor pipe: S_{g+3} overwrites P_g after PV_g read it).
+            // A late K_{g+3} holds back PV_{g+1}; an event loop issuing whichever
+            // is ready first measured slower (26.1 vs 23.5 ms at Wan2.1-14B,
+            // profiles/r02_k3_variants.log batch ae): S early feeds the softmax,
+            // the kernel's bottleneck, and PV_{g+1} before S_{g+3} delays it.
 #if PISA_PSPLIT
             mma_wait(&bar.p_half[sbv], php);
             mma_wait(&bar.v_full[sv], phv);
@@ -738,10 +646,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t kZero16[16] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
 
         // ---- Phase 1: exact blocks of the union, two per super-tile
-        UnionCursor cur(maskA, maskB);
         for (int g = 0; g < G1; ++g) {
             uint32_t e0, e1;
-            cur.pair(g, gAB, nPair, kPairX, kPairR, restA, e0, e1);  // pad: use flags 0
+            pair_of(g, e0, e1);  // pad: use flags 0
             const bool use0 = (e0 >> (14 + hh)) & 1u, use1 = (e1 >> (14 + hh)) & 1u;  // warp-uniform
             const int nv0 = (int(e0 & 0x3FFFu) == a.N - 1) ? n_last : 64;
             const int nv1 = (int(e1 & 0x3FFFu) == a.N - 1) ? n_last : 64;
@@ -989,8 +896,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 size_t fused_smem_bytes(int D, int N, int W) {
     const size_t core = (D == 128) ? size_t(FusedCfg<128>::kOffMask) : size_t(FusedCfg<64>::kOffMask);
-    (void)N;
-    return 1024 + core + size_t(2 * W) * 4 + 16;
+    // masks (2 W words) + the union list (<= N entries + 1 pad, 16-bit)
+    return 1024 + core + size_t(2 * W) * 4 + size_t(N + 2) * 2 + 16;
 }
 
 cudaError_t launch_fused(int D, const CUtensorMap& tmQ, const CUtensorMap& tmK, const CUtensorMap& tmV,

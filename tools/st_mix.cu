@@ -16,6 +16,11 @@
 //                          tile bound by the shared-memory port?
 //   mode 5  current tile with Q in TMEM (S as TS, A from TMEM) + 64 KB copies
 //                          per iteration: the shared-memory traffic of S halves
+//   mode 7  current tile + the softmax's TMEM traffic, paced: per MMA iteration
+//                          8 warps each load 64 fp32 columns of their 16-lane
+//                          half (64 KB, the S of a super-tile) and store 32
+//                          (32 KB, its P) with tcgen05.ld/st 16x32bx2
+//   mode 8  as 7, free-running TMEM traffic (an upper bound on contention)
 //   mode 6  transposed + 16 KB P^T stores + 64 KB bulk copies per iteration,
 //                          both paced (the full shared-memory load of a
 //                          transposed tile: K and V of 128 keys, P^T)
@@ -59,6 +64,26 @@ __global__ void __launch_bounds__(384, 1) st_mix(int mode, int iters, unsigned l
     tc_fence_after();
     const uint32_t tmem = *slot;
     const bool ptx = mode == 2 || mode == 3 || mode == 6;  // transposed modes with P^T stores
+    if (warp >= 4 && (mode == 7 || mode == 8)) {
+        // softmax-like TMEM traffic on columns [384, 512) (the MMAs use [0, 384))
+        const uint32_t base = tmem + (uint32_t((warp & 3) * 32 + ((warp - 4) >> 2) * 16) << 16) + 384;
+        for (uint32_t r = 0; __shfl_sync(0xffffffffu, *stop, 0) == 0; ++r) {
+            if (mode == 7)
+                while (__shfl_sync(0xffffffffu, (*stop == 0 && r >= (*ctr) + 2u) ? 1u : 0u, 0)) {
+                }
+            uint32_t a0[32], a1[32];
+            tmem_ld16x2_32<32>(base, a0);
+            tmem_ld16x2_32<32>(base + 64, a1);
+            tmem_ld_wait(a0);
+            tmem_ld_wait(a1);
+            uint32_t pk[16];
+#pragma unroll
+            for (int i = 0; i < 16; ++i) pk[i] = a0[2 * i] ^ a1[2 * i + 1];
+            tmem_st16x2_16<16>(base, pk);
+            tmem_st16x2_16<16>(base + 64, pk);
+            tmem_st_wait();
+        }
+    }
     if (warp >= 4 && ptx) {
         // P^T producer traffic: each of 8 warps stores 2 KB (16 B per lane x 4) per round
         uint4* pt = reinterpret_cast<uint4*>(smem + 65536) + (warp - 4) * 128;
@@ -103,7 +128,7 @@ __global__ void __launch_bounds__(384, 1) st_mix(int mode, int iters, unsigned l
         const long long t0 = clock64();
         for (int it = 0; it < iters; ++it) {
             if (elect_one()) {
-                if (mode == 0 || mode == 4 || mode == 5) {
+                if (mode == 0 || mode == 4 || mode == 5 || mode == 7 || mode == 8) {
                     if (mode == 5) {
 #pragma unroll
                         for (int ks = 0; ks < 8; ++ks)  // S = Q K^T with Q in TMEM (columns 448..511)
@@ -159,9 +184,10 @@ int main(int argc, char** argv) {
     const char* names[] = {"current union tile (8 SS N128 + 8 TS N128)", "transposed (8 SS N64 S^T + 8 SS N64 PV^T)",
                            "transposed + 16 KB P^T st.shared / iter", "transposed + P^T stores + bulk copies",
                            "current tile + 64 KB bulk copies / iter", "current, Q in TMEM + 64 KB copies / iter",
-                           "transposed + P^T + 64 KB copies / iter (paced)"};
-    const double useful[] = {2.25, 2.0, 2.0, 2.0, 2.25, 2.25, 2.0};  // useful (q-block, k-block) pairs / iter (gaussian)
-    for (int mode = 0; mode < 7; ++mode) {
+                           "transposed + P^T + 64 KB copies / iter (paced)",
+                           "current tile + softmax TMEM ld/st (paced)", "current tile + softmax TMEM ld/st (free)"};
+    const double useful[] = {2.25, 2.0, 2.0, 2.0, 2.25, 2.25, 2.0, 2.25, 2.25};  // useful (q-block, k-block) pairs / iter (gaussian)
+    for (int mode = 0; mode < 9; ++mode) {
         if (only >= 0 && mode != only) continue;
         st_mix<<<148, 384, smem>>>(mode, 16, d, g);
         cudaMemset(d, 0, 8);
