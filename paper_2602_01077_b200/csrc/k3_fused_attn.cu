@@ -139,13 +139,24 @@ __device__ __forceinline__ void softmax_wait(uint64_t* bar, uint32_t parity) {
 #define PISA_PSPLIT 0
 #endif
 __device__ __forceinline__ void mma_wait(uint64_t* bar, uint32_t parity) {
-#if PISA_MMA_WAIT
+#if PISA_MMA_WAIT == 2
+    mbar_wait<false>(bar, parity);  // hardware-suspended try_wait (time-limit hint)
+#elif PISA_MMA_WAIT
     mbar_wait_backoff<PISA_MMA_NS>(bar, parity);
 #else
     mbar_wait<true>(bar, parity);
 #endif
 }
 
+// The MMA warp (PISA_MMA_WARP 1 or 3) and the second V producer (the other of
+// the two) -- the MMA warp shares its SM sub-partition with softmax warps q4 =
+// PISA_MMA_WARP of both warpgroups.
+#ifndef PISA_MMA_WARP
+#define PISA_MMA_WARP 1
+#endif
+constexpr int kMmaWarp = PISA_MMA_WARP;
+constexpr int kVWarp1 = PISA_MMA_WARP == 1 ? 3 : 1;
+static_assert(PISA_MMA_WARP == 1 || PISA_MMA_WARP == 3, "MMA warp");
 // PISA_S_PREFETCH 1: the softmax loads the next super-tile's S early (Phase 1).
 // Off: measured slower (24.0 vs 22.9 ms gaussian, 18.4 vs 16.9 ms clustered at
 // Wan2.1-14B, profiles/r02_k3_variants.log batch ag) -- the poll and loads sit
@@ -423,12 +434,12 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             __syncwarp();
         }
-    } else if (warp == 2 || (warp == 3 && D == 128)) {
+    } else if (warp == 2 || (warp == kVWarp1 && D == 128)) {
 #if PISA_REGS_PRODUCER
         asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(PISA_REGS_PRODUCER));
 #endif
         // -------------------------------------------- producers: V halves --
-        const int vh = warp - 2;
+        const int vh = warp == 2 ? 0 : 1;
         int s = 0;
         uint32_t ph = 0;
         for (int g = 0; g < G; ++g) {
@@ -451,12 +462,12 @@ __global__ void __launch_bounds__(kThreads, 1)
             __syncwarp();
             if (++s == kSV) { s = 0; ph ^= 1u; }
         }
-    } else if (warp == 3) {
+    } else if (warp == kVWarp1) {
         // (D = 64: one V producer; warp 3 only joins its warpgroup's setmaxnreg)
 #if PISA_REGS_PRODUCER
         asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(PISA_REGS_PRODUCER));
 #endif
-    } else if (warp == 1) {
+    } else if (warp == kMmaWarp) {
 #if PISA_REGS_PRODUCER
         asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(PISA_REGS_PRODUCER));
 #endif
