@@ -59,6 +59,10 @@ struct pisa_ctx {
     // env PISA_B200_PAIRING, API pisa_b200_set_pairing
     int pairing = 1;
     int host_chunks = 16;  // head chunks of the host path's copy/compute pipeline (env PISA_B200_HOST_CHUNKS)
+    // K1b (H_bar reduce) runs on a side stream beside the select: ev_k1 forks
+    // it after K1, ev_k1b joins it back before K1c / K3
+    cudaStream_t side = nullptr;
+    cudaEvent_t ev_k1 = nullptr, ev_k1b = nullptr;
     unsigned long long* tiles_dev = nullptr;  // fused-kernel tile counter (profiling only)
 };
 
@@ -378,8 +382,11 @@ pisa_status workspace(pisa_ctx* ctx, const Plan& p, Work* w, cudaStream_t s) {
     return PISA_OK;
 }
 
+// fork: K1b goes to ctx->side after K1 (the caller joins with join_hbar
+// before anything that reads H_bar / k_bar_global: K1c, K3); the select only
+// needs K1's k_bar / q_bar, so at image sizes the reduce hides under it.
 pisa_status run_stats(pisa_ctx* ctx, const pisa_attn_desc& d, const Plan& p, const Work& w,
-                      const void* q, const void* k, const void* v, cudaStream_t s) {
+                      const void* q, const void* k, const void* v, cudaStream_t s, bool fork = false) {
     CUtensorMap tq, tk, tv;
     if (!make_qkv_map(&tq, q, d, d.q_strides, 64) || !make_qkv_map(&tk, k, d, d.k_strides, 64) ||
         !make_qkv_map(&tv, v, d, d.v_strides, 64))
@@ -393,12 +400,34 @@ pisa_status run_stats(pisa_ctx* ctx, const pisa_attn_desc& d, const Plan& p, con
         e = launch_block_stats(int(p.D), tq, tk, tv, sa, int(p.BH), s);
     }
     if (e != cudaSuccess) return cuda_fail(ctx, e, "block_stats launch");
-    ProfScope ps(ctx, kK1b, s);
-    e = launch_hbar_reduce(int(p.D), w.hpart, int(p.nchunk1), int(p.N), w.kbar, w.hbar, w.hbar_bf,
-                           d.variant == PISA_GLOBAL_CENTROID ? w.kglob : nullptr, int(p.BH), s);
+    cudaStream_t sr = s;
+    if (fork) {
+        if (!ctx->side) {
+            e = cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking);
+            if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->ev_k1, cudaEventDisableTiming);
+            if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->ev_k1b, cudaEventDisableTiming);
+            if (e != cudaSuccess) return cuda_fail(ctx, e, "side stream setup");
+        }
+        if ((e = cudaEventRecord(ctx->ev_k1, s)) != cudaSuccess ||
+            (e = cudaStreamWaitEvent(ctx->side, ctx->ev_k1, 0)) != cudaSuccess)
+            return cuda_fail(ctx, e, "K1b fork");
+        sr = ctx->side;
+    }
+    {
+        ProfScope ps(ctx, kK1b, sr);
+        e = launch_hbar_reduce(int(p.D), w.hpart, int(p.nchunk1), int(p.N), w.kbar, w.hbar, w.hbar_bf,
+                               d.variant == PISA_GLOBAL_CENTROID ? w.kglob : nullptr, int(p.BH), sr);
+    }
     if (e != cudaSuccess) return cuda_fail(ctx, e, "hbar_reduce launch");
+    if (fork && (e = cudaEventRecord(ctx->ev_k1b, sr)) != cudaSuccess) return cuda_fail(ctx, e, "K1b event");
     ctx->launches += 2;
     return PISA_OK;
+}
+
+// s waits for the forked K1b (run_stats(fork = true))
+pisa_status join_hbar(pisa_ctx* ctx, cudaStream_t s) {
+    const cudaError_t e = cudaStreamWaitEvent(s, ctx->ev_k1b, 0);
+    return e == cudaSuccess ? PISA_OK : cuda_fail(ctx, e, "K1b join");
 }
 
 // K1c: M_j = ||H_j - H_bar||_2 and the rectifier log(M_j + eps) (covariance router),
@@ -666,6 +695,9 @@ void pisa_b200_destroy(pisa_ctx* c) {
         if (c->ev_d2h[i]) cudaEventDestroy(c->ev_d2h[i]);
     }
     if (c->st_h2d) cudaStreamDestroy(c->st_h2d);
+    if (c->side) cudaStreamDestroy(c->side);
+    if (c->ev_k1) cudaEventDestroy(c->ev_k1);
+    if (c->ev_k1b) cudaEventDestroy(c->ev_k1b);
     if (c->st_comp) cudaStreamDestroy(c->st_comp);
     if (c->st_d2h) cudaStreamDestroy(c->st_d2h);
     delete c;
@@ -779,13 +811,20 @@ pisa_status fwd_range(pisa_ctx* ctx, const pisa_attn_desc* d, const void* q, con
     const cudaStream_t s = static_cast<cudaStream_t>(stream);
     Work w;
     if ((st = workspace(ctx, p, &w, s)) != PISA_OK) return st;
-    if ((st = run_stats(ctx, *d, p, w, q, k, v, s)) != PISA_OK) return st;
+    // (not under stream capture: a replayed graph with the fork/join measured
+    // slower than the serial one, 0.163 vs 0.149 ms at FLUX, while eager
+    // launches gain, 0.150 vs 0.158 ms; profiles/r02aq_ab_fork.log)
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    const bool fork = cudaStreamIsCapturing(s, &cap) == cudaSuccess && cap == cudaStreamCaptureStatusNone;
+    if ((st = run_stats(ctx, *d, p, w, q, k, v, s, fork)) != PISA_OK) return st;
     const bool cov = d->router == PISA_ROUTER_COVARIANCE;
-    if (cov && (st = run_norms(ctx, *d, p, w, k, v, s)) != PISA_OK) return st;
+    if (cov && ((fork && (st = join_hbar(ctx, s)) != PISA_OK) || (st = run_norms(ctx, *d, p, w, k, v, s)) != PISA_OK))
+        return st;
     int32_t* sel = (diag && diag->selected) ? diag->selected : nullptr;
     if ((st = run_select(ctx, *d, p, w.qbar, w.kbar, cov ? w.rect : nullptr, sel, w.mask, w.keys, s, w.ksplit)) !=
         PISA_OK)
         return st;
+    if (fork && !cov && (st = join_hbar(ctx, s)) != PISA_OK) return st;
     return run_fused(ctx, *d, p, w, q, k, v, o, diag, s, fm);
 }
 }  // namespace
