@@ -197,7 +197,8 @@ struct Bars {
     uint64_t k_full[kSK], v_full[kSV], v_empty[kSV];
     uint64_t s_full[kSB], p_full[kSB], p_half[kSB];
     uint32_t tmem_base;
-    uint32_t n_u;  // |A u B|
+    uint32_t n_u;     // |A u B|
+    uint32_t n_w[4];  // union entries per 32-word quarter (list build)
 };
 static_assert(sizeof(Bars) <= 512, "barrier block");
 
@@ -276,6 +277,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     const bool first_order = a.variant == 3 || a.variant == 4;
     const int n_last = a.L - (a.N - 1) * 64;
 
+    // the two selection bitmasks (K2's output, L2-resident): warps 0-3 load one
+    // word per lane first, so the round trip overlaps the setup below
+    const int wl = warp * 32 + lane;
+    uint32_t ra = 0u, rb = 0u;
+    if (warp < 4 && wl < a.W) {
+        ra = __ldcg(a.mask + (size_t(bh) * a.N + iA) * a.W + wl);
+        if (hasB) rb = __ldcg(a.mask + (size_t(bh) * a.N + iB) * a.W + wl);
+    }
     // ------------------------------------------------------------ setup --
     if (threadIdx.x == 0) {
         mbar_init(&bar.q_full, 1);
@@ -311,50 +320,48 @@ __global__ void __launch_bounds__(kThreads, 1)
         tmem_relinquish();
         TRACE(12, 0);  // (trace builds) prologue: TMEM allocated
     }
-    if (warp == 3) {
-        // selection bitmasks of the two query blocks into shared memory, and the
+    if (warp < 4) {
+        // Selection bitmasks of the two query blocks into shared memory, and the
         // ascending union as a list of 16-bit entries: block index | (selected by
         // A) << 14 | (by B) << 15, padded to an even length with a copy of the
         // last entry whose use flags are 0 (fully masked: P = 0, finite V rows).
         // Every role reads super-tile g's two entries with one shared load.
-        const uint32_t* mA = a.mask + (size_t(bh) * a.N + iA) * a.W;
-        const uint32_t* mB = a.mask + (size_t(bh) * a.N + iB) * a.W;
-        // all loads in flight at once (one L2 round trip; W <= 128 for N <= 4096)
-        uint32_t ra[4], rb[4];
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            const int w = lane + 32 * i;
-            ra[i] = w < a.W ? __ldcg(mA + w) : 0u;
-            rb[i] = (w < a.W && hasB) ? __ldcg(mB + w) : 0u;
+        // Warps 0-3 build it together, one word per lane (W <= 128), after their
+        // own prologue tasks (a serial build in one warp cost ~2.5K cycles per
+        // CTA: 11 % of a FLUX-sized CTA).
+        __syncwarp();
+        const int w = wl;
+        if (w < a.W) {
+            maskA[w] = ra;
+            maskB[w] = rb;
         }
-        uint32_t base = 0;  // entries before this lane's word of chunk i
+        const uint32_t u = ra | rb;
+        const uint32_t c = __popc(u);
+        uint32_t x = c;  // inclusive prefix over the warp's 32 words
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            const int w = lane + 32 * i;
-            if (w < a.W) {
-                maskA[w] = ra[i];
-                maskB[w] = rb[i];
-            }
-            const uint32_t u = ra[i] | rb[i];
-            const uint32_t c = __popc(u);
-            uint32_t x = c;  // inclusive prefix over the lanes of chunk i
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        if (lane == 31) bar.n_w[warp] = x;
+        asm volatile("bar.sync 1, 128;" ::: "memory");  // warps 0-3
+        uint32_t base = 0, total = 0;
 #pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-                if (lane >= o) x += y;
-            }
-            uint32_t pos = base + x - c;
-            for (uint32_t bits = u; bits; bits &= bits - 1) {
-                const int bt = __ffs(bits) - 1;
-                ulist[pos++] = uint16_t((w * 32 + bt) | (((ra[i] >> bt) & 1u) << 14) | (((rb[i] >> bt) & 1u) << 15));
-            }
-            base += __shfl_sync(0xffffffffu, x, 31);
+        for (int q = 0; q < 4; ++q) {
+            const uint32_t n = bar.n_w[q];
+            base += q < warp ? n : 0u;
+            total += n;
         }
-        if (lane == 0) {
-            bar.n_u = base;
-            if (base & 1u) ulist[base] = uint16_t(ulist[base - 1] & 0x3FFFu);
+        uint32_t pos = base + x - c;
+        uint16_t last = 0;
+        for (uint32_t bits = u; bits; bits &= bits - 1) {
+            const int bt = __ffs(bits) - 1;
+            last = uint16_t((w * 32 + bt) | (((ra >> bt) & 1u) << 14) | (((rb >> bt) & 1u) << 15));
+            ulist[pos++] = last;
         }
-        TRACE(13, 0);  // masks copied, union listed
+        if (c != 0 && pos == total && (total & 1u)) ulist[total] = uint16_t(last & 0x3FFFu);
+        if (warp == 3 && lane == 0) bar.n_u = total;
+        if (warp == 3) TRACE(13, 0);  // masks copied, union listed
     }
     tc_fence_before();
     __syncthreads();

@@ -283,6 +283,8 @@ pisa_status resolve(pisa_ctx* ctx, const pisa_attn_desc* d, Plan* p) {
     // how many other heads share the launch, so head-sharded ranks reproduce
     // the single-GPU result exactly.
     p->statsG = std::max<int64_t>(4, std::min<int64_t>(kStatsG, (N + 23) / 24));
+    if (const char* e = std::getenv("PISA_B200_STATS_G"))  // (A/B of K1's chunk size)
+        p->statsG = std::max<int64_t>(1, std::min<int64_t>(kStatsG, std::atoll(e)));
     p->nchunk1 = (N + p->statsG - 1) / p->statsG;
     p->nchunk2 = (N + 63) / 64;
     p->scale = d->scale > 0.0 ? d->scale : 1.0 / std::sqrt(double(D));  // attention.hpp:34-37
