@@ -836,11 +836,19 @@ __global__ void __launch_bounds__(kThreads, 1)
                     const float p1 = ex2_mix<kPolyBoth>(fmaf(__uint_as_float(r[i + 1]), sl2, -mm), i + 1);
                     q0 += p0;
                     q1 += p1;
-                    if (ragged) plast += (lbo == i ? p0 : 0.f) + (lbo == i + 1 ? p1 : 0.f);
                     pk[i >> 1] = pack_bf16(p0, p1);
                 }
                 ps += q0 + q1;
                 tmem_st16x2_16<16>(addr, pk);
+                // the ragged last block's p (weight n_last, not 64): only in the
+                // super-tile and thread half that hold it, picked by a static
+                // select chain (a dynamic index would put r in local memory)
+                if (ragged && lbo >= 0 && lbo < 32) {
+                    uint32_t sb_ = 0xff800000u;
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) sb_ = (i == lbo) ? r[i] : sb_;
+                    plast += ex2_mix<kPolyBoth>(fmaf(__uint_as_float(sb_), sl2, -mm), lbo);
+                }
             };
             auto run = [&](float mm) {
                 ps = plast = 0.f;
