@@ -714,7 +714,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 auto expo_store = [&](const uint32_t (&r)[32], uint32_t addr, bool both, float mm) {
                     uint32_t pk[16];
                     float ps[4] = {0.f, 0.f, 0.f, 0.f};
-                    if (both) {
+                    if (kPolyBoth != kPolyMask && both) {  // (one code path when the splits agree)
 #pragma unroll
                         for (int i = 0; i < 32; i += 2) {
                             const float p0 = ex2_mix<kPolyBoth>(fmaf(__uint_as_float(r[i]), sl2, -mm), i);
