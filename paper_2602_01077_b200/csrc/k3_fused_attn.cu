@@ -16,15 +16,14 @@
 // ceil(N/64) centroid tiles with a per-block column mask (the selection bitmask)
 // and per-column weight n_j. Phase 3 is one more MMA, Q . H_bar.
 //
-// Why this shape (tools/l2_bw.cu, profiles/): the kernel streams a random
-// 16 KB K tile and a 16 KB V tile from L2 per 512 tensor cycles, ~64 B/clk/SM,
-// close to the chip's TMA delivery limit (~70 B/clk/SM), and a 16 KB TMA tile
-// takes 1300-2000 cycles under that load. Latency x bandwidth ~ 100+ KB must be
-// in flight per SM, so the design spends shared memory on K/V stages:
-//   * ONE CTA per SM: Q (32 KB) + 3 K + 3 V stages of two key blocks each
-//     (224 KB at d = 128) in shared memory (no per-CTA union list: every
-//     consumer walks maskA | maskB with its own cursor); with two K stages the
-//     K load for S_{g+3} could only start after S_{g+1} and arrived late;
+// Why this shape (tools/l2_bw.cu, tools/st_mix.cu, profiles/): the kernel
+// streams a random 32 KB K tile and a 32 KB V tile from L2 per super-tile
+// (~220 GB per Wan2.1-14B step, 9-10 TB/s), and a tile takes 1500-3000 cycles
+// under that load, so the design spends shared memory on K/V stages:
+//   * ONE CTA per SM: Q (32 KB) + 2 K + 3 V stages of two key blocks each
+//     (192 KB at d = 128) in shared memory, plus the two selection bitmasks and
+//     the union list; a third K stage measured no faster and no longer fits
+//     beside the list;
 //   * key blocks go through the pipeline in pairs ("super-tiles" of 128 keys):
 //     S = Q [K_a; K_b]^T is one set of N=128 MMAs, and each barrier round trip,
 //     commit and softmax hand-off covers two blocks -- a single issuing thread
@@ -33,8 +32,10 @@
 //     written over the S_g columns it came from), so the chain
 //     S_g -> softmax_g -> PV_g -> S_{g+3} spans three super-tiles and the
 //     tensor pipe stays fed while one super-tile is in the softmax.
-//     (Q in TMEM, TS-form S MMAs, would free shared memory but leave room for
-//     only two S buffers: measured 24.7 ms vs the three-buffer design.)
+//     (Designs with two S buffers -- Q in TMEM, or O split per warpgroup --
+//     measured 10-20 % slower: tools/k3_variants/README.md. Issuing TMA boxes
+//     one per lane, which moves the first S MMA ~1.5K cycles earlier, measured
+//     neutral: profiles/r02_k3_variants.log batch ay.)
 //
 // Warp roles (384 threads):
 //   warp 0     TMA producer: Q (once), K / k_bar tiles (3-stage ring of pairs),
@@ -42,8 +43,9 @@
 //   warp 1     single-thread tcgen05.mma issuer: S_g = Q K_g^T (SS, K-major),
 //              O += P_g V_g (TS: P from TMEM, V MN-major), Q H_bar (SS)
 //   warp 2     TMEM allocator, then TMA producer for V columns [0, 64)
-//   warp 3     builds the union list from the two selection bitmasks, then TMA
-//              producer for V columns [64, 128) (two issue streams for V)
+//   warp 3     TMA producer for V columns [64, 128) (two issue streams for V)
+//   warps 0-3  first (prologue): copy the two selection bitmasks and build the
+//              union list together
 //   warps 4-7  softmax / correction / epilogue of query block 2t   (warpgroup A)
 //   warps 8-11 softmax / correction / epilogue of query block 2t+1 (warpgroup B)
 // TMEM lane layout: lane q4*32 + hh*16 + r16 holds row q4*16 + r16 of query
@@ -51,8 +53,9 @@
 // thread t holds row t & 15, columns [32*(t >> 4), +32) of each 64-key half), so
 // each block's exponentials use all four SM sub-partitions (all four MUFU
 // units), and the two blocks' online softmaxes run in parallel. exp2 with
-// log2(e)*scale folded into one FFMA; lazy rescale of O (only when the running
-// max grows by > 2^8); P written back to TMEM as bf16 over its S columns.
+// log2(e)*scale folded into one FFMA, single pass against the running max (see
+// Phase 1); lazy rescale of O (only when the running max grows by > 2^8); P
+// written back to TMEM as bf16 over its S columns.
 #include "kernels.h"
 #include "sm100.cuh"
 
