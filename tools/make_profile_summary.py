@@ -99,7 +99,10 @@ def main(tag, rep, launches):
     if os.path.exists(tp):
         j = json.load(open(tp))
     j["wan14b"] = {"round": tag, "fused_attn_kernel_bytes": traffic.get("fused_attn_kernel"),
-                   "per_kernel_bytes": traffic}
+                   "per_kernel_bytes": traffic,
+                   "source": ("not measured in this run: dram__bytes_read.sum + dram__bytes_write.sum of "
+                              f"fused_attn_kernel from the {tag} ncu --set full capture "
+                              f"(profiles/{tag}_ncu_summary.md), default gaussian Wan2.1-14B workload")}
     json.dump(j, open(tp, "w"), indent=1)
     print("\n".join(lines))
 
