@@ -315,8 +315,10 @@ __global__ void __launch_bounds__(kPThreads, 1)
         }
         for (int s = 0; s < 2; ++s) {
             mbar_init(&acc_full[s], 1);
-            mbar_init(&stats_full[s], 4);
-            mbar_init(&acc_empty[s], 4);
+            // every thread arrives (its own shared-memory stores / loads are
+            // ordered by its own release), 4 warps each side
+            mbar_init(&stats_full[s], 128);
+            mbar_init(&acc_empty[s], 128);
         }
         fence_mbar_init();
         tma_prefetch(&tmQ);
@@ -487,8 +489,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
                     a.vhat_bf[ob] = __float2bfloat16_rn(0.f);
                 }
             }
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&stats_full[buf]);  // (release: mbarrier arrive orders the smem stores)
+            mbar_arrive(&stats_full[buf]);  // release: orders this thread's k_bar / v_hat stores
         }
     } else {
         // Epilogue warps 6..9: H partial of chunk ci from TMEM buffer ci & 1,
@@ -527,8 +528,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
                 }
             }
             tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&acc_empty[buf]);
+            mbar_arrive(&acc_empty[buf]);  // release: this thread's reads of the chunk are done
         }
     }
     tc_fence_before();
