@@ -160,13 +160,10 @@ __device__ __forceinline__ void mma_wait(uint64_t* bar, uint32_t parity) {
 constexpr int kMmaWarp = PISA_MMA_WARP;
 constexpr int kVWarp1 = PISA_MMA_WARP == 1 ? 3 : 1;
 static_assert(PISA_MMA_WARP == 1 || PISA_MMA_WARP == 3, "MMA warp");
-// PISA_S_PREFETCH 1: the softmax loads the next super-tile's S early (Phase 1).
-// Off: measured slower (24.0 vs 22.9 ms gaussian, 18.4 vs 16.9 ms clustered at
-// Wan2.1-14B, profiles/r02_k3_variants.log batch ag) -- the poll and loads sit
-// in front of the publish of P_g, which the MMA warp is waiting for.
-#ifndef PISA_S_PREFETCH
-#define PISA_S_PREFETCH 0
-#endif
+// (An S prefetch -- the next super-tile's TMEM loads issued before P_g is
+// published -- measured slower: 24.0 vs 22.9 ms gaussian, batch ag; and 16
+// softmax warps, two per row set with 16 columns per thread, measured slower
+// too: 23.2-23.6 vs 22.2 ms gaussian, 17.6 vs 16.2 ms clustered, batch bb.)
 // PISA_SPEC_MAX 1: single-pass softmax (see Phase 1)
 #ifndef PISA_SPEC_MAX
 #define PISA_SPEC_MAX 1
@@ -678,10 +675,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t kZero16[16] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
 
         // ---- Phase 1: exact blocks of the union, two per super-tile
-        // (PISA_S_PREFETCH builds: when super-tile g+1's S is already complete
-        // at the end of g, its TMEM loads are issued before P_g is published)
         uint32_t r0[32], r1[32];  // scores of the used sub-tiles (raw bits)
-        bool pre = false;         // r0 / r1 already hold (in-flight loads of) super-tile g
         for (int g = 0; g < G1; ++g) {
             uint32_t e0, e1;
             pair_of(g, e0, e1);  // pad: use flags 0
@@ -689,13 +683,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int nv0 = (int(e0 & 0x3FFFu) == a.N - 1) ? n_last : 64;
             const int nv1 = (int(e1 & 0x3FFFu) == a.N - 1) ? n_last : 64;
             const uint32_t sc = lbase + kColS + sb * 128;
-            if (!pre) {
-                softmax_wait(&bar.s_full[sb], phs);
-                tc_fence_after();
-                if (use0) tmem_ld16x2_32<32>(sc, r0);
-                if (use1) tmem_ld16x2_32<32>(sc + 64, r1);
-            }
-            pre = false;
+            softmax_wait(&bar.s_full[sb], phs);
+            tc_fence_after();
+            if (use0) tmem_ld16x2_32<32>(sc, r0);
+            if (use1) tmem_ld16x2_32<32>(sc + 64, r1);
             if (q4 == 0) TRACE(4 + hh, g);
             if (use0 || use1) {
                 // scores as raw bits, masked in place (only the ragged last key
@@ -776,30 +767,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                 publish_half();
                 tmem_st16x2_16<16>(sc + 64, kZero16);
             }
-#if PISA_S_PREFETCH
-            if (g + 1 < G1) {
-                const int nsb = sb + 1 == kSB ? 0 : sb + 1;
-                const uint32_t nph = sb + 1 == kSB ? (phs ^ 1u) : phs;
-                uint32_t f0, f1;
-                pair_of(g + 1, f0, f1);
-                const bool n0 = (f0 >> (14 + hh)) & 1u, n1 = (f1 >> (14 + hh)) & 1u;
-                const uint32_t ok = (n0 || n1) && lane == 0 && mbar_try_wait_spin(smem_u32(&bar.s_full[nsb]), nph);
-                if (__shfl_sync(0xffffffffu, ok, 0)) {  // warp-uniform
-                    tc_fence_after();
-                    const uint32_t nsc = lbase + kColS + nsb * 128;
-                    if (n0) tmem_ld16x2_32<32>(nsc, r0);
-                    if (n1) tmem_ld16x2_32<32>(nsc + 64, r1);
-                    pre = true;
-                }
-            }
-#endif
             publish_p(g);
             advance();
             if (q4 == 0) TRACE(6 + hh, g);
-        }
-        if (pre) {  // (never: the last Phase-1 super-tile prefetches nothing)
-            tmem_ld_wait(r0);
-            tmem_ld_wait(r1);
         }
         // ---- Phase 2: centroid chunks, two per super-tile; column mask = own
         // selection, weight n_j (the ragged last block weighs n_last)
