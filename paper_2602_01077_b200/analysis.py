@@ -152,6 +152,42 @@ def theorem1_check(q, k, v, selected: torch.Tensor, B: int = 64, scale: float = 
                        max_slack_ratio=slack, **out)
 
 
+def pisa_fp64(q, k, v, selected: torch.Tensor, variant: str = "hybrid", B: int = 64, scale: float = 0.0,
+              row_chunk: int = 512) -> torch.Tensor:
+    """fp64 piecewise attention of one head (pisa_reference, engine.hpp:103-223)
+    for SparseOnly / Zeroth / Hybrid on the given plan: the exact softmax over
+    the selected key blocks, the zeroth-order centroid tail with weight B per
+    unselected block, and (Hybrid) the global first-order term
+    scale * ell_tail * (q . H_bar). q/k/v [L][d], L % B == 0; [L][d] fp64."""
+    q, k, v = q.double(), k.double(), v.double()
+    L, d = q.shape
+    N = L // B
+    scale = scale if scale > 0 else 1.0 / math.sqrt(d)
+    kbar, vhat, _, hbar, _ = _block_stats64(k, v, B)
+    sel = torch.zeros((N, N), dtype=torch.bool, device=q.device)
+    sel.scatter_(1, selected.long().to(q.device), True)
+    out = torch.empty((L, d), dtype=torch.float64, device=q.device)
+    for r0 in range(0, L, row_chunk):
+        r1 = min(L, r0 + row_chunk)
+        qr = q[r0:r1]
+        insel = sel[torch.arange(r0, r1, device=q.device) // B]
+        s = (scale * (qr @ k.T)).view(r1 - r0, N, B)
+        s = torch.where(insel[:, :, None], s, torch.full_like(s, -math.inf))
+        cent = scale * (qr @ kbar.T)
+        cent = torch.where(insel, torch.full_like(cent, -math.inf), cent)
+        if variant == "sparse_only":
+            cent = torch.full_like(cent, -math.inf)
+        mrow = torch.maximum(s.amax((1, 2)), cent.amax(1))
+        pe = torch.exp(s - mrow[:, None, None]).view(r1 - r0, L)
+        a = torch.exp(cent - mrow[:, None])
+        num = pe @ v + a @ vhat
+        den = pe.sum(1) + B * a.sum(1)
+        if variant == "hybrid":
+            num = num + (scale * a.sum(1))[:, None] * (qr @ hbar)
+        out[r0:r1] = num / den[:, None]
+    return out
+
+
 def jensen_check(q, k, selected: torch.Tensor, B: int = 64, scale: float = 0.0,
                  row_chunk: int = 512) -> int:
     """jensen_check (analysis.hpp:170-207): violation count (0 when correct)."""

@@ -1,11 +1,12 @@
 """Command-line harness of the GPU path, mirroring the reference CLI
-(tools/pisa_cli.cpp: gen / run / sweep / bench) so its parity and benchmark
-workflows run unchanged against the sm_100a kernels.
+(tools/pisa_cli.cpp: gen / run / sweep / bench / verify) so its parity,
+benchmark and invariant workflows run unchanged against the sm_100a kernels.
 
     python -m paper_2602_01077_b200.cli gen   --kind clustered --len 4096 --out x.pqkv
     python -m paper_2602_01077_b200.cli run   --in x.pqkv --sparsity 0.875
     python -m paper_2602_01077_b200.cli sweep --lengths 2048,4096 --sparsities 0.5,0.875
     python -m paper_2602_01077_b200.cli bench --len 75600 --heads 40 --dim 128
+    python -m paper_2602_01077_b200.cli verify [--only theorem1] [--seeds 5]
 
 Same options and JSON / CSV keys as the reference (pisa_cli.cpp:27-125,
 :222-262, :268-290, :703-767) and the same exit codes (:844-851): 0 ok,
@@ -314,6 +315,170 @@ def _run_opts(p, sparsity=True):
     p.add_argument("--ragged", action="store_true", help="allow L % block != 0 (GPU-path extension)")
 
 
+# ----------------------------------------------------------------- verify --
+# The reference's invariant suite (cmd_verify, pisa_cli.cpp:668-693) on the GPU
+# path: the same checks, at the GPU path's shapes (block 64, d 64 / 128; the
+# reference runs them at block 16, d 16-32) and with the bf16 tolerance of
+# north_star (max-abs <= 2e-2, cosine >= 0.999) where it compares against a
+# dense or fp64 computation. "cancellation" (a BlockFirst property) has no
+# GPU-path counterpart: BlockFirst is not on the GPU path.
+VERIFY_ATOL, VERIFY_COS = 2e-2, 0.999
+
+
+def _close(got: torch.Tensor, ref: torch.Tensor):
+    g, r = got.double().flatten(), ref.double().flatten()
+    err = float((g - r).abs().max().item())
+    cos = float((g @ r / (g.norm() * r.norm())).item())
+    return err, cos
+
+
+def _dense_fp32(q, k, v, scale):
+    s = scale * (q.float() @ k.float().transpose(-1, -2))
+    return torch.softmax(s, -1) @ v.float()
+
+
+def _verify_inputs(kind: str, seed: int, L: int, d: int):
+    from .generate import gen_clustered, gen_gaussian
+    gen = gen_clustered if kind == "clustered" else gen_gaussian
+    return tuple(x.cuda() for x in gen(seed, 1, L, d))
+
+
+def check_oracle_equivalence(seeds: int):
+    from .analysis import pisa_fp64
+    worst_err, worst_cos = 0.0, 1.0
+    for s in range(seeds):
+        for d in (64, 128):
+            q, k, v = _verify_inputs("clustered", s, 1024, d)
+            for name, var in (("sparse_only", P.PisaVariant.SparseOnly), ("zeroth", P.PisaVariant.Zeroth),
+                              ("hybrid", P.PisaVariant.Hybrid)):
+                o, ex = P.fwd(q[None], k[None], v[None], sparsity=0.75, variant=var, out_dtype=torch.float32,
+                              return_plan=True)
+                ref = pisa_fp64(q[0], k[0], v[0], ex["selected"][0, 0], name)
+                err, cos = _close(o[0, 0], ref)
+                worst_err, worst_cos = max(worst_err, err), min(worst_cos, cos)
+    return ("oracle_equivalence", worst_err <= VERIFY_ATOL and worst_cos >= VERIFY_COS,
+            f"max_abs={worst_err:.3e} min_cos={worst_cos:.7f} vs fp64 piecewise attention on the GPU plan")
+
+
+def check_full_coverage(seeds: int):
+    worst = 0.0
+    for s in range(seeds):
+        q, k, v = _verify_inputs("gaussian", s, 512, 64)
+        dense = _dense_fp32(q[0], k[0], v[0], 64 ** -0.5)
+        for var in (P.PisaVariant.SparseOnly, P.PisaVariant.Zeroth, P.PisaVariant.Hybrid,
+                    P.PisaVariant.GlobalCentroid):
+            o = P.fwd(q[None], k[None], v[None], sparsity=0.0, variant=var, out_dtype=torch.float32)
+            worst = max(worst, _close(o[0, 0], dense)[0])
+    return ("full_coverage", worst <= VERIFY_ATOL, f"max_abs={worst:.3e}")
+
+
+def check_constant_key(seeds: int):
+    worst = 0.0
+    L, d, B = 1024, 64, 64
+    for s in range(seeds):
+        q, _, v = _verify_inputs("gaussian", s, L, d)
+        g = torch.Generator().manual_seed(s + 7777)
+        kb = torch.randn((L // B, d), generator=g).to(torch.bfloat16).cuda()
+        k = kb.repeat_interleave(B, 0)[None]
+        dense = _dense_fp32(q[0], k[0], v[0], d ** -0.5)
+        for var in (P.PisaVariant.Zeroth, P.PisaVariant.Hybrid):
+            o = P.fwd(q[None], k[None], v[None], sparsity=0.75, variant=var, out_dtype=torch.float32)
+            worst = max(worst, _close(o[0, 0], dense)[0])
+    return ("constant_key_exactness", worst <= VERIFY_ATOL, f"max_abs={worst:.3e}")
+
+
+def _normalized(seed: int, L: int, d: int):
+    q, k, v = _verify_inputs("clustered", seed, L, d)
+    q = (q.double() / q.double().norm(dim=-1, keepdim=True)).to(torch.bfloat16)
+    k = (k.double() / k.double().norm(dim=-1, keepdim=True)).to(torch.bfloat16)
+    return q, k, v
+
+
+def check_theorem1(seeds: int):
+    from .analysis import theorem1_check
+    viol, slack = 0, 0.0
+    for s in range(seeds):
+        q, k, v = _normalized(s, 1024, 64)
+        _, ex = P.fwd(q[None], k[None], v[None], sparsity=0.875, return_plan=True)
+        rep = theorem1_check(q[0], k[0], v[0], ex["selected"][0, 0])
+        viol += rep.violations
+        slack = max(slack, rep.max_slack_ratio)
+    return ("theorem1", viol == 0, f"violations={viol} max_slack_ratio={slack:.4g} seeds={seeds}")
+
+
+def check_jensen(seeds: int):
+    from .analysis import jensen_check
+    viol = 0
+    for s in range(seeds):
+        q, k, v = _normalized(s, 1024, 64)
+        _, ex = P.fwd(q[None], k[None], v[None], sparsity=0.875, return_plan=True)
+        viol += jensen_check(q[0], k[0], ex["selected"][0, 0])
+    return ("jensen", viol == 0, f"violations={viol} seeds={seeds}")
+
+
+def check_streaming(seeds: int):
+    worst = 0.0
+    for s in range(seeds):
+        q, k, v = _verify_inputs("clustered", s, 1024, 64)
+        st = P.compute_prepare(q, k, v)
+        plan = P.select_topk_plain(st.q_bar, st.k_bar, 4, 64 ** -0.5)
+        ref, _ = P.pisa_reference(q, k, v, plan, st, P.PisaVariant.Hybrid, out_dtype=torch.float32)
+        stream, _ = P.pisa_streaming(q, k, v, plan, st, out_dtype=torch.float32)
+        worst = max(worst, _close(stream, ref)[0])
+    return ("streaming_equivalence", worst <= 1e-6, f"max_abs={worst:.3e}")
+
+
+def check_router_properties():
+    ok, notes = True, []
+    q, k, v = _verify_inputs("clustered", 3, 1024, 64)
+    st = P.compute_prepare(q, k, v)
+    m = P.block_norms(q, k, v)
+    scale = 0.25
+    base = P.select_topk_covariance(st.q_bar, st.k_bar, m, 1e-6, 4, scale)
+    scaled = P.select_topk_covariance(st.q_bar, st.k_bar, m * 37.5, 37.5e-6, 4, scale)
+    if not torch.equal(base, scaled):
+        ok = False
+        notes.append("joint-(M,eps)-scaling changed the plan")
+    zq = torch.zeros((1, 8, 64), device="cuda")  # (square: the GPU select scores N x N blocks)
+    zk = torch.zeros((1, 8, 64), device="cuda")
+    tie = P.select_topk_plain(zq, zk, 3, scale)
+    if not bool((tie == torch.tensor([0, 1, 2], device="cuda", dtype=tie.dtype)).all()):
+        ok = False
+        notes.append("tie-break mismatch")
+    plain = P.select_topk_plain(st.q_bar, st.k_bar, 4, scale)
+    cov_const = P.select_topk_covariance(st.q_bar, st.k_bar, torch.full_like(m, 2.0), 1e-6, 4, scale)
+    if not torch.equal(plain, cov_const):
+        ok = False
+        notes.append("constant-M covariance plan differs from plain")
+    return ("router_properties", ok, "; ".join(notes) if notes else "all router invariants hold")
+
+
+VERIFY_CHECKS = ("oracle_equivalence", "full_coverage", "constant_key_exactness", "theorem1", "jensen",
+                 "streaming_equivalence", "router_properties")
+
+
+def cmd_verify(args) -> int:
+    """cmd_verify (pisa_cli.cpp:668-693): each check prints pass / FAIL and a
+    detail; exit 0 when all pass, 1 on a failure, 2 for an unknown check."""
+    if args.only and args.only not in VERIFY_CHECKS:
+        sys.stderr.write(f"unknown check: {args.only}\n")
+        return 2
+    run = {"oracle_equivalence": lambda: check_oracle_equivalence(min(args.seeds, 3)),
+           "full_coverage": lambda: check_full_coverage(min(args.seeds, 5)),
+           "constant_key_exactness": lambda: check_constant_key(min(args.seeds, 5)),
+           "theorem1": lambda: check_theorem1(args.seeds),
+           "jensen": lambda: check_jensen(min(args.seeds, 20)),
+           "streaming_equivalence": lambda: check_streaming(min(args.seeds, 5)),
+           "router_properties": check_router_properties}
+    results = [run[n]() for n in VERIFY_CHECKS if not args.only or args.only == n]
+    ok = True
+    for name, passed, detail in results:
+        print(f"{'pass  ' if passed else 'FAIL  '}{name}  ({detail})")
+        ok = ok and passed
+    print("verify: all checks passed" if ok else "verify: FAILURES")
+    return 0 if ok else 1
+
+
 def main(argv: List[str] | None = None) -> int:
     ap = argparse.ArgumentParser(prog="pisa-b200", description=__doc__.split("\n")[0])
     sub = ap.add_subparsers(dest="cmd", required=True)
@@ -339,6 +504,9 @@ def main(argv: List[str] | None = None) -> int:
     _gen_opts(b)
     _run_opts(b)
     b.add_argument("--reps", type=int, default=5)
+    vf = sub.add_parser("verify", help="Invariant suite on the GPU path")
+    vf.add_argument("--only", default="", help="run one check (" + ", ".join(VERIFY_CHECKS) + ")")
+    vf.add_argument("--seeds", type=int, default=5)
     try:
         args = ap.parse_args(argv)
     except SystemExit as e:
@@ -348,7 +516,8 @@ def main(argv: List[str] | None = None) -> int:
             for v in ([args.variant] if args.cmd != "sweep" else args.variants):
                 if v not in VARIANTS:
                     raise P.InvalidDimension(f"InvalidDimension: unknown variant {v}")
-        return {"gen": cmd_gen, "run": cmd_run, "sweep": cmd_sweep, "bench": cmd_bench}[args.cmd](args)
+        return {"gen": cmd_gen, "run": cmd_run, "sweep": cmd_sweep, "bench": cmd_bench,
+                "verify": cmd_verify}[args.cmd](args)
     except P.Error as e:  # exit codes of pisa_cli.cpp:844-851
         sys.stderr.write(f"error: {e}\n")
         return {P.ErrorKind.Validation: 2, P.ErrorKind.Io: 3, P.ErrorKind.Invariant: 1}[e.kind]

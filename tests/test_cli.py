@@ -145,3 +145,23 @@ def test_cli_gen_run_sweep_bench(tmp_path, capsys):
                      "--sparsity", "0.875"]) == 0
     b = json.loads(capsys.readouterr().out)
     assert b["hybrid_ms"] > 0 and b["speedup"] > 0
+
+
+def test_verify_unknown_check_exit_code():
+    """cmd_verify (pisa_cli.cpp:668-693): an unknown --only is exit code 2."""
+    from paper_2602_01077_b200 import cli
+    assert cli.main(["verify", "--only", "no_such_check"]) == 2
+
+
+@pytest.mark.gpu
+def test_verify_all_checks_pass(capsys):
+    """The reference's invariant suite on the GPU path (cmd_verify): oracle
+    equivalence vs fp64 piecewise attention, full coverage == dense, constant-key
+    exactness, Theorem 1 and Jensen bounds on the GPU plans, streaming ==
+    reference, router properties."""
+    from paper_2602_01077_b200 import cli
+    rc = cli.main(["verify", "--seeds", "2"])
+    out = capsys.readouterr().out
+    assert rc == 0, out
+    for name in cli.VERIFY_CHECKS:
+        assert f"pass  {name}" in out
