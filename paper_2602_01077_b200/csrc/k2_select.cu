@@ -180,6 +180,12 @@ __global__ void __launch_bounds__(kScoreThreads, 1) score_kernel(const float* __
 // top), then a ballot compaction in ascending index order takes every key above
 // it plus the lowest-index ties: topk_ascending semantics (router.hpp:96-108).
 constexpr int kRowsPerCta = 4;
+#ifndef PISA_TOPK_MATCH
+#define PISA_TOPK_MATCH 0  // 1: match_any-aggregated counts on the top digit, 2: on every digit
+#endif
+#ifndef PISA_TOPK_LOAD_BATCH
+#define PISA_TOPK_LOAD_BATCH 0  // > 0: row load with this many independent loads per lane
+#endif
 
 // One query block's top-k from its N order keys in shared memory (kr), one
 // warp: radix-select the k-th largest key (8-bit digits from the top, hw = 256
@@ -195,10 +201,27 @@ __device__ __forceinline__ void select_row(const uint32_t* kr, uint32_t* hw, int
     for (int shift = 24; shift >= 0; shift -= 8) {
         for (int b = lane; b < 256; b += 32) hw[b] = 0;
         __syncwarp();
+#if PISA_TOPK_MATCH
+        // lanes with the same digit add once (the top digits of a row's keys
+        // are mostly equal: 32-way conflicts on one counter otherwise)
+        for (int j0 = 0; j0 < N; j0 += 32) {
+            const int j = j0 + lane;
+            const uint32_t key = j < N ? kr[j] : 0u;
+            const bool in = j < N && (key & pmask) == prefix;
+            if (PISA_TOPK_MATCH == 1 && shift != 24) {
+                if (in) atomicAdd(&hw[(key >> shift) & 255u], 1u);
+                continue;
+            }
+            const uint32_t d = in ? (key >> shift) & 255u : 256u + uint32_t(lane);
+            const uint32_t peers = __match_any_sync(0xffffffffu, d);
+            if (in && __ffs(peers) - 1 == lane) atomicAdd(&hw[d], uint32_t(__popc(peers)));
+        }
+#else
         for (int j = lane; j < N; j += 32) {
             const uint32_t key = kr[j];
             if ((key & pmask) == prefix) atomicAdd(&hw[(key >> shift) & 255u], 1u);
         }
+#endif
         __syncwarp();
         // lane l owns digits [255 - 8l - 7, 255 - 8l], scanned from the top
         int cnt[8], tot = 0;
@@ -292,7 +315,26 @@ __global__ void __launch_bounds__(kRowsPerCta * 32) topk_kernel(const uint32_t* 
     uint32_t* hw = kr + N;
     if (i >= N) return;
     const uint32_t* src = keys + (size_t(bh) * N + i) * N;
+#if PISA_TOPK_LOAD_BATCH
+    // kBatch independent loads in flight per lane (the row is ~N / 32 loads
+    // per lane; one at a time each waits a full L2 / HBM latency)
+    constexpr int kBatch = PISA_TOPK_LOAD_BATCH;
+    for (int j0 = 0; j0 < N; j0 += 32 * kBatch) {
+        uint32_t v[kBatch];
+#pragma unroll
+        for (int t = 0; t < kBatch; ++t) {
+            const int j = j0 + t * 32 + lane;
+            v[t] = j < N ? __ldcs(src + j) : 0u;
+        }
+#pragma unroll
+        for (int t = 0; t < kBatch; ++t) {
+            const int j = j0 + t * 32 + lane;
+            if (j < N) kr[j] = v[t];
+        }
+    }
+#else
     for (int j = lane; j < N; j += 32) kr[j] = src[j];
+#endif
     __syncwarp();
     select_row(kr, hw, N, a.k, i, a.force_diagonal != 0,
                a.selected ? a.selected + (size_t(bh) * N + i) * a.k : nullptr,
@@ -322,6 +364,8 @@ struct FusedSelCfg {
     static constexpr int kStage = 3 * kPart;     // hi | mid | lo
     static constexpr int kSmem = 1024 + 2 * kStage + 256;
     static constexpr int kAcol = D / 2;          // TMEM columns per A part
+    static constexpr int kOffT = 2 * kStage + 256;               // score-only: 4 x [32][33] u32 transposes
+    static constexpr int kSmemScore = 1024 + kOffT + 4 * 32 * 33 * 4;
 };
 
 __device__ __forceinline__ uint32_t smid() {
@@ -330,7 +374,12 @@ __device__ __forceinline__ uint32_t smid() {
     return r;
 }
 
-template <int D>
+// kScoreOnly: the same pipelined scoring, but the keys go to the row-major
+// [BH][N][N] array of the two-kernel path (each epilogue warp transposes its
+// 32 x 32 block in shared memory so every row leaves as 128-byte warp stores)
+// and topk_kernel selects afterwards at full occupancy: score_kernel's
+// operands without its one-CTA-per-tile load -> MMA -> store serialisation.
+template <int D, bool kScoreOnly = false>
 __global__ void __launch_bounds__(kFThreads, 1)
     select_fused_kernel(const __grid_constant__ CUtensorMap tmKs, SelectArgs a, uint32_t* __restrict__ scratch,
                         int BH) {
@@ -348,7 +397,7 @@ __global__ void __launch_bounds__(kFThreads, 1)
     const int i0 = blockIdx.x * 128;
     const int bh = blockIdx.y;
     const int nt = (N + 127) / 128;
-    const uint32_t sm = smid();
+    const uint32_t sm = kScoreOnly ? 0u : smid();
     if (sm >= uint32_t(kScratchSlots)) __trap();  // the scratch has one slot per SM id
     uint32_t* ks = scratch + size_t(sm) * 128 * N;  // [key][row], this SM's slot
 
@@ -454,13 +503,31 @@ __global__ void __launch_bounds__(kFThreads, 1)
                 tmem_ld32(acc + cc, v);
                 tmem_ld_wait(v);
                 const int j0 = t * 128 + cc;
+                if constexpr (kScoreOnly) {
+                    uint32_t* T = reinterpret_cast<uint32_t*>(smem + Cfg::kOffT) + q4 * 32 * 33;
 #pragma unroll
-                for (int e = 0; e < 32; ++e) {
-                    const int j = j0 + e;
-                    if (j < N) {
+                    for (int e = 0; e < 32; ++e) {
                         float x = a.scale * __uint_as_float(v[e]);
-                        if (rc) x += rc[j];
-                        ks[size_t(j) * 128 + r] = order_key(x);
+                        if (rc && j0 + e < N) x += rc[j0 + e];
+                        T[lane * 33 + e] = order_key(x);
+                    }
+                    __syncwarp();
+                    const int rb = i0 + q4 * 32, nr = min(32, N - rb);
+                    if (j0 + lane < N) {
+                        uint32_t* dst = scratch + (size_t(bh) * N + rb) * N + j0 + lane;
+#pragma unroll 4
+                        for (int rr = 0; rr < nr; ++rr) dst[size_t(rr) * N] = T[rr * 33 + lane];
+                    }
+                    __syncwarp();
+                } else {
+#pragma unroll
+                    for (int e = 0; e < 32; ++e) {
+                        const int j = j0 + e;
+                        if (j < N) {
+                            float x = a.scale * __uint_as_float(v[e]);
+                            if (rc) x += rc[j];
+                            ks[size_t(j) * 128 + r] = order_key(x);
+                        }
                     }
                 }
             }
@@ -472,6 +539,10 @@ __global__ void __launch_bounds__(kFThreads, 1)
     tc_fence_before();
     __syncthreads();  // every key of the CTA's rows is in the scratch (block-scope ordering)
     tc_fence_after();
+    if constexpr (kScoreOnly) {
+        if (warp == 1) tmem_dealloc(tmem, 512);
+        return;
+    }
     // top-k of rows [i0, i0 + nrows): RB rows per round, transposed into smem
     // (coalesced 128-byte reads of the [key][row] scratch), one warp per row
     const int nrows = min(128, N - i0);
@@ -525,6 +596,26 @@ cudaError_t launch_select(int D, const SelectArgs& a, int BH, uint32_t* keys, cu
     } else {
         cudaFuncSetAttribute(score_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, ScoreCfg<64>::kSmem);
         score_kernel<64><<<g1, kScoreThreads, ScoreCfg<64>::kSmem, s>>>(a.qbar, a.kbar, a.rect, keys, a.N, a.scale);
+    }
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    const size_t smem = sizeof(uint32_t) * size_t(kRowsPerCta) * (a.N + 256);
+    cudaFuncSetAttribute(topk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    topk_kernel<<<dim3((a.N + kRowsPerCta - 1) / kRowsPerCta, BH), kRowsPerCta * 32, smem, s>>>(keys, a);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_select_stream(int D, const CUtensorMap& tmKs, const SelectArgs& a, int BH, uint32_t* keys,
+                                 cudaStream_t s) {
+    dim3 grid((a.N + 127) / 128, BH);
+    if (D == 128) {
+        auto k = select_fused_kernel<128, true>;
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, FusedSelCfg<128>::kSmemScore);
+        k<<<grid, kFThreads, FusedSelCfg<128>::kSmemScore, s>>>(tmKs, a, keys, BH);
+    } else {
+        auto k = select_fused_kernel<64, true>;
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, FusedSelCfg<64>::kSmemScore);
+        k<<<grid, kFThreads, FusedSelCfg<64>::kSmemScore, s>>>(tmKs, a, keys, BH);
     }
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;

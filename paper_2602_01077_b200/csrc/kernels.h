@@ -86,6 +86,10 @@ constexpr int kSelectFusedMinN = 512;
 constexpr int kScratchSlots = 256;  // scratch rows: kScratchSlots x 128 x N uint32 (one slot per SM id)
 cudaError_t launch_select_fused(int D, const CUtensorMap& tmKs, const SelectArgs& a, int BH, uint32_t* keys,
                                 cudaStream_t s);
+// K2 streamed (N >= kSelectFusedMinN): the fused kernel's pipelined scoring
+// writing the [BH][N][N] keys, then topk_kernel. keys: scratch uint32 [BH][N][N].
+cudaError_t launch_select_stream(int D, const CUtensorMap& tmKs, const SelectArgs& a, int BH, uint32_t* keys,
+                                 cudaStream_t s);
 
 // K2c/K2d: overlap-aware pairing of query blocks for the fused kernel.
 // cand: scratch int [BH][N][kPairCand]; pairs: int2 [BH][ceil(N/2)].

@@ -183,15 +183,22 @@ bool make_3d_map(CUtensorMap* m, const void* base, uint64_t D, uint64_t rows, ui
     return make_map(m, base, 3, dims, strides, box);
 }
 
-// The one-launch select is opt-in (env PISA_B200_FUSED_SELECT=1): measured
-// 1.32 ms against 0.56 ms for score_kernel + topk_kernel at Wan2.1-14B
-// (profiles/r02c_ab_select.log): its 400 CTAs leave 2.7 waves on 148 SMs and
-// each selects 128 rows with 8 warps, where topk_kernel spreads one row per
-// warp over the whole chip.
-// (read per call, so a test can switch it)
-bool fused_select_off() {
+// Select path when K1 emitted the k_bar splits (N >= kSelectFusedMinN), env
+// PISA_B200_FUSED_SELECT (read per call, so a test can switch it):
+//   unset / other  streamed scoring (select_fused_kernel<D, true>: q_bar split
+//                  in TMEM, k_bar splits by TMA, double-buffered accumulators,
+//                  row-major keys) + topk_kernel;
+//   1              the one-launch select (top-k in the scoring CTA): 1.32 ms
+//                  against 0.56 ms at Wan2.1-14B (profiles/r02c_ab_select.log):
+//                  its 400 CTAs select 128 rows each with 8 warps, where
+//                  topk_kernel spreads one row per warp over the whole chip;
+//   0              score_kernel (one CTA per 128 x 128 tile) + topk_kernel.
+enum SelectMode { kSelectTiles = 0, kSelectOneLaunch = 1, kSelectStream = 2 };
+SelectMode select_mode() {
     const char* e = std::getenv("PISA_B200_FUSED_SELECT");
-    return !(e && e[0] == '1');
+    if (e && e[0] == '1') return kSelectOneLaunch;
+    if (e && e[0] == '0') return kSelectTiles;
+    return kSelectStream;
 }
 
 // heads per two-kernel select chunk (env PISA_B200_SELECT_CHUNK_MB: key
@@ -458,14 +465,16 @@ pisa_status run_select(pisa_ctx* ctx, const pisa_attn_desc& d, const Plan& p, co
                        uint32_t* keys, cudaStream_t s, const __nv_bfloat16* ksplit = nullptr) {
     SelectArgs a{qbar, kbar, rect, selected, mask, int(p.N), int(p.W), int(p.k), d.force_diagonal,
                  float(p.scale)};
-    if (ksplit && !fused_select_off()) {
+    const SelectMode mode = select_mode();
+    if (ksplit && mode != kSelectTiles && (mode == kSelectOneLaunch || select_chunk_heads(p.N, p.BH) >= p.BH)) {
         CUtensorMap tks;
         if (!make_3d_map(&tks, ksplit, p.D, p.N, 3 * p.BH, 128))
             return fail(ctx, PISA_ERR_CUDA, "TMA descriptor creation failed (k_bar split)");
         ProfScope ps(ctx, kK2, s);
-        const cudaError_t e = launch_select_fused(int(p.D), tks, a, int(p.BH), keys, s);
+        const cudaError_t e = mode == kSelectOneLaunch ? launch_select_fused(int(p.D), tks, a, int(p.BH), keys, s)
+                                                       : launch_select_stream(int(p.D), tks, a, int(p.BH), keys, s);
         if (e != cudaSuccess) return cuda_fail(ctx, e, "select launch");
-        ctx->launches += 1;
+        ctx->launches += mode == kSelectOneLaunch ? 1 : 2;
         return PISA_OK;
     }
     // (optionally) heads in chunks whose N x N key matrix (u32) stays

@@ -121,16 +121,22 @@ def test_select_index_sets_exact(P, oracle_mod, kind, L, d, r, fd):
                                               ("clustered", 3, 33000, 64, 0.75, True),
                                               ("clustered", 1, 118800, 128, 0.9, False),
                                               ("gaussian", 1, 262144, 64, 0.99, True)])
-def test_fused_select_equals_two_kernel_select(P, kind, H, L, d, r, fd, monkeypatch):
-    """With PISA_B200_FUSED_SELECT=1 (opt-in: slower than the two kernels at
-    Wan2.1-14B, profiles/r02c_ab_select.log) the forward routes from N = 512 key
-    blocks with the fused select kernel (q_bar split in TMEM, K1's k_bar splits
-    by TMA, keys in an L2 scratch, top-k in the same CTA); its plans equal the
-    two-kernel select (score_kernel + topk_kernel) on the same statistics bit
-    for bit, for the plain and the covariance router, d = 64 / 128, up to
+@pytest.mark.parametrize("mode", ["1", "stream"])
+def test_fused_select_equals_two_kernel_select(P, kind, H, L, d, r, fd, mode, monkeypatch):
+    """From N = 512 key blocks the forward scores with the pipelined select
+    kernel (q_bar split in TMEM, K1's k_bar splits by TMA, double-buffered
+    accumulators): by default ("stream") it writes the row-major keys and
+    topk_kernel selects; with PISA_B200_FUSED_SELECT=1 (opt-in one launch,
+    keys in an L2 scratch, top-k in the same CTA; slower at Wan2.1-14B,
+    profiles/r02c_ab_select.log). Either way the plans equal the tile select
+    (score_kernel + topk_kernel, the step entry's path) on the same statistics
+    bit for bit, for the plain and the covariance router, d = 64 / 128, up to
     N = 4096."""
     import torch
-    monkeypatch.setenv("PISA_B200_FUSED_SELECT", "1")
+    if mode == "1":
+        monkeypatch.setenv("PISA_B200_FUSED_SELECT", "1")
+    else:
+        monkeypatch.delenv("PISA_B200_FUSED_SELECT", raising=False)
     gen = P.gen_gaussian if kind == "gaussian" else P.gen_clustered
     q, k, v = (x.reshape(1, H, L, d).cuda() for x in gen(7, H, L, d))
     N = -(-L // 64)
