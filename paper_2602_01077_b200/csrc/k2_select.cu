@@ -2,11 +2,12 @@
 //
 // Replaces select_topk_plain (router.hpp:126-151) with topk_ascending (:96-108)
 // and force_block (:111-121), in two launches:
-//   K2a score_kernel : s_ij = scale * <q_bar_i, k_bar_j>, a register-tiled fp32
-//                      FMA GEMM per (batch, head), fixed summation order over d
-//                      (fp32 scoring keeps the index sets bit-exact
-//                      against the fp64 reference on the Wan shapes; bf16 / TF32
-//                      scoring does not), stored as order-preserving uint32 keys
+//   K2a score_kernel : s_ij = scale * <q_bar_i, k_bar_j> on tcgen05 from an exact
+//                      3-way bf16 split (fp32-accurate, deterministic; SURVEY.md
+//                      §0: fp32 scoring keeps the index sets bit-exact against
+//                      the fp64 reference on the Wan shapes, plain bf16 / TF32
+//                      does not), stored as order-preserving uint32 keys; from
+//                      N >= 512 the pipelined select_fused_kernel<D, true>
 //   K2b topk_kernel  : one warp per query block: radix select of the k-th largest
 //                      key, ties to the LOWER index, ballot compaction to the
 //                      ascending index list plus the bitmask row.
@@ -183,6 +184,9 @@ constexpr int kRowsPerCta = 4;
 #ifndef PISA_TOPK_MATCH
 #define PISA_TOPK_MATCH 0  // 1: match_any-aggregated counts on the top digit, 2: on every digit
 #endif
+#ifndef PISA_TOPK_EARLY
+#define PISA_TOPK_EARLY 1  // stop the radix once the k-th key's bin is taken whole
+#endif
 #ifndef PISA_TOPK_LOAD_BATCH
 #define PISA_TOPK_LOAD_BATCH 0  // > 0: row load with this many independent loads per lane
 #endif
@@ -257,6 +261,23 @@ __device__ __forceinline__ void select_row(const uint32_t* kr, uint32_t* hw, int
         prefix |= uint32_t(digit) << shift;
         pmask |= 255u << shift;
         __syncwarp();
+#if PISA_TOPK_EARLY
+        // the bin holds exactly the keys still wanted: all of it is taken (see
+        // select_row_reg); T = its minimum, every tie of T kept
+        const int dcnt = int(hw[digit]);  // (warp-uniform digit; counts complete since the last __syncwarp)
+        if (dcnt == rem && shift > 0) {
+            uint32_t mn = 0xffffffffu;
+            for (int j = lane; j < N; j += 32) {
+                const uint32_t key = kr[j];
+                if ((key & pmask) == prefix) mn = min(mn, key);
+            }
+            prefix = __reduce_min_sync(0xffffffffu, mn);
+            int ties = 0;
+            for (int j = lane; j < N; j += 32) ties += kr[j] == prefix;
+            rem = __reduce_add_sync(0xffffffffu, ties);
+            break;
+        }
+#endif
     }
     const uint32_t T = prefix;  // key of the k-th largest; take `rem` ties, lowest indices first
 
@@ -302,6 +323,149 @@ __device__ __forceinline__ void select_row(const uint32_t* kr, uint32_t* hw, int
         out += __popc(tb);
         ties += __popc(eqb);
     }
+}
+
+// select_row with the row's keys in registers (key j = t * 32 + lane in
+// kr[t], kPer >= ceil(N / 32)): no shared-memory round trip per element and
+// pass, and the radix stops early once the bin holding the k-th largest key
+// holds exactly the keys still wanted -- then every key of that bin is taken,
+// T is its minimum and all of T's ties are kept, which is the same index set
+// the full radix yields (topk_kernel was instruction-issue bound: 3.9K warp
+// instructions per row, profiles/r02i_topk_ncu.md).
+template <int kPer>
+__device__ __forceinline__ void select_row_reg(const uint32_t (&kr)[kPer], uint32_t* hw, int N, int kk, int i,
+                                               bool force_diagonal, int32_t* sel, uint32_t* mrow, int lane) {
+    uint32_t prefix = 0, pmask = 0;
+    int rem = kk;
+    bool whole = false;  // early exit: every key matching prefix / pmask is taken
+    for (int shift = 24; shift >= 0; shift -= 8) {
+        for (int b = lane; b < 256; b += 32) hw[b] = 0;
+        __syncwarp();
+#pragma unroll
+        for (int t = 0; t < kPer; ++t) {
+            const int j = t * 32 + lane;
+            if (j < N && (kr[t] & pmask) == prefix) atomicAdd(&hw[(kr[t] >> shift) & 255u], 1u);
+        }
+        __syncwarp();
+        int cnt[8], tot = 0;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            cnt[u] = int(hw[255 - lane * 8 - u]);
+            tot += cnt[u];
+        }
+        int incl = tot;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int v = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += v;
+        }
+        const int excl = incl - tot;
+        int digit = -1, above = 0, dcnt = 0;
+        if (rem > excl && rem <= incl) {
+            int run = excl;
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                if (digit < 0 && rem <= run + cnt[u]) {
+                    digit = 255 - lane * 8 - u;
+                    above = run;
+                    dcnt = cnt[u];
+                }
+                run += cnt[u];
+            }
+        }
+        const uint32_t owner = __ballot_sync(0xffffffffu, digit >= 0);
+        const int src_lane = __ffs(owner) - 1;
+        digit = __shfl_sync(0xffffffffu, digit, src_lane);
+        above = __shfl_sync(0xffffffffu, above, src_lane);
+        dcnt = __shfl_sync(0xffffffffu, dcnt, src_lane);
+        rem -= above;
+        prefix |= uint32_t(digit) << shift;
+        pmask |= 255u << shift;
+        __syncwarp();
+        if (dcnt == rem) {
+            whole = shift > 0;
+            break;
+        }
+    }
+    uint32_t T = prefix;  // the k-th largest key (full radix), or the bin's minimum (early exit)
+    if (whole) {
+        uint32_t mn = 0xffffffffu;
+#pragma unroll
+        for (int t = 0; t < kPer; ++t)
+            if (t * 32 + lane < N && (kr[t] & pmask) == prefix) mn = min(mn, kr[t]);
+        T = __reduce_min_sync(0xffffffffu, mn);
+        int ties = 0;
+#pragma unroll
+        for (int t = 0; t < kPer; ++t) ties += __popc(__ballot_sync(0xffffffffu, t * 32 + lane < N && kr[t] == T));
+        rem = ties;  // every tie of T is kept
+    }
+
+    const uint32_t lt_mask = (1u << lane) - 1u;
+    int swap_out = -1;
+    bool swap_in = false;
+    if (force_diagonal && i < N) {
+        int ties = 0, last_tie = -1;
+        bool diag_sel = false;
+#pragma unroll
+        for (int t = 0; t < kPer; ++t) {
+            const int j = t * 32 + lane;
+            const uint32_t key = j < N ? kr[t] : 0u;
+            const bool eq = j < N && key == T;
+            const uint32_t eqb = __ballot_sync(0xffffffffu, eq);
+            const int rank = ties + __popc(eqb & lt_mask);
+            const bool take = j < N && (key > T || (eq && rank < rem));
+            if (j == i) diag_sel = take;
+            const uint32_t tb = __ballot_sync(0xffffffffu, eq && rank < rem);
+            if (tb) last_tie = t * 32 + 31 - __clz(tb);
+            ties += __popc(eqb);
+        }
+        diag_sel = __shfl_sync(0xffffffffu, diag_sel, i & 31);
+        if (!diag_sel) {
+            swap_out = last_tie;
+            swap_in = true;
+        }
+    }
+    int ties = 0, out = 0;
+#pragma unroll
+    for (int t = 0; t < kPer; ++t) {
+        if (t * 32 >= N) break;
+        const int j = t * 32 + lane;
+        const uint32_t key = j < N ? kr[t] : 0u;
+        const bool eq = j < N && key == T;
+        const uint32_t eqb = __ballot_sync(0xffffffffu, eq);
+        const int rank = ties + __popc(eqb & lt_mask);
+        bool take = j < N && (key > T || (eq && rank < rem));
+        if (swap_in) {
+            if (j == swap_out) take = false;
+            if (j == i) take = true;
+        }
+        const uint32_t tb = __ballot_sync(0xffffffffu, take);
+        if (take && sel) sel[out + __popc(tb & lt_mask)] = j;
+        if (lane == 0) mrow[t] = tb;
+        out += __popc(tb);
+        ties += __popc(eqb);
+    }
+}
+
+template <int kPer>
+__global__ void __launch_bounds__(kRowsPerCta * 32) topk_reg_kernel(const uint32_t* __restrict__ keys,
+                                                                    SelectArgs a) {
+    __shared__ uint32_t hist[kRowsPerCta][256];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int bh = blockIdx.y;
+    const int i = blockIdx.x * kRowsPerCta + warp;
+    const int N = a.N;
+    if (i >= N) return;
+    const uint32_t* src = keys + (size_t(bh) * N + i) * N;
+    uint32_t kr[kPer];
+#pragma unroll
+    for (int t = 0; t < kPer; ++t) {
+        const int j = t * 32 + lane;
+        kr[t] = j < N ? __ldcs(src + j) : 0u;
+    }
+    select_row_reg<kPer>(kr, hist[warp], N, a.k, i, a.force_diagonal != 0,
+                         a.selected ? a.selected + (size_t(bh) * N + i) * a.k : nullptr,
+                         a.mask + (size_t(bh) * N + i) * a.W, lane);
 }
 
 __global__ void __launch_bounds__(kRowsPerCta * 32) topk_kernel(const uint32_t* __restrict__ keys,
@@ -585,6 +749,35 @@ __global__ void plan_to_mask_kernel(const int32_t* __restrict__ selected, int N,
     }
 }
 
+// K2b: the register-resident top-k up to N = 2048 key blocks, keys per lane
+// rounded up to a few buckets (Wan2.1-14B's N = 1182: 40); PISA_TOPK_REG=0:
+// always the shared-memory form
+#ifndef PISA_TOPK_REG
+#define PISA_TOPK_REG 8  // largest keys-per-lane bucket of the register form (0: never)
+#endif
+cudaError_t launch_topk(const SelectArgs& a, int BH, const uint32_t* keys, cudaStream_t s) {
+    const dim3 grid((a.N + kRowsPerCta - 1) / kRowsPerCta, BH), block(kRowsPerCta * 32);
+    const int per = (a.N + 31) / 32;
+#define PISA_TOPK_BUCKET(P)                                      \
+    if (P <= PISA_TOPK_REG && per <= P) {                             \
+        topk_reg_kernel<P><<<grid, block, 0, s>>>(keys, a);      \
+        return cudaGetLastError();                               \
+    }
+    PISA_TOPK_BUCKET(4)
+    PISA_TOPK_BUCKET(8)
+    PISA_TOPK_BUCKET(16)
+    PISA_TOPK_BUCKET(24)
+    PISA_TOPK_BUCKET(32)
+    PISA_TOPK_BUCKET(40)
+    PISA_TOPK_BUCKET(48)
+    PISA_TOPK_BUCKET(64)
+#undef PISA_TOPK_BUCKET
+    const size_t smem = sizeof(uint32_t) * size_t(kRowsPerCta) * (a.N + 256);
+    cudaFuncSetAttribute(topk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    topk_kernel<<<grid, block, smem, s>>>(keys, a);
+    return cudaGetLastError();
+}
+
 }  // namespace
 
 cudaError_t launch_select(int D, const SelectArgs& a, int BH, uint32_t* keys, cudaStream_t s) {
@@ -599,10 +792,7 @@ cudaError_t launch_select(int D, const SelectArgs& a, int BH, uint32_t* keys, cu
     }
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
-    const size_t smem = sizeof(uint32_t) * size_t(kRowsPerCta) * (a.N + 256);
-    cudaFuncSetAttribute(topk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    topk_kernel<<<dim3((a.N + kRowsPerCta - 1) / kRowsPerCta, BH), kRowsPerCta * 32, smem, s>>>(keys, a);
-    return cudaGetLastError();
+    return launch_topk(a, BH, keys, s);
 }
 
 cudaError_t launch_select_stream(int D, const CUtensorMap& tmKs, const SelectArgs& a, int BH, uint32_t* keys,
@@ -619,10 +809,7 @@ cudaError_t launch_select_stream(int D, const CUtensorMap& tmKs, const SelectArg
     }
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
-    const size_t smem = sizeof(uint32_t) * size_t(kRowsPerCta) * (a.N + 256);
-    cudaFuncSetAttribute(topk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    topk_kernel<<<dim3((a.N + kRowsPerCta - 1) / kRowsPerCta, BH), kRowsPerCta * 32, smem, s>>>(keys, a);
-    return cudaGetLastError();
+    return launch_topk(a, BH, keys, s);
 }
 
 cudaError_t launch_select_fused(int D, const CUtensorMap& tmKs, const SelectArgs& a, int BH, uint32_t* keys,

@@ -278,6 +278,29 @@ def test_select_edge_cases(P):
         sel_of([[1.0]] * 4, [[1.0]] * 4, 5)
 
 
+@pytest.mark.parametrize("N", [200, 700, 1500, 2100])
+@pytest.mark.parametrize("fd", [False, True])
+def test_select_heavy_ties(P, oracle_mod, N, fd):
+    """Integer-valued q_bar / k_bar make every score an exact small integer, so
+    rows carry long runs of equal keys: the top-k (register form up to 256 key
+    blocks, shared-memory form above, both with the radix early exit, and the
+    plain form past 2048) must equal the oracle's select_plain exactly -- ties
+    to the lower index (router.hpp:96-108), force_block (:111-121)."""
+    import torch
+    rng = np.random.default_rng(N + fd)
+    d = 64
+    qb = rng.integers(-2, 3, size=(N, d)).astype(np.float64)
+    kb = rng.integers(-1, 2, size=(N, d)).astype(np.float64)
+    kb[rng.random(N) < 0.5] = kb[0]          # half the key blocks identical: one huge tie class
+    qb[: N // 3] = 0.0                        # all-tied rows (every score 0)
+    for k in sorted({1, max(1, N // 7), N // 2, N - 1, N}):
+        ref = oracle_mod.select_plain(qb, kb, k, 1.0, force_diagonal=fd)
+        got = P.select_topk_plain(torch.tensor(qb, dtype=torch.float32).cuda()[None],
+                                  torch.tensor(kb, dtype=torch.float32).cuda()[None], k, 1.0,
+                                  force_diagonal=fd).cpu().numpy()[0]
+        assert np.array_equal(got, ref), (N, k, fd, np.where((got != ref).any(1))[0][:5])
+
+
 # ------------------------------------------------------------ fused forward --
 SHAPES = [
     ("gaussian", 2, 1024, 128, 0.75),

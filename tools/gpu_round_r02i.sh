@@ -1,3 +1,9 @@
-# round-2 batch i: K/V stage split of the fused kernel (3K+3V vs 2K+4V), both routings
-L=$PWD/paper_2602_01077_b200/lib
-timeout 1200 bash tools/ab_lib.sh $L/libpisa_b200.so $L/libpisa_b200_k2v4.so gaussian clustered > gpurun_out/ab_k3_i.log 2>&1
+# round-2 batch i: ncu --set full of topk_kernel, pair_candidates_kernel, pair_match_kernel (Wan2.1-14B)
+# and block_stats_persistent_kernel at FLUX
+set -x
+B="python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu --no-dense"
+for k in topk_kernel pair_candidates_kernel pair_match_kernel; do
+  timeout 600 ncu --set full --clock-control none --import-source on -k regex:$k -c 1 -f -o gpurun_out/r02i_$k $B > /dev/null 2>&1
+done
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:block_stats_persistent -c 1 -f -o gpurun_out/r02i_k1_flux $B --workload flux > /dev/null 2>&1
+ls -la gpurun_out/
