@@ -270,6 +270,12 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
 // stream chunk i + 1. Every chunk is computed exactly as in the one-chunk-per-
 // CTA kernel above (same block order, same reductions), so the outputs are
 // bit-identical; only which CTA computes a chunk changes.
+#ifndef PISA_K1_DIAG
+#define PISA_K1_DIAG 0
+#endif
+#ifndef PISA_K1_STG256
+#define PISA_K1_STG256 1  // H partial written with 32-byte stores (0: 16-byte)
+#endif
 constexpr int kPThreads = 320;  // warp 0 TMA, 1 MMA, 2-5 columns, 6-9 epilogue
 
 template <int D>
@@ -416,6 +422,11 @@ __global__ void __launch_bounds__(kPThreads, 1)
             for (int jl = 0; jl < nb; ++jl, ++it) {
                 const int s = it % kS;
                 mbar_wait(&full[s], (it / kS) & 1);
+#if PISA_K1_DIAG == 1  // diagnostic only (wrong statistics): the column warps release the stage at once
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&empty[s]);
+                continue;
+#endif
                 const int j = j0 + jl;
                 const int nrow = min(64, a.L - j * 64);
                 const uint8_t* st = ring + s * Cfg::kStage;
@@ -506,7 +517,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
             tc_fence_after();
             const float* kbs = kb_s + buf * kStatsG * D;
             const float* vhs = vh_s + buf * kStatsG * D;
-            if (q < D / 32) {
+            if (q < D / 32 && PISA_K1_DIAG != 2) {  // (2: diagnostic, no H partial written)
                 float* dst = a.hpart + ((size_t(bh) * a.nchunk + chunk) * D + arow) * D;
 #pragma unroll 1
                 for (int cc = 0; cc < D; cc += 32) {
@@ -521,10 +532,22 @@ __global__ void __launch_bounds__(kPThreads, 1)
 #pragma unroll
                         for (int i = 0; i < 32; ++i) acc[i] = fmaf(-ka, vhs[jl * D + cc + i], acc[i]);
                     }
+#if PISA_K1_STG256
+                    // 32-byte stores: every lane writes a whole sector of its row
+                    // (the row-per-thread TMEM layout scatters a warp's store over
+                    // 32 lines; 16-byte stores half-filled 32 sectors per instruction)
+#pragma unroll
+                    for (int i = 0; i < 32; i += 8)
+                        asm volatile("st.global.v8.f32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(dst + cc + i),
+                                     "f"(acc[i]), "f"(acc[i + 1]), "f"(acc[i + 2]), "f"(acc[i + 3]), "f"(acc[i + 4]),
+                                     "f"(acc[i + 5]), "f"(acc[i + 6]), "f"(acc[i + 7])
+                                     : "memory");
+#else
 #pragma unroll
                     for (int i = 0; i < 32; i += 4)
                         *reinterpret_cast<float4*>(dst + cc + i) =
                             make_float4(acc[i], acc[i + 1], acc[i + 2], acc[i + 3]);
+#endif
                 }
             }
             tc_fence_before();

@@ -284,12 +284,15 @@ pisa_status resolve(pisa_ctx* ctx, const pisa_attn_desc* d, Plan* p) {
     p->Npad = (N + 127) / 128 * 128;  // K3 reads 128-centroid tiles
     p->W = (N + 31) / 32;
     p->k = k;
-    // K1: up to kStatsG key blocks per CTA, fewer for short heads (FLUX's N = 72
-    // at 32 per CTA would be 3 CTAs per head). A function of N only: a head's
-    // H_bar partial sums -- and with them its output bits -- do not depend on
-    // how many other heads share the launch, so head-sharded ranks reproduce
-    // the single-GPU result exactly.
-    p->statsG = std::max<int64_t>(4, std::min<int64_t>(kStatsG, (N + 23) / 24));
+    // K1: up to kStatsG key blocks per chunk (work unit), at least ~6 chunks
+    // per head so that 24 heads still cover the 148 SMs at image sizes (FLUX's
+    // N = 72: 6 chunks of 12 -- 144 units -- measured 0.141 ms a step against
+    // 0.143 for 18 chunks of 4, profiles/r02m_ab_k1.log), and as large as
+    // that allows: every chunk writes a D x D fp32 H partial. A function of N
+    // only: a head's H_bar partial sums -- and with them its output bits -- do
+    // not depend on how many other heads share the launch, so head-sharded
+    // ranks reproduce the single-GPU result exactly.
+    p->statsG = std::max<int64_t>(4, std::min<int64_t>(kStatsG, (N + 5) / 6));
     if (const char* e = std::getenv("PISA_B200_STATS_G"))  // (A/B of K1's chunk size)
         p->statsG = std::max<int64_t>(1, std::min<int64_t>(kStatsG, std::atoll(e)));
     p->nchunk1 = (N + p->statsG - 1) / p->statsG;
