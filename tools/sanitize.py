@@ -6,7 +6,8 @@
     compute-sanitizer --tool initcheck python tools/sanitize.py --quick
 
 Covers K1 block statistics, K1c block norms (d 128 and the paired d 64
-kernel), K2a/K2b routing, K2c/K2d pairing (forced on), K3 in every variant,
+kernel), K2a/K2b routing (tile, streamed and one-launch select from N = 516),
+K2c/K2d pairing (forced on), K3 in every variant,
 ragged lengths, the query-range entry point and the chunked host path. The
 outputs are only checked for finiteness here; parity lives in tests/."""
 import os
@@ -49,6 +50,18 @@ def main():
             P.fwd(q, k, v, out, sparsity=0.75, ctx=ctx, q_blocks=(1, Nq))
             n += 1
     ctx.set_pairing(1)
+    # N >= 512 key blocks: K1's k_bar split, the streamed select (pipelined
+    # scoring + top-k) and the one-launch select (sparsity 0.98 keeps K3 short)
+    for si, d in enumerate((128, 64)):
+        q, k, v = (rnd((1, 1, 33000, d), 50 + 3 * si + i) for i in range(3))
+        for mode in ("stream", "1"):
+            if mode == "1":
+                os.environ["PISA_B200_FUSED_SELECT"] = "1"
+            for router in (P.RouterStrategy.Plain, P.RouterStrategy.CovarianceAware):
+                out = P.fwd(q, k, v, sparsity=0.98, router=router, ctx=ctx, out_dtype=torch.float32)
+                assert torch.isfinite(out).all(), (d, mode, router)
+                n += 1
+            os.environ.pop("PISA_B200_FUSED_SELECT", None)
     B, H, L, d = 1, 5, 1000, 128
     hq, hk, hv = (rnd((B, H, L, d), 100 + i).cpu().pin_memory() for i in range(3))
     ho = torch.empty((B, H, L, d), dtype=torch.bfloat16).pin_memory()
