@@ -109,29 +109,67 @@ __global__ void __launch_bounds__(256) pair_candidates_kernel(const uint32_t* __
     }
 }
 
-__global__ void __launch_bounds__(1024) pair_match_kernel(const int* __restrict__ cand, int N, int qb0,
-                                                          int qb1, int2* __restrict__ pairs) {
-    extern __shared__ int partner[];  // [N], then prop [N]
+// kSmemC: the candidate lists staged in shared memory as 16-bit indices (one
+// coalesced pass over global memory instead of a dependent L2 load per
+// candidate and round), and each block's scan resumes where the previous
+// round's stopped (a matched block stays matched, so candidates passed over
+// never become available again): the same proposals, round by round, as the
+// plain form.
+constexpr int kMatchThreads = 1024;
+constexpr int kMatchPer = 4;  // blocks per thread in the staged form (N <= 4096)
+
+template <bool kSmemC>
+__global__ void __launch_bounds__(kMatchThreads) pair_match_kernel(const int* __restrict__ cand, int N, int qb0,
+                                                                   int qb1, int2* __restrict__ pairs) {
+    extern __shared__ int partner[];  // [N], then prop [N], then (kSmemC) cs [N][kCand] int16
     int* prop = partner + N;
+    int16_t* cs = reinterpret_cast<int16_t*>(prop + N);
     __shared__ int progress;
     const int bh = blockIdx.x;
     const int* C = cand + size_t(bh) * N * kCand;
     for (int i = qb0 + threadIdx.x; i < qb1; i += blockDim.x) partner[i] = -1;
+    if constexpr (kSmemC) {
+        for (int e = qb0 * kCand + threadIdx.x; e < qb1 * kCand; e += blockDim.x) cs[e] = int16_t(__ldg(C + e));
+    }
     __syncthreads();
+    int cur[kMatchPer];  // kSmemC: first candidate of block i still worth looking at
+#pragma unroll
+    for (int u = 0; u < kMatchPer; ++u) cur[u] = 0;
     for (int round = 0; round < 64; ++round) {
         // every unmatched block proposes its best unmatched candidate
-        for (int i = qb0 + threadIdx.x; i < qb1; i += blockDim.x) {
-            int p = -1;
-            if (partner[i] < 0) {
-                for (int c = 0; c < kCand; ++c) {
-                    const int j = C[size_t(i) * kCand + c];
-                    if (j >= 0 && partner[j] < 0) {
-                        p = j;
-                        break;
+        if constexpr (kSmemC) {
+#pragma unroll
+            for (int u = 0; u < kMatchPer; ++u) {
+                const int i = qb0 + threadIdx.x + u * kMatchThreads;
+                if (i >= qb1) break;
+                int p = -1;
+                if (partner[i] < 0) {
+                    int c = cur[u];
+                    for (; c < kCand; ++c) {
+                        const int j = cs[i * kCand + c];
+                        if (j >= 0 && partner[j] < 0) {
+                            p = j;
+                            break;
+                        }
+                    }
+                    cur[u] = c;
+                }
+                prop[i] = p;
+            }
+        } else {
+            for (int i = qb0 + threadIdx.x; i < qb1; i += blockDim.x) {
+                int p = -1;
+                if (partner[i] < 0) {
+                    for (int c = 0; c < kCand; ++c) {
+                        const int j = C[size_t(i) * kCand + c];
+                        if (j >= 0 && partner[j] < 0) {
+                            p = j;
+                            break;
+                        }
                     }
                 }
+                prop[i] = p;
             }
-            prop[i] = p;
         }
         if (threadIdx.x == 0) progress = 0;
         __syncthreads();
@@ -166,6 +204,10 @@ __global__ void __launch_bounds__(1024) pair_match_kernel(const int* __restrict_
     }
 }
 
+#ifndef PISA_MATCH_SMEM
+#define PISA_MATCH_SMEM 1
+#endif
+
 }  // namespace
 
 cudaError_t launch_pairing(const uint32_t* mask, int N, int W, int qb0, int qb1, int BH, int* cand,
@@ -176,8 +218,14 @@ cudaError_t launch_pairing(const uint32_t* mask, int N, int W, int qb0, int qb1,
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     const size_t sm2 = size_t(2) * N * 4;
-    cudaFuncSetAttribute(pair_match_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm2));
-    pair_match_kernel<<<BH, 1024, sm2, s>>>(cand, N, qb0, qb1, pairs);
+    const size_t sm2c = sm2 + size_t(N) * kCand * 2;
+    if (PISA_MATCH_SMEM && N <= kMatchPer * kMatchThreads && N < 32768 && sm2c <= 200 * 1024) {
+        cudaFuncSetAttribute(pair_match_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm2c));
+        pair_match_kernel<true><<<BH, kMatchThreads, sm2c, s>>>(cand, N, qb0, qb1, pairs);
+    } else {
+        cudaFuncSetAttribute(pair_match_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm2));
+        pair_match_kernel<false><<<BH, kMatchThreads, sm2, s>>>(cand, N, qb0, qb1, pairs);
+    }
     return cudaGetLastError();
 }
 
