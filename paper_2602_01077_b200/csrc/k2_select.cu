@@ -241,7 +241,7 @@ __device__ __forceinline__ void select_row(const uint32_t* kr, uint32_t* hw, int
             if (lane >= o) incl += v;
         }
         const int excl = incl - tot;
-        int digit = -1, above = 0;
+        int digit = -1, above = 0, dcnt = 0;
         if (rem > excl && rem <= incl) {
             int run = excl;
 #pragma unroll
@@ -249,6 +249,7 @@ __device__ __forceinline__ void select_row(const uint32_t* kr, uint32_t* hw, int
                 if (digit < 0 && rem <= run + cnt[t]) {
                     digit = 255 - lane * 8 - t;
                     above = run;
+                    dcnt = cnt[t];
                 }
                 run += cnt[t];
             }
@@ -257,15 +258,15 @@ __device__ __forceinline__ void select_row(const uint32_t* kr, uint32_t* hw, int
         const int src_lane = __ffs(owner) - 1;
         digit = __shfl_sync(0xffffffffu, digit, src_lane);
         above = __shfl_sync(0xffffffffu, above, src_lane);
+        dcnt = __shfl_sync(0xffffffffu, dcnt, src_lane);
         rem -= above;
         prefix |= uint32_t(digit) << shift;
         pmask |= 255u << shift;
-        __syncwarp();
+        __syncwarp();  // every read of hw precedes the next pass's clear
 #if PISA_TOPK_EARLY
         // the bin holds exactly the keys still wanted: all of it is taken (see
         // select_row_reg); T = its minimum, every tie of T kept
-        const int dcnt = int(hw[digit]);  // (warp-uniform digit; counts complete since the last __syncwarp)
-        if (dcnt == rem && shift > 0) {
+        if (PISA_TOPK_EARLY && dcnt == rem && shift > 0) {
             uint32_t mn = 0xffffffffu;
             for (int j = lane; j < N; j += 32) {
                 const uint32_t key = kr[j];

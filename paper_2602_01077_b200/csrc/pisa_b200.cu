@@ -284,15 +284,17 @@ pisa_status resolve(pisa_ctx* ctx, const pisa_attn_desc* d, Plan* p) {
     p->Npad = (N + 127) / 128 * 128;  // K3 reads 128-centroid tiles
     p->W = (N + 31) / 32;
     p->k = k;
-    // K1: up to kStatsG key blocks per chunk (work unit), at least ~6 chunks
-    // per head so that 24 heads still cover the 148 SMs at image sizes (FLUX's
-    // N = 72: 6 chunks of 12 -- 144 units -- measured 0.141 ms a step against
-    // 0.143 for 18 chunks of 4, profiles/r02m_ab_k1.log), and as large as
-    // that allows: every chunk writes a D x D fp32 H partial. A function of N
+    // K1: up to kStatsG key blocks per chunk (work unit; every chunk writes a
+    // D x D fp32 H partial). Short (image) heads: 6 chunks per head, so that
+    // their 24 heads make about one wave of work units on 148 SMs (FLUX's
+    // N = 72: 6 chunks of 12 -- 144 units -- 0.141 ms a step against 0.143 for
+    // 18 chunks of 4, profiles/r02m_ab_k1.log); longer heads: 24 chunks per
+    // head (Wan2.1-1.3B, N = 512 with 12 heads: 16 chunks of 32 measured 0.097
+    // ms against 0.076 for 24 chunks of 22, profiles/r02n_*). A function of N
     // only: a head's H_bar partial sums -- and with them its output bits -- do
     // not depend on how many other heads share the launch, so head-sharded
     // ranks reproduce the single-GPU result exactly.
-    p->statsG = std::max<int64_t>(4, std::min<int64_t>(kStatsG, (N + 5) / 6));
+    p->statsG = std::max<int64_t>(4, std::min<int64_t>(kStatsG, N < 256 ? (N + 5) / 6 : (N + 23) / 24));
     if (const char* e = std::getenv("PISA_B200_STATS_G"))  // (A/B of K1's chunk size)
         p->statsG = std::max<int64_t>(1, std::min<int64_t>(kStatsG, std::atoll(e)));
     p->nchunk1 = (N + p->statsG - 1) / p->statsG;
