@@ -17,7 +17,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIBDIR = os.path.join(PKG, "lib")
 LIB = os.path.join(LIBDIR, "libpisa_b200.so")
-SOURCES = ["k1_block_stats.cu", "k1c_block_norms.cu", "k2_select.cu", "k2p_pairing.cu", "k3_fused_attn.cu", "selftest_mma.cu",
+SOURCES = ["k1_block_stats.cu", "k1c_block_norms.cu", "k2_select.cu", "k2p_pairing.cu", "k2q_overlap.cu", "k3_fused_attn.cu", "selftest_mma.cu",
            "generate.cu", "pisa_b200.cu"]
 HEADERS = ["sm100.cuh", "kernels.h", os.path.join("..", "..", "include", "pisa_b200.h")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")

@@ -211,11 +211,16 @@ __global__ void __launch_bounds__(kMatchThreads) pair_match_kernel(const int* __
 }  // namespace
 
 cudaError_t launch_pairing(const uint32_t* mask, int N, int W, int qb0, int qb1, int BH, int* cand,
-                           int2* pairs, cudaStream_t s) {
-    const size_t sm1 = size_t(8 + 2 * kWindow) * W * 4;
-    cudaFuncSetAttribute(pair_candidates_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm1));
-    pair_candidates_kernel<<<dim3((qb1 - qb0 + 7) / 8, BH), 256, sm1, s>>>(mask, N, W, qb0, qb1, cand);
-    cudaError_t e = cudaGetLastError();
+                           int2* pairs, cudaStream_t s, uint16_t* ov) {
+    cudaError_t e;
+    if (ov && pairing_full_supported(qb0, qb1, W)) {
+        e = launch_pairing_full_candidates(mask, N, W, qb0, qb1, BH, ov, cand, s);
+    } else {
+        const size_t sm1 = size_t(8 + 2 * kWindow) * W * 4;
+        cudaFuncSetAttribute(pair_candidates_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm1));
+        pair_candidates_kernel<<<dim3((qb1 - qb0 + 7) / 8, BH), 256, sm1, s>>>(mask, N, W, qb0, qb1, cand);
+        e = cudaGetLastError();
+    }
     if (e != cudaSuccess) return e;
     const size_t sm2 = size_t(2) * N * 4;
     const size_t sm2c = sm2 + size_t(N) * kCand * 2;

@@ -97,8 +97,13 @@ cudaError_t launch_select_stream(int D, const CUtensorMap& tmKs, const SelectArg
 #define PISA_PAIR_CAND 16
 #endif
 constexpr int kPairCand = PISA_PAIR_CAND;  // candidate partners kept per query block
+// ov: scratch u16 [BH][N][N] for the full-range candidate search (K2c over
+// every block of the range, k2q_overlap.cu), or null: the +-kWindow search.
 cudaError_t launch_pairing(const uint32_t* mask, int N, int W, int qb0, int qb1, int BH, int* cand, int2* pairs,
-                           cudaStream_t s);
+                           cudaStream_t s, uint16_t* ov = nullptr);
+bool pairing_full_supported(int qb0, int qb1, int W);
+cudaError_t launch_pairing_full_candidates(const uint32_t* mask, int N, int W, int qb0, int qb1, int BH,
+                                           uint16_t* ov, int* cand, cudaStream_t s);
 
 // Plan (ascending lists) -> bitmask, with SelectionPlan::validate semantics
 // (router.hpp:50-70): sets *bad = 1 on out-of-range / non-ascending entries.

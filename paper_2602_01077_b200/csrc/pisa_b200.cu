@@ -201,6 +201,18 @@ SelectMode select_mode() {
     return kSelectStream;
 }
 
+// K2c candidate search over the whole query-block range (k2q_overlap.cu),
+// opt-in with env PISA_B200_PAIR_FULL=1 (read per call). It cuts the union
+// tiles of independent routing by 2.2 % (Wan2.1-14B gaussian: union/k 1.781 ->
+// 1.741, K3 -0.1..-0.5 ms) but costs 0.44 ms against the window's 0.25 ms:
+// -0.1..-0.5 ms a step at Wan2.1-14B gaussian, +0.1..+0.2 ms on clustered
+// routing and on HunyuanVideo (N = 1856: the N^3 overlap grows),
+// profiles/r02qrtu_ab_pair_full.log.
+bool pair_full_on() {
+    const char* e = std::getenv("PISA_B200_PAIR_FULL");
+    return e && e[0] == '1';
+}
+
 // heads per two-kernel select chunk (env PISA_B200_SELECT_CHUNK_MB: key
 // matrices of at most that many MB, so they stay L2-resident between the two
 // kernels). Default 0 = all heads in one pair of launches: at Wan2.1-14B the
@@ -355,8 +367,9 @@ pisa_status workspace(pisa_ctx* ctx, const Plan& p, Work* w, cudaStream_t s) {
                  o_kbf = take(BH * p.Npad * D * 2), o_vbf = take(BH * p.Npad * D * 2),
                  o_hbf = take(BH * D * D * 2), o_sel = take(BH * N * p.k * 4),
                  o_mask = take(BH * N * p.W * 4),
-                 o_keys = take(std::max(size_t(select_chunk_heads(p.N, p.BH)) * N * N,
-                                        p.N >= kSelectFusedMinN ? size_t(kScratchSlots) * 128 * N : 0) * 4),
+                 o_keys = take(std::max({size_t(select_chunk_heads(p.N, p.BH)) * N * N,
+                                         p.N >= kSelectFusedMinN ? size_t(kScratchSlots) * 128 * N : size_t(0),
+                                         (BH * N * N + 1) / 2}) * 4),  // (+ K2c's u16 overlap matrix)
                  o_ksplit = take(p.N >= kSelectFusedMinN ? 3 * BH * N * D * 2 : 0),
                  o_norms = take(BH * N * 4), o_rect = take(BH * N * 4), o_tri = take(BH * N * kTriStride * 4),
                  o_cand = take(BH * N * kPairCand * 4), o_pairs = take(BH * ((N + 1) / 2) * 8);
@@ -527,9 +540,13 @@ pisa_status run_fused(pisa_ctx* ctx, const pisa_attn_desc& d, const Plan& p, con
     const bool pairing = qb1 - qb0 > 2 && (ctx->pairing == 2 || (ctx->pairing == 1 && qb1 - qb0 >= kPairMinBlocks));
     if (pairing) {
         ProfScope ps(ctx, kPair, s);
-        const cudaError_t e = launch_pairing(w.mask, int(p.N), int(p.W), qb0, qb1, int(p.BH), w.cand, w.pairs, s);
+        // opt-in full-range candidate search (overlap matrix on the tensor cores,
+        // in the keys scratch: the select is done with it)
+        const bool full = pair_full_on() && pairing_full_supported(qb0, qb1, int(p.W));
+        const cudaError_t e = launch_pairing(w.mask, int(p.N), int(p.W), qb0, qb1, int(p.BH), w.cand, w.pairs, s,
+                                             full ? reinterpret_cast<uint16_t*>(w.keys) : nullptr);
         if (e != cudaSuccess) return cuda_fail(ctx, e, "pairing launch");
-        ctx->launches += 2;
+        ctx->launches += full ? 3 : 2;
     }
     FusedArgs a{};
     a.pairs = pairing ? w.pairs : nullptr;

@@ -797,6 +797,35 @@ def test_pairing_modes_agree_and_fewer_tiles(P, oracle_mod):
         ctx.set_pairing(3)
 
 
+@pytest.mark.parametrize("kind", ["gaussian", "clustered"])
+def test_pairing_full_search(P, oracle_mod, kind, monkeypatch):
+    """K2c over the whole query-block range (PISA_B200_PAIR_FULL=1: overlap
+    matrix on tcgen05 kind::i8, nearest-first ties) against the default +-48
+    window: the same plan, outputs equal to rounding, and on independent
+    (gaussian) routing fewer union tiles."""
+    import torch
+    q, k, v = (dev_bf16(x) for x in oracle_mod.gen(kind, 5, 2, 64000, 128))
+    ctx = P.Context.get(0)
+    res = {}
+    try:
+        ctx.set_pairing(2)
+        for full in ("1", "0"):
+            monkeypatch.setenv("PISA_B200_PAIR_FULL", full)
+            ctx.set_profiling(True)
+            ctx.fused_tiles()
+            o, ex = P.fwd(q, k, v, sparsity=0.875, return_plan=True)
+            torch.cuda.synchronize()
+            res[full] = (o, ex["selected"], ctx.fused_tiles())
+            ctx.set_profiling(False)
+    finally:
+        ctx.set_pairing(1)
+        ctx.set_profiling(False)
+    assert torch.equal(res["1"][1], res["0"][1])
+    assert (res["1"][0].float() - res["0"][0].float()).abs().max().item() <= 4e-3
+    if kind == "gaussian":
+        assert res["1"][2] < res["0"][2], (res["1"][2], res["0"][2])
+
+
 @pytest.mark.parametrize("L,d", [(1024, 128), (1000, 64)])
 def test_dense_online_matches_reference(P, oracle_mod, L, d):
     """dense_online (attention.hpp:186-193), the baseline PISA is timed against,

@@ -1,5 +1,12 @@
-# round-2 batch q: image-size breakdowns (plain / covariance router), current library
-for w in flux sd35; do for r in plain covariance; do
-  timeout 300 python bench.py --workload $w --router $r --no-cpu --no-e2e > gpurun_out/img_${w}_${r}.json 2> gpurun_out/img_${w}_${r}.err
-done; done
-ncu --metrics gpu__time_duration.sum --clock-control none -c 200 --csv --log-file gpurun_out/launches_flux_cov.csv python bench.py --workload flux --router covariance --steps 2 --warmup 3 --no-e2e --no-cpu --no-dense > /dev/null 2>&1
+# round-2 batch q: K2c full-range candidate search (int8 tensor-core overlap matrix) vs the +-48 window
+set -x
+timeout 900 python -m pytest tests/test_gpu.py -m gpu -q -x -k "pairing" 2>&1 | tail -4 > gpurun_out/gpu_tests_q.log
+sel() { python -c "import json,sys; j=json.loads(sys.stdin.read()); k=j['kernels']; print('$1', round(j['ms_per_step'],4), 'U/k', round(j['roofline']['union_over_k'],4), {n:round(v['ms_per_launch'],4) for n,v in k.items()}, j['clocks']['sm_mhz'])"; }
+for r in 1 2; do
+  for f in 1 0; do
+    PISA_B200_PAIR_FULL=$f timeout 300 python bench.py --steps 10 --no-e2e --no-cpu --no-dense 2>/dev/null | tail -1 | sel "wan full=$f" >> gpurun_out/ab_pair_q.log 2>&1
+    PISA_B200_PAIR_FULL=$f timeout 300 python bench.py --data clustered --steps 10 --no-e2e --no-cpu --no-dense 2>/dev/null | tail -1 | sel "wan-clustered full=$f" >> gpurun_out/ab_pair_q.log 2>&1
+    PISA_B200_PAIR_FULL=$f timeout 300 python bench.py --workload hunyuan --steps 5 --no-e2e --no-cpu --no-dense 2>/dev/null | tail -1 | sel "hunyuan full=$f" >> gpurun_out/ab_pair_q.log 2>&1
+  done
+done
+ncu --metrics gpu__time_duration.sum --clock-control none -c 60 --csv --log-file gpurun_out/launches_q.csv python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu --no-dense > /dev/null 2>&1

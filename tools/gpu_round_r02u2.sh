@@ -1,0 +1,7 @@
+# round-2 batch u2: overlap_tc with two chunks of mask words in flight
+sel() { python -c "import json,sys; j=json.loads(sys.stdin.read()); k=j['kernels']; print('$1', round(j['ms_per_step'],4), 'U/k', round(j['roofline']['union_over_k'],4), {n:round(v['ms_per_launch'],4) for n,v in k.items()}, j['clocks']['sm_mhz'])"; }
+timeout 600 python tools/hash_outputs.py > gpurun_out/hash_u2.log 2>&1
+for r in 1 2; do for f in 1 0; do
+  PISA_B200_PAIR_FULL=$f timeout 300 python bench.py --steps 10 --no-e2e --no-cpu --no-dense 2>/dev/null | tail -1 | sel "wan full=$f" >> gpurun_out/ab_pair_u2.log 2>&1
+done; done
+ncu --metrics gpu__time_duration.sum --clock-control none -c 60 --csv --log-file gpurun_out/launches_u2.csv python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu --no-dense > /dev/null 2>&1
