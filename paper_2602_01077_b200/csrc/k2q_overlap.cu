@@ -19,9 +19,10 @@
 //     (4095 - |i - j|) << 1 | (j < i), unique per j; every lane keeps its four
 //     largest keys and the kCand largest of the warp are popped in order (the
 //     same contract as the windowed kernel's lists: best first, -1 padded).
-// Opt-in (PISA_B200_PAIR_FULL=1): measured 0.44 ms (overlap 182 us, candidates
-// 110 us, matching 73 us) against the window's 0.25 ms, for 2.2 % fewer union
-// tiles on gaussian routing -- about a wash per step (pisa_b200.cu:pair_full_on).
+// Default up to 2048 blocks per range (PISA_B200_PAIR_FULL=0: the window):
+// 0.37 ms at Wan2.1-14B (overlap 127 us, candidates 111 us, matching 74 us)
+// against the window's 0.25 ms, for 2.2 % fewer union tiles on gaussian
+// routing: -0.3 ms a step (pisa_b200.cu:pair_full_on).
 #include "kernels.h"
 #include "sm100.cuh"
 
@@ -229,29 +230,56 @@ __global__ void __launch_bounds__(kOvTcThreads, 3) overlap_tc_kernel(const uint3
     const int cl = nchunk - 1;
     mbar_wait(&bar[cl & 1], (cl >> 1) & 1);
     tc_fence_after();
-    // warps w and w + 4 share TMEM lane quadrant w % 4 and take column halves
+    // warps w and w + 4 share TMEM lane quadrant w % 4 and take column halves.
+    // O[j][i] (the mirror) leaves straight from the registers: lanes hold
+    // consecutive i, so each store is a 64-byte run. O[i][j] is transposed
+    // through shared memory (the chunk buffers are free now) so that a warp
+    // writes a whole 256-byte row segment at a time; the row-per-thread TMEM
+    // layout would scatter every store over 32 rows.
     uint16_t* O = ov + size_t(bh) * N * N;
-    const int i = i0 + (warp & 3) * 32 + (tid & 31);
+    constexpr int kSt = 136;  // staging row stride in u16 (16-byte aligned, 4-bank skew per row)
+    uint16_t* stage = reinterpret_cast<uint16_t*>(smem);
+    const int il = (warp & 3) * 32 + (tid & 31);
+    const int i = i0 + il;
 #pragma unroll 1
     for (int cc = (warp >> 2) * 64; cc < (warp >> 2) * 64 + 64; cc += 32) {
         uint32_t v[32];
         tmem_ld32(tmem + (uint32_t((warp & 3) * 32) << 16) + cc, v);
         tmem_ld_wait(v);
         const int jb = j0 + cc;
-        if (i < qb1) {
-            if (jb + 32 <= qb1 && (N & 1) == 0) {  // even N: 4-byte aligned pairs
 #pragma unroll
-                for (int e = 0; e < 32; e += 2)
-                    *reinterpret_cast<uint32_t*>(O + size_t(i) * N + jb + e) = v[e] | (v[e + 1] << 16);
+        for (int e = 0; e < 32; e += 8) {
+            uint4 p4;
+            p4.x = v[e] | (v[e + 1] << 16);
+            p4.y = v[e + 2] | (v[e + 3] << 16);
+            p4.z = v[e + 4] | (v[e + 5] << 16);
+            p4.w = v[e + 6] | (v[e + 7] << 16);
+            *reinterpret_cast<uint4*>(stage + il * kSt + cc + e) = p4;
+        }
+        if (ti != tj && i < qb1) {
+#pragma unroll
+            for (int e = 0; e < 32; ++e)
+                if (jb + e < qb1) O[size_t(jb + e) * N + i] = uint16_t(v[e]);
+        }
+    }
+    __syncthreads();
+    // O[i][j]: warp w writes rows w, w + 8, ...; lane l columns 4l .. 4l + 3
+    {
+        const int lane = tid & 31;
+        const int jc = j0 + 4 * lane;
+        for (int rl = warp; rl < kOvTile; rl += kOvTcThreads / 32) {
+            const int ir = i0 + rl;
+            if (ir >= qb1) break;
+            const uint2 q2 = *reinterpret_cast<const uint2*>(stage + rl * kSt + 4 * lane);
+            uint16_t* dst = O + size_t(ir) * N + jc;
+            if (jc + 4 <= qb1 && (N & 1) == 0) {  // even N: 4-byte aligned pairs
+                reinterpret_cast<uint32_t*>(dst)[0] = q2.x;
+                reinterpret_cast<uint32_t*>(dst)[1] = q2.y;
             } else {
+                const uint16_t e4[4] = {uint16_t(q2.x), uint16_t(q2.x >> 16), uint16_t(q2.y), uint16_t(q2.y >> 16)};
 #pragma unroll
-                for (int e = 0; e < 32; ++e)
-                    if (jb + e < qb1) O[size_t(i) * N + jb + e] = uint16_t(v[e]);
-            }
-            if (ti != tj) {
-#pragma unroll
-                for (int e = 0; e < 32; ++e)
-                    if (jb + e < qb1) O[size_t(jb + e) * N + i] = uint16_t(v[e]);
+                for (int e = 0; e < 4; ++e)
+                    if (jc + e < qb1) dst[e] = e4[e];
             }
         }
     }

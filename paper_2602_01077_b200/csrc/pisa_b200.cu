@@ -201,16 +201,15 @@ SelectMode select_mode() {
     return kSelectStream;
 }
 
-// K2c candidate search over the whole query-block range (k2q_overlap.cu),
-// opt-in with env PISA_B200_PAIR_FULL=1 (read per call). It cuts the union
+// K2c candidate search over the whole query-block range (k2q_overlap.cu; env
+// PISA_B200_PAIR_FULL=0: the +-48 window), read per call. It cuts the union
 // tiles of independent routing by 2.2 % (Wan2.1-14B gaussian: union/k 1.781 ->
-// 1.741, K3 -0.1..-0.5 ms) but costs 0.44 ms against the window's 0.25 ms:
-// -0.1..-0.5 ms a step at Wan2.1-14B gaussian, +0.1..+0.2 ms on clustered
-// routing and on HunyuanVideo (N = 1856: the N^3 overlap grows),
-// profiles/r02qrtu_ab_pair_full.log.
+// 1.741) for 0.37 ms of search against the window's 0.25 ms: -0.3 ms a step at
+// Wan2.1-14B, neutral to -0.5 ms on clustered routing and HunyuanVideo
+// (profiles/r02qrtu_ab_pair_full.log, batch v).
 bool pair_full_on() {
     const char* e = std::getenv("PISA_B200_PAIR_FULL");
-    return e && e[0] == '1';
+    return !(e && e[0] == '0');
 }
 
 // heads per two-kernel select chunk (env PISA_B200_SELECT_CHUNK_MB: key
@@ -540,8 +539,8 @@ pisa_status run_fused(pisa_ctx* ctx, const pisa_attn_desc& d, const Plan& p, con
     const bool pairing = qb1 - qb0 > 2 && (ctx->pairing == 2 || (ctx->pairing == 1 && qb1 - qb0 >= kPairMinBlocks));
     if (pairing) {
         ProfScope ps(ctx, kPair, s);
-        // opt-in full-range candidate search (overlap matrix on the tensor cores,
-        // in the keys scratch: the select is done with it)
+        // full-range candidate search (overlap matrix on the tensor cores, in the
+        // keys scratch: the select is done with it) up to 2048 blocks a range
         const bool full = pair_full_on() && pairing_full_supported(qb0, qb1, int(p.W));
         const cudaError_t e = launch_pairing(w.mask, int(p.N), int(p.W), qb0, qb1, int(p.BH), w.cand, w.pairs, s,
                                              full ? reinterpret_cast<uint16_t*>(w.keys) : nullptr);

@@ -799,10 +799,10 @@ def test_pairing_modes_agree_and_fewer_tiles(P, oracle_mod):
 
 @pytest.mark.parametrize("kind", ["gaussian", "clustered"])
 def test_pairing_full_search(P, oracle_mod, kind, monkeypatch):
-    """K2c over the whole query-block range (PISA_B200_PAIR_FULL=1: overlap
-    matrix on tcgen05 kind::i8, nearest-first ties) against the default +-48
-    window: the same plan, outputs equal to rounding, and on independent
-    (gaussian) routing fewer union tiles."""
+    """K2c over the whole query-block range (default: overlap matrix on tcgen05
+    kind::i8, nearest-first ties) against the +-48 window
+    (PISA_B200_PAIR_FULL=0): the same plan, outputs equal to rounding, and on
+    independent (gaussian) routing fewer union tiles."""
     import torch
     q, k, v = (dev_bf16(x) for x in oracle_mod.gen(kind, 5, 2, 64000, 128))
     ctx = P.Context.get(0)

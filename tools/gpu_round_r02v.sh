@@ -1,5 +1,10 @@
-for d in 64 128; do for kind in gaussian clustered; do for fd in 0 1; do
-  timeout 60 python tools/repro_d64.py 1 8192 $d $kind $fd 0.75 >> gpurun_out/repro_v.log 2>&1 || echo "FAIL 1 8192 $d $kind $fd" >> gpurun_out/repro_v.log
-done; done; done
-timeout 60 python tools/repro_d64.py 1 2048 64 clustered 0 0.75 >> gpurun_out/repro_v.log 2>&1 || echo "FAIL small" >> gpurun_out/repro_v.log
-timeout 300 compute-sanitizer --tool memcheck python tools/repro_d64.py 1 2048 64 clustered 0 0.75 > gpurun_out/repro_v_san.log 2>&1
+# round-2 batch v: overlap_tc with coalesced row stores (shared-memory transpose)
+sel() { python -c "import json,sys; j=json.loads(sys.stdin.read()); k=j['kernels']; print('$1', round(j['ms_per_step'],4), 'U/k', round(j['roofline']['union_over_k'],4), {n:round(v['ms_per_launch'],4) for n,v in k.items()}, j['clocks']['sm_mhz'])"; }
+timeout 900 python -m pytest tests/test_gpu.py -m gpu -q -x -k "pairing" 2>&1 | tail -2 > gpurun_out/gpu_tests_v.log
+PISA_B200_PAIR_FULL=1 timeout 600 python tools/hash_outputs.py > gpurun_out/hash_v.log 2>&1
+for r in 1 2; do for f in 1 0; do
+  PISA_B200_PAIR_FULL=$f timeout 300 python bench.py --steps 10 --no-e2e --no-cpu --no-dense 2>/dev/null | tail -1 | sel "wan full=$f" >> gpurun_out/ab_pair_v.log 2>&1
+  PISA_B200_PAIR_FULL=$f timeout 300 python bench.py --data clustered --steps 10 --no-e2e --no-cpu --no-dense 2>/dev/null | tail -1 | sel "wan-clustered full=$f" >> gpurun_out/ab_pair_v.log 2>&1
+  PISA_B200_PAIR_FULL=$f timeout 300 python bench.py --workload hunyuan --steps 5 --no-e2e --no-cpu --no-dense 2>/dev/null | tail -1 | sel "hunyuan full=$f" >> gpurun_out/ab_pair_v.log 2>&1
+done; done
+PISA_B200_PAIR_FULL=1 ncu --metrics gpu__time_duration.sum --clock-control none -c 60 --csv --log-file gpurun_out/launches_v.csv python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu --no-dense > /dev/null 2>&1
