@@ -272,7 +272,8 @@ __global__ void __launch_bounds__(kOvTcThreads, 3) overlap_tc_kernel(const uint3
             if (ir >= qb1) break;
             const uint2 q2 = *reinterpret_cast<const uint2*>(stage + rl * kSt + 4 * lane);
             uint16_t* dst = O + size_t(ir) * N + jc;
-            if (jc + 4 <= qb1 && (N & 1) == 0) {  // even N: 4-byte aligned pairs
+            if (jc + 4 <= qb1 && ((reinterpret_cast<uintptr_t>(dst) & 3u) == 0)) {  // 4-byte aligned pairs
+                // (an odd N, or an odd first block qb0 of a query range, shifts the pairs)
                 reinterpret_cast<uint32_t*>(dst)[0] = q2.x;
                 reinterpret_cast<uint32_t*>(dst)[1] = q2.y;
             } else {

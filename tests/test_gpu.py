@@ -826,6 +826,31 @@ def test_pairing_full_search(P, oracle_mod, kind, monkeypatch):
         assert res["1"][2] < res["0"][2], (res["1"][2], res["0"][2])
 
 
+@pytest.mark.parametrize("q_blocks,N", [((1, 130), 131), ((3, 300), 300), ((0, 257), 257)])
+def test_pairing_full_search_ranges(P, oracle_mod, q_blocks, N):
+    """The full-range pairing search on query-block ranges with an odd first
+    block or an odd N (the overlap matrix's row stores lose 4-byte alignment):
+    forced on, the range's output equals the unpaired range's to rounding and the
+    rest of O is untouched."""
+    import torch
+    L = N * 64 - 17
+    q, k, v = (dev_bf16(x) for x in oracle_mod.gen("gaussian", 8, 1, L, 128))
+    ctx = P.Context.get(0)
+    outs = []
+    try:
+        for mode in (2, 0):
+            ctx.set_pairing(mode)
+            out = torch.zeros_like(q)
+            P.fwd(q, k, v, out, sparsity=0.75, ctx=ctx, q_blocks=q_blocks)
+            torch.cuda.synchronize()
+            outs.append(out)
+    finally:
+        ctx.set_pairing(1)
+    r0, r1 = q_blocks[0] * 64, min(L, q_blocks[1] * 64)
+    assert (outs[0][..., :r0, :] == 0).all() and (outs[0][..., r1:, :] == 0).all()
+    assert (outs[0].float() - outs[1].float()).abs().max().item() <= 4e-3
+
+
 @pytest.mark.parametrize("L,d", [(1024, 128), (1000, 64)])
 def test_dense_online_matches_reference(P, oracle_mod, L, d):
     """dense_online (attention.hpp:186-193), the baseline PISA is timed against,

@@ -1,6 +1,7 @@
-L=$PWD/paper_2602_01077_b200/lib
-for lib in libpisa_b200_spec0.so libpisa_b200_spec1k3.so libpisa_b200.so; do
-  for cfg in "1 33000 64 clustered 1 0.75" "1 33000 128 gaussian 0 0.875" "1 16424 128 gaussian 0 0.875"; do
-    PISA_B200_LIB=$L/$lib timeout 60 python tools/repro_d64.py $cfg > /tmp/o.txt 2>&1 && echo "$lib $cfg ok" >> gpurun_out/repro_x.log || echo "$lib $cfg FAIL" >> gpurun_out/repro_x.log
-  done
+# round-2 batch x: overlap row-store alignment fix -- pairing tests incl. odd ranges, full sanitizer pass
+set -x
+timeout 900 python -m pytest tests/test_gpu.py -m gpu -q -x -k "pairing or qrange or range or shard" 2>&1 | tail -3 > gpurun_out/gpu_tests_x.log
+for tool in memcheck racecheck synccheck initcheck; do
+  q=--quick; [ $tool = memcheck ] && q=
+  timeout 1200 compute-sanitizer --tool $tool --print-limit 50 python tools/sanitize.py $q > gpurun_out/sanitize_r02x_$tool.log 2>&1; echo "rc=$?" >> gpurun_out/sanitize_r02x_$tool.log
 done
