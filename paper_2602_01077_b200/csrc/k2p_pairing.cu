@@ -185,7 +185,72 @@ __global__ void __launch_bounds__(kMatchThreads) pair_match_kernel(const int* __
         __syncthreads();
     }
     // emit pairs in order of the lower index; leftovers paired in index order
-    if (threadIdx.x == 0) {
+    if constexpr (kSmemC) {
+        // in parallel: tile t of a matched block i < partner is ML(< i) +
+        // floor(U(< i) / 2) (ML: matched leads, U: unmatched blocks before i);
+        // the u-th unmatched block (u odd) closes the tile (unm[u - 1], i)
+        __shared__ int wsum[2][kMatchThreads / 32];
+        const int n = qb1 - qb0;
+        const int seg = (n + kMatchThreads - 1) / kMatchThreads;  // <= kMatchPer
+        const int b0 = qb0 + threadIdx.x * seg, b1 = min(qb1, b0 + seg);
+        int ml = 0, un = 0;
+        for (int i = b0; i < b1; ++i) {
+            const int j = partner[i];
+            ml += j > i;
+            un += j < 0;
+        }
+        const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
+        int sml = ml, sun = un;  // inclusive warp scans
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int a = __shfl_up_sync(0xffffffffu, sml, o), b = __shfl_up_sync(0xffffffffu, sun, o);
+            if (lane >= o) {
+                sml += a;
+                sun += b;
+            }
+        }
+        if (lane == 31) {
+            wsum[0][wp] = sml;
+            wsum[1][wp] = sun;
+        }
+        __syncthreads();
+        if (wp == 0) {
+            int a = wsum[0][lane], b = wsum[1][lane];
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int x = __shfl_up_sync(0xffffffffu, a, o), y = __shfl_up_sync(0xffffffffu, b, o);
+                if (lane >= o) {
+                    a += x;
+                    b += y;
+                }
+            }
+            wsum[0][lane] = a;  // inclusive over warps
+            wsum[1][lane] = b;
+        }
+        __syncthreads();
+        int ML = sml - ml + (wp > 0 ? wsum[0][wp - 1] : 0);  // exclusive prefixes of this segment
+        int U = sun - un + (wp > 0 ? wsum[1][wp - 1] : 0);
+        const int Utot = wsum[1][kMatchThreads / 32 - 1], MLtot = wsum[0][kMatchThreads / 32 - 1];
+        int* unm = prop;  // unmatched blocks in index order
+        {
+            int u = U;
+            for (int i = b0; i < b1; ++i)
+                if (partner[i] < 0) unm[u++] = i;
+        }
+        __syncthreads();
+        int2* P = pairs + size_t(bh) * ((N + 1) / 2);
+        for (int i = b0; i < b1; ++i) {
+            const int j = partner[i];
+            if (j > i) {
+                P[ML + U / 2] = make_int2(i, j);
+                ++ML;
+            } else if (j < 0) {
+                if (U & 1) P[ML + U / 2] = make_int2(unm[U - 1], i);
+                ++U;
+            }
+        }
+        if (threadIdx.x == 0 && (Utot & 1)) P[MLtot + Utot / 2] = make_int2(unm[Utot - 1], -1);
+    } else if (threadIdx.x == 0) {
         int t = 0, pending = -1;
         for (int i = qb0; i < qb1; ++i) {
             const int j = partner[i];

@@ -1,1 +1,10 @@
-PISA_B200_LIB=$PWD/paper_2602_01077_b200/lib/libpisa_b200_trace.so timeout 120 python tools/trace_hang.py 1 16424 128 gaussian 0 0.875 128 > gpurun_out/trace_hang.txt 2>&1
+# round-2 batch y: pair_match emits the pairs in parallel (prefix sums) instead of one thread
+sel() { python -c "import json,sys; j=json.loads(sys.stdin.read()); k=j['kernels']; print('$1', round(j['ms_per_step'],4), 'U/k', round(j['roofline']['union_over_k'],4), {n:round(v['ms_per_launch'],4) for n,v in k.items()}, j['clocks']['sm_mhz'])"; }
+timeout 900 python -m pytest tests/test_gpu.py -m gpu -q -x -k "pairing or range" 2>&1 | tail -2 > gpurun_out/gpu_tests_y.log
+timeout 600 python tools/hash_outputs.py > gpurun_out/hash_y.log 2>&1
+PISA_B200_PAIR_FULL=0 timeout 600 python tools/hash_outputs.py > gpurun_out/hash_y_window.log 2>&1
+for r in 1 2; do
+  timeout 300 python bench.py --steps 10 --no-e2e --no-cpu --no-dense 2>/dev/null | tail -1 | sel "wan" >> gpurun_out/ab_y.log 2>&1
+  timeout 300 python bench.py --workload hunyuan --steps 5 --no-e2e --no-cpu --no-dense 2>/dev/null | tail -1 | sel "hunyuan" >> gpurun_out/ab_y.log 2>&1
+done
+ncu --metrics gpu__time_duration.sum --clock-control none -c 60 --csv --log-file gpurun_out/launches_y.csv python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu --no-dense > /dev/null 2>&1
