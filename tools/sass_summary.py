@@ -1,7 +1,7 @@
 #!/usr/bin/env python3
 """Per-kernel SASS opcode counts of the built library's objects (cuobjdump
 -sass), highlighting the instructions that prove the sm_100a paths:
-UTCHMMA / UTCQMMA (tcgen05.mma), UTMALDG / UTMASTG (TMA), LDTM / STTM
+UTCHMMA / UTCQMMA / UTCIMMA (tcgen05.mma kind::f16 / f8f6f4 / i8), UTMALDG / UTMASTG (TMA), LDTM / STTM
 (tcgen05.ld / st), UTCBAR (tcgen05.commit), SYNCS (mbarrier), MUFU (ex2).
 
     python tools/sass_summary.py > profiles/r02_sass_summary.md
@@ -14,7 +14,7 @@ import subprocess
 import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-KEY = ["UTCHMMA", "UTCQMMA", "UTMALDG", "UTMASTG", "UTMAPF", "LDTM", "STTM", "UTCBAR", "SYNCS", "MUFU",
+KEY = ["UTCHMMA", "UTCQMMA", "UTCIMMA", "IMMA", "UTMALDG", "UTMASTG", "UTMAPF", "LDTM", "STTM", "UTCBAR", "SYNCS", "MUFU",
        "FFMA", "HMMA"]
 
 
