@@ -20,7 +20,7 @@
 //     largest keys and the kCand largest of the warp are popped in order (the
 //     same contract as the windowed kernel's lists: best first, -1 padded).
 // Default up to 2048 blocks per range (PISA_B200_PAIR_FULL=0: the window):
-// 0.37 ms at Wan2.1-14B (overlap 127 us, candidates 111 us, matching 74 us)
+// 0.29 ms at Wan2.1-14B (overlap 123 us, candidates 92 us, matching 30 us)
 // against the window's 0.25 ms, for 2.2 % fewer union tiles on gaussian
 // routing: -0.3 ms a step (pisa_b200.cu:pair_full_on).
 #include "kernels.h"
@@ -298,14 +298,28 @@ __global__ void __launch_bounds__(256) cand_full_kernel(const uint16_t* __restri
     const int i = qb0 + blockIdx.x * 8 + warp;
     if (i >= qb1) return;
     const uint16_t* row = ov + (size_t(bh) * N + i) * N;
+    auto make_key = [&](int j, uint32_t o) -> uint32_t {
+        if (j >= qb1 || j == i) return 0u;
+        const int dist = j > i ? j - i : i - j;
+        return (o << 14) | (uint32_t(4095 - dist) << 1) | uint32_t(j < i) | 0x40000000u;
+    };
     uint32_t key[kPer];
+    if (((reinterpret_cast<uintptr_t>(row + qb0)) & 3u) == 0) {
+        // pairs of overlaps per 4-byte load (lane l: j = qb0 + 64 t + 2 l, + 1);
+        // which lane holds which key does not change the kCand largest
+        const uint32_t* row2 = reinterpret_cast<const uint32_t*>(row + qb0);
 #pragma unroll
-    for (int t = 0; t < kPer; ++t) {
-        const int j = qb0 + t * 32 + lane;
-        key[t] = 0u;
-        if (j < qb1 && j != i) {
-            const int dist = j > i ? j - i : i - j;
-            key[t] = (uint32_t(row[j]) << 14) | (uint32_t(4095 - dist) << 1) | uint32_t(j < i) | 0x40000000u;
+        for (int t = 0; t < kPer / 2; ++t) {
+            const int j = qb0 + 64 * t + 2 * lane;
+            const uint32_t w = j < qb1 ? row2[32 * t + lane] : 0u;  // (j + 1 < N: the row holds it)
+            key[2 * t] = make_key(j, w & 0xffffu);
+            key[2 * t + 1] = make_key(j + 1, w >> 16);
+        }
+    } else {
+#pragma unroll
+        for (int t = 0; t < kPer; ++t) {
+            const int j = qb0 + t * 32 + lane;
+            key[t] = j < qb1 ? make_key(j, row[j]) : 0u;
         }
     }
     // this lane's four largest keys, descending (a min / max insertion network)

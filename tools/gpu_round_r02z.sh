@@ -1,6 +1,6 @@
-# round-2 batch z: A/B of the committed kernel against the round-start kernel, image sizes
-L=$PWD/paper_2602_01077_b200/lib
-timeout 1200 bash tools/ab_lib.sh $L/libpisa_b200_k3old.so $L/libpisa_b200.so gaussian clustered > gpurun_out/ab_k3_z.log 2>&1
-for w in flux sd35; do for lib in libpisa_b200_k3old.so libpisa_b200.so; do
-  PISA_B200_LIB=$L/$lib timeout 300 python bench.py --workload $w --no-cpu --no-e2e 2>/dev/null | tail -1 | python -c "import json,sys; j=json.loads(sys.stdin.read()); k=j['kernels']; print('$lib', '$w', round(j['ms_per_step'],4), 'fused', round(k['fused_attn_kernel']['ms_per_launch'],4), 'graph', round(j['graph']['ms_per_step'],4), 'dense', round(j['dense_baseline']['ms'],4), j['clocks'])" >> gpurun_out/ab_k3_z.log 2>&1
-done; done
+# round-2 batch z: candidate kernel with paired 4-byte overlap loads
+sel() { python -c "import json,sys; j=json.loads(sys.stdin.read()); k=j['kernels']; print('$1', round(j['ms_per_step'],4), 'U/k', round(j['roofline']['union_over_k'],4), {n:round(v['ms_per_launch'],4) for n,v in k.items()}, j['clocks']['sm_mhz'])"; }
+timeout 900 python -m pytest tests/test_gpu.py -m gpu -q -x -k "pairing or range" 2>&1 | tail -2 > gpurun_out/gpu_tests_z.log
+timeout 600 python tools/hash_outputs.py > gpurun_out/hash_z.log 2>&1
+timeout 300 python bench.py --steps 10 --no-e2e --no-cpu --no-dense 2>/dev/null | tail -1 | sel "wan" >> gpurun_out/ab_z.log 2>&1
+ncu --metrics gpu__time_duration.sum --clock-control none -c 60 --csv --log-file gpurun_out/launches_z.csv python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu --no-dense > /dev/null 2>&1
