@@ -1,13 +1,8 @@
-# round-2 final measurement batch (single-pass softmax K3): bench line, sweep of
-# every BASELINE config vs dense, Hunyuan density sweep, parity vs the reference,
-# ncu launch list + --set full capture
+# round-2 final-code check: full GPU suite, smoke, default bench line (+ clustered), launch list
 set -x
-python bench.py > gpurun_out/bench_r02f.json 2> gpurun_out/bench_r02f.err
-python bench.py --data clustered --no-cpu > gpurun_out/bench_r02f_clustered.json 2> gpurun_out/bench_r02f_clustered.err
-python bench.py --router covariance --no-cpu --no-e2e > gpurun_out/bench_r02f_covariance.json 2> /dev/null
-for w in flux sd35 wan13b hunyuan; do python bench.py --workload $w --no-cpu --no-e2e > gpurun_out/sweep_r02f_$w.json 2>/dev/null; done
-for w in flux sd35; do python bench.py --workload $w --router covariance --no-cpu --no-e2e > gpurun_out/sweep_r02f_${w}_covariance.json 2>/dev/null; done
-for dd in 0.1 0.25 0.5; do python bench.py --workload hunyuan --density $dd --no-e2e --no-cpu > gpurun_out/sweep_r02f_hunyuan_d$dd.json 2>/dev/null; done
-python tools/parity.py --out gpurun_out/PARITY_r02f.json > gpurun_out/parity_r02f.log 2>&1
-ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches_r02f.csv python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu --no-dense > /dev/null 2>&1
-ncu --set full --clock-control none --import-source on -k regex:"block_stats_persistent|score_kernel|topk_kernel|fused_attn|pair_cand" -s 8 -c 5 -o gpurun_out/prof_r02f python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu --no-dense > gpurun_out/ncu_r02f.log 2>&1
+python -m pytest tests -m gpu -q 2>&1 | tail -3 > gpurun_out/gpu_tests_final.log
+python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke_final.log 2>&1; echo "smoke rc=$?" >> gpurun_out/smoke_final.log
+python bench.py > gpurun_out/bench_final.json 2> gpurun_out/bench_final.err
+python bench.py --data clustered --no-cpu > gpurun_out/bench_final_clustered.json 2> /dev/null
+python bench.py --workload hunyuan --no-cpu --no-e2e > gpurun_out/sweep_final_hunyuan.json 2> /dev/null
+ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches_final.csv python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu --no-dense > /dev/null 2>&1
