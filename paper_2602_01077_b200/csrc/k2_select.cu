@@ -181,14 +181,8 @@ __global__ void __launch_bounds__(kScoreThreads, 1) score_kernel(const float* __
 // top), then a ballot compaction in ascending index order takes every key above
 // it plus the lowest-index ties: topk_ascending semantics (router.hpp:96-108).
 constexpr int kRowsPerCta = 4;
-#ifndef PISA_TOPK_MATCH
-#define PISA_TOPK_MATCH 0  // 1: match_any-aggregated counts on the top digit, 2: on every digit
-#endif
 #ifndef PISA_TOPK_EARLY
 #define PISA_TOPK_EARLY 1  // stop the radix once the k-th key's bin is taken whole
-#endif
-#ifndef PISA_TOPK_LOAD_BATCH
-#define PISA_TOPK_LOAD_BATCH 0  // > 0: row load with this many independent loads per lane
 #endif
 
 // One query block's top-k from its N order keys in shared memory (kr), one
@@ -205,27 +199,10 @@ __device__ __forceinline__ void select_row(const uint32_t* kr, uint32_t* hw, int
     for (int shift = 24; shift >= 0; shift -= 8) {
         for (int b = lane; b < 256; b += 32) hw[b] = 0;
         __syncwarp();
-#if PISA_TOPK_MATCH
-        // lanes with the same digit add once (the top digits of a row's keys
-        // are mostly equal: 32-way conflicts on one counter otherwise)
-        for (int j0 = 0; j0 < N; j0 += 32) {
-            const int j = j0 + lane;
-            const uint32_t key = j < N ? kr[j] : 0u;
-            const bool in = j < N && (key & pmask) == prefix;
-            if (PISA_TOPK_MATCH == 1 && shift != 24) {
-                if (in) atomicAdd(&hw[(key >> shift) & 255u], 1u);
-                continue;
-            }
-            const uint32_t d = in ? (key >> shift) & 255u : 256u + uint32_t(lane);
-            const uint32_t peers = __match_any_sync(0xffffffffu, d);
-            if (in && __ffs(peers) - 1 == lane) atomicAdd(&hw[d], uint32_t(__popc(peers)));
-        }
-#else
         for (int j = lane; j < N; j += 32) {
             const uint32_t key = kr[j];
             if ((key & pmask) == prefix) atomicAdd(&hw[(key >> shift) & 255u], 1u);
         }
-#endif
         __syncwarp();
         // lane l owns digits [255 - 8l - 7, 255 - 8l], scanned from the top
         int cnt[8], tot = 0;
@@ -480,26 +457,7 @@ __global__ void __launch_bounds__(kRowsPerCta * 32) topk_kernel(const uint32_t* 
     uint32_t* hw = kr + N;
     if (i >= N) return;
     const uint32_t* src = keys + (size_t(bh) * N + i) * N;
-#if PISA_TOPK_LOAD_BATCH
-    // kBatch independent loads in flight per lane (the row is ~N / 32 loads
-    // per lane; one at a time each waits a full L2 / HBM latency)
-    constexpr int kBatch = PISA_TOPK_LOAD_BATCH;
-    for (int j0 = 0; j0 < N; j0 += 32 * kBatch) {
-        uint32_t v[kBatch];
-#pragma unroll
-        for (int t = 0; t < kBatch; ++t) {
-            const int j = j0 + t * 32 + lane;
-            v[t] = j < N ? __ldcs(src + j) : 0u;
-        }
-#pragma unroll
-        for (int t = 0; t < kBatch; ++t) {
-            const int j = j0 + t * 32 + lane;
-            if (j < N) kr[j] = v[t];
-        }
-    }
-#else
     for (int j = lane; j < N; j += 32) kr[j] = src[j];
-#endif
     __syncwarp();
     select_row(kr, hw, N, a.k, i, a.force_diagonal != 0,
                a.selected ? a.selected + (size_t(bh) * N + i) * a.k : nullptr,
