@@ -626,10 +626,18 @@ __global__ void __launch_bounds__(kTcThreads, 3)
         float2 y0 = make_float2(0.f, 0.f), y1 = y0, y2 = y0, y3 = y0;
         auto matvec = [&](auto c_begin) {
             constexpr int cb = decltype(c_begin)::value;
+#if PISA_K1C_DIAG_NOLDS  // diagnostic only (wrong numerics): one vector load per step, not 32
+            const float4 v4c = *reinterpret_cast<const float4*>(vs + cb);
+            const float4 w4c = *reinterpret_cast<const float4*>(vs + cb + 4);
+#endif
 #pragma unroll
             for (int c = cb; c < cb + (kPair ? 64 : D); c += 8) {
+#if PISA_K1C_DIAG_NOLDS
+                const float4 v4 = v4c, w4 = w4c;
+#else
                 const float4 v4 = *reinterpret_cast<const float4*>(vs + c);
                 const float4 w4 = *reinterpret_cast<const float4*>(vs + c + 4);
+#endif
                 y0 = ffma2(make_float2(x[c], x[c + 1]), make_float2(v4.x, v4.y), y0);
                 y1 = ffma2(make_float2(x[c + 2], x[c + 3]), make_float2(v4.z, v4.w), y1);
                 y2 = ffma2(make_float2(x[c + 4], x[c + 5]), make_float2(w4.x, w4.y), y2);
